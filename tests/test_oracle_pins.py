@@ -1,0 +1,384 @@
+"""Pins of the CPU oracle against things other than itself (runs without a GPU).
+
+Every test compares the oracle with a value the paper / SPEC prints, a closed form, an
+invariant of discrete Morse theory, or an independent brute force (tests/brute.py:
+Kruskal over all edges and the boundary-matrix column reduction).
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+import brute
+import oracle
+from synth import fields
+
+
+def ids_to_sets(shape, dim, ids):
+    return [frozenset(int(v) for v in oracle.simplex_vertices(shape, dim, int(i))) for i in ids]
+
+
+def sqdist_field(shape, sign):
+    g = np.meshgrid(*[np.arange(s) for s in shape], indexing="ij")
+    r2 = sum((c - 2) ** 2 for c in g)
+    return (sign * r2).astype(np.float32)
+
+
+# ------------------------------------------------------------------ O1 order
+
+@pytest.mark.parametrize(
+    "vals,expect",
+    [([0, 3, 1, 2], [0, 3, 1, 2]), ([1, 1, 1], [0, 1, 2]), ([5, -1], [1, 0])],
+)
+def test_ranks_spec_examples(vals, expect):
+    assert list(oracle.ranks(np.array(vals, np.float32))) == expect
+
+
+def test_ranks_equal_numpy_stable_argsort():
+    rng = np.random.default_rng(1)
+    f = rng.integers(0, 50, size=5000).astype(np.float32)  # heavy ties
+    f[::7] = -0.0
+    f[1::7] = 0.0  # -0 == +0 (reading Z3)
+    f[3] = np.inf
+    f[4] = -np.inf
+    perm = np.argsort(f, kind="stable")
+    expect = np.empty_like(perm)
+    expect[perm] = np.arange(f.size)
+    assert np.array_equal(oracle.ranks(f), expect)
+
+
+def test_ranks_nan_rejected():
+    with pytest.raises(oracle.OracleError):
+        oracle.ranks(np.array([0.0, np.nan], np.float32))
+
+
+# ------------------------------------------------------------------ O2 complex and ids
+
+@pytest.mark.parametrize("shape", [(5,), (3, 4), (2, 2), (3, 3, 4), (2, 2, 2), (2, 3, 2)])
+def test_anchored_ids_biject_onto_freudenthal_complex(shape):
+    cx = brute.freudenthal(shape)
+    d = len(shape)
+    N = int(np.prod(shape))
+    for k in range(d + 1):
+        got = set()
+        per = oracle.cells_per_vertex(d, k)
+        for sid in range(per * N):
+            try:
+                s = frozenset(int(v) for v in oracle.simplex_vertices(shape, k, sid))
+            except oracle.OracleError:
+                continue
+            assert s not in got
+            got.add(s)
+        assert got == cx[k], (shape, k)
+
+
+def test_cells_per_vertex_and_counts():
+    # App. A counts; (2,2,1) -> 4 V, 5 E, 2 T; (2,2,2) -> 6 tets, chi = 1
+    assert [oracle.cells_per_vertex(3, k) for k in range(4)] == [1, 7, 12, 6]
+    assert [oracle.cells_per_vertex(2, k) for k in range(3)] == [1, 3, 2]
+    assert [oracle.cells_per_vertex(1, k) for k in range(2)] == [1, 1]
+    cx = brute.freudenthal((2, 2))
+    assert [len(cx[k]) for k in range(3)] == [4, 5, 2]
+    cx = brute.freudenthal((2, 2, 2))
+    assert len(cx[3]) == 6
+    assert sum((-1) ** k * len(cx[k]) for k in cx) == 1
+    for L in [(3, 4, 5), (2, 3, 7)]:
+        cx = brute.freudenthal(tuple(reversed(L)))
+        ax, ay, az = (l - 1 for l in L)
+        Lx, Ly, Lz = L
+        E = ax * Ly * Lz + Lx * ay * Lz + Lx * Ly * az + ax * ay * Lz + ax * Ly * az + Lx * ay * az + ax * ay * az
+        F = 2 * (ax * ay * Lz + ax * Ly * az + Lx * ay * az) + 6 * ax * ay * az
+        T = 6 * ax * ay * az
+        assert (len(cx[1]), len(cx[2]), len(cx[3])) == (E, F, T)
+
+
+# ------------------------------------------------------------------ O3 gradient validity
+
+def check_gradient(f, res):
+    """Validity of a discrete gradient plus the partition of
+    the complex into pairs and critical simplices."""
+    shape = f.shape
+    d = len(shape)
+    cx = brute.freudenthal(shape)
+    r = brute.ranks(f)
+    seen = set()
+    head_of = {}  # tail -> head
+    for tdim, tid, hid in res.pairs:
+        t = ids_to_sets(shape, int(tdim), [tid])[0]
+        h = ids_to_sets(shape, int(tdim) + 1, [hid])[0]
+        assert t < h and len(h) == len(t) + 1  # facet / cofacet
+        assert brute.maxvertex(t, r) == brute.maxvertex(h, r)  # same lower star: zero persistence
+        assert t not in seen and h not in seen  # at most one vector per simplex
+        seen.add(t)
+        seen.add(h)
+        head_of[t] = h
+    crit = set()
+    for k in range(d + 1):
+        for s in ids_to_sets(shape, k, res.crit[k]):
+            assert s not in seen and s not in crit
+            crit.add(s)
+    allsimp = set(s for k in cx for s in cx[k])
+    assert seen | crit == allsimp
+    # acyclicity: v-paths  t -> head(t) -> other facet t' of head(t) -> head(t') ...
+    succ = {}
+    for t, h in head_of.items():
+        succ[t] = [h - {v} for v in h if (h - {v}) != t and (h - {v}) in head_of]
+    color = {}
+
+    def dfs(u):
+        stack = [(u, iter(succ.get(u, ())))]
+        color[u] = 1
+        while stack:
+            node, it = stack[-1]
+            nxt = next(it, None)
+            if nxt is None:
+                color[node] = 2
+                stack.pop()
+                continue
+            c = color.get(nxt, 0)
+            assert c != 1, "cycle in the discrete gradient"
+            if c == 0:
+                color[nxt] = 1
+                stack.append((nxt, iter(succ.get(nxt, ()))))
+
+    for t in head_of:
+        if color.get(t, 0) == 0:
+            dfs(t)
+    # Euler characteristic of a grid (a ball): sum (-1)^k |C_k| = 1
+    assert sum((-1) ** k * len(res.crit[k]) for k in range(d + 1)) == 1
+    return cx, r
+
+
+def robins_guarantee(f, res, cx, r):
+    """Robins et al.: the critical k-simplices in St^-(x) number beta~_{k-1}(Lk^-(x))
+    (P:1049-1054); critical edges are canonical (reading Z16)."""
+    shape = f.shape
+    d = len(shape)
+    crit_by_x = {}
+    for k in range(d + 1):
+        for s in ids_to_sets(shape, k, res.crit[k]):
+            crit_by_x.setdefault(brute.maxvertex(s, r), []).append(s)
+    for x in range(len(r)):
+        lk = brute.lower_link(cx, x, r)
+        b = brute.reduced_betti(lk)
+        got = [0] * (d + 1)
+        for s in crit_by_x.get(x, []):
+            got[len(s) - 1] += 1
+        for k in range(d + 1):
+            assert got[k] == b[k - 1], (x, k, got, b)
+        # canonical critical edges: one per component of Lk^-(x) other than the one
+        # holding the lowest lower neighbour, joined to that component's lowest vertex
+        verts = [next(iter(s)) for s in lk if len(s) == 1]
+        if not verts:
+            continue
+        comp = {v: v for v in verts}
+
+        def find(a):
+            while comp[a] != a:
+                a = comp[a]
+            return a
+
+        for s in lk:
+            if len(s) == 2:
+                a, bb = (find(v) for v in s)
+                if a != bb:
+                    comp[a] = bb
+        lowest = {}
+        for v in verts:
+            c = find(v)
+            if c not in lowest or r[v] < r[lowest[c]]:
+                lowest[c] = v
+        glob = min(verts, key=lambda v: r[v])
+        expect = set(frozenset((x, lowest[c])) for c in lowest if c != find(glob))
+        gotedges = set(s for s in crit_by_x.get(x, []) if len(s) == 2)
+        assert gotedges == expect
+
+
+SMALL_SHAPES = [(9,), (17,), (5, 6), (7, 7), (4, 4, 4), (3, 5, 4), (5, 5, 5)]
+
+
+@pytest.mark.parametrize("shape", SMALL_SHAPES)
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_gradient_valid_and_robins(shape, seed):
+    rng = np.random.default_rng(100 + seed)
+    f = rng.random(shape, dtype=np.float32)
+    if seed == 2:  # heavy ties: the index tie-break decides
+        f = np.floor(f * 4).astype(np.float32)
+    res = oracle.run(f)
+    cx, r = check_gradient(f, res)
+    robins_guarantee(f, res, cx, r)
+
+
+def test_gradient_constant_and_elevation():
+    # pure index order -> one critical simplex; elevation -> one bar
+    for f in [np.zeros((4, 4, 4), np.float32), np.tile(np.arange(6, dtype=np.float32), (5, 1)),
+              np.arange(20, dtype=np.float32)]:
+        res = oracle.run(f)
+        assert [len(c) for c in res.crit] == [1] + [0] * (f.ndim)
+        assert len(res.d0) == 1 and res.d0[0]["death_id"] == -1
+        assert res.d0[0]["birth_value"] == f.min() and res.d0[0]["death_value"] == f.max()
+        assert len(res.dtop) == (1 if f.ndim == 1 else 0)
+
+
+# ------------------------------------------------------------------ hand-built fields
+
+def test_spec_path_example():
+    # [0,2,1,3] -> criticals {v0, v2, e(v1,v2)}, D0 {(1,2)}, inf 0
+    f = np.array([0, 2, 1, 3], np.float32)
+    res = oracle.run(f)
+    assert list(res.crit[0]) == [0, 2]
+    assert ids_to_sets(f.shape, 1, res.crit[1]) == [frozenset((1, 2))]
+    d0 = [(float(p["birth_value"]), float(p["death_value"]), int(p["death_id"]) < 0) for p in res.d0]
+    assert d0 == [(1.0, 2.0, False), (0.0, 3.0, True)]
+
+
+def test_1d_example_table():
+    f = np.array([0, 2, 1, 3, 1.5, 4, 0.5, 5, 2.5], np.float32)
+    res = oracle.run(f)
+    assert [len(c) for c in res.crit] == [5, 4]
+    fin = sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] >= 0)
+    assert fin == [(0.5, 4.0), (1.0, 2.0), (1.5, 3.0), (2.5, 5.0)]
+    inf = [(float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] < 0]
+    assert inf == [(0.0, 5.0)]
+    # 1D: D_{d-1} = D0 (duality), including the infinite class
+    top = sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.dtop)
+    assert top == sorted(fin + inf)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_negative_paraboloid(d):
+    f = sqdist_field((5,) * d, -1)
+    res = oracle.run(f)
+    if d == 2:
+        assert [len(c) for c in res.crit] == [4, 4, 1]
+        assert sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] >= 0) == [(-8.0, -4.0)] * 3
+        assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.dtop] == [(-4.0, 0.0)]
+    else:
+        assert [len(c) for c in res.crit] == [8, 12, 6, 1]
+        assert sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] >= 0) == [(-12.0, -8.0)] * 7
+        assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.dtop] == [(-4.0, 0.0)]
+        # |D1| = |C1| - |D0 finite| = |C2| - |D2|
+        assert len(res.crit[1]) - 7 == len(res.crit[2]) - len(res.dtop) == 5
+    inf = [p for p in res.d0 if p["death_id"] < 0]
+    assert len(inf) == 1 and float(inf[0]["birth_value"]) == -4.0 * d and float(inf[0]["death_value"]) == 0.0
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_bowl(d):
+    f = sqdist_field((5,) * d, +1)
+    res = oracle.run(f)
+    assert [len(c) for c in res.crit] == [1] + [0] * d
+    assert len(res.dtop) == 0
+    assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.d0] == [(0.0, 4.0 * d)]
+
+
+# ------------------------------------------------------------------ O5 / O6 vs brute force
+
+def pair_sets(shape, res_pairs, bdim):
+    out = set()
+    for p in res_pairs:
+        if p["death_id"] < 0:
+            continue
+        b = ids_to_sets(shape, bdim, [p["birth_id"]])[0]
+        dd = ids_to_sets(shape, bdim + 1, [p["death_id"]])[0]
+        out.add((b, dd))
+    return out
+
+
+BRUTE_SHAPES = [(12,), (30,), (4, 5), (6, 6), (3, 3, 3), (4, 3, 4), (4, 4, 4)]
+
+
+@pytest.mark.parametrize("shape", BRUTE_SHAPES)
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_diagrams_vs_brute_force(shape, seed):
+    rng = np.random.default_rng(1000 + seed)
+    f = rng.random(shape, dtype=np.float32)
+    if seed == 3:
+        f = np.floor(f * 3).astype(np.float32)  # ties
+    d = len(shape)
+    res = oracle.run(f)
+    # D0 at simplex level = Kruskal over all edges (elder rule, zero persistence dropped)
+    kr, r = brute.kruskal_d0(f)
+    kr_set = set((frozenset([b]), e) for b, e in kr)
+    assert pair_sets(shape, res.d0, 0) == kr_set
+    # D0 and D_{d-1} vs the boundary-matrix reduction (vertex level: max vertices)
+    red, unpaired, r = brute.diagrams_by_reduction(f)
+
+    def vlevel(pairs):
+        return sorted((brute.maxvertex(b, r), brute.maxvertex(dd, r)) for b, dd in pairs)
+
+    assert vlevel(pair_sets(shape, res.d0, 0)) == vlevel(red.get(0, []))
+    top = pair_sets(shape, res.dtop, d - 1)
+    assert vlevel(top) == vlevel(red.get(d - 1, []))
+    # simplex level too (holds for this pinned gradient, reading Z14)
+    assert top == set(red.get(d - 1, []))
+    # field values of the pairs are f at the max vertices
+    for p in list(res.d0) + list(res.dtop):
+        assert p["birth_value"] == f.ravel()[p["birth_vertex"]]
+        if p["death_id"] >= 0:
+            assert p["death_value"] == f.ravel()[p["death_vertex"]]
+        else:
+            assert p["death_value"] == f.max()
+    # exactly one infinite class (a ball: beta = (1,0,0)), the global minimum
+    inf = [p for p in res.d0 if p["death_id"] < 0]
+    assert len(inf) == 1 and inf[0]["birth_vertex"] == int(np.argmin(np.asarray(r)))
+    assert len([u for u in unpaired]) == 1
+    # cross-checks
+    nfin0 = len(res.d0) - 1
+    assert nfin0 == len(res.crit[0]) - 1
+    if d >= 2:
+        assert len(res.dtop) == len(res.crit[d])
+    if d == 2:
+        # C_1 = D0 death edges + D1 birth edges, disjoint
+        deaths = set(int(p["death_id"]) for p in res.d0 if p["death_id"] >= 0)
+        births = set(int(p["birth_id"]) for p in res.dtop)
+        assert deaths.isdisjoint(births) and deaths | births == set(int(i) for i in res.crit[1])
+        assert set(int(i) for i in res.unpaired_top) == deaths
+    if d == 3:
+        assert len(res.crit[1]) - nfin0 == len(res.crit[2]) - len(res.dtop)
+    if d == 1:
+        fin = sorted((int(p["birth_vertex"]), int(p["death_vertex"])) for p in res.d0)
+        top = sorted((int(p["birth_vertex"]), int(p["death_vertex"])) for p in res.dtop)
+        assert fin == top
+    # the critical lists are sorted by the lexicographic order (Alg. 2 l. 13)
+    for k in range(d + 1):
+        keys = [brute.lexkey(s, r) for s in ids_to_sets(shape, k, res.crit[k])]
+        assert keys == sorted(keys)
+
+
+def test_sample_mode_matches_full_run():
+    f = fields.uniform((6, 7, 5), seed=3)
+    full = oracle.run(f)
+    verts = np.array([0, 5, 17, 60, 100, 209], np.int64)
+    smp = oracle.gradient_sample(f, verts, nthreads=2)
+    r = brute.ranks(f)
+    shape = f.shape
+    for tdim, tid, hid in smp.pairs:
+        assert any((full.pairs == [tdim, tid, hid]).all(1))
+        t = ids_to_sets(shape, int(tdim), [tid])[0]
+        assert brute.maxvertex(t, r) in set(int(v) for v in verts)
+    for k in range(4):
+        sub = [i for i in full.crit[k] if brute.maxvertex(ids_to_sets(shape, k, [i])[0], r) in set(verts.tolist())]
+        assert sorted(sub) == sorted(smp.crit[k].tolist())
+
+
+def test_threads_deterministic():
+    f = fields.uniform((10, 11, 12), seed=5)
+    a = oracle.run(f, nthreads=1)
+    b = oracle.run(f, nthreads=4)
+    assert np.array_equal(a.pairs, b.pairs)
+    for k in range(4):
+        assert np.array_equal(a.crit[k], b.crit[k])
+    assert a.d0.tobytes() == b.d0.tobytes() and a.dtop.tobytes() == b.dtop.tobytes()
+
+
+def test_degenerate_rejected():
+    for f in [np.zeros((1, 4, 4), np.float32), np.zeros((1,), np.float32)]:
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.run(f)
+        assert e.value.code == 2
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.run(np.array([0.0, np.nan, 1.0], np.float32))
+    assert e.value.code == 3
