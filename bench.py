@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the DMS front end (vertex order, lower-star gradient, critical
+simplices, D0, D_{d-1}) on one B200 per rank.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+
+A step is one pass of the whole hot path over the
+configured synthetic field, which is resident in HBM before the timed region.  Under
+torchrun every rank runs an independent replica (its own seed): the path does not
+shard, so scaling is weak and there is no
+data-path collective; the timing is the max over ranks.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "M vertices/s (gradient + D0 + D_{d-1}, 1 B200) and % of HBM roofline"
+UNIT = "M vertices/s"
+
+CONFIG_DESC = {
+    "c1": "3D 32^3 float32 iid U[0,1)",
+    "c2": "3D 128^3 float32 sum of 32 Gaussians + 1e-3 noise",
+    "c3": "3D 256^3 float32 iid U[0,1)",
+    "c4": "3D 512^3 float32 5-octave value noise (period 64, gain 0.5) + N(0,1e-2)",
+    "c5a": "2D 8192^2 float32 fBm H=0.7 (spectral)",
+    "c5b": "1D 2^27 float32 random walk",
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except Exception:
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(N, ndim, ncrit, npairs):
+    """B_min = N (4 read f + 4 write rank + G_w) + 8 sum|C_k| + 32 pairs,
+    G_w = 8 / 2 / 0.25 B per vertex (3D / 2D / 1D reference gradient layout)."""
+    gw = {3: 8.0, 2: 2.0, 1: 0.25}[ndim]
+    e2e = N * (4 + 4 + gw) + 8 * sum(ncrit) + 32 * npairs
+    grad_kernel = N * (4 + gw) + 8 * sum(ncrit)
+    return e2e, grad_kernel
+
+
+def cpu_oracle_sample(f_full, budget_s=20.0):
+    """The oracle (as it stands) on a bounded crop of the same field, on the host cores."""
+    import numpy as np
+
+    import oracle
+
+    cores = os.cpu_count() or 1
+    d = f_full.ndim
+    side = {3: 48, 2: 512, 1: 1 << 18}[d]
+    t_all, nv = 0.0, 0
+    reps = 0
+    while t_all < budget_s and reps < 8:
+        sl = tuple(slice(0, min(side, s)) for s in f_full.shape)
+        crop = np.ascontiguousarray(f_full[sl])
+        t0 = time.perf_counter()
+        oracle.run(crop, nthreads=cores, want_pairs=False)
+        t_all += time.perf_counter() - t0
+        nv += crop.size
+        reps += 1
+        if t_all > budget_s / 2 and reps >= 1:
+            break
+        side = int(side * (1.5 if d == 3 else 2))
+    return {"value": nv / t_all / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "%d run(s) of the full front end on crops of the same field (up to %s), %.1f s" % (
+                reps, "x".join(str(min(side, s)) for s in f_full.shape), t_all)}
+
+
+def make_field(cfg, seed):
+    from synth import fields
+
+    return fields.make(cfg, seed=seed)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle, as it stands, on this config's field."""
+    if rank != 0:
+        return
+    f = make_field(args.config, 0)
+    import numpy as np  # noqa: F401
+
+    base = cpu_oracle_sample(f, budget_s=max(10.0, 60.0 / max(1, args.steps + args.warmup)))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (ranked; integer arithmetic)", "data": "synthetic",
+        "config": {"workload": args.config, "desc": CONFIG_DESC[args.config]},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--impl", default="dms", choices=["dms", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2206_13932_b200 as dms
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    f_host = make_field(args.config, seed=rank)
+    N = f_host.size
+    ndim = f_host.ndim
+    f_dev = torch.from_numpy(f_host).cuda()
+    stream = torch.cuda.current_stream()
+    ctx = dms.DMS(f_dev, stream)
+    rank_buf = torch.empty(N, dtype=torch.int32, device="cuda")
+    grad_buf = torch.empty(dms.dms_gradient_bytes(ctx.ctx), dtype=torch.uint8, device="cuda")
+
+    def step():
+        ctx.run_all(rank_buf, grad_buf)
+        # the step's results are complete once the diagram calls return (they sync)
+        dms.dms_diagram0(ctx.ctx)
+        dms.dms_diagram_top(ctx.ctx)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launch_count()
+    dms.dms_set_timing(ctx.ctx, True)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    stages = dms.dms_stage_ms(ctx.ctx)
+    dms.dms_set_timing(ctx.ctx, False)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+
+    if dist is not None:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+
+    ms_step = ms_total / args.steps
+    value = world * N * args.steps / (ms_total / 1e3) / 1e6
+
+    counts, _ = dms.dms_critical(ctx.ctx)
+    ncrit = counts[: ndim + 1]
+    _, nd0 = dms.dms_diagram0(ctx.ctx)
+    _, ndt = dms.dms_diagram_top(ctx.ctx)
+    bmin_e2e, bmin_grad = algorithmic_bytes(N, ndim, ncrit, nd0 + ndt)
+    peak, peak_kind = load_peaks()
+    g_ms = stages["gradient_kernel"] / max(1, stages["gradient_launches"])
+    g_ach = bmin_grad / (g_ms / 1e3) / 1e9
+    roofline = {
+        "kernel": "k_gradient<%d> (lower-star gradient + critical compaction)" % ndim,
+        "bound": "hbm", "achieved": round(g_ach, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(g_ach / peak, 4), "traffic": None,
+        "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(bmin_grad), "ms_per_launch": round(g_ms, 4),
+        "end_to_end_frac_of_hbm": round(bmin_e2e / (ms_step / 1e3) / 1e9 / peak, 4),
+        "end_to_end_frac_of_8TBps": round(bmin_e2e / (ms_step / 1e3) / 8e12, 4),
+    }
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                tr = json.load(fh).get(args.config)
+            if tr:
+                roofline["traffic"] = tr["bytes_per_launch"]
+                roofline["traffic_source"] = tr.get("source")
+        except Exception:
+            pass
+
+    # end to end through the public API: pinned host input -> device, run, diagrams back
+    e2e = None
+    if not args.no_e2e:
+        f_pin = torch.from_numpy(f_host).pin_memory()
+        h2d = f_pin.numel() * 4
+
+        def e2e_step():
+            f_dev.copy_(f_pin, non_blocking=True)
+            step()
+            a = ctx.diagram0()
+            b = ctx.diagram_top()
+            return a.nbytes + b.nbytes
+
+        d2h = e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            d2h = e2e_step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = t0.elapsed_time(t1)
+        if dist is not None:
+            t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": round(world * N * args.steps / (ms_e2e / 1e3) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(ms_e2e / args.steps, 3)}
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_base = cpu_oracle_sample(f_host)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 in, integer arithmetic (ordered uint32 keys)", "data": "synthetic",
+            "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "N": N,
+                       "l2": "input (%d MB) larger than L2; no flush" % (N * 4 >> 20),
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "stages_ms_per_step": {k: round(v / args.steps, 4) for k, v in stages.items() if k != "gradient_launches"},
+            "counts": {"critical": ncrit, "d0_pairs": nd0, "dtop_pairs": ndt},
+            "roofline": roofline,
+            "cpu_baseline": cpu_base,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

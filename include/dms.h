@@ -1,0 +1,161 @@
+/*
+ * dms.h -- C ABI of the B200-native Discrete Morse Sandwich front end.
+ *
+ * Computes, for a float32 scalar field on a Freudenthal-triangulated regular grid
+ * (1D/2D/3D), the pieces of arXiv 2206.13932 ("Discrete Morse Sandwich") that
+ * precede the D1 stage:
+ *   dms_order        global vertex order              PAPER.md 1368-1372 (Sec. 2.1), 1069-1071 (Sec. 7.1)
+ *   dms_gradient     lower-star discrete gradient     PAPER.md 1965-1971 (Sec. 2.6), 272-294 (Sec. 4.1c)
+ *   dms_critical     critical simplices C_k, sorted   PAPER.md 317-362 (Alg. 2)
+ *   dms_diagram0     D0 (minimum-saddle pairs)        PAPER.md 2481-2685 (Sec. 5.1)
+ *   dms_diagram_top  D_{d-1} (saddle-maximum pairs)   PAPER.md 2690-2825 (Sec. 5.2)
+ *   infinite classes (inside the two diagram calls)   PAPER.md 2860-2878 (Sec. 6)
+ * Everything runs in hand-written CUDA kernels for sm_100a on the caller's stream;
+ * there is no CPU fallback.  Readings of the paper's silent points (tie-break,
+ * simplex ids, boundary handling, output order) are listed in DESIGN.md.
+ *
+ * Conventions
+ *   grid      dims[0] = Lx (fastest), dims[1] = Ly, dims[2] = Lz; vertex id
+ *             v = x + Lx*(y + Ly*z); ndim in {1,2,3}, every used extent >= 2, N < 2^31.
+ *   order     K(u) < K(v)  iff  f(u) < f(v) (IEEE, so -0 == +0) or (f(u) == f(v) and u < v).
+ *   simplex   anchored id = C_k * vid(anchor) + chain index,
+ *             C_k = cells per vertex: 3D 1/7/12/6, 2D 1/3/2, 1D 1/1 for k = 0..d.
+ *   lex order the lexicographic order of PAPER.md 1380-1414 (decreasing K tuples).
+ *
+ * Memory ownership
+ *   d_f is BORROWED (device, read-only) and must stay valid until dms_destroy.
+ *   d_rank / d_grad are CALLER-OWNED device buffers written asynchronously.
+ *   Arrays returned through pointer-to-pointer arguments are LIBRARY-OWNED device
+ *   buffers, valid until the next call that recomputes them or dms_destroy.
+ *   The workspace is allocated at dms_create.
+ *
+ * Errors
+ *   Every entry point returns a dms_status; no C++ exception crosses the ABI.
+ *   Argument/shape errors are synchronous.  A NaN in f is detected on the device and
+ *   reported by the next synchronising call (dms_critical, dms_diagram0,
+ *   dms_diagram_top, dms_sync) as DMS_ERR_NAN.  CUDA errors -> DMS_ERR_CUDA
+ *   (sticky: later calls on the same context return DMS_ERR_STATE).
+ *
+ * Synchronisation
+ *   Only calls returning host counts (h_count, h_n) synchronise the stream.
+ */
+#ifndef DMS_H
+#define DMS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dms_ctx dms_ctx; /* opaque */
+
+typedef enum {
+    DMS_OK = 0,
+    DMS_ERR_ARG = 1,        /* NULL pointer, bad enum                           */
+    DMS_ERR_DEGENERATE = 2, /* ndim not in {1,2,3} or a used extent < 2 */
+    DMS_ERR_NAN = 3,        /* f contains NaN                           */
+    DMS_ERR_TOO_LARGE = 4,  /* N >= 2^31 or simplex ids overflow int32 indexing  */
+    DMS_ERR_STATE = 5,      /* sticky earlier error, or an unsupported mode      */
+    DMS_ERR_CUDA = 6,       /* a CUDA call failed                               */
+    DMS_ERR_OOM = 7,        /* device allocation failed                          */
+    DMS_ERR_INVARIANT = 8   /* an internal invariant check failed                */
+} dms_status;
+
+typedef enum {
+    DMS_BOUNDARY_EXACT = 0, /* virtual maximum on the boundary (PAPER.md 2787-2825) */
+    DMS_BOUNDARY_IGNORE = 1 /* Appendix A variant: not built, returns DMS_ERR_STATE  */
+} dms_boundary;
+
+/* One persistence pair (PAPER.md 1641-1697).  death_id = -1 marks an infinite class
+ * (Sec. 6), whose death_value is f* = max f. Values are f at the simplices' highest
+ * vertices (PAPER.md 1662-1664). 32 bytes. */
+typedef struct {
+    int64_t birth_id, death_id;         /* anchored simplex ids                 */
+    int32_t birth_vertex, death_vertex; /* highest vertex of each (-1 infinite) */
+    float birth_value, death_value;
+} dms_pair;
+
+/* Create a context for the field d_f (device float32, N values, x fastest) on the
+ * CUDA stream `stream` (cudaStream_t, may be 0).  Validates the shape synchronously
+ * and allocates the device workspace. */
+dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* stream, dms_ctx** out);
+
+/* Vertex order (PAPER.md 1368-1372; Sec. 7.1 "global sort"): d_rank[v] = number of
+ * vertices u with K(u) < K(v), i.e. a key-value radix sort of (value, index).
+ * d_rank: caller-owned device int32[N].  Asynchronous. */
+dms_status dms_order(dms_ctx* ctx, int32_t* d_rank);
+
+/* Bytes of the packed gradient: 3D 16 B/vertex, 2D 2 B/vertex, 1D 1 B/vertex. */
+size_t dms_gradient_bytes(const dms_ctx* ctx);
+
+/* Lower-star discrete gradient (Robins et al. ProcessLowerStars, PAPER.md 1965-1971)
+ * of every vertex, plus the critical simplices of every lower star (Alg. 2).
+ * d_grad: caller-owned device buffer of dms_gradient_bytes(ctx) bytes, one packed
+ * word per vertex encoding, for every simplex of the vertex's lower star that is the
+ * head of a discrete vector, which facet it is paired with (layout: DESIGN.md
+ * "Gradient words").  Runs dms_order first if it has not run.  Asynchronous. */
+dms_status dms_gradient(dms_ctx* ctx, void* d_grad);
+
+/* Critical simplices C_0..C_d, each sorted by the lexicographic order (Alg. 2 l. 13,
+ * PAPER.md 357-359).  h_count[k] = |C_k| (k > d: 0); d_ids_out[k] = library-owned
+ * device int64 array of anchored ids.  Synchronises. */
+dms_status dms_critical(dms_ctx* ctx, int64_t h_count[4], const int64_t* d_ids_out[4]);
+
+/* D0 (Sec. 5.1): pairs (minimum, critical edge) in increasing death-edge lex order,
+ * then the one infinite class (global minimum, f*).  *d_pairs: library-owned device
+ * array of *h_n records.  Synchronises. */
+dms_status dms_diagram0(dms_ctx* ctx, const dms_pair** d_pairs, int64_t* h_n);
+
+/* D_{d-1} (Sec. 5.2): pairs (critical (d-1)-simplex, critical d-simplex) in
+ * decreasing birth lex order; for d = 1 the infinite class of the global minimum
+ * follows.  mode must be DMS_BOUNDARY_EXACT.  Synchronises. */
+dms_status dms_diagram_top(dms_ctx* ctx, int mode, const dms_pair** d_pairs, int64_t* h_n);
+
+/* Critical saddles left unpaired (hand-off to the D1 stage): which = 0: critical edges
+ * unpaired by D0 (1-cycle creators); which = 1: critical (d-1)-simplices unpaired by
+ * D_{d-1}.  Ascending lex order; library-owned device int64.  Synchronises. */
+dms_status dms_unpaired_saddles(dms_ctx* ctx, int which, const int64_t** d_ids, int64_t* h_n);
+
+/* Run the whole front end (order, gradient, critical lists, D0, D_{d-1}) on the
+ * stream; the host only synchronises to read the critical counts and the union-find
+ * progress counters.  Results are read with the calls above afterwards.
+ * d_rank / d_grad may be NULL (library-owned scratch). */
+dms_status dms_run_all(dms_ctx* ctx, int32_t* d_rank, void* d_grad);
+
+/* Wait for the stream and report a pending device-side error (NaN, overflow). */
+dms_status dms_sync(dms_ctx* ctx);
+
+/* Host-side decode of packed gradient words of vertices [v0, v1) into discrete
+ * vectors (tail dim, tail id, head id), int64 triples.  h_words: host copy of the
+ * words of those vertices.  Returns the number of triples written (<= cap), or -1. */
+int64_t dms_decode_pairs(const int64_t dims[3], int ndim, const void* h_words, int64_t v0, int64_t v1,
+                         int64_t* h_triples, int64_t cap);
+
+/* Copy `bytes` between device/host buffers on the context's stream and wait
+ * (cudaMemcpyDefault); used by the binding to move library-owned results. */
+dms_status dms_copy(dms_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* Per-stage device timing with CUDA events recorded on the context's stream.
+ * enable != 0 starts recording (and clears the accumulators); dms_stage_ms waits for
+ * the stream and writes the accumulated milliseconds of stages
+ * 0 order, 1 gradient (+ compaction), 2 critical sort, 3 D0, 4 D_{d-1},
+ * 5 gradient kernel alone, and the number of timed gradient launches in ms_out[6]. */
+dms_status dms_set_timing(dms_ctx* ctx, int enable);
+dms_status dms_stage_ms(dms_ctx* ctx, double ms_out[7]);
+
+/* Number of kernel launches issued by this context so far (bench accounting). */
+int64_t dms_launch_count(const dms_ctx* ctx);
+
+/* Last error message of the context (static storage of the context). */
+const char* dms_last_error(const dms_ctx* ctx);
+
+/* Free the context and every library-owned buffer. NULL is a no-op. */
+void dms_destroy(dms_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DMS_H */

@@ -1,0 +1,412 @@
+// diag.cuh -- extremum diagrams D0 and D_{d-1} (Sec. 5) on sm_100a.
+//
+// D0 (Sec. 5.1, PAPER.md 2481-2685):
+//   (a)+(b) k_d0_arcs: for every critical edge (sorted, Alg. 2), follow the two
+//           descending v-paths (vertex -> paired edge -> other vertex) from its
+//           vertices to minima.  The paired edge of a vertex is its steepest-descent
+//           edge, so this is root finding in the steepest-descent forest.  Arc =
+//           (node of minimum a, node of minimum b); nodes = positions in sorted C_0.
+//   (c)+(d) union-find over the arcs in increasing lexicographic order with the
+//           Elder rule, done as parallel mutual-minimum contraction rounds (DESIGN.md
+//           "Union-find"), finished by a sequential tail kernel.
+// D_{d-1} (Sec. 5.2, PAPER.md 2690-2825): the same on the dual gradient: stable sets
+//   of the critical (d-1)-simplices, followed through the d-simplices (d-simplex ->
+//   its paired facet -> the other cofacet of that facet), a virtual maximum on the
+//   boundary (exact mode), union-find in decreasing order, the virtual maximum oldest.
+#pragma once
+#include "common.cuh"
+#include "star.cuh"
+
+namespace dms {
+
+struct Geo3 {
+    int ndim;
+    int32_t Lx, Ly, Lz;
+    int64_t N;
+    int64_t ncell[4];
+    const float* f;
+    const void* grad;
+    const StarTab* tab;
+};
+
+__device__ __forceinline__ int64_t lin_mask(const Geo3& g, int m) {
+    return (int64_t)(m & 1) + (int64_t)g.Lx * ((m >> 1) & 1) + (int64_t)g.Lx * g.Ly * ((m >> 2) & 1);
+}
+
+__device__ __forceinline__ bool kless_v(const Geo3& g, int64_t u, int64_t v) {
+    const uint32_t ou = ord_of(__ldg(g.f + u)), ov = ord_of(__ldg(g.f + v));
+    return k_less(ou, u, ov, v);
+}
+
+// vertex code of v (edge slot paired with v), -1 if v is a minimum
+__device__ __forceinline__ int vcode_of(const Geo3& g, int64_t v) {
+    if (g.ndim == 3) {
+        int c = (int)((__ldg(reinterpret_cast<const uint32_t*>(g.grad) + 4 * v + 3) >> 24) & 15u);
+        return c == 15 ? -1 : c;
+    } else if (g.ndim == 2) {
+        int c = (int)(__ldg(reinterpret_cast<const uint16_t*>(g.grad) + v) & 7u);
+        return c == 7 ? -1 : c;
+    }
+    int c = (int)__ldg(reinterpret_cast<const uint8_t*>(g.grad) + v);
+    return c == 3 ? -1 : c;
+}
+
+__device__ __forceinline__ void coords_of(const Geo3& g, int64_t v, int& x, int& y, int& z) {
+    const int vv = (int)v;
+    x = vv % g.Lx;
+    const int t = vv / g.Lx;
+    y = t % g.Ly;
+    z = t / g.Ly;
+}
+
+__device__ __forceinline__ bool slot_in(const Geo3& g, const StarTab& S, int x, int y, int z, int s) {
+    const int nx = x + S.off[s][0], ny = y + S.off[s][1], nz = z + S.off[s][2];
+    return nx >= 0 && nx < g.Lx && ny >= 0 && ny < g.Ly && nz >= 0 && nz < g.Lz;
+}
+
+// follow the descending v-path from v to its minimum (Sec. 5.1(a))
+__device__ __forceinline__ int64_t descend(const Geo3& g, const StarTab& S, int64_t v) {
+    while (true) {
+        const int c = vcode_of(g, v);
+        if (c < 0) return v;
+        v += S.lin[c];
+    }
+}
+
+__global__ void k_node_map(const int64_t* __restrict__ ids, int64_t m, int32_t* __restrict__ node_of) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) node_of[ids[i]] = (int32_t)i;
+}
+
+__global__ void k_d0_arcs(Geo3 g, const int64_t* __restrict__ c1, int64_t m, const int32_t* __restrict__ node_of0,
+                          int32_t* __restrict__ arc_a, int32_t* __restrict__ arc_b) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const StarTab& S = *g.tab;
+    const int64_t id = c1[i];
+    const int64_t a = id / g.ncell[1];
+    const int k = (int)(id % g.ncell[1]);
+    const int64_t b = a + lin_mask(g, S.chain[1][k][0]);
+    arc_a[i] = node_of0[descend(g, S, a)];
+    arc_b[i] = node_of0[descend(g, S, b)];
+}
+
+// ---------------------------------------------------------------- dual tracing
+
+// 3D: chase from tetrahedron c (anchored id, or -1 = virtual) to a critical
+// tetrahedron's node, or the virtual node `vnode`
+__device__ int32_t chase_tet(const Geo3& g, const StarTab& S, int64_t c, const int32_t* node_of, int32_t vnode) {
+    while (c >= 0) {
+        const int64_t a = c / 6;
+        const int k = (int)(c % 6);
+        int64_t p[4];
+        p[0] = a;
+        p[1] = a + lin_mask(g, S.chain[3][k][0]);
+        p[2] = a + lin_mask(g, S.chain[3][k][1]);
+        p[3] = a + lin_mask(g, 7);
+        int jx = 0;
+        for (int j = 1; j < 4; j++) if (kless_v(g, p[jx], p[j])) jx = j;
+        const int64_t x = p[jx];
+        const int T = S.q_slot[k][jx];
+        const uint64_t hi = __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * x + 1);
+        const int code = (int)((hi >> (8 + 2 * T)) & 3ull);
+        if (code == 0) return node_of[c];  // a critical tetrahedron (a maximum)
+        const int tt = S.tet_tri[T][code - 1];      // s' = Pair(c)
+        const int other = S.tri_tet[tt][0] == T ? S.tri_tet[tt][1] : S.tri_tet[tt][0];
+        int cx, cy, cz;
+        coords_of(g, x, cx, cy, cz);
+        if (other == 255 || !slot_in(g, S, cx, cy, cz, S.tet_a[other]) || !slot_in(g, S, cx, cy, cz, S.tet_b[other]) ||
+            !slot_in(g, S, cx, cy, cz, S.tet_c[other]))
+            return vnode;  // s' on the boundary: the virtual maximum
+        c = 6 * (x + S.q_anc[other][0] + (int64_t)g.Lx * S.q_anc[other][1] + (int64_t)g.Lx * g.Ly * S.q_anc[other][2]) +
+            S.q_k[other];
+    }
+    return vnode;
+}
+
+// 2D: same over triangles
+__device__ int32_t chase_tri2(const Geo3& g, const StarTab& S, int64_t c, const int32_t* node_of, int32_t vnode) {
+    while (c >= 0) {
+        const int64_t a = c / 2;
+        const int k = (int)(c % 2);
+        int64_t p[3];
+        p[0] = a;
+        p[1] = a + lin_mask(g, S.chain[2][k][0]);
+        p[2] = a + lin_mask(g, 3);
+        int jx = 0;
+        for (int j = 1; j < 3; j++) if (kless_v(g, p[jx], p[j])) jx = j;
+        const int64_t x = p[jx];
+        const int t = S.t_slot[k][jx];
+        const uint32_t w = __ldg(reinterpret_cast<const uint16_t*>(g.grad) + x);
+        const int code = (int)((w >> (3 + 2 * t)) & 3u);
+        if (code == 0) return node_of[c];
+        const int e = code == 1 ? S.tri_a[t] : S.tri_b[t];
+        const int other = S.edge_tri[e][0] == t ? S.edge_tri[e][1] : S.edge_tri[e][0];
+        int cx, cy, cz;
+        coords_of(g, x, cx, cy, cz);
+        if (other == 255 || !slot_in(g, S, cx, cy, cz, S.tri_a[other]) || !slot_in(g, S, cx, cy, cz, S.tri_b[other]))
+            return vnode;
+        c = 2 * (x + S.t_anc[other][0] + (int64_t)g.Lx * S.t_anc[other][1]) + S.t_k[other];
+    }
+    return vnode;
+}
+
+// 1D: edges (a, a+1) have id a
+__device__ int32_t chase_edge1(const Geo3& g, int64_t c, const int32_t* node_of, int32_t vnode) {
+    while (c >= 0) {
+        const bool right_hi = kless_v(g, c, c + 1);
+        const int64_t x = right_hi ? c + 1 : c;
+        const int slot = right_hi ? 0 : 1;  // the edge seen from x: 0 = left, 1 = right
+        const int code = vcode_of(g, x);
+        if (code != slot) return node_of[c];  // not paired with its highest vertex: critical
+        if (slot == 0) c = (x < g.N - 1) ? x : -1;  // x's other (right) edge
+        else c = (x > 0) ? x - 1 : -1;              // x's other (left) edge
+    }
+    return vnode;
+}
+
+// arcs of G_{D_{d-1}}: processing order j = 0.. is DEcreasing lex order (Sec. 5.2)
+__global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ cs, int64_t m, const int32_t* __restrict__ node_of,
+                            int32_t vnode, int32_t* __restrict__ arc_a, int32_t* __restrict__ arc_b) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const StarTab& S = *g.tab;
+    const int64_t id = cs[m - 1 - j];
+    int32_t end[2];
+    if (g.ndim == 3) {
+        const int64_t a = id / 12;
+        const int k = (int)(id % 12);
+        int64_t p[3];
+        p[0] = a;
+        p[1] = a + lin_mask(g, S.chain[2][k][0]);
+        p[2] = a + lin_mask(g, S.chain[2][k][1]);
+        int jx = 0;
+        for (int q = 1; q < 3; q++) if (kless_v(g, p[jx], p[q])) jx = q;
+        const int64_t x = p[jx];
+        const int t = S.t_slot[k][jx];
+        int cx, cy, cz;
+        coords_of(g, x, cx, cy, cz);
+        for (int side = 0; side < 2; side++) {
+            const int T = S.tri_tet[t][side];
+            int64_t c = -1;
+            if (T != 255 && slot_in(g, S, cx, cy, cz, S.tet_a[T]) && slot_in(g, S, cx, cy, cz, S.tet_b[T]) &&
+                slot_in(g, S, cx, cy, cz, S.tet_c[T]))
+                c = 6 * (x + S.q_anc[T][0] + (int64_t)g.Lx * S.q_anc[T][1] + (int64_t)g.Lx * g.Ly * S.q_anc[T][2]) +
+                    S.q_k[T];
+            end[side] = chase_tet(g, S, c, node_of, vnode);
+        }
+    } else if (g.ndim == 2) {
+        const int64_t a = id / 3;
+        const int k = (int)(id % 3);
+        const int64_t p0 = a, p1 = a + lin_mask(g, S.chain[1][k][0]);
+        const int jx = kless_v(g, p0, p1) ? 1 : 0;
+        const int64_t x = jx ? p1 : p0;
+        const int s = S.e_slot[k][jx];
+        int cx, cy, cz;
+        coords_of(g, x, cx, cy, cz);
+        for (int side = 0; side < 2; side++) {
+            const int t = S.edge_tri[s][side];
+            int64_t c = -1;
+            if (t != 255 && slot_in(g, S, cx, cy, cz, S.tri_a[t]) && slot_in(g, S, cx, cy, cz, S.tri_b[t]))
+                c = 2 * (x + S.t_anc[t][0] + (int64_t)g.Lx * S.t_anc[t][1]) + S.t_k[t];
+            end[side] = chase_tri2(g, S, c, node_of, vnode);
+        }
+    } else {
+        end[0] = chase_edge1(g, id > 0 ? id - 1 : -1, node_of, vnode);
+        end[1] = chase_edge1(g, id < g.N - 1 ? id : -1, node_of, vnode);
+    }
+    arc_a[j] = end[0];
+    arc_b[j] = end[1];
+}
+
+// ---------------------------------------------------------------- union-find
+// Arcs are indexed in processing order; an arc's index is its key.  Seniority:
+// older_is_smaller = true for D0 (node = position in ascending C_0), false for
+// D_{d-1} (node = position in ascending C_d, the virtual node the largest = oldest).
+// out[i]: -2 undecided, -1 unpaired (cycle), >= 0 the node that dies at arc i.
+
+__device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t a) {
+    int32_t p = parent[a];
+    while (p != a) {
+        const int32_t gp = parent[p];
+        if (gp != p) parent[a] = gp;  // path halving (only ever points to an ancestor)
+        a = p;
+        p = gp;
+        if (gp == a) break;
+        p = parent[a];
+    }
+    return a;
+}
+
+__global__ void k_uf_init(int32_t* parent, uint32_t* best, int64_t n, int32_t* out, int64_t m) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) { parent[i] = (int32_t)i; best[i] = 0xffffffffu; }
+    if (i < m) out[i] = -2;
+}
+
+__global__ void k_uf_round1(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b, int64_t m,
+                            int32_t* parent, uint32_t* best, int32_t* ra, int32_t* rb, int32_t* out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (out[i] != -2) continue;
+        const int32_t a = uf_find(parent, arc_a[i]);
+        const int32_t b = uf_find(parent, arc_b[i]);
+        ra[i] = a;
+        rb[i] = b;
+        if (a == b) { out[i] = -1; continue; }  // the arc closes a cycle: stays unpaired
+        atomicMin(&best[a], (uint32_t)i);
+        atomicMin(&best[b], (uint32_t)i);
+    }
+}
+
+__global__ void k_uf_round2(int64_t m, int32_t* parent, const uint32_t* best, const int32_t* ra, const int32_t* rb,
+                            int32_t* out, bool older_is_smaller) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (out[i] != -2) continue;
+        const int32_t a = ra[i], b = rb[i];
+        if (best[a] == (uint32_t)i && best[b] == (uint32_t)i) {
+            // mutual minimum: Kruskal would merge exactly these two components here
+            const bool a_older = older_is_smaller ? (a < b) : (a > b);
+            const int32_t young = a_older ? b : a, old = a_older ? a : b;
+            parent[young] = old;
+            out[i] = young;
+        }
+    }
+}
+
+__global__ void k_uf_round3(int64_t m, uint32_t* best, const int32_t* ra, const int32_t* rb, const int32_t* out,
+                            unsigned long long* remaining) {
+    uint32_t live = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t o = out[i];
+        if (o == -1) continue;
+        // reset the candidates of this round (roots of every arc visited this round)
+        if (o == -2 || o >= 0) {
+            best[ra[i]] = 0xffffffffu;
+            best[rb[i]] = 0xffffffffu;
+        }
+        if (o == -2) live++;
+    }
+    for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+    if ((threadIdx.x & 31) == 0 && live) atomicAdd(remaining, (unsigned long long)live);
+}
+
+__global__ void k_flag_undecided(const int32_t* out, int64_t m, uint32_t* flags) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) flags[i] = out[i] == -2 ? 1u : 0u;
+}
+
+__global__ void k_gather_undecided(const int32_t* out, int64_t m, const uint32_t* pos, int32_t* list) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m && out[i] == -2) list[pos[i]] = (int32_t)i;
+}
+
+// sequential Kruskal over the undecided arcs in processing order (the result equals
+// the full sequential union-find: DESIGN.md "Union-find")
+__global__ void k_uf_tail(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b, const int32_t* list,
+                          const uint32_t* n_list_from_scan, const uint32_t* flags_last, int64_t m, int32_t* parent,
+                          int32_t* out, bool older_is_smaller) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    const int64_t n = (int64_t)n_list_from_scan[0] + flags_last[0];
+    for (int64_t j = 0; j < n; j++) {
+        const int32_t i = list[j];
+        int32_t a = arc_a[i], b = arc_b[i];
+        while (parent[a] != a) a = parent[a];
+        while (parent[b] != b) b = parent[b];
+        if (a == b) { out[i] = -1; continue; }
+        const bool a_older = older_is_smaller ? (a < b) : (a > b);
+        const int32_t young = a_older ? b : a, old = a_older ? a : b;
+        parent[young] = old;
+        out[i] = young;
+    }
+}
+
+// ---------------------------------------------------------------- emission
+
+struct PairRec {
+    int64_t birth_id, death_id;
+    int32_t birth_vertex, death_vertex;
+    float birth_value, death_value;
+};
+
+// highest vertex (in K) of an anchored simplex
+__device__ __forceinline__ int64_t max_vertex(const Geo3& g, const StarTab& S, int dim, int64_t id) {
+    if (dim == 0) return id;
+    const int64_t a = id / g.ncell[dim];
+    const int k = (int)(id % g.ncell[dim]);
+    int64_t best = a;
+    for (int j = 0; j < dim; j++) {
+        const int64_t p = a + lin_mask(g, S.chain[dim][k][j]);
+        if (kless_v(g, best, p)) best = p;
+    }
+    return best;
+}
+
+__global__ void k_flag_ge0(const int32_t* out, int64_t m, uint32_t* flags, int want_unpaired) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) flags[i] = want_unpaired ? (out[i] == -1 ? 1u : 0u) : (out[i] >= 0 ? 1u : 0u);
+}
+
+// D0 pairs (birth = the dying minimum, death = the critical edge), ascending arcs
+__global__ void k_emit_d0(Geo3 g, const int32_t* out, int64_t m, const uint32_t* pos, const int64_t* c0,
+                          const int64_t* c1, PairRec* pairs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m || out[i] < 0) return;
+    const StarTab& S = *g.tab;
+    PairRec r;
+    r.birth_id = c0[out[i]];
+    r.birth_vertex = (int32_t)r.birth_id;
+    r.birth_value = g.f[r.birth_id];
+    r.death_id = c1[i];
+    const int64_t dv = max_vertex(g, S, 1, r.death_id);
+    r.death_vertex = (int32_t)dv;
+    r.death_value = g.f[dv];
+    pairs[pos[i]] = r;
+}
+
+// D_{d-1} pairs (birth = critical (d-1)-simplex, death = the dying maximum), in
+// processing (decreasing) order
+__global__ void k_emit_dtop(Geo3 g, const int32_t* out, int64_t m, const uint32_t* pos, const int64_t* cdm1,
+                            const int64_t* cd, PairRec* pairs) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m || out[j] < 0) return;
+    const StarTab& S = *g.tab;
+    const int d = g.ndim;
+    PairRec r;
+    r.birth_id = cdm1[m - 1 - j];
+    const int64_t bv = max_vertex(g, S, d - 1, r.birth_id);
+    r.birth_vertex = (int32_t)bv;
+    r.birth_value = g.f[bv];
+    r.death_id = cd[out[j]];
+    const int64_t dv = max_vertex(g, S, d, r.death_id);
+    r.death_vertex = (int32_t)dv;
+    r.death_value = g.f[dv];
+    pairs[pos[j]] = r;
+}
+
+// an infinite class record (Sec. 6): (f(sigma), f*), death_id = -1
+__global__ void k_emit_inf(Geo3 g, int dim, const int64_t* id_ptr, const unsigned int* fmax_ord, PairRec* slot) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const StarTab& S = *g.tab;
+    PairRec r;
+    r.birth_id = *id_ptr;
+    const int64_t bv = max_vertex(g, S, dim, r.birth_id);
+    r.birth_vertex = (int32_t)bv;
+    r.birth_value = g.f[bv];
+    r.death_id = -1;
+    r.death_vertex = -1;
+    const uint32_t o = *fmax_ord;
+    const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    r.death_value = __uint_as_float(u);
+    *slot = r;
+}
+
+// unpaired saddles, in ascending lex order.  rev: the arcs are in decreasing order.
+__global__ void k_emit_unpaired(const int32_t* out, int64_t m, const uint32_t* pos, int64_t n, const int64_t* ids,
+                                int64_t* list, int rev) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m || out[j] != -1) return;
+    const int64_t id = rev ? ids[m - 1 - j] : ids[j];
+    list[rev ? n - 1 - pos[j] : pos[j]] = id;
+}
+
+}  // namespace dms

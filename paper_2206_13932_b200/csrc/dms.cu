@@ -1,0 +1,779 @@
+// dms.cu -- C-ABI entry points (include/dms.h) and host orchestration.
+//
+// One context = one field on one stream.  The pipeline (Fig. 4 overview,
+// 1236-1332, restricted to the front end):
+//   order    k_order_keys + radix sort -> rank                     (Sec. 2.1, 7.1)
+//   gradient k_gradient<D> (+ fused critical compaction)          (Sec. 2.6, Alg. 2)
+//   critical radix sort of each C_k by lexicographic key           (Alg. 2 l. 13)
+//   D0       node map, k_d0_arcs, union-find rounds, emission      (Sec. 5.1, 6)
+//   D_{d-1}  node map, k_dtop_arcs, union-find rounds, emission    (Sec. 5.2, 6)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <utility>
+#include <vector>
+
+#include "../../include/dms.h"
+#include "common.cuh"
+#include "diag.cuh"
+#include "grad.cuh"
+#include "sort.cuh"
+#include "star.cuh"
+#include "star_build.cuh"
+
+using namespace dms;
+
+static_assert(sizeof(PairRec) == sizeof(dms_pair), "pair layout");
+
+namespace {
+
+__global__ void k_order_keys(const float* __restrict__ f, int64_t n, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals, int* err, unsigned long long* kmax) {
+    unsigned long long m = 0;
+    bool nan = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = f[i];
+        nan |= is_nan_bits(x);
+        const uint32_t o = ord_of(x);
+        keys[i] = o;
+        vals[i] = (uint32_t)i;
+        const unsigned long long k = ((unsigned long long)o << 32) | (unsigned long long)i;
+        m = k > m ? k : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+        m = y > m ? y : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(kmax, m);
+    if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
+}
+
+__global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsigned long long* kmax, PairRec* slot) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const StarTab& S = *g.tab;
+    PairRec r;
+    r.birth_id = *id_ptr;
+    const int64_t bv = max_vertex(g, S, dim, r.birth_id);
+    r.birth_vertex = (int32_t)bv;
+    r.birth_value = g.f[bv];
+    r.death_id = -1;
+    r.death_vertex = -1;
+    r.death_value = g.f[(int64_t)(*kmax & 0xffffffffull)];  // f* = f at the highest vertex
+    *slot = r;
+}
+
+struct UFBuf {
+    int32_t *arc_a = nullptr, *arc_b = nullptr, *ra = nullptr, *rb = nullptr, *out = nullptr, *list = nullptr;
+    int32_t* parent = nullptr;
+    uint32_t *best = nullptr, *flags = nullptr, *pos = nullptr;
+    int64_t cap_arcs = 0, cap_nodes = 0;
+};
+
+}  // namespace
+
+struct dms_ctx {
+    int ndim = 0;
+    int64_t L[3] = {1, 1, 1};
+    int64_t N = 0;
+    const float* f = nullptr;
+    cudaStream_t st = nullptr;
+    int64_t ncell[4] = {1, 0, 0, 0};
+    StarTab htab;
+    StarTab* dtab = nullptr;
+    // caller or scratch buffers
+    int32_t* rank = nullptr;
+    void* grad = nullptr;
+    int32_t* rank_scratch = nullptr;
+    void* grad_scratch = nullptr;
+    // order sort
+    uint32_t *okeys[2] = {nullptr, nullptr}, *ovals[2] = {nullptr, nullptr};
+    SortScratch ss;
+    // critical records
+    int64_t cap[4] = {0, 0, 0, 0};
+    int64_t* cid[2][4] = {};
+    uint64_t* ckey[2][4] = {};
+    int cur[4] = {0, 0, 0, 0};
+    int64_t ncrit[4] = {0, 0, 0, 0};
+    unsigned long long* status = nullptr;
+    int64_t status_words = 0;
+    int* tile_ctr = nullptr;
+    unsigned long long* totals = nullptr;
+    int* err = nullptr;
+    unsigned long long* kmax = nullptr;
+    unsigned long long* remaining = nullptr;
+    unsigned long long* h_pinned = nullptr;  // small pinned host scratch
+    // diagrams
+    int32_t *node_of0 = nullptr, *node_oftop = nullptr;
+    UFBuf uf[2];
+    PairRec* pairs[2] = {nullptr, nullptr};
+    int64_t npairs[2] = {0, 0};
+    int64_t* unp[2] = {nullptr, nullptr};
+    int64_t nunp[2] = {0, 0};
+    // state
+    bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[6];
+    int64_t launches = 0;
+    dms_status sticky = DMS_OK;
+    char msg[256] = {0};
+};
+
+namespace {
+
+// records a (start, stop) event pair on the context's stream around a stage
+struct StageTimer {
+    dms_ctx* c;
+    int stage;
+    cudaEvent_t a = nullptr;
+    StageTimer(dms_ctx* c_, int s) : c(c_), stage(s) {
+        if (c->timing && cudaEventCreate(&a) == cudaSuccess) cudaEventRecord(a, c->st);
+    }
+    ~StageTimer() {
+        if (!a) return;
+        cudaEvent_t b = nullptr;
+        if (cudaEventCreate(&b) == cudaSuccess) {
+            cudaEventRecord(b, c->st);
+            c->ev[stage].emplace_back(a, b);
+        } else {
+            cudaEventDestroy(a);
+        }
+    }
+};
+
+void clear_events(dms_ctx* c) {
+    for (auto& v : c->ev) {
+        for (auto& p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+        v.clear();
+    }
+}
+
+dms_status fail(dms_ctx* c, dms_status s, const char* what) {
+    if (c) {
+        std::snprintf(c->msg, sizeof c->msg, "%s", what);
+        if (s == DMS_ERR_CUDA) c->sticky = s;
+    }
+    return s;
+}
+
+#define CU(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            char b_[200];                                                                \
+            std::snprintf(b_, sizeof b_, "%s: %s", #call, cudaGetErrorString(e_));       \
+            return fail(c, e_ == cudaErrorMemoryAllocation ? DMS_ERR_OOM : DMS_ERR_CUDA, b_); \
+        }                                                                                \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, int64_t n) {
+    *p = nullptr;
+    if (n <= 0) n = 1;
+    return cudaMalloc((void**)p, (size_t)n * sizeof(T));
+}
+
+inline unsigned grid_for(int64_t n, int block = kBlock) { return (unsigned)std::max<int64_t>(1, ceil_div(n, block)); }
+
+Geo3 geo(const dms_ctx* c) {
+    Geo3 g;
+    g.ndim = c->ndim;
+    g.Lx = (int32_t)c->L[0];
+    g.Ly = (int32_t)c->L[1];
+    g.Lz = (int32_t)c->L[2];
+    g.N = c->N;
+    for (int k = 0; k < 4; k++) g.ncell[k] = c->ncell[k];
+    g.f = c->f;
+    g.grad = c->grad;
+    g.tab = c->dtab;
+    return g;
+}
+
+dms_status check_sticky(dms_ctx* c) {
+    if (!c) return DMS_ERR_ARG;
+    if (c->sticky != DMS_OK) return DMS_ERR_STATE;
+    return DMS_OK;
+}
+
+dms_status alloc_crit(dms_ctx* c) {
+    for (int b = 0; b < 2; b++)
+        for (int k = 0; k <= c->ndim; k++) {
+            cudaFree(c->cid[b][k]);
+            cudaFree(c->ckey[b][k]);
+            CU(dalloc(&c->cid[b][k], c->cap[k]));
+            CU(dalloc(&c->ckey[b][k], c->cap[k]));
+        }
+    return DMS_OK;
+}
+
+dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
+    arcs = std::max<int64_t>(arcs, 1);
+    nodes = std::max<int64_t>(nodes, 1);
+    if (arcs > u.cap_arcs) {
+        for (int32_t** p : {&u.arc_a, &u.arc_b, &u.ra, &u.rb, &u.out, &u.list}) { cudaFree(*p); CU(dalloc(p, arcs)); }
+        for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
+        u.cap_arcs = arcs;
+    }
+    if (nodes > u.cap_nodes) {
+        cudaFree(u.parent);
+        cudaFree(u.best);
+        CU(dalloc(&u.parent, nodes));
+        CU(dalloc(&u.best, nodes));
+        u.cap_nodes = nodes;
+    }
+    return DMS_OK;
+}
+
+dms_status read_err(dms_ctx* c) {
+    int e = 0;
+    CU(cudaMemcpyAsync(&e, c->err, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    if (e & 1) return fail(c, DMS_ERR_NAN, "NaN in the scalar field");
+    return DMS_OK;
+}
+
+// ------------------------------------------------------------------ stages
+
+dms_status run_order(dms_ctx* c, int32_t* d_rank) {
+    StageTimer tm(c, 0);
+    c->rank = d_rank ? d_rank : c->rank_scratch;
+    CU(cudaMemsetAsync(c->kmax, 0, sizeof(unsigned long long), c->st));
+    const int64_t n = c->N;
+    k_order_keys<<<std::min<int64_t>(grid_for(n), 148 * 16), kBlock, 0, c->st>>>(c->f, n, c->okeys[0], c->ovals[0],
+                                                                                c->err, c->kmax);
+    c->launches++;
+    radix_sort<uint32_t, uint32_t, 16>(c->okeys[0], c->ovals[0], c->okeys[1], c->ovals[1], n, 0, 32, c->ss, c->st,
+                                       &c->launches, c->rank);
+    CU(cudaGetLastError());
+    c->have_order = true;
+    c->have_grad = c->have_crit = c->have_d[0] = c->have_d[1] = false;
+    return DMS_OK;
+}
+
+dms_status launch_gradient(dms_ctx* c) {
+    const int64_t ntiles = ceil_div(c->N, kBlock);
+    const int dims = c->ndim + 1;
+    if (ntiles * dims > c->status_words) {
+        cudaFree(c->status);
+        CU(dalloc(&c->status, ntiles * 4));
+        c->status_words = ntiles * 4;
+    }
+    CU(cudaMemsetAsync(c->status, 0, ntiles * dims * sizeof(unsigned long long), c->st));
+    CU(cudaMemsetAsync(c->tile_ctr, 0, sizeof(int), c->st));
+    GradArgs A;
+    A.f = c->f;
+    A.Lx = (int32_t)c->L[0];
+    A.Ly = (int32_t)c->L[1];
+    A.Lz = (int32_t)c->L[2];
+    A.N = c->N;
+    A.tab = c->dtab;
+    A.grad = c->grad;
+    A.rank = c->rank;
+    for (int k = 0; k < 4; k++) {
+        A.crit_id[k] = c->cid[0][k];
+        A.crit_key[k] = c->ckey[0][k];
+        A.cap[k] = c->cap[k];
+        A.ncell[k] = c->ncell[k];
+    }
+    A.status = c->status;
+    A.tile_ctr = c->tile_ctr;
+    A.totals = c->totals;
+    A.err = c->err;
+    A.ntiles = ntiles;
+    StageTimer tm(c, 5);
+    if (c->ndim == 3) k_gradient<3><<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
+    else if (c->ndim == 2) k_gradient<2><<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
+    else k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
+    c->launches++;
+    CU(cudaGetLastError());
+    return DMS_OK;
+}
+
+dms_status run_gradient(dms_ctx* c, void* d_grad) {
+    if (!c->have_order) {
+        dms_status s = run_order(c, nullptr);
+        if (s) return s;
+    }
+    c->grad = d_grad ? d_grad : c->grad_scratch;
+    StageTimer tm(c, 1);
+    dms_status s = launch_gradient(c);
+    if (s) return s;
+    c->have_grad = true;
+    c->have_crit = c->have_d[0] = c->have_d[1] = false;
+    return DMS_OK;
+}
+
+int bits_for(int64_t n) {
+    int b = 0;
+    while (b < 40 && ((int64_t)1 << b) < n) b++;
+    return b;
+}
+
+dms_status run_critical(dms_ctx* c) {
+    if (!c->have_grad) {
+        dms_status s = run_gradient(c, nullptr);
+        if (s) return s;
+    }
+    StageTimer tm(c, 2);
+    unsigned long long tot[4] = {0, 0, 0, 0};
+    CU(cudaMemcpyAsync(tot, c->totals, sizeof tot, cudaMemcpyDeviceToHost, c->st));
+    dms_status s = read_err(c);
+    if (s) return s;
+    bool overflow = false;
+    for (int k = 0; k <= c->ndim; k++)
+        if ((int64_t)tot[k] > c->cap[k]) { c->cap[k] = (int64_t)tot[k] + 1024; overflow = true; }
+    if (overflow) {  // rare: grow the record buffers and recompute
+        s = alloc_crit(c);
+        if (s) return s;
+        s = launch_gradient(c);
+        if (s) return s;
+    }
+    for (int k = 0; k <= c->ndim; k++) c->ncrit[k] = (int64_t)tot[k];
+    const int kbits = 12 + bits_for(c->N);
+    for (int k = 0; k <= c->ndim; k++) {
+        c->cur[k] = radix_sort<uint64_t, int64_t, 8>(c->ckey[0][k], c->cid[0][k], c->ckey[1][k], c->cid[1][k],
+                                                     c->ncrit[k], 0, kbits, c->ss, c->st, &c->launches);
+    }
+    CU(cudaGetLastError());
+    c->have_crit = true;
+    return DMS_OK;
+}
+
+const int64_t* crit_ids(dms_ctx* c, int k) { return c->cid[c->cur[k]][k]; }
+
+// union-find over arcs (processing order), see diag.cuh
+dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older_is_smaller) {
+    const unsigned gi = grid_for(std::max(m, nodes));
+    k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.out, m);
+    c->launches++;
+    CU(cudaMemsetAsync(u.ra, 0xff, std::max<int64_t>(m, 1) * sizeof(int32_t), c->st));
+    if (m == 0) return DMS_OK;
+    const unsigned gr = (unsigned)std::min<int64_t>(grid_for(m), 148 * 8);
+    int64_t prev = m;
+    for (int iter = 0; iter < 100000; iter++) {
+        const int batch = 4;
+        for (int r = 0; r < batch; r++) {
+            if (r == batch - 1) CU(cudaMemsetAsync(c->remaining, 0, sizeof(unsigned long long), c->st));
+            k_uf_round1<<<gr, kBlock, 0, c->st>>>(u.arc_a, u.arc_b, m, u.parent, u.best, u.ra, u.rb, u.out);
+            k_uf_round2<<<gr, kBlock, 0, c->st>>>(m, u.parent, u.best, u.ra, u.rb, u.out, older_is_smaller);
+            k_uf_round3<<<gr, kBlock, 0, c->st>>>(m, u.best, u.ra, u.rb, u.out, c->remaining);
+            c->launches += 3;
+        }
+        CU(cudaMemcpyAsync(c->h_pinned, c->remaining, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        const int64_t rem = (int64_t)c->h_pinned[0];
+        if (rem == 0) return DMS_OK;
+        if (rem <= 4096 || (rem < 65536 && rem * 4 > prev * 3)) {
+            // sequential tail over the undecided arcs, in order
+            k_flag_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags);
+            scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
+            k_gather_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, u.list);
+            k_uf_tail<<<1, 32, 0, c->st>>>(u.arc_a, u.arc_b, u.list, u.pos + (m - 1), u.flags + (m - 1), m, u.parent,
+                                          u.out, older_is_smaller);
+            c->launches += 3;
+            CU(cudaGetLastError());
+            return DMS_OK;
+        }
+        prev = rem;
+    }
+    return fail(c, DMS_ERR_INVARIANT, "union-find did not converge");
+}
+
+// stable compaction count: pos = exclusive scan of flags; returns the total
+dms_status flag_scan(dms_ctx* c, UFBuf& u, int64_t m, int want_unpaired, int64_t* total) {
+    *total = 0;
+    if (m == 0) return DMS_OK;
+    k_flag_ge0<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags, want_unpaired);
+    c->launches++;
+    scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
+    uint32_t h[2];
+    CU(cudaMemcpyAsync(&h[0], u.pos + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(&h[1], u.flags + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    *total = (int64_t)h[0] + h[1];
+    return DMS_OK;
+}
+
+dms_status emit_unpaired(dms_ctx* c, int which, UFBuf& u, int64_t m, const int64_t* ids, int rev) {
+    int64_t n = 0;
+    dms_status s = flag_scan(c, u, m, 1, &n);
+    if (s) return s;
+    cudaFree(c->unp[which]);
+    c->unp[which] = nullptr;
+    CU(dalloc(&c->unp[which], n));
+    c->nunp[which] = n;
+    if (n) {
+        k_emit_unpaired<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, n, ids, c->unp[which], rev);
+        c->launches++;
+    }
+    return DMS_OK;
+}
+
+dms_status run_d0(dms_ctx* c) {
+    if (!c->have_crit) {
+        dms_status s = run_critical(c);
+        if (s) return s;
+    }
+    StageTimer tm(c, 3);
+    UFBuf& u = c->uf[0];
+    const int64_t m = c->ncrit[1], n0 = c->ncrit[0];
+    dms_status s = alloc_uf(c, u, m, n0);
+    if (s) return s;
+    Geo3 g = geo(c);
+    k_node_map<<<grid_for(n0), kBlock, 0, c->st>>>(crit_ids(c, 0), n0, c->node_of0);
+    c->launches++;
+    if (m) {
+        k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
+        c->launches++;
+    }
+    s = union_find(c, u, m, n0, true);
+    if (s) return s;
+    int64_t np = 0;
+    s = flag_scan(c, u, m, 0, &np);
+    if (s) return s;
+    cudaFree(c->pairs[0]);
+    CU(dalloc(&c->pairs[0], np + 1));
+    if (np) {
+        k_emit_d0<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, 0), crit_ids(c, 1), c->pairs[0]);
+        c->launches++;
+    }
+    // Sec. 6: the global minimum (oldest node, position 0 of C_0) never dies
+    k_emit_inf_k<<<1, 32, 0, c->st>>>(g, 0, crit_ids(c, 0), c->kmax, c->pairs[0] + np);
+    c->launches++;
+    c->npairs[0] = np + 1;
+    s = emit_unpaired(c, 0, u, m, crit_ids(c, 1), 0);
+    if (s) return s;
+    CU(cudaGetLastError());
+    c->have_d[0] = true;
+    return DMS_OK;
+}
+
+dms_status run_dtop(dms_ctx* c) {
+    if (!c->have_crit) {
+        dms_status s = run_critical(c);
+        if (s) return s;
+    }
+    StageTimer tm(c, 4);
+    const int d = c->ndim;
+    UFBuf& u = c->uf[1];
+    const int64_t m = c->ncrit[d - 1], nd = c->ncrit[d];
+    dms_status s = alloc_uf(c, u, m, nd + 1);
+    if (s) return s;
+    Geo3 g = geo(c);
+    k_node_map<<<grid_for(nd), kBlock, 0, c->st>>>(crit_ids(c, d), nd, c->node_oftop);
+    c->launches++;
+    if (m) {
+        k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids(c, d - 1), m, c->node_oftop, (int32_t)nd, u.arc_a,
+                                                      u.arc_b);
+        c->launches++;
+    }
+    s = union_find(c, u, m, nd + 1, false);
+    if (s) return s;
+    int64_t np = 0;
+    s = flag_scan(c, u, m, 0, &np);
+    if (s) return s;
+    s = emit_unpaired(c, 1, u, m, crit_ids(c, d - 1), 1);
+    if (s) return s;
+    const int64_t ninf = d == 1 ? c->nunp[1] : 0;  // Sec. 6: in 1D the unpaired minimum is infinite
+    cudaFree(c->pairs[1]);
+    CU(dalloc(&c->pairs[1], np + ninf + 1));
+    if (np) {
+        // recompute the pair positions (emit_unpaired reused the scan buffers)
+        int64_t np2 = 0;
+        s = flag_scan(c, u, m, 0, &np2);
+        if (s) return s;
+        k_emit_dtop<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, d - 1), crit_ids(c, d),
+                                                      c->pairs[1]);
+        c->launches++;
+    }
+    for (int64_t i = 0; i < ninf; i++) {
+        k_emit_inf_k<<<1, 32, 0, c->st>>>(g, 0, c->unp[1] + i, c->kmax, c->pairs[1] + np + i);
+        c->launches++;
+    }
+    c->npairs[1] = np + ninf;
+    CU(cudaGetLastError());
+    c->have_d[1] = true;
+    return DMS_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* stream, dms_ctx** out) {
+    if (!dims || !d_f || !out) return DMS_ERR_ARG;
+    *out = nullptr;
+    if (ndim < 1 || ndim > 3) return DMS_ERR_DEGENERATE;
+    int64_t N = 1;
+    for (int i = 0; i < ndim; i++) {
+        if (dims[i] < 2) return DMS_ERR_DEGENERATE;
+        N *= dims[i];
+        if (N >= ((int64_t)1 << 31)) return DMS_ERR_TOO_LARGE;
+    }
+    dms_ctx* c = new (std::nothrow) dms_ctx();
+    if (!c) return DMS_ERR_OOM;
+    c->ndim = ndim;
+    for (int i = 0; i < 3; i++) c->L[i] = i < ndim ? dims[i] : 1;
+    c->N = N;
+    c->f = d_f;
+    c->st = (cudaStream_t)stream;
+    const int64_t per[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 3, 2, 0}, {1, 7, 12, 6}};
+    for (int k = 0; k < 4; k++) c->ncell[k] = per[ndim][k];
+    if (c->ncell[ndim] * N >= ((int64_t)1 << 31)) { delete c; return DMS_ERR_TOO_LARGE; }
+    if (!build_star_tables(ndim, c->L, &c->htab)) { delete c; return DMS_ERR_INVARIANT; }
+    auto bail = [&](dms_status s) { dms_destroy(c); return s; };
+#define CA(call) do { if ((call) != cudaSuccess) return bail(DMS_ERR_OOM); } while (0)
+    CA(dalloc(&c->dtab, 1));
+    if (cudaMemcpy(c->dtab, &c->htab, sizeof(StarTab), cudaMemcpyHostToDevice) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    CA(dalloc(&c->rank_scratch, N));
+    CA(cudaMalloc(&c->grad_scratch, dms_gradient_bytes(c)));
+    for (int b = 0; b < 2; b++) { CA(dalloc(&c->okeys[b], N)); CA(dalloc(&c->ovals[b], N)); }
+    const int64_t max_tiles = ceil_div(N, (int64_t)kBlock * 8);
+    CA(dalloc(&c->ss.counts, max_tiles * kRadix));
+    CA(dalloc(&c->ss.counts_scan, max_tiles * kRadix));
+    CA(dalloc(&c->ss.status, ceil_div(std::max<int64_t>(max_tiles * kRadix, N), (int64_t)kBlock * kScanItems) + 1));
+    CA(dalloc(&c->ss.tile_ctr, 1));
+    c->ss.max_tiles = max_tiles;
+    CA(dalloc(&c->tile_ctr, 1));
+    CA(dalloc(&c->totals, 4));
+    CA(dalloc(&c->err, 1));
+    CA(dalloc(&c->kmax, 1));
+    CA(dalloc(&c->remaining, 1));
+    if (cudaMallocHost(&c->h_pinned, 64) != cudaSuccess) return bail(DMS_ERR_OOM);
+    CA(dalloc(&c->node_of0, N));
+    CA(dalloc(&c->node_oftop, c->ncell[ndim] * N));
+    for (int k = 0; k <= ndim; k++) c->cap[k] = N / 2 + 1024;
+    if (alloc_crit(c) != DMS_OK) return bail(DMS_ERR_OOM);
+    if (cudaMemsetAsync(c->err, 0, sizeof(int), c->st) != cudaSuccess) return bail(DMS_ERR_CUDA);
+#undef CA
+    *out = c;
+    return DMS_OK;
+}
+
+size_t dms_gradient_bytes(const dms_ctx* c) {
+    if (!c) return 0;
+    const size_t per = c->ndim == 3 ? 16 : (c->ndim == 2 ? 2 : 1);
+    return per * (size_t)c->N;
+}
+
+dms_status dms_order(dms_ctx* c, int32_t* d_rank) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!d_rank) return DMS_ERR_ARG;
+    return run_order(c, d_rank);
+}
+
+dms_status dms_gradient(dms_ctx* c, void* d_grad) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!d_grad) return DMS_ERR_ARG;
+    return run_gradient(c, d_grad);
+}
+
+dms_status dms_critical(dms_ctx* c, int64_t h_count[4], const int64_t* d_ids_out[4]) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!h_count || !d_ids_out) return DMS_ERR_ARG;
+    if (!c->have_crit) {
+        s = run_critical(c);
+        if (s) return s;
+    }
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+    for (int k = 0; k < 4; k++) {
+        h_count[k] = k <= c->ndim ? c->ncrit[k] : 0;
+        d_ids_out[k] = k <= c->ndim ? crit_ids(c, k) : nullptr;
+    }
+    return DMS_OK;
+}
+
+dms_status dms_diagram0(dms_ctx* c, const dms_pair** d_pairs, int64_t* h_n) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!d_pairs || !h_n) return DMS_ERR_ARG;
+    if (!c->have_d[0]) {
+        s = run_d0(c);
+        if (s) return s;
+    }
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+    *d_pairs = reinterpret_cast<const dms_pair*>(c->pairs[0]);
+    *h_n = c->npairs[0];
+    return DMS_OK;
+}
+
+dms_status dms_diagram_top(dms_ctx* c, int mode, const dms_pair** d_pairs, int64_t* h_n) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!d_pairs || !h_n) return DMS_ERR_ARG;
+    if (mode == DMS_BOUNDARY_IGNORE) return fail(c, DMS_ERR_STATE, "DMS_BOUNDARY_IGNORE is not built");
+    if (mode != DMS_BOUNDARY_EXACT) return DMS_ERR_ARG;
+    if (!c->have_d[1]) {
+        s = run_dtop(c);
+        if (s) return s;
+    }
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+    *d_pairs = reinterpret_cast<const dms_pair*>(c->pairs[1]);
+    *h_n = c->npairs[1];
+    return DMS_OK;
+}
+
+dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, int64_t* h_n) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!d_ids || !h_n || (which != 0 && which != 1)) return DMS_ERR_ARG;
+    if (!c->have_d[which]) {
+        s = which == 0 ? run_d0(c) : run_dtop(c);
+        if (s) return s;
+    }
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+    *d_ids = c->unp[which];
+    *h_n = c->nunp[which];
+    return DMS_OK;
+}
+
+dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if ((s = run_order(c, d_rank))) return s;
+    if ((s = run_gradient(c, d_grad))) return s;
+    if ((s = run_critical(c))) return s;
+    if ((s = run_d0(c))) return s;
+    if ((s = run_dtop(c))) return s;
+    return DMS_OK;
+}
+
+dms_status dms_sync(dms_ctx* c) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+    return read_err(c);
+}
+
+int64_t dms_decode_pairs(const int64_t dims[3], int ndim, const void* h_words, int64_t v0, int64_t v1,
+                         int64_t* h_triples, int64_t cap) {
+    if (!dims || !h_words || !h_triples || ndim < 1 || ndim > 3 || v0 < 0 || v1 < v0) return -1;
+    int64_t L[3] = {1, 1, 1};
+    for (int i = 0; i < ndim; i++) L[i] = dims[i];
+    StarTab T;
+    if (!build_star_tables(ndim, L, &T)) return -1;
+    const int64_t per[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 3, 2, 0}, {1, 7, 12, 6}};
+    const int64_t* nc = per[ndim];
+    int64_t n = 0;
+    auto put = [&](int64_t a, int64_t b, int64_t c3) {
+        if (n < cap) { h_triples[3 * n] = a; h_triples[3 * n + 1] = b; h_triples[3 * n + 2] = c3; }
+        n++;
+    };
+    auto anc = [&](int64_t v, const int8_t o[3]) { return v + o[0] + L[0] * o[1] + L[0] * L[1] * o[2]; };
+    for (int64_t v = v0; v < v1; v++) {
+        const int64_t i = v - v0;
+        if (ndim == 1) {
+            const uint8_t w = reinterpret_cast<const uint8_t*>(h_words)[i];
+            if (w == 0) put(0, v, v - 1);
+            else if (w == 1) put(0, v, v);
+            continue;
+        }
+        int vcode;
+        uint64_t lo = 0, hi = 0;
+        if (ndim == 3) {
+            lo = reinterpret_cast<const uint64_t*>(h_words)[2 * i];
+            hi = reinterpret_cast<const uint64_t*>(h_words)[2 * i + 1];
+            vcode = (int)((hi >> 56) & 15);
+            if (vcode == 15) vcode = -1;
+        } else {
+            const uint16_t w = reinterpret_cast<const uint16_t*>(h_words)[i];
+            vcode = w & 7;
+            if (vcode == 7) vcode = -1;
+            lo = (uint64_t)(w >> 3);
+        }
+        if (vcode >= 0) put(0, v, nc[1] * anc(v, T.e_anc[vcode]) + T.e_k[vcode]);
+        for (int t = 0; t < T.nt; t++) {
+            const int code = (int)((t < 32 ? (lo >> (2 * t)) : (hi >> (2 * (t - 32)))) & 3);
+            if (!code) continue;
+            const int e = code == 1 ? T.tri_a[t] : T.tri_b[t];
+            put(1, nc[1] * anc(v, T.e_anc[e]) + T.e_k[e], nc[2] * anc(v, T.t_anc[t]) + T.t_k[t]);
+        }
+        for (int q = 0; q < T.nq; q++) {
+            const int code = (int)((hi >> (8 + 2 * q)) & 3);
+            if (!code) continue;
+            const int t = T.tet_tri[q][code - 1];
+            put(2, nc[2] * anc(v, T.t_anc[t]) + T.t_k[t], nc[3] * anc(v, T.q_anc[q]) + T.q_k[q]);
+        }
+    }
+    return n;
+}
+
+dms_status dms_copy(dms_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (!c || (!dst && bytes) || (!src && bytes)) return DMS_ERR_ARG;
+    if (!bytes) return DMS_OK;
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return DMS_OK;
+}
+
+dms_status dms_set_timing(dms_ctx* c, int enable) {
+    if (!c) return DMS_ERR_ARG;
+    cudaStreamSynchronize(c->st);
+    clear_events(c);
+    c->timing = enable != 0;
+    return DMS_OK;
+}
+
+dms_status dms_stage_ms(dms_ctx* c, double ms_out[7]) {
+    if (!c || !ms_out) return DMS_ERR_ARG;
+    CU(cudaStreamSynchronize(c->st));
+    for (int s = 0; s < 6; s++) {
+        double t = 0;
+        for (auto& p : c->ev[s]) {
+            float x = 0;
+            CU(cudaEventElapsedTime(&x, p.first, p.second));
+            t += x;
+        }
+        ms_out[s] = t;
+    }
+    ms_out[6] = (double)c->ev[5].size();
+    return DMS_OK;
+}
+
+int64_t dms_launch_count(const dms_ctx* c) { return c ? c->launches : 0; }
+
+const char* dms_last_error(const dms_ctx* c) { return c ? c->msg : "null context"; }
+
+void dms_destroy(dms_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->st);
+    clear_events(c);
+    cudaFree(c->dtab);
+    cudaFree(c->rank_scratch);
+    cudaFree(c->grad_scratch);
+    for (int b = 0; b < 2; b++) { cudaFree(c->okeys[b]); cudaFree(c->ovals[b]); }
+    cudaFree(c->ss.counts);
+    cudaFree(c->ss.counts_scan);
+    cudaFree(c->ss.status);
+    cudaFree(c->ss.tile_ctr);
+    for (int b = 0; b < 2; b++)
+        for (int k = 0; k < 4; k++) { cudaFree(c->cid[b][k]); cudaFree(c->ckey[b][k]); }
+    cudaFree(c->status);
+    cudaFree(c->tile_ctr);
+    cudaFree(c->totals);
+    cudaFree(c->err);
+    cudaFree(c->kmax);
+    cudaFree(c->remaining);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    cudaFree(c->node_of0);
+    cudaFree(c->node_oftop);
+    for (int b = 0; b < 2; b++) {
+        UFBuf& u = c->uf[b];
+        for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.ra, (void*)u.rb, (void*)u.out, (void*)u.list,
+                        (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
+            cudaFree(p);
+        cudaFree(c->pairs[b]);
+        cudaFree(c->unp[b]);
+    }
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,454 @@
+// grad.cuh -- lower-star discrete gradient + critical-simplex compaction (sm_100a).
+//
+// One thread per vertex x runs Robins et al.'s ProcessLowerStars (the "expansions"
+// of PAPER.md 1965-1971, 272-276; Alg. 2 l. 2, PAPER.md 330-333) on St^-(x)
+// (PAPER.md 1443-1451), with:
+//   * the lower neighbours relabelled by local rank r in [0,14) (4 bits each, packed
+//     in one 64-bit register), so the lexicographic key G of a star cell
+//     (PAPER.md 1380-1414: decreasing vertex sequence, face before coface) is the
+//     12-bit integer (r_a+1)<<8 | (r_b+1)<<4 | (r_c+1) (absent vertices = 0);
+//   * the two priority queues (PQzero / PQone) and the classification state as bit
+//     masks over the star's edge / triangle / tetrahedron slots; popping the minimum
+//     scans the (few) members of a queue.
+// The critical cells of every lower star (Alg. 2 l. 10-12) are written compactly
+// with a single-pass decoupled look-back scan over CTAs (dynamic tile ids), each as an
+// (anchored id, sort key) record; sort key = rank(x) << 12 | G.
+//
+// Gradient words:
+//   3D uint64 lo : 2-bit code of tri slots 0..31 (1: paired with edge tri_a, 2: tri_b)
+//      uint64 hi : tri slots 32..35 (bits 0-7) | tet codes, 2 bits x 24 (bits 8-55,
+//                  j+1: paired with triangle tet_tri[T][j]) | vertex code (bits 56-59:
+//                  edge slot paired with x, 15 = x is a minimum)
+//   2D uint16    : vertex code (bits 0-2, 7 = minimum) | tri codes 2 bits x 6 (bits 3-14)
+//   1D uint8     : vertex code (0 = left edge, 1 = right edge, 3 = minimum)
+#pragma once
+#include "common.cuh"
+#include "star.cuh"
+
+namespace dms {
+
+template <int D> struct Geo;
+template <> struct Geo<3> { static constexpr int NE = 14, NT = 36, NQ = 24; };
+template <> struct Geo<2> { static constexpr int NE = 6, NT = 6, NQ = 0; };
+
+// Neighbour offsets (dx,dy,dz), slots sorted by linear index offset (star.cuh).
+__device__ constexpr int8_t kOff3[14][3] = {{-1, -1, -1}, {0, -1, -1}, {-1, 0, -1}, {0, 0, -1}, {-1, -1, 0},
+                                            {0, -1, 0},   {-1, 0, 0},  {1, 0, 0},   {0, 1, 0},  {1, 1, 0},
+                                            {0, 0, 1},    {1, 0, 1},   {0, 1, 1},   {1, 1, 1}};
+__device__ constexpr int8_t kOff2[6][3] = {{-1, -1, 0}, {0, -1, 0}, {-1, 0, 0}, {1, 0, 0}, {0, 1, 0}, {1, 1, 0}};
+
+template <int D>
+__device__ __forceinline__ int off_c(int s, int ax) {
+    return D == 3 ? kOff3[s][ax] : kOff2[s][ax];
+}
+
+struct GradArgs {
+    const float* f;
+    int32_t Lx, Ly, Lz;
+    int64_t N;
+    const StarTab* tab;
+    void* grad;
+    const int32_t* rank;
+    int64_t* crit_id[4];
+    uint64_t* crit_key[4];
+    int64_t cap[4];
+    int64_t ncell[4];
+    unsigned long long* status;  // 4 words per tile, zeroed
+    int* tile_ctr;               // zeroed
+    unsigned long long* totals;  // [4]
+    int* err;                    // bit 0: NaN seen
+    int64_t ntiles;
+};
+
+__device__ __forceinline__ int rk(uint64_t R, int s) { return (int)((R >> (4 * s)) & 15ull); }
+
+__device__ __forceinline__ uint32_t key_edge(uint64_t R, int s) { return (uint32_t)(rk(R, s) + 1) << 8; }
+
+__device__ __forceinline__ uint32_t key_tri(const StarTab& S, uint64_t R, int t) {
+    int a = rk(R, S.tri_a[t]), b = rk(R, S.tri_b[t]);
+    int hi = max(a, b), lo = min(a, b);
+    return ((uint32_t)(hi + 1) << 8) | ((uint32_t)(lo + 1) << 4);
+}
+
+__device__ __forceinline__ uint32_t key_tet(const StarTab& S, uint64_t R, int q) {
+    int a = rk(R, S.tet_a[q]), b = rk(R, S.tet_b[q]), c = rk(R, S.tet_c[q]);
+    int hi = max(a, max(b, c)), lo = min(a, min(b, c));
+    int mid = a + b + c - hi - lo;
+    return ((uint32_t)(hi + 1) << 8) | ((uint32_t)(mid + 1) << 4) | (uint32_t)(lo + 1);
+}
+
+// minimum-key member of (me edges, mt triangles, mq tets): returns dim << 6 | slot
+__device__ __forceinline__ int pop_min(const StarTab& S, uint64_t R, uint32_t me, uint64_t mt, uint32_t mq) {
+    uint32_t best = 0xffffffffu;
+    int bc = -1;
+    while (me) {
+        int s = __ffs(me) - 1;
+        me &= me - 1;
+        uint32_t k = key_edge(R, s);
+        if (k < best) { best = k; bc = 64 + s; }
+    }
+    while (mt) {
+        int t = __ffsll((long long)mt) - 1;
+        mt &= mt - 1;
+        uint32_t k = key_tri(S, R, t);
+        if (k < best) { best = k; bc = 128 + t; }
+    }
+    while (mq) {
+        int q = __ffs(mq) - 1;
+        mq &= mq - 1;
+        uint32_t k = key_tet(S, R, q);
+        if (k < best) { best = k; bc = 192 + q; }
+    }
+    return bc;
+}
+
+struct StarState {
+    uint32_t Le, Lq;
+    uint64_t Lt;
+    uint32_t cls_e, cls_q, pq0_e, pq0_q, pq1_q, crit_e, crit_q;
+    uint64_t cls_t, pq0_t, pq1_t, crit_t;
+    uint64_t tcode_lo, tcode_hi;  // 2 bits per tri slot
+    uint64_t qcode;               // 2 bits per tet slot
+    int vcode;                    // edge slot paired with x, -1 = minimum
+};
+
+template <int D>
+__device__ __forceinline__ void push_tris_of_edge(const StarTab& S, StarState& st, int e) {
+    uint64_t cand = S.edge_tri_mask[e] & st.Lt & ~st.cls_t;
+    while (cand) {
+        int t = __ffsll((long long)cand) - 1;
+        cand &= cand - 1;
+        int nu = (int)(!((st.cls_e >> S.tri_a[t]) & 1u)) + (int)(!((st.cls_e >> S.tri_b[t]) & 1u));
+        if (nu == 1) st.pq1_t |= 1ull << t;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void push_tets_of_tri(const StarTab& S, StarState& st, int t) {
+    if (D < 3) return;
+    uint32_t cand = S.tri_tet_mask[t] & st.Lq & ~st.cls_q;
+    while (cand) {
+        int q = __ffs(cand) - 1;
+        cand &= cand - 1;
+        int nu = (int)(!((st.cls_t >> S.tet_tri[q][0]) & 1ull)) + (int)(!((st.cls_t >> S.tet_tri[q][1]) & 1ull)) +
+                 (int)(!((st.cls_t >> S.tet_tri[q][2]) & 1ull));
+        if (nu == 1) st.pq1_q |= 1u << q;
+    }
+}
+
+__device__ __forceinline__ void set_tcode(StarState& st, int t, uint64_t code) {
+    if (t < 32) st.tcode_lo |= code << (2 * t);
+    else st.tcode_hi |= code << (2 * (t - 32));
+}
+
+// ProcessLowerStars on one lower star (Robins et al., as pinned in DESIGN.md Z1)
+template <int D>
+__device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, int delta, StarState& st) {
+    st.vcode = delta;
+    st.cls_e = 1u << delta;
+    st.pq0_e = st.Le & ~st.cls_e;
+    st.pq1_t = S.edge_tri_mask[delta] & st.Lt;
+    while (true) {
+        while (st.pq1_t | st.pq1_q) {
+            const int c = pop_min(S, R, 0u, st.pq1_t, st.pq1_q);
+            const int s = c & 63;
+            if ((c >> 6) == 2) {
+                st.pq1_t &= ~(1ull << s);
+                if ((st.cls_t >> s) & 1ull) continue;
+                const int a = S.tri_a[s], b = S.tri_b[s];
+                const bool ua = !((st.cls_e >> a) & 1u), ub = !((st.cls_e >> b) & 1u);
+                if (!ua && !ub) { st.pq0_t |= 1ull << s; continue; }
+                const int e = ua ? a : b;  // the unique unclassified facet
+                set_tcode(st, s, ua ? 1ull : 2ull);
+                st.cls_e |= 1u << e;
+                st.cls_t |= 1ull << s;
+                st.pq0_e &= ~(1u << e);
+                push_tets_of_tri<D>(S, st, s);  // cofacets of alpha
+                push_tris_of_edge<D>(S, st, e);  // cofacets of pair(alpha)
+            } else {
+                st.pq1_q &= ~(1u << s);
+                if ((st.cls_q >> s) & 1u) continue;
+                const int t0 = S.tet_tri[s][0], t1 = S.tet_tri[s][1], t2 = S.tet_tri[s][2];
+                const bool u0 = !((st.cls_t >> t0) & 1ull), u1 = !((st.cls_t >> t1) & 1ull),
+                           u2 = !((st.cls_t >> t2) & 1ull);
+                if (!u0 && !u1 && !u2) { st.pq0_q |= 1u << s; continue; }
+                const int j = u0 ? 0 : (u1 ? 1 : 2);
+                const int tt = u0 ? t0 : (u1 ? t1 : t2);
+                st.qcode |= (uint64_t)(j + 1) << (2 * s);
+                st.cls_t |= 1ull << tt;
+                st.cls_q |= 1u << s;
+                st.pq0_t &= ~(1ull << tt);
+                push_tets_of_tri<D>(S, st, tt);
+            }
+        }
+        if (!(st.pq0_e | st.pq0_t | st.pq0_q)) break;
+        const int c = pop_min(S, R, st.pq0_e, st.pq0_t, st.pq0_q);
+        const int s = c & 63, dim = c >> 6;
+        if (dim == 1) {
+            st.pq0_e &= ~(1u << s);
+            if ((st.cls_e >> s) & 1u) continue;
+            st.cls_e |= 1u << s;
+            st.crit_e |= 1u << s;
+            push_tris_of_edge<D>(S, st, s);
+        } else if (dim == 2) {
+            st.pq0_t &= ~(1ull << s);
+            if ((st.cls_t >> s) & 1ull) continue;
+            st.cls_t |= 1ull << s;
+            st.crit_t |= 1ull << s;
+            push_tets_of_tri<D>(S, st, s);
+        } else {
+            st.pq0_q &= ~(1u << s);
+            if ((st.cls_q >> s) & 1u) continue;
+            st.cls_q |= 1u << s;
+            st.crit_q |= 1u << s;
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
+    constexpr int NE = Geo<D>::NE, NT = Geo<D>::NT, NQ = Geo<D>::NQ;
+    __shared__ StarTab S;
+    __shared__ long long s_tile;
+    __shared__ uint32_t sw[4][kBlock / 32 + 1];
+    __shared__ unsigned long long s_excl[4];
+    {
+        const int4* src = reinterpret_cast<const int4*>(A.tab);
+        int4* dst = reinterpret_cast<int4*>(&S);
+        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlock) dst[i] = src[i];
+    }
+    if (threadIdx.x == 0) s_tile = atomicAdd(A.tile_ctr, 1);
+    __syncthreads();
+    const long long tile = s_tile;
+    const int64_t v = tile * kBlock + threadIdx.x;
+    const bool active = v < A.N;
+
+    StarState st;
+    st.Le = 0; st.Lq = 0; st.Lt = 0;
+    st.cls_e = st.cls_q = st.pq0_e = st.pq0_q = st.pq1_q = st.crit_e = st.crit_q = 0;
+    st.cls_t = st.pq0_t = st.pq1_t = st.crit_t = 0;
+    st.tcode_lo = st.tcode_hi = st.qcode = 0;
+    st.vcode = -1;
+    uint64_t R = 0;
+    bool crit_v = false;
+    int cx = 0, cy = 0, cz = 0;
+    if (active) {
+        const int vv = (int)v;
+        cx = vv % A.Lx;
+        const int t = vv / A.Lx;
+        cy = t % A.Ly;
+        cz = t / A.Ly;
+        const int LxLy = A.Lx * A.Ly;
+        const float fx = A.f[v];
+        if (is_nan_bits(fx)) atomicOr(A.err, 1);
+        const uint32_t ox = ord_of(fx);
+        uint32_t o[NE];
+#pragma unroll
+        for (int s = 0; s < NE; s++) {
+            const int dx = off_c<D>(s, 0), dy = off_c<D>(s, 1), dz = off_c<D>(s, 2);
+            bool in = true;
+            if (dx < 0) in &= cx > 0;
+            if (dx > 0) in &= cx < A.Lx - 1;
+            if (dy < 0) in &= cy > 0;
+            if (dy > 0) in &= cy < A.Ly - 1;
+            if (dz < 0) in &= cz > 0;
+            if (dz > 0) in &= cz < A.Lz - 1;
+            o[s] = 0xffffffffu;
+            if (in) {
+                const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
+                const bool lower = (os < ox) || (os == ox && s < NE / 2);
+                if (lower) { o[s] = os; st.Le |= 1u << s; }
+            }
+        }
+        if (st.Le == 0) {
+            crit_v = true;
+        } else {
+            // local ranks among the lower neighbours (non-lower ones hold the 0xffffffff
+            // sentinel, larger than any ordered float, so they never count)
+            int r[NE];
+#pragma unroll
+            for (int s = 0; s < NE; s++) r[s] = 0;
+#pragma unroll
+            for (int s = 0; s < NE; s++)
+#pragma unroll
+                for (int u = s + 1; u < NE; u++) {
+                    const bool s_lt_u = o[s] <= o[u];  // equal values: the smaller slot first
+                    r[u] += s_lt_u ? 1 : 0;
+                    r[s] += s_lt_u ? 0 : 1;
+                }
+            int delta = 0;
+#pragma unroll
+            for (int s = 0; s < NE; s++) {
+                if ((st.Le >> s) & 1u) {
+                    R |= (uint64_t)r[s] << (4 * s);
+                    if (r[s] == 0) delta = s;
+                }
+            }
+            // lower triangles / tets: all their link vertices lower
+            uint64_t ta = 0, tb = 0;
+            uint32_t qa = 0, qb = 0, qc = 0;
+            uint32_t le = st.Le;
+            while (le) {
+                const int s = __ffs(le) - 1;
+                le &= le - 1;
+                ta |= S.tri_amask[s];
+                tb |= S.tri_bmask[s];
+                if (D == 3) {
+                    qa |= S.tet_amask[s];
+                    qb |= S.tet_bmask[s];
+                    qc |= S.tet_cmask[s];
+                }
+            }
+            st.Lt = ta & tb;
+            st.Lq = qa & qb & qc;
+            process_star<D>(S, R, delta, st);
+        }
+        // gradient word
+        if (D == 3) {
+            const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
+            const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
+            reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
+        } else {
+            const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
+            reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
+        }
+    }
+    (void)NT;
+    (void)NQ;
+
+    // ---- compaction of the critical cells (Alg. 2 l. 10-12)
+    uint32_t cnt[4];
+    cnt[0] = crit_v ? 1u : 0u;
+    cnt[1] = __popc(st.crit_e);
+    cnt[2] = __popcll(st.crit_t);
+    cnt[3] = __popc(st.crit_q);
+    uint32_t loc[4], tot[4];
+#pragma unroll
+    for (int k = 0; k <= D; k++) loc[k] = block_excl_sum<kBlock / 32>(cnt[k], sw[k], &tot[k]);
+    if (threadIdx.x < 32) {
+        for (int k = 0; k <= D; k++) {
+            // status words are interleaved per dimension: [k * ntiles + tile]
+            unsigned long long e = lookback_warp(A.status + (int64_t)k * A.ntiles, tile, tot[k], threadIdx.x);
+            if (threadIdx.x == 0) {
+                s_excl[k] = e;
+                if (tile == A.ntiles - 1) A.totals[k] = e + tot[k];
+            }
+        }
+    }
+    __syncthreads();
+    if (!active || (cnt[0] | cnt[1] | cnt[2] | cnt[3]) == 0) return;
+    const uint64_t rkey = (uint64_t)(uint32_t)A.rank[v] << 12;
+    const int LxLy = A.Lx * A.Ly;
+    if (crit_v) {
+        const int64_t p = (int64_t)s_excl[0] + loc[0];
+        if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
+    }
+    {
+        int64_t p = (int64_t)s_excl[1] + loc[1];
+        uint32_t m = st.crit_e;
+        while (m) {
+            const int s = __ffs(m) - 1;
+            m &= m - 1;
+            if (p < A.cap[1]) {
+                const int64_t anc = v + S.e_anc[s][0] + A.Lx * S.e_anc[s][1] + LxLy * S.e_anc[s][2];
+                A.crit_id[1][p] = A.ncell[1] * anc + S.e_k[s];
+                A.crit_key[1][p] = rkey | key_edge(R, s);
+            }
+            p++;
+        }
+    }
+    {
+        int64_t p = (int64_t)s_excl[2] + loc[2];
+        uint64_t m = st.crit_t;
+        while (m) {
+            const int t = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            if (p < A.cap[2]) {
+                const int64_t anc = v + S.t_anc[t][0] + A.Lx * S.t_anc[t][1] + LxLy * S.t_anc[t][2];
+                A.crit_id[2][p] = A.ncell[2] * anc + S.t_k[t];
+                A.crit_key[2][p] = rkey | key_tri(S, R, t);
+            }
+            p++;
+        }
+    }
+    if (D == 3) {
+        int64_t p = (int64_t)s_excl[3] + loc[3];
+        uint32_t m = st.crit_q;
+        while (m) {
+            const int q = __ffs(m) - 1;
+            m &= m - 1;
+            if (p < A.cap[3]) {
+                const int64_t anc = v + S.q_anc[q][0] + A.Lx * S.q_anc[q][1] + LxLy * S.q_anc[q][2];
+                A.crit_id[3][p] = A.ncell[3] * anc + S.q_k[q];
+                A.crit_key[3][p] = rkey | key_tet(S, R, q);
+            }
+            p++;
+        }
+    }
+}
+
+// 1D: the lower star of x holds at most two edges; ProcessLowerStars reduces to:
+// no lower neighbour -> minimum; otherwise pair x with the edge to the lower (in K)
+// lower neighbour; a second lower edge is critical (SURVEY App. B closed form, which
+// the oracle's generic expansion reproduces).
+__global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
+    __shared__ long long s_tile;
+    __shared__ uint32_t sw[2][kBlock / 32 + 1];
+    __shared__ unsigned long long s_excl[2];
+    if (threadIdx.x == 0) s_tile = atomicAdd(A.tile_ctr, 1);
+    __syncthreads();
+    const long long tile = s_tile;
+    const int64_t v = tile * kBlock + threadIdx.x;
+    const bool active = v < A.N;
+    bool crit_v = false, crit_e = false;
+    int crit_slot = 0;
+    if (active) {
+        const float fx = A.f[v];
+        if (is_nan_bits(fx)) atomicOr(A.err, 1);
+        const uint32_t ox = ord_of(fx);
+        uint32_t ol = 0xffffffffu, orr = 0xffffffffu;
+        bool ll = false, lr = false;
+        if (v > 0) { ol = ord_of(A.f[v - 1]); ll = ol <= ox; }        // left index smaller: ties lower
+        if (v < A.N - 1) { orr = ord_of(A.f[v + 1]); lr = orr < ox; }  // right index larger
+        uint8_t code;
+        if (!ll && !lr) { code = 3; crit_v = true; }
+        else if (ll && !lr) code = 0;
+        else if (!ll && lr) code = 1;
+        else {
+            const bool left_lower = ol <= orr;  // K(v-1) < K(v+1)
+            code = left_lower ? 0 : 1;
+            crit_e = true;
+            crit_slot = left_lower ? 1 : 0;
+        }
+        reinterpret_cast<uint8_t*>(A.grad)[v] = code;
+    }
+    uint32_t cnt0 = crit_v ? 1u : 0u, cnt1 = crit_e ? 1u : 0u;
+    uint32_t tot0, tot1;
+    const uint32_t loc0 = block_excl_sum<kBlock / 32>(cnt0, sw[0], &tot0);
+    const uint32_t loc1 = block_excl_sum<kBlock / 32>(cnt1, sw[1], &tot1);
+    if (threadIdx.x < 32) {
+        unsigned long long e0 = lookback_warp(A.status, tile, tot0, threadIdx.x);
+        unsigned long long e1 = lookback_warp(A.status + A.ntiles, tile, tot1, threadIdx.x);
+        if (threadIdx.x == 0) {
+            s_excl[0] = e0;
+            s_excl[1] = e1;
+            if (tile == A.ntiles - 1) { A.totals[0] = e0 + tot0; A.totals[1] = e1 + tot1; }
+        }
+    }
+    __syncthreads();
+    if (!active || !(crit_v || crit_e)) return;
+    const uint64_t rkey = (uint64_t)(uint32_t)A.rank[v] << 12;
+    if (crit_v) {
+        const int64_t p = (int64_t)s_excl[0] + loc0;
+        if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
+    }
+    if (crit_e) {
+        const int64_t p = (int64_t)s_excl[1] + loc1;
+        if (p < A.cap[1]) {
+            A.crit_id[1][p] = crit_slot == 0 ? v - 1 : v;  // edge (a, a+1) has id a
+            A.crit_key[1][p] = rkey | (2u << 8);            // the higher of the two lower edges
+        }
+    }
+}
+
+}  // namespace dms

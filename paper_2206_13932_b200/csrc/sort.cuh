@@ -1,0 +1,194 @@
+// sort.cuh -- hand-written stable LSD radix sort (8-bit digits) for sm_100a.
+//
+// Used for the global vertex order (a key-value sort of (value, index), PAPER.md
+// 1069-1071 / 1121 "parallel sort") and for sorting the critical simplices by their
+// lexicographic keys (Alg. 2 l. 13, PAPER.md 357-359).
+//
+// Per pass: k_hist (per-tile digit histogram, digit-major counts), k_scan_excl
+// (single-pass decoupled look-back scan of the counts), k_scatter (stable in-tile
+// ranking with warp match + per-warp digit counters, then scatter).  The last pass of
+// the vertex order writes rank[value] = position directly.
+#pragma once
+#include "common.cuh"
+
+namespace dms {
+
+constexpr int kRadix = 256;
+
+template <typename Key>
+__device__ __forceinline__ uint32_t digit_of(Key k, int shift) {
+    return (uint32_t)((k >> shift) & (Key)0xff);
+}
+
+template <typename Key, int ITEMS>
+__global__ void __launch_bounds__(kBlock) k_hist(const Key* __restrict__ keys, int64_t n, int shift,
+                                                 uint32_t* __restrict__ counts, int64_t ntiles) {
+    __shared__ uint32_t h[kRadix];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * (kBlock * ITEMS);
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
+        if (idx < n) atomicAdd(&h[digit_of(keys[idx], shift)], 1u);
+    }
+    __syncthreads();
+    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of n uint32 (single pass, decoupled look-back). status[ntiles] and
+// *tile_ctr must be zero before the launch.
+constexpr int kScanItems = 16;
+__global__ void __launch_bounds__(kBlock) k_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                      int64_t n, unsigned long long* status, int* tile_ctr) {
+    __shared__ uint32_t sw[kBlock / 32 + 1];
+    __shared__ long long s_tile;
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);
+    __syncthreads();
+    const long long tile = s_tile;
+    const int64_t base = tile * (kBlock * kScanItems) + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        v[j] = (base + j < n) ? in[base + j] : 0u;
+        sum += v[j];
+    }
+    uint32_t total;
+    uint32_t excl = block_excl_sum<kBlock / 32>(sum, sw, &total);
+    if (threadIdx.x < 32) {
+        unsigned long long e = lookback_warp(status, tile, total, threadIdx.x);
+        if (threadIdx.x == 0) s_excl = e;
+    }
+    __syncthreads();
+    uint32_t run = (uint32_t)s_excl + excl;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        if (base + j < n) out[base + j] = run;
+        run += v[j];
+    }
+}
+
+// Stable scatter. RANK_OUT: write rank_out[val] = position instead of key/val.
+template <typename Key, typename Val, int ITEMS, bool RANK_OUT>
+__global__ void __launch_bounds__(kBlock) k_scatter(const Key* __restrict__ kin, const Val* __restrict__ vin,
+                                                    Key* __restrict__ kout, Val* __restrict__ vout,
+                                                    int32_t* __restrict__ rank_out, int64_t n, int shift,
+                                                    const uint32_t* __restrict__ counts_scanned, int64_t ntiles) {
+    constexpr int NW = kBlock / 32;
+    __shared__ uint32_t wcnt[NW][kRadix];
+    __shared__ uint32_t gbase[kRadix];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int w = 0; w < NW; w++) wcnt[w][threadIdx.x] = 0;
+    gbase[threadIdx.x] = counts_scanned[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+    __syncthreads();
+    const int64_t seg = (int64_t)blockIdx.x * (kBlock * ITEMS) + (int64_t)warp * (32 * ITEMS);
+    Key k[ITEMS];
+    Val v[ITEMS];
+    uint32_t pos[ITEMS];
+    uint32_t dg[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        int64_t idx = seg + i * 32 + lane;
+        if (idx < n) {
+            k[i] = kin[idx];
+            v[i] = vin[idx];
+            dg[i] = digit_of(k[i], shift);
+        } else {
+            dg[i] = kRadix;  // sentinel, never written
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const uint32_t d = dg[i];
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t r = __popc(peers & lanemask_lt());
+        const int leader = __ffs(peers) - 1;
+        uint32_t b = 0;
+        if (d < kRadix) b = wcnt[warp][d];
+        __syncwarp();
+        if (d < kRadix && lane == leader) wcnt[warp][d] = b + __popc(peers);
+        __syncwarp();
+        pos[i] = b + r;
+    }
+    __syncthreads();
+    {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+            uint32_t c = wcnt[w][threadIdx.x];
+            wcnt[w][threadIdx.x] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        const uint32_t d = dg[i];
+        if (d < kRadix) {
+            const uint32_t p = gbase[d] + wcnt[warp][d] + pos[i];
+            if (RANK_OUT) {
+                rank_out[v[i]] = (int32_t)p;
+            } else {
+                kout[p] = k[i];
+                vout[p] = v[i];
+            }
+        }
+    }
+}
+
+struct SortScratch {
+    uint32_t* counts = nullptr;       // kRadix * max tiles
+    uint32_t* counts_scan = nullptr;  // same
+    unsigned long long* status = nullptr;
+    int* tile_ctr = nullptr;
+    int64_t max_tiles = 0;
+    int64_t max_scan_tiles = 0;
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline cudaError_t scan_excl(const uint32_t* in, uint32_t* out, int64_t n, SortScratch& s, cudaStream_t st,
+                             int64_t* launches) {
+    int64_t tiles = ceil_div(n, (int64_t)kBlock * kScanItems);
+    cudaMemsetAsync(s.status, 0, tiles * sizeof(unsigned long long), st);
+    cudaMemsetAsync(s.tile_ctr, 0, sizeof(int), st);
+    k_scan_excl<<<(unsigned)tiles, kBlock, 0, st>>>(in, out, n, s.status, s.tile_ctr);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+// Sort (keys, vals) by bits [bit0, bit1) of the key.  Buffers a -> b -> a ...; returns
+// 0 if the result is in (ka, va), 1 if in (kb, vb).  With rank_out != nullptr the last
+// pass writes rank_out[val] = position and the return value is meaningless.
+template <typename Key, typename Val, int ITEMS>
+inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, int bit1, SortScratch& s,
+                      cudaStream_t st, int64_t* launches, int32_t* rank_out = nullptr) {
+    if (n <= 0) return 0;
+    const int64_t tiles = ceil_div(n, (int64_t)kBlock * ITEMS);
+    int cur = 0;
+    for (int shift = bit0; shift < bit1; shift += 8) {
+        const bool last = shift + 8 >= bit1;
+        Key* ki = cur ? kb : ka;
+        Val* vi = cur ? vb : va;
+        Key* ko = cur ? ka : kb;
+        Val* vo = cur ? va : vb;
+        k_hist<Key, ITEMS><<<(unsigned)tiles, kBlock, 0, st>>>(ki, n, shift, s.counts, tiles);
+        *launches += 1;
+        scan_excl(s.counts, s.counts_scan, tiles * kRadix, s, st, launches);
+        if (last && rank_out) {
+            k_scatter<Key, Val, ITEMS, true><<<(unsigned)tiles, kBlock, 0, st>>>(ki, vi, ko, vo, rank_out, n, shift,
+                                                                               s.counts_scan, tiles);
+        } else {
+            k_scatter<Key, Val, ITEMS, false><<<(unsigned)tiles, kBlock, 0, st>>>(ki, vi, ko, vo, nullptr, n,
+                                                                                shift, s.counts_scan, tiles);
+        }
+        *launches += 1;
+        cur ^= 1;
+    }
+    return cur;
+}
+
+}  // namespace dms

@@ -1,0 +1,52 @@
+// star.cuh -- the star of a vertex in the Freudenthal triangulation, as small tables.
+//
+// PAPER.md 1360-1366 (Sec. 2.1): grids are triangulated by the Freudenthal (Kuhn)
+// scheme, giving the 6-vertex (2D) / 14-vertex (3D) neighbourhood.  A set of lattice
+// points {0, o_1, ..., o_k} spans a simplex of that triangulation iff, sorted by
+// coordinate sum, the points increase component-wise and the last minus the first is
+// a 0/1 vector.  The tables below are derived from that rule on the host at context
+// creation (no enumeration is shared with the oracle).
+//
+// Slots: the neighbours n_s = x + off[s] are numbered by increasing linear index
+// offset, so for equal values the index tie-break of K is a slot comparison:
+//   K(n_s) < K(n_t) <=> f_s < f_t or (f_s == f_t and s < t), and x sits between slot
+//   NE/2-1 and NE/2.
+// Star cells of x: edge (x, n_s) = slot s; triangle (x, n_a, n_b) = "tri slot";
+// tetrahedron (x, n_a, n_b, n_c) = "tet slot".
+#pragma once
+#include <cstdint>
+
+namespace dms {
+
+constexpr int kMaxNE = 14, kMaxNT = 36, kMaxNQ = 24;
+
+struct alignas(16) StarTab {
+    int ndim, ne, nt, nq;
+    int8_t off[kMaxNE][3];
+    int32_t lin[kMaxNE];              // linear index offsets for the grid
+    uint8_t tri_a[kMaxNT], tri_b[kMaxNT];                 // neighbour slots, a < b
+    uint8_t tet_a[kMaxNQ], tet_b[kMaxNQ], tet_c[kMaxNQ];  // a < b < c
+    uint8_t tet_tri[kMaxNQ][3];       // tri slots (a,b), (a,c), (b,c)
+    uint8_t tri_tet[kMaxNT][2];       // tet slots containing the tri (255: none)
+    uint8_t edge_tri[kMaxNE][6];      // tri slots containing edge s (255: none)
+    uint64_t edge_tri_mask[kMaxNE];   // same as a mask over tri slots
+    uint32_t tri_tet_mask[kMaxNT];    // tet slots containing the tri
+    uint64_t tri_amask[kMaxNE], tri_bmask[kMaxNE];  // tri slots whose a (b) end is slot s
+    uint32_t tet_amask[kMaxNE], tet_bmask[kMaxNE], tet_cmask[kMaxNE];
+    // anchored ids of star cells: anchor offset from x and chain index
+    int8_t e_anc[kMaxNE][3];  uint8_t e_k[kMaxNE];
+    int8_t t_anc[kMaxNT][3];  uint8_t t_k[kMaxNT];
+    int8_t q_anc[kMaxNQ][3];  uint8_t q_k[kMaxNQ];
+    // chain index k and position j of the star centre inside the chain -> slot
+    uint8_t e_slot[7][2];     // edges:     7 chains x 2 positions
+    uint8_t t_slot[12][3];    // triangles
+    uint8_t q_slot[6][4];     // tetrahedra
+    // chains per dimension: masks S_1..S_k (x=1,y=2,z=4) of chain index k
+    uint8_t chain[4][12][3];
+    int nchain[4];
+};
+
+// Build the tables for a grid (host).  Returns false if something is inconsistent.
+bool build_star_tables(int ndim, const int64_t L[3], StarTab* T);
+
+}  // namespace dms

@@ -1,0 +1,153 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle, bit-exact
+(tolerance 0: every output is integer / index data or a copied float value,
+BASELINE.json north_star)."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import fields
+
+pytestmark = pytest.mark.gpu
+
+NCPU = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def env():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build_lib()
+    import paper_2206_13932_b200 as dms
+
+    return torch, dms
+
+
+def gpu_run(env, f):
+    torch, dms = env
+    d = dms.DMS(torch.from_numpy(np.ascontiguousarray(f)).cuda())
+    rank = d.order()
+    grad = d.gradient()
+    out = dict(
+        rank=rank.cpu().numpy(),
+        grad=grad.cpu().numpy(),
+        crit=[c.cpu().numpy() for c in d.critical()],
+        d0=d.diagram0(),
+        dtop=d.diagram_top(),
+        un0=d.unpaired_saddles(0),
+        untop=d.unpaired_saddles(1),
+        launches=d.launch_count(),
+    )
+    d.close()
+    return out
+
+
+def compare_full(env, f, nthreads=NCPU):
+    _, dms = env
+    ref = oracle.run(f, nthreads=nthreads)
+    got = gpu_run(env, f)
+    d = f.ndim
+    assert np.array_equal(got["rank"], oracle.ranks(f)), "ranks"
+    pairs = dms.dms_decode_pairs(f.shape, got["grad"], 0, f.size)
+    pairs = pairs[np.lexsort((pairs[:, 2], pairs[:, 1], pairs[:, 0]))]
+    assert np.array_equal(pairs, ref.pairs), "gradient pairs"
+    for k in range(d + 1):
+        assert np.array_equal(got["crit"][k], ref.crit[k]), ("C_%d" % k)
+    assert got["d0"].tobytes() == ref.d0.tobytes(), "D0"
+    assert got["dtop"].tobytes() == ref.dtop.tobytes(), "D_{d-1}"
+    assert np.array_equal(got["un0"], ref.unpaired0), "unpaired after D0"
+    assert np.array_equal(got["untop"], ref.unpaired_top), "unpaired after D_{d-1}"
+    assert got["launches"] > 0
+    return ref, got
+
+
+SHAPES = [
+    (2, 2, 2), (2, 3, 5), (3, 3, 3), (9, 10, 11), (16, 16, 16), (7, 33, 20), (33, 17, 5),
+    (2, 2), (2, 9), (37, 41), (64, 3), (100, 129),
+    (2,), (3,), (1000,), (4099,),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("kind", ["uniform", "ties", "signed_zero"])
+def test_small_grids(env, shape, kind):
+    rng = np.random.default_rng(hash((shape, kind)) % (2**32))
+    f = fields.uniform(shape, seed=int(rng.integers(1 << 30)))
+    if kind == "ties":
+        f = np.floor(f * 5).astype(np.float32)  # the index tie-break decides
+    if kind == "signed_zero":
+        f = np.where(f < 0.5, np.float32(0.0), np.float32(-0.0)).astype(np.float32)  # -0 == +0
+        f[rng.random(shape) < 0.1] = np.inf
+        f[rng.random(shape) < 0.1] = -np.inf
+    compare_full(env, f)
+
+
+@pytest.mark.parametrize("shape", [(6, 7, 8), (20, 21), (50,)])
+def test_constant_elevation_bowl(env, shape):
+    d = len(shape)
+    for f in [np.zeros(shape, np.float32),
+              np.indices(shape).sum(0).astype(np.float32),
+              -np.indices(shape).sum(0).astype(np.float32),
+              (sum((c - s / 2.0) ** 2 for c, s in zip(np.indices(shape), shape))).astype(np.float32),
+              (-sum((c - s / 2.0) ** 2 for c, s in zip(np.indices(shape), shape))).astype(np.float32)]:
+        ref, got = compare_full(env, f)
+        inf = [p for p in got["d0"] if p["death_id"] < 0]
+        assert len(inf) == 1
+        assert sum((-1) ** k * len(got["crit"][k]) for k in range(d + 1)) == 1
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_seed_sweep_c1_recipe(env, seed):
+    compare_full(env, fields.make("c1", seed=seed, shape=(20, 24, 28)))
+
+
+def test_config_c1(env):
+    compare_full(env, fields.make("c1"))
+
+
+def test_config_c2(env):
+    compare_full(env, fields.make("c2"))
+
+
+def test_config_small_versions_of_c4_c5(env):
+    compare_full(env, fields.make("c4", shape=(64, 64, 64)))
+    compare_full(env, fields.make("c5a", shape=(512, 512)))
+    compare_full(env, fields.make("c5b", shape=(1 << 16,)))
+
+
+def test_nan_rejected(env):
+    torch, dms = env
+    f = np.zeros((4, 5, 6), np.float32)
+    f[1, 2, 3] = np.nan
+    d = dms.DMS(torch.from_numpy(f).cuda())
+    with pytest.raises(dms.DMSError) as e:
+        d.run_all()
+        d.critical()
+    assert e.value.name == "DMS_ERR_NAN"
+
+
+def test_degenerate_and_ignore_mode(env):
+    torch, dms = env
+    for shape in [(1, 4, 4), (4, 1), (1,)]:
+        with pytest.raises(dms.DMSError) as e:
+            dms.DMS(torch.zeros(shape, device="cuda"))
+        assert e.value.name == "DMS_ERR_DEGENERATE"
+    d = dms.DMS(torch.rand(5, 5, 5, device="cuda"))
+    with pytest.raises(dms.DMSError) as e:
+        d.diagram_top(mode=1)
+    assert e.value.name == "DMS_ERR_STATE"
+
+
+def test_deterministic_repeat(env):
+    f = fields.make("c1", seed=9)
+    a = gpu_run(env, f)
+    b = gpu_run(env, f)
+    for key in ("rank", "grad"):
+        assert np.array_equal(a[key], b[key])
+    assert a["d0"].tobytes() == b["d0"].tobytes() and a["dtop"].tobytes() == b["dtop"].tobytes()

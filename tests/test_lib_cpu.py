@@ -1,0 +1,120 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/dms.h
+declares, and its host-side gradient decoder agrees with the oracle's simplex ids."""
+from __future__ import annotations
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def dms():
+    import __graft_entry__
+
+    __graft_entry__.build_lib()
+    import paper_2206_13932_b200 as m
+
+    m.lib()
+    return m
+
+
+def test_header_symbols_exported(dms):
+    hdr = open(os.path.join(ROOT, "include", "dms.h")).read()
+    declared = sorted(set(re.findall(r"\b(dms_[a-z0-9_]+)\s*\(", hdr)))
+    assert declared, "no declarations found"
+    L = dms.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert sorted(dms.ABI_SYMBOLS) == declared
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2206_13932_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h", ".c")):
+                src = open(os.path.join(dirpath, fn)).read()
+                assert not re.search(r"(import\s+oracle|from\s+oracle|#include[^\n]*oracle|dms_oracle|orc_)", src), fn
+
+
+def _vertices(shape, dim, sid):
+    return set(int(v) for v in oracle.simplex_vertices(shape, dim, sid))
+
+
+@pytest.mark.parametrize("shape", [(4, 5, 6), (5, 7), (9,)])
+def test_decode_vertex_codes_match_oracle_ids(dms, shape):
+    """A word whose vertex code points at neighbour slot s decodes to the edge (v, v+off_s);
+    the product's anchored-id tables must agree with the oracle's id convention."""
+    d = len(shape)
+    Lx = shape[-1]
+    Ly = shape[-2] if d > 1 else 1
+    Lz = shape[-3] if d > 2 else 1
+    v = Lx // 2 + Lx * (Ly // 2 + Ly * (Lz // 2))  # an interior vertex
+    nslots = {3: 14, 2: 6, 1: 2}[d]
+    seen = set()
+    for s in range(nslots):
+        if d == 3:
+            w = np.zeros(2, dtype=np.uint64)
+            w[1] = np.uint64(s) << np.uint64(56)
+            w[0] = 0
+        elif d == 2:
+            w = np.array([s], dtype=np.uint16)
+        else:
+            w = np.array([s], dtype=np.uint8)
+        tr = dms.dms_decode_pairs(shape, w.view(np.uint8), v, v + 1)
+        assert tr.shape == (1, 3) and tr[0, 0] == 0 and tr[0, 1] == v
+        verts = _vertices(shape, 1, int(tr[0, 2]))
+        assert v in verts
+        (u,) = verts - {v}
+        seen.add(u - v)
+    assert len(seen) == nslots
+    # the offsets are exactly the Freudenthal neighbourhood (PAPER.md 1362-1364)
+    offs = set()
+    for dz in (-1, 0, 1) if d == 3 else (0,):
+        for dy in (-1, 0, 1) if d >= 2 else (0,):
+            for dx in (-1, 0, 1):
+                o = (dx, dy, dz)
+                if any(o) and not (min(o) < 0 < max(o)):
+                    offs.add(dx + Lx * dy + Lx * Ly * dz)
+    assert seen == offs
+
+
+def test_decode_all_codes_are_facet_pairs(dms):
+    """Every tri/tet code decodes to a (facet, cofacet) pair of the complex that both
+    contain the star centre."""
+    shape = (5, 5, 5)
+    v = 62  # interior
+    for t in range(36):
+        for code in (1, 2):
+            w = np.zeros(2, dtype=np.uint64)
+            if t < 32:
+                w[0] = np.uint64(code) << np.uint64(2 * t)
+            else:
+                w[1] = np.uint64(code) << np.uint64(2 * (t - 32))
+            w[1] |= np.uint64(15) << np.uint64(56)
+            tr = dms.dms_decode_pairs(shape, w.view(np.uint8), v, v + 1)
+            assert tr.shape == (1, 3) and tr[0, 0] == 1
+            a, b = _vertices(shape, 1, int(tr[0, 1])), _vertices(shape, 2, int(tr[0, 2]))
+            assert a < b and v in a
+    for q in range(24):
+        for code in (1, 2, 3):
+            w = np.zeros(2, dtype=np.uint64)
+            w[1] = (np.uint64(code) << np.uint64(8 + 2 * q)) | (np.uint64(15) << np.uint64(56))
+            tr = dms.dms_decode_pairs(shape, w.view(np.uint8), v, v + 1)
+            assert tr.shape == (1, 3) and tr[0, 0] == 2
+            a, b = _vertices(shape, 2, int(tr[0, 1])), _vertices(shape, 3, int(tr[0, 2]))
+            assert a < b and v in a
+
+
+def test_no_cpu_fallback_without_device(dms):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(TypeError):
+        dms.dms_create(torch.zeros(4, 4))
