@@ -873,8 +873,8 @@ int64_t orc_count(const orc_result *r, int what, int k)
     case ORC_DTOP: return r->ndtop;
     case ORC_UN0: return r->nun0;
     case ORC_UNTOP: return r->nuntop;
-    case ORC_ARCS0: return r->arcs0 ? 2 * r->ncrit[1] : 0;
-    case ORC_ARCSTOP: return r->arcstop ? 2 * r->ncrit[r->g.ndim - 1] : 0;
+    case ORC_ARCS0: return r->arcs0 ? r->ncrit[1] : 0;
+    case ORC_ARCSTOP: return r->arcstop ? r->ncrit[r->g.ndim - 1] : 0;
     case ORC_MS: return 5;
     }
     return 0;
@@ -890,8 +890,8 @@ void orc_copy(const orc_result *r, int what, int k, void *dst)
     case ORC_DTOP: memcpy(dst, r->dtop, n * sizeof(orc_pair)); break;
     case ORC_UN0: memcpy(dst, r->un0, n * sizeof(int64_t)); break;
     case ORC_UNTOP: memcpy(dst, r->untop, n * sizeof(int64_t)); break;
-    case ORC_ARCS0: memcpy(dst, r->arcs0, n * sizeof(int64_t)); break;
-    case ORC_ARCSTOP: memcpy(dst, r->arcstop, n * sizeof(int64_t)); break;
+    case ORC_ARCS0: memcpy(dst, r->arcs0, 2 * n * sizeof(int64_t)); break;
+    case ORC_ARCSTOP: memcpy(dst, r->arcstop, 2 * n * sizeof(int64_t)); break;
     case ORC_MS: memcpy(dst, r->ms, 5 * sizeof(double)); break;
     }
 }

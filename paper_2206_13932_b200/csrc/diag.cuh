@@ -220,34 +220,46 @@ __global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ cs, int64_t m, c
 }
 
 // ---------------------------------------------------------------- union-find
-// Arcs are indexed in processing order; an arc's index is its key.  Seniority:
-// older_is_smaller = true for D0 (node = position in ascending C_0), false for
-// D_{d-1} (node = position in ascending C_d, the virtual node the largest = oldest).
+// Arcs are indexed in processing order; an arc's index is its key.  Nodes are the
+// extrema; older_is_smaller = true for D0 (node = position in ascending C_0), false
+// for D_{d-1} (node = position in ascending C_d, the virtual node the largest = the
+// oldest).  Hooks always go younger -> older, so a root is its component's oldest node.
 // out[i]: -2 undecided, -1 unpaired (cycle), >= 0 the node that dies at arc i.
+//
+// A round: every live arc finds its two roots; every root
+// takes the minimum index m(R) of its live outgoing arcs.  Then for an arc e = m(A)
+// joining roots A and B:
+//   * e == m(B) (mutual): the younger of A, B dies at e  (both sides are exactly the
+//     Kruskal components at e);
+//   * else, if A is younger than B: A dies at e  (A is exactly its Kruskal component
+//     at e, and B's Kruskal component at e already holds B's oldest node);
+//   * else the arc waits.
+// Both rules keep the invariant "for every outgoing arc of a component, its Kruskal
+// component at that arc's key contains the component's oldest node", so every
+// decision equals the sequential elder-rule union-find's.
 
 __device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t a) {
-    int32_t p = parent[a];
-    while (p != a) {
+    while (true) {
+        const int32_t p = parent[a];
+        if (p == a) return a;
         const int32_t gp = parent[p];
         if (gp != p) parent[a] = gp;  // path halving (only ever points to an ancestor)
-        a = p;
-        p = gp;
-        if (gp == a) break;
-        p = parent[a];
+        a = gp;
     }
-    return a;
 }
 
-__global__ void k_uf_init(int32_t* parent, uint32_t* best, int64_t n, int32_t* out, int64_t m) {
+__global__ void k_uf_init(int32_t* parent, uint32_t* best, int64_t n, int32_t* out, int32_t* live, int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) { parent[i] = (int32_t)i; best[i] = 0xffffffffu; }
-    if (i < m) out[i] = -2;
+    if (i < m) { out[i] = -2; live[i] = (int32_t)i; }
 }
 
-__global__ void k_uf_round1(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b, int64_t m,
-                            int32_t* parent, uint32_t* best, int32_t* ra, int32_t* rb, int32_t* out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        if (out[i] != -2) continue;
+__global__ void k_uf_round1(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b,
+                            const int32_t* __restrict__ live, const int* nlive, int32_t* parent, uint32_t* best,
+                            int32_t* ra, int32_t* rb, int32_t* out) {
+    const int n = *nlive;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+        const int32_t i = live[idx];
         const int32_t a = uf_find(parent, arc_a[i]);
         const int32_t b = uf_find(parent, arc_b[i]);
         ra[i] = a;
@@ -258,36 +270,54 @@ __global__ void k_uf_round1(const int32_t* __restrict__ arc_a, const int32_t* __
     }
 }
 
-__global__ void k_uf_round2(int64_t m, int32_t* parent, const uint32_t* best, const int32_t* ra, const int32_t* rb,
-                            int32_t* out, bool older_is_smaller) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void k_uf_round2(const int32_t* __restrict__ live, const int* nlive, int32_t* parent, const uint32_t* best,
+                            const int32_t* ra, const int32_t* rb, int32_t* out, bool older_is_smaller) {
+    const int n = *nlive;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+        const int32_t i = live[idx];
         if (out[i] != -2) continue;
         const int32_t a = ra[i], b = rb[i];
-        if (best[a] == (uint32_t)i && best[b] == (uint32_t)i) {
-            // mutual minimum: Kruskal would merge exactly these two components here
-            const bool a_older = older_is_smaller ? (a < b) : (a > b);
+        const bool ma = best[a] == (uint32_t)i, mb = best[b] == (uint32_t)i;
+        const bool a_older = older_is_smaller ? (a < b) : (a > b);
+        if (ma && mb) {
             const int32_t young = a_older ? b : a, old = a_older ? a : b;
             parent[young] = old;
             out[i] = young;
+        } else if (ma && !a_older) {
+            parent[a] = b;
+            out[i] = a;
+        } else if (mb && a_older) {
+            parent[b] = a;
+            out[i] = b;
         }
     }
 }
 
-__global__ void k_uf_round3(int64_t m, uint32_t* best, const int32_t* ra, const int32_t* rb, const int32_t* out,
-                            unsigned long long* remaining) {
-    uint32_t live = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t o = out[i];
-        if (o == -1) continue;
-        // reset the candidates of this round (roots of every arc visited this round)
-        if (o == -2 || o >= 0) {
-            best[ra[i]] = 0xffffffffu;
-            best[rb[i]] = 0xffffffffu;
+__global__ void k_uf_round3(const int32_t* __restrict__ live, const int* nlive, uint32_t* best, const int32_t* ra,
+                            const int32_t* rb, const int32_t* out, int32_t* live_out, int* nlive_out) {
+    const int n = *nlive;
+    const int lane = threadIdx.x & 31;
+    // uniform trip count so the warp-aggregated append can use full-warp intrinsics
+    const int stride = gridDim.x * blockDim.x;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int idx = base + threadIdx.x;
+        bool keep = false;
+        int32_t i = 0;
+        if (idx < n) {
+            i = live[idx];
+            const int32_t o = out[i];
+            if (o != -1) {
+                best[ra[i]] = 0xffffffffu;  // reset this round's candidates
+                best[rb[i]] = 0xffffffffu;
+            }
+            keep = o == -2;
         }
-        if (o == -2) live++;
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        int basepos = 0;
+        if (lane == 0 && mk) basepos = atomicAdd(nlive_out, __popc(mk));
+        basepos = __shfl_sync(0xffffffffu, basepos, 0);
+        if (keep) live_out[basepos + __popc(mk & lanemask_lt())] = i;
     }
-    for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
-    if ((threadIdx.x & 31) == 0 && live) atomicAdd(remaining, (unsigned long long)live);
 }
 
 __global__ void k_flag_undecided(const int32_t* out, int64_t m, uint32_t* flags) {

@@ -68,6 +68,8 @@ __global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsig
 
 struct UFBuf {
     int32_t *arc_a = nullptr, *arc_b = nullptr, *ra = nullptr, *rb = nullptr, *out = nullptr, *list = nullptr;
+    int32_t* live2 = nullptr;
+    int* nlive = nullptr;  // two device counters
     int32_t* parent = nullptr;
     uint32_t *best = nullptr, *flags = nullptr, *pos = nullptr;
     int64_t cap_arcs = 0, cap_nodes = 0;
@@ -213,7 +215,11 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
     arcs = std::max<int64_t>(arcs, 1);
     nodes = std::max<int64_t>(nodes, 1);
     if (arcs > u.cap_arcs) {
-        for (int32_t** p : {&u.arc_a, &u.arc_b, &u.ra, &u.rb, &u.out, &u.list}) { cudaFree(*p); CU(dalloc(p, arcs)); }
+        for (int32_t** p : {&u.arc_a, &u.arc_b, &u.ra, &u.rb, &u.out, &u.list, &u.live2}) {
+            cudaFree(*p);
+            CU(dalloc(p, arcs));
+        }
+        if (!u.nlive) CU(dalloc(&u.nlive, 2));
         for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
         u.cap_arcs = arcs;
     }
@@ -347,27 +353,38 @@ const int64_t* crit_ids(dms_ctx* c, int k) { return c->cid[c->cur[k]][k]; }
 // union-find over arcs (processing order), see diag.cuh
 dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older_is_smaller) {
     const unsigned gi = grid_for(std::max(m, nodes));
-    k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.out, m);
+    k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.out, u.list, m);
     c->launches++;
-    CU(cudaMemsetAsync(u.ra, 0xff, std::max<int64_t>(m, 1) * sizeof(int32_t), c->st));
     if (m == 0) return DMS_OK;
+    int hm[2] = {(int)m, 0};
+    CU(cudaMemcpyAsync(u.nlive, hm, sizeof hm, cudaMemcpyHostToDevice, c->st));
     const unsigned gr = (unsigned)std::min<int64_t>(grid_for(m), 148 * 8);
-    int64_t prev = m;
-    for (int iter = 0; iter < 100000; iter++) {
-        const int batch = 4;
+    int32_t* live[2] = {u.list, u.live2};
+    int cur = 0;
+    int64_t rem = m;
+    for (int iter = 0; iter < 200000; iter++) {
+        const int batch = rem > 100000 ? 2 : 8;
         for (int r = 0; r < batch; r++) {
-            if (r == batch - 1) CU(cudaMemsetAsync(c->remaining, 0, sizeof(unsigned long long), c->st));
-            k_uf_round1<<<gr, kBlock, 0, c->st>>>(u.arc_a, u.arc_b, m, u.parent, u.best, u.ra, u.rb, u.out);
-            k_uf_round2<<<gr, kBlock, 0, c->st>>>(m, u.parent, u.best, u.ra, u.rb, u.out, older_is_smaller);
-            k_uf_round3<<<gr, kBlock, 0, c->st>>>(m, u.best, u.ra, u.rb, u.out, c->remaining);
+            const int nxt = cur ^ 1;
+            CU(cudaMemsetAsync(u.nlive + nxt, 0, sizeof(int), c->st));
+            k_uf_round1<<<gr, kBlock, 0, c->st>>>(u.arc_a, u.arc_b, live[cur], u.nlive + cur, u.parent, u.best, u.ra,
+                                                 u.rb, u.out);
+            k_uf_round2<<<gr, kBlock, 0, c->st>>>(live[cur], u.nlive + cur, u.parent, u.best, u.ra, u.rb, u.out,
+                                                 older_is_smaller);
+            k_uf_round3<<<gr, kBlock, 0, c->st>>>(live[cur], u.nlive + cur, u.best, u.ra, u.rb, u.out, live[nxt],
+                                                 u.nlive + nxt);
             c->launches += 3;
+            cur = nxt;
         }
-        CU(cudaMemcpyAsync(c->h_pinned, c->remaining, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
+        int h = 0;
+        CU(cudaMemcpyAsync(c->h_pinned, u.nlive + cur, sizeof(int), cudaMemcpyDeviceToHost, c->st));
         CU(cudaStreamSynchronize(c->st));
-        const int64_t rem = (int64_t)c->h_pinned[0];
+        std::memcpy(&h, c->h_pinned, sizeof(int));
+        const int64_t prev = rem;
+        rem = h;
         if (rem == 0) return DMS_OK;
-        if (rem <= 4096 || (rem < 65536 && rem * 4 > prev * 3)) {
-            // sequential tail over the undecided arcs, in order
+        if (rem <= 2048 || (rem <= 65536 && rem * 8 > prev * 7)) {
+            // sequential tail over the undecided arcs, in processing order
             k_flag_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags);
             scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
             k_gather_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, u.list);
@@ -377,7 +394,6 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older
             CU(cudaGetLastError());
             return DMS_OK;
         }
-        prev = rem;
     }
     return fail(c, DMS_ERR_INVARIANT, "union-find did not converge");
 }
@@ -768,6 +784,7 @@ void dms_destroy(dms_ctx* c) {
     for (int b = 0; b < 2; b++) {
         UFBuf& u = c->uf[b];
         for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.ra, (void*)u.rb, (void*)u.out, (void*)u.list,
+                        (void*)u.live2, (void*)u.nlive,
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
             cudaFree(p);
         cudaFree(c->pairs[b]);
