@@ -261,14 +261,7 @@ dms_status run_order(dms_ctx* c, int32_t* d_rank) {
 
 dms_status launch_gradient(dms_ctx* c) {
     const int64_t ntiles = ceil_div(c->N, kBlock);
-    const int dims = c->ndim + 1;
-    if (ntiles * dims > c->status_words) {
-        cudaFree(c->status);
-        CU(dalloc(&c->status, ntiles * 4));
-        c->status_words = ntiles * 4;
-    }
-    CU(cudaMemsetAsync(c->status, 0, ntiles * dims * sizeof(unsigned long long), c->st));
-    CU(cudaMemsetAsync(c->tile_ctr, 0, sizeof(int), c->st));
+    CU(cudaMemsetAsync(c->totals, 0, 4 * sizeof(unsigned long long), c->st));
     GradArgs A;
     A.f = c->f;
     A.Lx = (int32_t)c->L[0];
@@ -284,11 +277,8 @@ dms_status launch_gradient(dms_ctx* c) {
         A.cap[k] = c->cap[k];
         A.ncell[k] = c->ncell[k];
     }
-    A.status = c->status;
-    A.tile_ctr = c->tile_ctr;
     A.totals = c->totals;
     A.err = c->err;
-    A.ntiles = ntiles;
     StageTimer tm(c, 5);
     if (c->ndim == 3) k_gradient<3><<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
     else if (c->ndim == 2) k_gradient<2><<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);

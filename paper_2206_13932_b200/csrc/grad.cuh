@@ -53,11 +53,8 @@ struct GradArgs {
     uint64_t* crit_key[4];
     int64_t cap[4];
     int64_t ncell[4];
-    unsigned long long* status;  // 4 words per tile, zeroed
-    int* tile_ctr;               // zeroed
-    unsigned long long* totals;  // [4]
+    unsigned long long* totals;  // [4], zeroed: running record counts
     int* err;                    // bit 0: NaN seen
-    int64_t ntiles;
 };
 
 __device__ __forceinline__ int rk(uint64_t R, int s) { return (int)((R >> (4 * s)) & 15ull); }
@@ -77,49 +74,74 @@ __device__ __forceinline__ uint32_t key_tet(const StarTab& S, uint64_t R, int q)
     return ((uint32_t)(hi + 1) << 8) | ((uint32_t)(mid + 1) << 4) | (uint32_t)(lo + 1);
 }
 
-// minimum-key member of (me edges, mt triangles, mq tets): returns dim << 6 | slot
-__device__ __forceinline__ int pop_min(const StarTab& S, uint64_t R, uint32_t me, uint64_t mt, uint32_t mq) {
+// Triangle priority queues are kept in "key index" space: the triangle (x, a, b) with
+// local ranks hi > lo has index C(hi,2) + lo < 91, and index order == key order, so
+// popping the minimum is a find-first-set over two 64-bit words.
+__device__ __forceinline__ int tri_kidx(const StarTab& S, uint64_t R, int t) {
+    const int a = rk(R, S.tri_a[t]), b = rk(R, S.tri_b[t]);
+    const int hi = max(a, b), lo = min(a, b);
+    return (hi * (hi - 1) >> 1) + lo;
+}
+__device__ __forceinline__ int kidx_tri(const StarTab& S, uint64_t IV, int ki) {
+    const int hl = S.hl[ki];
+    return S.tri_of[rk(IV, hl >> 4)][rk(IV, hl & 15)];
+}
+__device__ __forceinline__ uint32_t kidx_key(const StarTab& S, int ki) {
+    const int hl = S.hl[ki];
+    return ((uint32_t)((hl >> 4) + 1) << 8) | ((uint32_t)((hl & 15) + 1) << 4);
+}
+struct KMask {  // 128-bit set over triangle key indices (kept in registers)
+    uint64_t lo, hi;
+};
+__device__ __forceinline__ void kset(KMask& m, int ki) {
+    if (ki < 64) m.lo |= 1ull << ki;
+    else m.hi |= 1ull << (ki - 64);
+}
+__device__ __forceinline__ void kclr(KMask& m, int ki) {
+    if (ki < 64) m.lo &= ~(1ull << ki);
+    else m.hi &= ~(1ull << (ki - 64));
+}
+__device__ __forceinline__ int kfirst(const KMask& m) {
+    if (m.lo) return __ffsll((long long)m.lo) - 1;
+    if (m.hi) return 64 + __ffsll((long long)m.hi) - 1;
+    return -1;
+}
+
+// minimum-key member of a tet slot mask: returns slot, key via *k (0xffffffff if empty)
+__device__ __forceinline__ int tet_min(const StarTab& S, uint64_t R, uint32_t mq, uint32_t* k) {
     uint32_t best = 0xffffffffu;
-    int bc = -1;
-    while (me) {
-        int s = __ffs(me) - 1;
-        me &= me - 1;
-        uint32_t k = key_edge(R, s);
-        if (k < best) { best = k; bc = 64 + s; }
-    }
-    while (mt) {
-        int t = __ffsll((long long)mt) - 1;
-        mt &= mt - 1;
-        uint32_t k = key_tri(S, R, t);
-        if (k < best) { best = k; bc = 128 + t; }
-    }
+    int bq = -1;
     while (mq) {
-        int q = __ffs(mq) - 1;
+        const int q = __ffs(mq) - 1;
         mq &= mq - 1;
-        uint32_t k = key_tet(S, R, q);
-        if (k < best) { best = k; bc = 192 + q; }
+        const uint32_t kk = key_tet(S, R, q);
+        if (kk < best) { best = kk; bq = q; }
     }
-    return bc;
+    *k = best;
+    return bq;
 }
 
 struct StarState {
     uint32_t Le, Lq;
     uint64_t Lt;
-    uint32_t cls_e, cls_q, pq0_e, pq0_q, pq1_q, crit_e, crit_q;
-    uint64_t cls_t, pq0_t, pq1_t, crit_t;
-    uint64_t tcode_lo, tcode_hi;  // 2 bits per tri slot
-    uint64_t qcode;               // 2 bits per tet slot
-    int vcode;                    // edge slot paired with x, -1 = minimum
+    uint32_t cls_e, crit_e;
+    uint32_t pq0_er;                   // PQzero edges, indexed by local rank
+    uint64_t cls_t, crit_t;            // triangle slot masks
+    KMask pq0_t, pq1_t;                // triangle queues, key-index space
+    uint32_t cls_q, crit_q, pq0_q, pq1_q;  // tetrahedron slot masks
+    uint64_t tcode_lo, tcode_hi;       // 2 bits per tri slot
+    uint64_t qcode;                    // 2 bits per tet slot
+    int vcode;                         // edge slot paired with x, -1 = minimum
 };
 
 template <int D>
-__device__ __forceinline__ void push_tris_of_edge(const StarTab& S, StarState& st, int e) {
+__device__ __forceinline__ void push_tris_of_edge(const StarTab& S, uint64_t R, StarState& st, int e) {
     uint64_t cand = S.edge_tri_mask[e] & st.Lt & ~st.cls_t;
     while (cand) {
-        int t = __ffsll((long long)cand) - 1;
+        const int t = __ffsll((long long)cand) - 1;
         cand &= cand - 1;
-        int nu = (int)(!((st.cls_e >> S.tri_a[t]) & 1u)) + (int)(!((st.cls_e >> S.tri_b[t]) & 1u));
-        if (nu == 1) st.pq1_t |= 1ull << t;
+        const int nu = (int)(!((st.cls_e >> S.tri_a[t]) & 1u)) + (int)(!((st.cls_e >> S.tri_b[t]) & 1u));
+        if (nu == 1) kset(st.pq1_t, tri_kidx(S, R, t));
     }
 }
 
@@ -128,10 +150,11 @@ __device__ __forceinline__ void push_tets_of_tri(const StarTab& S, StarState& st
     if (D < 3) return;
     uint32_t cand = S.tri_tet_mask[t] & st.Lq & ~st.cls_q;
     while (cand) {
-        int q = __ffs(cand) - 1;
+        const int q = __ffs(cand) - 1;
         cand &= cand - 1;
-        int nu = (int)(!((st.cls_t >> S.tet_tri[q][0]) & 1ull)) + (int)(!((st.cls_t >> S.tet_tri[q][1]) & 1ull)) +
-                 (int)(!((st.cls_t >> S.tet_tri[q][2]) & 1ull));
+        const int nu = (int)(!((st.cls_t >> S.tet_tri[q][0]) & 1ull)) +
+                       (int)(!((st.cls_t >> S.tet_tri[q][1]) & 1ull)) +
+                       (int)(!((st.cls_t >> S.tet_tri[q][2]) & 1ull));
         if (nu == 1) st.pq1_q |= 1u << q;
     }
 }
@@ -141,103 +164,120 @@ __device__ __forceinline__ void set_tcode(StarState& st, int t, uint64_t code) {
     else st.tcode_hi |= code << (2 * (t - 32));
 }
 
-// ProcessLowerStars on one lower star (Robins et al., as pinned in DESIGN.md Z1)
+// ProcessLowerStars on one lower star (Robins et al., as pinned in DESIGN.md Z1).
+// R: slot -> local rank, IV: local rank -> slot (4 bits each).
 template <int D>
-__device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, int delta, StarState& st) {
+__device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint64_t IV, int nlow, int delta,
+                                             StarState& st) {
     st.vcode = delta;
     st.cls_e = 1u << delta;
-    st.pq0_e = st.Le & ~st.cls_e;
-    st.pq1_t = S.edge_tri_mask[delta] & st.Lt;
+    st.pq0_er = ((1u << nlow) - 1u) & ~1u;  // every lower edge but delta (rank 0)
+    {
+        uint64_t cand = S.edge_tri_mask[delta] & st.Lt;  // cofacets of delta: one unpaired facet each
+        while (cand) {
+            const int t = __ffsll((long long)cand) - 1;
+            cand &= cand - 1;
+            kset(st.pq1_t, tri_kidx(S, R, t));
+        }
+    }
     while (true) {
-        while (st.pq1_t | st.pq1_q) {
-            const int c = pop_min(S, R, 0u, st.pq1_t, st.pq1_q);
-            const int s = c & 63;
-            if ((c >> 6) == 2) {
-                st.pq1_t &= ~(1ull << s);
+        while ((st.pq1_t.lo | st.pq1_t.hi) | st.pq1_q) {
+            const int ki = kfirst(st.pq1_t);
+            const uint32_t ktri = ki >= 0 ? kidx_key(S, ki) : 0xffffffffu;
+            uint32_t ktet = 0xffffffffu;
+            const int q = (D == 3 && st.pq1_q) ? tet_min(S, R, st.pq1_q, &ktet) : -1;
+            if (ktri < ktet) {
+                kclr(st.pq1_t, ki);
+                const int s = kidx_tri(S, IV, ki);
                 if ((st.cls_t >> s) & 1ull) continue;
                 const int a = S.tri_a[s], b = S.tri_b[s];
                 const bool ua = !((st.cls_e >> a) & 1u), ub = !((st.cls_e >> b) & 1u);
-                if (!ua && !ub) { st.pq0_t |= 1ull << s; continue; }
+                if (!ua && !ub) { kset(st.pq0_t, ki); continue; }
                 const int e = ua ? a : b;  // the unique unclassified facet
                 set_tcode(st, s, ua ? 1ull : 2ull);
                 st.cls_e |= 1u << e;
                 st.cls_t |= 1ull << s;
-                st.pq0_e &= ~(1u << e);
-                push_tets_of_tri<D>(S, st, s);  // cofacets of alpha
-                push_tris_of_edge<D>(S, st, e);  // cofacets of pair(alpha)
-            } else {
-                st.pq1_q &= ~(1u << s);
-                if ((st.cls_q >> s) & 1u) continue;
-                const int t0 = S.tet_tri[s][0], t1 = S.tet_tri[s][1], t2 = S.tet_tri[s][2];
+                st.pq0_er &= ~(1u << rk(R, e));
+                push_tets_of_tri<D>(S, st, s);      // cofacets of alpha
+                push_tris_of_edge<D>(S, R, st, e);  // cofacets of pair(alpha)
+            } else if constexpr (D == 3) {
+                st.pq1_q &= ~(1u << q);
+                if ((st.cls_q >> q) & 1u) continue;
+                const int t0 = S.tet_tri[q][0], t1 = S.tet_tri[q][1], t2 = S.tet_tri[q][2];
                 const bool u0 = !((st.cls_t >> t0) & 1ull), u1 = !((st.cls_t >> t1) & 1ull),
                            u2 = !((st.cls_t >> t2) & 1ull);
-                if (!u0 && !u1 && !u2) { st.pq0_q |= 1u << s; continue; }
+                if (!u0 && !u1 && !u2) { st.pq0_q |= 1u << q; continue; }
                 const int j = u0 ? 0 : (u1 ? 1 : 2);
                 const int tt = u0 ? t0 : (u1 ? t1 : t2);
-                st.qcode |= (uint64_t)(j + 1) << (2 * s);
+                st.qcode |= (uint64_t)(j + 1) << (2 * q);
                 st.cls_t |= 1ull << tt;
-                st.cls_q |= 1u << s;
-                st.pq0_t &= ~(1ull << tt);
+                st.cls_q |= 1u << q;
+                kclr(st.pq0_t, tri_kidx(S, R, tt));
                 push_tets_of_tri<D>(S, st, tt);
             }
         }
-        if (!(st.pq0_e | st.pq0_t | st.pq0_q)) break;
-        const int c = pop_min(S, R, st.pq0_e, st.pq0_t, st.pq0_q);
-        const int s = c & 63, dim = c >> 6;
-        if (dim == 1) {
-            st.pq0_e &= ~(1u << s);
-            if ((st.cls_e >> s) & 1u) continue;
-            st.cls_e |= 1u << s;
-            st.crit_e |= 1u << s;
-            push_tris_of_edge<D>(S, st, s);
-        } else if (dim == 2) {
-            st.pq0_t &= ~(1ull << s);
+        // PQzero: minimum over edges (rank space), triangles (key space), tets
+        const uint32_t ke = st.pq0_er ? ((uint32_t)(__ffs(st.pq0_er)) << 8) : 0xffffffffu;  // (rank+1) << 8
+        const int ki = kfirst(st.pq0_t);
+        const uint32_t kt = ki >= 0 ? kidx_key(S, ki) : 0xffffffffu;
+        uint32_t kq = 0xffffffffu;
+        const int q = (D == 3 && st.pq0_q) ? tet_min(S, R, st.pq0_q, &kq) : -1;
+        if (ke == 0xffffffffu && kt == 0xffffffffu && kq == 0xffffffffu) break;
+        if (ke < kt && ke < kq) {
+            const int r = __ffs(st.pq0_er) - 1;
+            st.pq0_er &= ~(1u << r);
+            const int e = rk(IV, r);
+            if ((st.cls_e >> e) & 1u) continue;
+            st.cls_e |= 1u << e;
+            st.crit_e |= 1u << e;
+            push_tris_of_edge<D>(S, R, st, e);
+        } else if (kt < kq) {
+            kclr(st.pq0_t, ki);
+            const int s = kidx_tri(S, IV, ki);
             if ((st.cls_t >> s) & 1ull) continue;
             st.cls_t |= 1ull << s;
             st.crit_t |= 1ull << s;
             push_tets_of_tri<D>(S, st, s);
-        } else {
-            st.pq0_q &= ~(1u << s);
-            if ((st.cls_q >> s) & 1u) continue;
-            st.cls_q |= 1u << s;
-            st.crit_q |= 1u << s;
+        } else if constexpr (D == 3) {
+            st.pq0_q &= ~(1u << q);
+            if ((st.cls_q >> q) & 1u) continue;
+            st.cls_q |= 1u << q;
+            st.crit_q |= 1u << q;
         }
     }
 }
 
 template <int D>
 __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
-    constexpr int NE = Geo<D>::NE, NT = Geo<D>::NT, NQ = Geo<D>::NQ;
+    constexpr int NE = Geo<D>::NE;
     __shared__ StarTab S;
-    __shared__ long long s_tile;
     __shared__ uint32_t sw[4][kBlock / 32 + 1];
-    __shared__ unsigned long long s_excl[4];
+    __shared__ unsigned long long s_base[4];
     {
         const int4* src = reinterpret_cast<const int4*>(A.tab);
         int4* dst = reinterpret_cast<int4*>(&S);
         for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlock) dst[i] = src[i];
     }
-    if (threadIdx.x == 0) s_tile = atomicAdd(A.tile_ctr, 1);
     __syncthreads();
-    const long long tile = s_tile;
-    const int64_t v = tile * kBlock + threadIdx.x;
+    const int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     const bool active = v < A.N;
 
     StarState st;
     st.Le = 0; st.Lq = 0; st.Lt = 0;
-    st.cls_e = st.cls_q = st.pq0_e = st.pq0_q = st.pq1_q = st.crit_e = st.crit_q = 0;
-    st.cls_t = st.pq0_t = st.pq1_t = st.crit_t = 0;
+    st.cls_e = st.crit_e = st.pq0_er = 0;
+    st.cls_t = st.crit_t = 0;
+    st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
+    st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
     st.tcode_lo = st.tcode_hi = st.qcode = 0;
     st.vcode = -1;
-    uint64_t R = 0;
+    uint64_t R = 0, IV = 0;
     bool crit_v = false;
-    int cx = 0, cy = 0, cz = 0;
     if (active) {
         const int vv = (int)v;
-        cx = vv % A.Lx;
+        const int cx = vv % A.Lx;
         const int t = vv / A.Lx;
-        cy = t % A.Ly;
-        cz = t / A.Ly;
+        const int cy = t % A.Ly;
+        const int cz = t / A.Ly;
         const int LxLy = A.Lx * A.Ly;
         const float fx = A.f[v];
         if (is_nan_bits(fx)) atomicOr(A.err, 1);
@@ -281,6 +321,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
             for (int s = 0; s < NE; s++) {
                 if ((st.Le >> s) & 1u) {
                     R |= (uint64_t)r[s] << (4 * s);
+                    IV |= (uint64_t)s << (4 * r[s]);
                     if (r[s] == 0) delta = s;
                 }
             }
@@ -301,7 +342,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
             }
             st.Lt = ta & tb;
             st.Lq = qa & qb & qc;
-            process_star<D>(S, R, delta, st);
+            process_star<D>(S, R, IV, __popc(st.Le), delta, st);
         }
         // gradient word
         if (D == 3) {
@@ -313,10 +354,9 @@ __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
             reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
         }
     }
-    (void)NT;
-    (void)NQ;
 
-    // ---- compaction of the critical cells (Alg. 2 l. 10-12)
+    // ---- critical cells (Alg. 2 l. 10-12): appended with one atomic per CTA and
+    // dimension; their order is irrelevant because C_k is sorted by key afterwards.
     uint32_t cnt[4];
     cnt[0] = crit_v ? 1u : 0u;
     cnt[1] = __popc(st.crit_e);
@@ -325,26 +365,20 @@ __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
     uint32_t loc[4], tot[4];
 #pragma unroll
     for (int k = 0; k <= D; k++) loc[k] = block_excl_sum<kBlock / 32>(cnt[k], sw[k], &tot[k]);
-    if (threadIdx.x < 32) {
-        for (int k = 0; k <= D; k++) {
-            // status words are interleaved per dimension: [k * ntiles + tile]
-            unsigned long long e = lookback_warp(A.status + (int64_t)k * A.ntiles, tile, tot[k], threadIdx.x);
-            if (threadIdx.x == 0) {
-                s_excl[k] = e;
-                if (tile == A.ntiles - 1) A.totals[k] = e + tot[k];
-            }
-        }
+    if (threadIdx.x <= D) {
+        const int k = threadIdx.x;
+        s_base[k] = tot[k] ? atomicAdd(&A.totals[k], (unsigned long long)tot[k]) : 0ull;
     }
     __syncthreads();
     if (!active || (cnt[0] | cnt[1] | cnt[2] | cnt[3]) == 0) return;
     const uint64_t rkey = (uint64_t)(uint32_t)A.rank[v] << 12;
     const int LxLy = A.Lx * A.Ly;
     if (crit_v) {
-        const int64_t p = (int64_t)s_excl[0] + loc[0];
+        const int64_t p = (int64_t)s_base[0] + loc[0];
         if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
     }
     {
-        int64_t p = (int64_t)s_excl[1] + loc[1];
+        int64_t p = (int64_t)s_base[1] + loc[1];
         uint32_t m = st.crit_e;
         while (m) {
             const int s = __ffs(m) - 1;
@@ -358,7 +392,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
         }
     }
     {
-        int64_t p = (int64_t)s_excl[2] + loc[2];
+        int64_t p = (int64_t)s_base[2] + loc[2];
         uint64_t m = st.crit_t;
         while (m) {
             const int t = __ffsll((long long)m) - 1;
@@ -372,7 +406,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
         }
     }
     if (D == 3) {
-        int64_t p = (int64_t)s_excl[3] + loc[3];
+        int64_t p = (int64_t)s_base[3] + loc[3];
         uint32_t m = st.crit_q;
         while (m) {
             const int q = __ffs(m) - 1;
@@ -392,13 +426,9 @@ __global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
 // lower neighbour; a second lower edge is critical (SURVEY App. B closed form, which
 // the oracle's generic expansion reproduces).
 __global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
-    __shared__ long long s_tile;
     __shared__ uint32_t sw[2][kBlock / 32 + 1];
-    __shared__ unsigned long long s_excl[2];
-    if (threadIdx.x == 0) s_tile = atomicAdd(A.tile_ctr, 1);
-    __syncthreads();
-    const long long tile = s_tile;
-    const int64_t v = tile * kBlock + threadIdx.x;
+    __shared__ unsigned long long s_base[2];
+    const int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     const bool active = v < A.N;
     bool crit_v = false, crit_e = false;
     int crit_slot = 0;
@@ -422,28 +452,22 @@ __global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
         }
         reinterpret_cast<uint8_t*>(A.grad)[v] = code;
     }
-    uint32_t cnt0 = crit_v ? 1u : 0u, cnt1 = crit_e ? 1u : 0u;
     uint32_t tot0, tot1;
-    const uint32_t loc0 = block_excl_sum<kBlock / 32>(cnt0, sw[0], &tot0);
-    const uint32_t loc1 = block_excl_sum<kBlock / 32>(cnt1, sw[1], &tot1);
-    if (threadIdx.x < 32) {
-        unsigned long long e0 = lookback_warp(A.status, tile, tot0, threadIdx.x);
-        unsigned long long e1 = lookback_warp(A.status + A.ntiles, tile, tot1, threadIdx.x);
-        if (threadIdx.x == 0) {
-            s_excl[0] = e0;
-            s_excl[1] = e1;
-            if (tile == A.ntiles - 1) { A.totals[0] = e0 + tot0; A.totals[1] = e1 + tot1; }
-        }
+    const uint32_t loc0 = block_excl_sum<kBlock / 32>(crit_v ? 1u : 0u, sw[0], &tot0);
+    const uint32_t loc1 = block_excl_sum<kBlock / 32>(crit_e ? 1u : 0u, sw[1], &tot1);
+    if (threadIdx.x < 2) {
+        const uint32_t t = threadIdx.x ? tot1 : tot0;
+        s_base[threadIdx.x] = t ? atomicAdd(&A.totals[threadIdx.x], (unsigned long long)t) : 0ull;
     }
     __syncthreads();
     if (!active || !(crit_v || crit_e)) return;
     const uint64_t rkey = (uint64_t)(uint32_t)A.rank[v] << 12;
     if (crit_v) {
-        const int64_t p = (int64_t)s_excl[0] + loc0;
+        const int64_t p = (int64_t)s_base[0] + loc0;
         if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
     }
     if (crit_e) {
-        const int64_t p = (int64_t)s_excl[1] + loc1;
+        const int64_t p = (int64_t)s_base[1] + loc1;
         if (p < A.cap[1]) {
             A.crit_id[1][p] = crit_slot == 0 ? v - 1 : v;  // edge (a, a+1) has id a
             A.crit_key[1][p] = rkey | (2u << 8);            // the higher of the two lower edges

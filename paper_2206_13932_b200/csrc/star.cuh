@@ -33,6 +33,8 @@ struct alignas(16) StarTab {
     uint32_t tri_tet_mask[kMaxNT];    // tet slots containing the tri
     uint64_t tri_amask[kMaxNE], tri_bmask[kMaxNE];  // tri slots whose a (b) end is slot s
     uint32_t tet_amask[kMaxNE], tet_bmask[kMaxNE], tet_cmask[kMaxNE];
+    uint8_t tri_of[kMaxNE][kMaxNE];   // (slot a, slot b) -> tri slot (255: not a triangle)
+    uint8_t hl[96];                   // triangle key index C(hi,2)+lo -> hi << 4 | lo
     // anchored ids of star cells: anchor offset from x and chain index
     int8_t e_anc[kMaxNE][3];  uint8_t e_k[kMaxNE];
     int8_t t_anc[kMaxNT][3];  uint8_t t_k[kMaxNT];

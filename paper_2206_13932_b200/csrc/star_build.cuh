@@ -126,6 +126,13 @@ inline bool build_star_tables(int ndim, const int64_t L[3], StarTab* T) {
                 nt++;
             }
     T->nt = nt;
+    std::memset(T->tri_of, 255, sizeof(T->tri_of));
+    for (int t = 0; t < nt; t++) {
+        T->tri_of[T->tri_a[t]][T->tri_b[t]] = (uint8_t)t;
+        T->tri_of[T->tri_b[t]][T->tri_a[t]] = (uint8_t)t;
+    }
+    for (int hi = 1; hi < kMaxNE; hi++)
+        for (int lo = 0; lo < hi; lo++) T->hl[hi * (hi - 1) / 2 + lo] = (uint8_t)(hi << 4 | lo);
     int nq = 0;
     for (int a = 0; a < T->ne; a++)
         for (int b = a + 1; b < T->ne; b++)
