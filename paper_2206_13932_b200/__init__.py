@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdms.so")
+LIB_PATH = os.environ.get("DMS_LIB") or os.path.join(_HERE, "libdms.so")  # DMS_LIB: A/B experiments
 
 PAIR_DTYPE = np.dtype(
     [

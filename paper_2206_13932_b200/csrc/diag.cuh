@@ -14,6 +14,8 @@
 //   its paired facet -> the other cofacet of that facet), a virtual maximum on the
 //   boundary (exact mode), union-find in decreasing order, the virtual maximum oldest.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "star.cuh"
 
@@ -328,6 +330,141 @@ __global__ void k_flag_undecided(const int32_t* out, int64_t m, uint32_t* flags)
 __global__ void k_gather_undecided(const int32_t* out, int64_t m, const uint32_t* pos, int32_t* list) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m && out[i] == -2) list[pos[i]] = (int32_t)i;
+}
+
+// All union-find rounds in one cooperative launch (grid-wide barriers between the
+// phases, no host round trip), then block 0 sorts the (few) undecided arcs and runs
+// the sequential elder-rule union-find over them in processing order.
+constexpr int kUFTail = 2048;
+
+struct UFArgs {
+    const int32_t* arc_a;
+    const int32_t* arc_b;
+    int32_t* parent;
+    uint32_t* best;
+    int32_t* ra;
+    int32_t* rb;
+    int32_t* out;
+    int32_t* live0;
+    int32_t* live1;
+    int* nlive;   // [2]
+    int* status;  // [1]: -1 finished, else the number of undecided arcs left in live[cur]
+    int* cur_out; // [1]
+    bool older_is_smaller;
+    int max_rounds;
+};
+
+__device__ __forceinline__ int ld_cg_int(const int* p) { return __ldcg(p); }
+
+__global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t s_list[kUFTail];
+    const int stride = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    int cur = 0;
+    for (int round = 0; round < U.max_rounds; round++) {
+        int32_t* live = cur ? U.live1 : U.live0;
+        int32_t* nxt = cur ? U.live0 : U.live1;
+        const int n = ld_cg_int(&U.nlive[cur]);
+        if (n <= kUFTail) break;
+        // phase 1: roots, cycle arcs, lightest arc of every root
+        for (int idx = gtid; idx < n; idx += stride) {
+            const int32_t i = live[idx];
+            const int32_t a = uf_find(U.parent, U.arc_a[i]);
+            const int32_t b = uf_find(U.parent, U.arc_b[i]);
+            U.ra[i] = a;
+            U.rb[i] = b;
+            if (a == b) { U.out[i] = -1; continue; }
+            atomicMin(&U.best[a], (uint32_t)i);
+            atomicMin(&U.best[b], (uint32_t)i);
+        }
+        if (gtid == 0) U.nlive[cur ^ 1] = 0;
+        grid.sync();
+        // phase 2: mutual minimum, or a younger root dying at its lightest arc
+        for (int idx = gtid; idx < n; idx += stride) {
+            const int32_t i = live[idx];
+            if (U.out[i] != -2) continue;
+            const int32_t a = U.ra[i], b = U.rb[i];
+            const bool ma = __ldcg(&U.best[a]) == (uint32_t)i, mb = __ldcg(&U.best[b]) == (uint32_t)i;
+            const bool a_older = U.older_is_smaller ? (a < b) : (a > b);
+            if (ma && mb) {
+                const int32_t young = a_older ? b : a, old = a_older ? a : b;
+                U.parent[young] = old;
+                U.out[i] = young;
+            } else if (ma && !a_older) {
+                U.parent[a] = b;
+                U.out[i] = a;
+            } else if (mb && a_older) {
+                U.parent[b] = a;
+                U.out[i] = b;
+            }
+        }
+        grid.sync();
+        // phase 3: reset the candidates, compact the undecided arcs
+        for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+            const int idx = base + threadIdx.x;
+            bool keep = false;
+            int32_t i = 0;
+            if (idx < n) {
+                i = live[idx];
+                const int32_t o = U.out[i];
+                if (o != -1) {
+                    U.best[U.ra[i]] = 0xffffffffu;
+                    U.best[U.rb[i]] = 0xffffffffu;
+                }
+                keep = o == -2;
+            }
+            const unsigned mk = __ballot_sync(0xffffffffu, keep);
+            int bp = 0;
+            if (lane == 0 && mk) bp = atomicAdd(&U.nlive[cur ^ 1], __popc(mk));
+            bp = __shfl_sync(0xffffffffu, bp, 0);
+            if (keep) nxt[bp + __popc(mk & lanemask_lt())] = i;
+        }
+        grid.sync();
+        cur ^= 1;
+    }
+    if (blockIdx.x != 0) return;
+    const int n = ld_cg_int(&U.nlive[cur]);
+    if (threadIdx.x == 0) *U.cur_out = cur;
+    if (n > kUFTail) {  // did not converge within max_rounds: the host finishes the tail
+        if (threadIdx.x == 0) *U.status = n;
+        return;
+    }
+    const int32_t* live = cur ? U.live1 : U.live0;
+    int p2 = 1;
+    while (p2 < n) p2 <<= 1;
+    for (int j = threadIdx.x; j < p2; j += blockDim.x) s_list[j] = j < n ? live[j] : 0x7fffffff;
+    __syncthreads();
+    // bitonic sort (ascending processing order)
+    for (int k = 2; k <= p2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < p2; t += blockDim.x) {
+                const int o = t ^ j;
+                if (o > t) {
+                    const int32_t x = s_list[t], y = s_list[o];
+                    const bool up = (t & k) == 0;
+                    if ((x > y) == up) { s_list[t] = y; s_list[o] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < n; j++) {
+            const int32_t i = s_list[j];
+            int32_t a = U.arc_a[i], b = U.arc_b[i];
+            while (U.parent[a] != a) a = U.parent[a];
+            while (U.parent[b] != b) b = U.parent[b];
+            if (a == b) { U.out[i] = -1; continue; }
+            const bool a_older = U.older_is_smaller ? (a < b) : (a > b);
+            const int32_t young = a_older ? b : a, old = a_older ? a : b;
+            U.parent[young] = old;
+            U.out[i] = young;
+        }
+        *U.status = -1;
+    }
 }
 
 // sequential Kruskal over the undecided arcs in processing order (the result equals

@@ -219,7 +219,7 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
             cudaFree(*p);
             CU(dalloc(p, arcs));
         }
-        if (!u.nlive) CU(dalloc(&u.nlive, 2));
+        if (!u.nlive) CU(dalloc(&u.nlive, 4));
         for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
         u.cap_arcs = arcs;
     }
@@ -280,9 +280,25 @@ dms_status launch_gradient(dms_ctx* c) {
     A.totals = c->totals;
     A.err = c->err;
     StageTimer tm(c, 5);
-    if (c->ndim == 3) k_gradient<3><<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
-    else if (c->ndim == 2) k_gradient<2><<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
-    else k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
+    if (c->ndim >= 2) {
+        // persistent grid: as many CTAs as fit on the device, each warp strides over
+        // 32-vertex chunks
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (c->ndim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gradient<3>, kBlockG, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gradient<2>, kBlockG, 0);
+        const int64_t need = ceil_div(ceil_div(c->N, 32), kBlockG / 32);
+#ifndef DMS_PERSISTENT
+#define DMS_PERSISTENT 0
+#endif
+        const unsigned grid = (unsigned)std::max<int64_t>(
+            1, DMS_PERSISTENT ? std::min<int64_t>(need, (int64_t)sms * std::max(per, 1)) : need);
+        if (c->ndim == 3) k_gradient<3><<<grid, kBlockG, 0, c->st>>>(A);
+        else k_gradient<2><<<grid, kBlockG, 0, c->st>>>(A);
+    } else {
+        k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
+    }
     c->launches++;
     CU(cudaGetLastError());
     return DMS_OK;
@@ -346,46 +362,46 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older
     k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.out, u.list, m);
     c->launches++;
     if (m == 0) return DMS_OK;
-    int hm[2] = {(int)m, 0};
+    int hm[4] = {(int)m, 0, 0, 0};  // nlive[2], status, cur
     CU(cudaMemcpyAsync(u.nlive, hm, sizeof hm, cudaMemcpyHostToDevice, c->st));
-    const unsigned gr = (unsigned)std::min<int64_t>(grid_for(m), 148 * 8);
-    int32_t* live[2] = {u.list, u.live2};
-    int cur = 0;
-    int64_t rem = m;
-    for (int iter = 0; iter < 200000; iter++) {
-        const int batch = rem > 100000 ? 2 : 8;
-        for (int r = 0; r < batch; r++) {
-            const int nxt = cur ^ 1;
-            CU(cudaMemsetAsync(u.nlive + nxt, 0, sizeof(int), c->st));
-            k_uf_round1<<<gr, kBlock, 0, c->st>>>(u.arc_a, u.arc_b, live[cur], u.nlive + cur, u.parent, u.best, u.ra,
-                                                 u.rb, u.out);
-            k_uf_round2<<<gr, kBlock, 0, c->st>>>(live[cur], u.nlive + cur, u.parent, u.best, u.ra, u.rb, u.out,
-                                                 older_is_smaller);
-            k_uf_round3<<<gr, kBlock, 0, c->st>>>(live[cur], u.nlive + cur, u.best, u.ra, u.rb, u.out, live[nxt],
-                                                 u.nlive + nxt);
-            c->launches += 3;
-            cur = nxt;
-        }
-        int h = 0;
-        CU(cudaMemcpyAsync(c->h_pinned, u.nlive + cur, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-        CU(cudaStreamSynchronize(c->st));
-        std::memcpy(&h, c->h_pinned, sizeof(int));
-        const int64_t prev = rem;
-        rem = h;
-        if (rem == 0) return DMS_OK;
-        if (rem <= 2048 || (rem <= 65536 && rem * 8 > prev * 7)) {
-            // sequential tail over the undecided arcs, in processing order
-            k_flag_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags);
-            scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
-            k_gather_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, u.list);
-            k_uf_tail<<<1, 32, 0, c->st>>>(u.arc_a, u.arc_b, u.list, u.pos + (m - 1), u.flags + (m - 1), m, u.parent,
-                                          u.out, older_is_smaller);
-            c->launches += 3;
-            CU(cudaGetLastError());
-            return DMS_OK;
-        }
-    }
-    return fail(c, DMS_ERR_INVARIANT, "union-find did not converge");
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_uf_coop, kBlock, 0);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(m), (int64_t)sms * std::max(per, 1)));
+    UFArgs U;
+    U.arc_a = u.arc_a;
+    U.arc_b = u.arc_b;
+    U.parent = u.parent;
+    U.best = u.best;
+    U.ra = u.ra;
+    U.rb = u.rb;
+    U.out = u.out;
+    U.live0 = u.list;
+    U.live1 = u.live2;
+    U.nlive = u.nlive;
+    U.status = u.nlive + 2;
+    U.cur_out = u.nlive + 3;
+    U.older_is_smaller = older_is_smaller;
+    U.max_rounds = 4096;
+    void* args[] = {&U};
+    CU(cudaLaunchCooperativeKernel((void*)k_uf_coop, grid, kBlock, args, 0, c->st));
+    c->launches++;
+    int st = -1;
+    CU(cudaMemcpyAsync(c->h_pinned, u.nlive + 2, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    std::memcpy(&st, c->h_pinned, sizeof(int));
+    if (st < 0) return DMS_OK;
+    // pathological input (no convergence within max_rounds): sequential tail over
+    // the undecided arcs in processing order
+    k_flag_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags);
+    scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
+    k_gather_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, u.list);
+    k_uf_tail<<<1, 32, 0, c->st>>>(u.arc_a, u.arc_b, u.list, u.pos + (m - 1), u.flags + (m - 1), m, u.parent, u.out,
+                                  older_is_smaller);
+    c->launches += 3;
+    CU(cudaGetLastError());
+    return DMS_OK;
 }
 
 // stable compaction count: pos = exclusive scan of flags; returns the total

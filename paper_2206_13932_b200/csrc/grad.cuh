@@ -107,14 +107,36 @@ __device__ __forceinline__ int kfirst(const KMask& m) {
     return -1;
 }
 
+#ifndef DMS_KEYCACHE
+#define DMS_KEYCACHE 1
+#endif
+constexpr int kBlockG = 128;  // threads per CTA of the (persistent) gradient kernel
+
+// Per-thread key caches in shared memory, laid out [cell][thread] (bank-conflict
+// free): tri slot -> key index, tet slot -> 12-bit key.  Filled once per vertex.
+struct KeyCache {
+    uint8_t* tki;   // tki[t * kBlockG]
+    uint16_t* qk;   // qk[q * kBlockG]
+    uint64_t R;
+    const StarTab* S;
+    __device__ __forceinline__ int tri(int t) const {
+        if (DMS_KEYCACHE) return tki[t * kBlockG];
+        return tri_kidx(*S, R, t);
+    }
+    __device__ __forceinline__ uint32_t tet(int q) const {
+        if (DMS_KEYCACHE) return qk[q * kBlockG];
+        return key_tet(*S, R, q);
+    }
+};
+
 // minimum-key member of a tet slot mask: returns slot, key via *k (0xffffffff if empty)
-__device__ __forceinline__ int tet_min(const StarTab& S, uint64_t R, uint32_t mq, uint32_t* k) {
+__device__ __forceinline__ int tet_min(const KeyCache& C, uint32_t mq, uint32_t* k) {
     uint32_t best = 0xffffffffu;
     int bq = -1;
     while (mq) {
         const int q = __ffs(mq) - 1;
         mq &= mq - 1;
-        const uint32_t kk = key_tet(S, R, q);
+        const uint32_t kk = C.tet(q);
         if (kk < best) { best = kk; bq = q; }
     }
     *k = best;
@@ -135,13 +157,13 @@ struct StarState {
 };
 
 template <int D>
-__device__ __forceinline__ void push_tris_of_edge(const StarTab& S, uint64_t R, StarState& st, int e) {
+__device__ __forceinline__ void push_tris_of_edge(const StarTab& S, const KeyCache& C, StarState& st, int e) {
     uint64_t cand = S.edge_tri_mask[e] & st.Lt & ~st.cls_t;
     while (cand) {
         const int t = __ffsll((long long)cand) - 1;
         cand &= cand - 1;
         const int nu = (int)(!((st.cls_e >> S.tri_a[t]) & 1u)) + (int)(!((st.cls_e >> S.tri_b[t]) & 1u));
-        if (nu == 1) kset(st.pq1_t, tri_kidx(S, R, t));
+        if (nu == 1) kset(st.pq1_t, C.tri(t));
     }
 }
 
@@ -167,8 +189,8 @@ __device__ __forceinline__ void set_tcode(StarState& st, int t, uint64_t code) {
 // ProcessLowerStars on one lower star (Robins et al., as pinned in DESIGN.md Z1).
 // R: slot -> local rank, IV: local rank -> slot (4 bits each).
 template <int D>
-__device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint64_t IV, int nlow, int delta,
-                                             StarState& st) {
+__device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C, uint64_t R, uint64_t IV, int nlow,
+                                             int delta, StarState& st) {
     st.vcode = delta;
     st.cls_e = 1u << delta;
     st.pq0_er = ((1u << nlow) - 1u) & ~1u;  // every lower edge but delta (rank 0)
@@ -177,7 +199,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint6
         while (cand) {
             const int t = __ffsll((long long)cand) - 1;
             cand &= cand - 1;
-            kset(st.pq1_t, tri_kidx(S, R, t));
+            kset(st.pq1_t, C.tri(t));
         }
     }
     while (true) {
@@ -185,7 +207,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint6
             const int ki = kfirst(st.pq1_t);
             const uint32_t ktri = ki >= 0 ? kidx_key(S, ki) : 0xffffffffu;
             uint32_t ktet = 0xffffffffu;
-            const int q = (D == 3 && st.pq1_q) ? tet_min(S, R, st.pq1_q, &ktet) : -1;
+            const int q = (D == 3 && st.pq1_q) ? tet_min(C, st.pq1_q, &ktet) : -1;
             if (ktri < ktet) {
                 kclr(st.pq1_t, ki);
                 const int s = kidx_tri(S, IV, ki);
@@ -199,7 +221,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint6
                 st.cls_t |= 1ull << s;
                 st.pq0_er &= ~(1u << rk(R, e));
                 push_tets_of_tri<D>(S, st, s);      // cofacets of alpha
-                push_tris_of_edge<D>(S, R, st, e);  // cofacets of pair(alpha)
+                push_tris_of_edge<D>(S, C, st, e);  // cofacets of pair(alpha)
             } else if constexpr (D == 3) {
                 st.pq1_q &= ~(1u << q);
                 if ((st.cls_q >> q) & 1u) continue;
@@ -212,7 +234,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint6
                 st.qcode |= (uint64_t)(j + 1) << (2 * q);
                 st.cls_t |= 1ull << tt;
                 st.cls_q |= 1u << q;
-                kclr(st.pq0_t, tri_kidx(S, R, tt));
+                kclr(st.pq0_t, C.tri(tt));
                 push_tets_of_tri<D>(S, st, tt);
             }
         }
@@ -221,7 +243,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint6
         const int ki = kfirst(st.pq0_t);
         const uint32_t kt = ki >= 0 ? kidx_key(S, ki) : 0xffffffffu;
         uint32_t kq = 0xffffffffu;
-        const int q = (D == 3 && st.pq0_q) ? tet_min(S, R, st.pq0_q, &kq) : -1;
+        const int q = (D == 3 && st.pq0_q) ? tet_min(C, st.pq0_q, &kq) : -1;
         if (ke == 0xffffffffu && kt == 0xffffffffu && kq == 0xffffffffu) break;
         if (ke < kt && ke < kq) {
             const int r = __ffs(st.pq0_er) - 1;
@@ -230,7 +252,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint6
             if ((st.cls_e >> e) & 1u) continue;
             st.cls_e |= 1u << e;
             st.crit_e |= 1u << e;
-            push_tris_of_edge<D>(S, R, st, e);
+            push_tris_of_edge<D>(S, C, st, e);
         } else if (kt < kq) {
             kclr(st.pq0_t, ki);
             const int s = kidx_tri(S, IV, ki);
@@ -247,176 +269,205 @@ __device__ __forceinline__ void process_star(const StarTab& S, uint64_t R, uint6
     }
 }
 
+// warp-level append of `cnt` records per lane: returns this lane's first position
+__device__ __forceinline__ int64_t warp_append(unsigned long long* total, uint32_t cnt) {
+    const int lane = threadIdx.x & 31;
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && tot) base = atomicAdd(total, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    return (int64_t)base + (inc - cnt);
+}
+
+// Persistent kernel: each warp takes 32 consecutive vertices at a time (one per lane).
 template <int D>
-__global__ void __launch_bounds__(kBlock) k_gradient(GradArgs A) {
+__global__ void __launch_bounds__(kBlockG) k_gradient(GradArgs A) {
     constexpr int NE = Geo<D>::NE;
     __shared__ StarTab S;
-    __shared__ uint32_t sw[4][kBlock / 32 + 1];
-    __shared__ unsigned long long s_base[4];
+    __shared__ uint8_t s_tki[kMaxNT * kBlockG];
+    __shared__ uint16_t s_qk[(D == 3 ? kMaxNQ : 1) * kBlockG];
     {
         const int4* src = reinterpret_cast<const int4*>(A.tab);
         int4* dst = reinterpret_cast<int4*>(&S);
-        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlock) dst[i] = src[i];
+        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlockG) dst[i] = src[i];
     }
     __syncthreads();
-    const int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    const bool active = v < A.N;
-
-    StarState st;
-    st.Le = 0; st.Lq = 0; st.Lt = 0;
-    st.cls_e = st.crit_e = st.pq0_er = 0;
-    st.cls_t = st.crit_t = 0;
-    st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
-    st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
-    st.tcode_lo = st.tcode_hi = st.qcode = 0;
-    st.vcode = -1;
-    uint64_t R = 0, IV = 0;
-    bool crit_v = false;
-    if (active) {
-        const int vv = (int)v;
-        const int cx = vv % A.Lx;
-        const int t = vv / A.Lx;
-        const int cy = t % A.Ly;
-        const int cz = t / A.Ly;
-        const int LxLy = A.Lx * A.Ly;
-        const float fx = A.f[v];
-        if (is_nan_bits(fx)) atomicOr(A.err, 1);
-        const uint32_t ox = ord_of(fx);
-        uint32_t o[NE];
-#pragma unroll
-        for (int s = 0; s < NE; s++) {
-            const int dx = off_c<D>(s, 0), dy = off_c<D>(s, 1), dz = off_c<D>(s, 2);
-            bool in = true;
-            if (dx < 0) in &= cx > 0;
-            if (dx > 0) in &= cx < A.Lx - 1;
-            if (dy < 0) in &= cy > 0;
-            if (dy > 0) in &= cy < A.Ly - 1;
-            if (dz < 0) in &= cz > 0;
-            if (dz > 0) in &= cz < A.Lz - 1;
-            o[s] = 0xffffffffu;
-            if (in) {
-                const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
-                const bool lower = (os < ox) || (os == ox && s < NE / 2);
-                if (lower) { o[s] = os; st.Le |= 1u << s; }
-            }
-        }
-        if (st.Le == 0) {
-            crit_v = true;
-        } else {
-            // local ranks among the lower neighbours (non-lower ones hold the 0xffffffff
-            // sentinel, larger than any ordered float, so they never count)
-            int r[NE];
-#pragma unroll
-            for (int s = 0; s < NE; s++) r[s] = 0;
-#pragma unroll
-            for (int s = 0; s < NE; s++)
-#pragma unroll
-                for (int u = s + 1; u < NE; u++) {
-                    const bool s_lt_u = o[s] <= o[u];  // equal values: the smaller slot first
-                    r[u] += s_lt_u ? 1 : 0;
-                    r[s] += s_lt_u ? 0 : 1;
-                }
-            int delta = 0;
+    KeyCache C;
+    C.tki = s_tki + threadIdx.x;
+    C.qk = s_qk + threadIdx.x;
+    C.S = &S;
+    C.R = 0;
+    const int64_t nchunks = (A.N + 31) >> 5;
+    const int64_t nwarps = (int64_t)gridDim.x * (kBlockG / 32);
+    const int LxLy = A.Lx * A.Ly;
+    for (int64_t chunk = ((int64_t)blockIdx.x * kBlockG + threadIdx.x) >> 5; chunk < nchunks; chunk += nwarps) {
+        const int64_t v = chunk * 32 + (threadIdx.x & 31);
+        const bool active = v < A.N;
+        StarState st;
+        st.Le = 0; st.Lq = 0; st.Lt = 0;
+        st.cls_e = st.crit_e = st.pq0_er = 0;
+        st.cls_t = st.crit_t = 0;
+        st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
+        st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
+        st.tcode_lo = st.tcode_hi = st.qcode = 0;
+        st.vcode = -1;
+        uint64_t R = 0, IV = 0;
+        bool crit_v = false;
+        if (active) {
+            const int vv = (int)v;
+            const int cx = vv % A.Lx;
+            const int t = vv / A.Lx;
+            const int cy = t % A.Ly;
+            const int cz = t / A.Ly;
+            const float fx = A.f[v];
+            if (is_nan_bits(fx)) atomicOr(A.err, 1);
+            const uint32_t ox = ord_of(fx);
+            uint32_t o[NE];
 #pragma unroll
             for (int s = 0; s < NE; s++) {
-                if ((st.Le >> s) & 1u) {
-                    R |= (uint64_t)r[s] << (4 * s);
-                    IV |= (uint64_t)s << (4 * r[s]);
-                    if (r[s] == 0) delta = s;
+                const int dx = off_c<D>(s, 0), dy = off_c<D>(s, 1), dz = off_c<D>(s, 2);
+                bool in = true;
+                if (dx < 0) in &= cx > 0;
+                if (dx > 0) in &= cx < A.Lx - 1;
+                if (dy < 0) in &= cy > 0;
+                if (dy > 0) in &= cy < A.Ly - 1;
+                if (dz < 0) in &= cz > 0;
+                if (dz > 0) in &= cz < A.Lz - 1;
+                o[s] = 0xffffffffu;
+                if (in) {
+                    const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
+                    const bool lower = (os < ox) || (os == ox && s < NE / 2);
+                    if (lower) { o[s] = os; st.Le |= 1u << s; }
                 }
             }
-            // lower triangles / tets: all their link vertices lower
-            uint64_t ta = 0, tb = 0;
-            uint32_t qa = 0, qb = 0, qc = 0;
-            uint32_t le = st.Le;
-            while (le) {
-                const int s = __ffs(le) - 1;
-                le &= le - 1;
-                ta |= S.tri_amask[s];
-                tb |= S.tri_bmask[s];
-                if (D == 3) {
-                    qa |= S.tet_amask[s];
-                    qb |= S.tet_bmask[s];
-                    qc |= S.tet_cmask[s];
-                }
-            }
-            st.Lt = ta & tb;
-            st.Lq = qa & qb & qc;
-            process_star<D>(S, R, IV, __popc(st.Le), delta, st);
-        }
-        // gradient word
-        if (D == 3) {
-            const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
-            const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
-            reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
-        } else {
-            const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
-            reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
-        }
-    }
-
-    // ---- critical cells (Alg. 2 l. 10-12): appended with one atomic per CTA and
-    // dimension; their order is irrelevant because C_k is sorted by key afterwards.
-    uint32_t cnt[4];
-    cnt[0] = crit_v ? 1u : 0u;
-    cnt[1] = __popc(st.crit_e);
-    cnt[2] = __popcll(st.crit_t);
-    cnt[3] = __popc(st.crit_q);
-    uint32_t loc[4], tot[4];
+            if (st.Le == 0) {
+                crit_v = true;
+            } else {
+                // local ranks among the lower neighbours (non-lower ones hold the 0xffffffff
+                // sentinel, larger than any ordered float, so they never count)
+                int r[NE];
 #pragma unroll
-    for (int k = 0; k <= D; k++) loc[k] = block_excl_sum<kBlock / 32>(cnt[k], sw[k], &tot[k]);
-    if (threadIdx.x <= D) {
-        const int k = threadIdx.x;
-        s_base[k] = tot[k] ? atomicAdd(&A.totals[k], (unsigned long long)tot[k]) : 0ull;
-    }
-    __syncthreads();
-    if (!active || (cnt[0] | cnt[1] | cnt[2] | cnt[3]) == 0) return;
-    const uint64_t rkey = (uint64_t)(uint32_t)A.rank[v] << 12;
-    const int LxLy = A.Lx * A.Ly;
-    if (crit_v) {
-        const int64_t p = (int64_t)s_base[0] + loc[0];
-        if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
-    }
-    {
-        int64_t p = (int64_t)s_base[1] + loc[1];
-        uint32_t m = st.crit_e;
-        while (m) {
-            const int s = __ffs(m) - 1;
-            m &= m - 1;
-            if (p < A.cap[1]) {
-                const int64_t anc = v + S.e_anc[s][0] + A.Lx * S.e_anc[s][1] + LxLy * S.e_anc[s][2];
-                A.crit_id[1][p] = A.ncell[1] * anc + S.e_k[s];
-                A.crit_key[1][p] = rkey | key_edge(R, s);
+                for (int s = 0; s < NE; s++) r[s] = 0;
+#pragma unroll
+                for (int s = 0; s < NE; s++)
+#pragma unroll
+                    for (int u = s + 1; u < NE; u++) {
+                        const bool s_lt_u = o[s] <= o[u];  // equal values: the smaller slot first
+                        r[u] += s_lt_u ? 1 : 0;
+                        r[s] += s_lt_u ? 0 : 1;
+                    }
+                int delta = 0;
+#pragma unroll
+                for (int s = 0; s < NE; s++) {
+                    if ((st.Le >> s) & 1u) {
+                        R |= (uint64_t)r[s] << (4 * s);
+                        IV |= (uint64_t)s << (4 * r[s]);
+                        if (r[s] == 0) delta = s;
+                    }
+                }
+                // lower triangles / tets: all their link vertices lower
+                uint64_t ta = 0, tb = 0;
+                uint32_t qa = 0, qb = 0, qc = 0;
+                uint32_t le = st.Le;
+                while (le) {
+                    const int s = __ffs(le) - 1;
+                    le &= le - 1;
+                    ta |= S.tri_amask[s];
+                    tb |= S.tri_bmask[s];
+                    if (D == 3) {
+                        qa |= S.tet_amask[s];
+                        qb |= S.tet_bmask[s];
+                        qc |= S.tet_cmask[s];
+                    }
+                }
+                st.Lt = ta & tb;
+                st.Lq = qa & qb & qc;
+                if (DMS_KEYCACHE) {
+                    uint64_t m = st.Lt;
+                    while (m) {
+                        const int tt = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        C.tki[tt * kBlockG] = (uint8_t)tri_kidx(S, R, tt);
+                    }
+                    if (D == 3) {
+                        uint32_t mq = st.Lq;
+                        while (mq) {
+                            const int q = __ffs(mq) - 1;
+                            mq &= mq - 1;
+                            C.qk[q * kBlockG] = (uint16_t)key_tet(S, R, q);
+                        }
+                    }
+                }
+                C.R = R;
+                process_star<D>(S, C, R, IV, __popc(st.Le), delta, st);
             }
-            p++;
+            // gradient word
+            if (D == 3) {
+                const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
+                const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
+                reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
+            } else {
+                const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
+                reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
+            }
         }
-    }
-    {
-        int64_t p = (int64_t)s_base[2] + loc[2];
-        uint64_t m = st.crit_t;
-        while (m) {
-            const int t = __ffsll((long long)m) - 1;
-            m &= m - 1;
-            if (p < A.cap[2]) {
-                const int64_t anc = v + S.t_anc[t][0] + A.Lx * S.t_anc[t][1] + LxLy * S.t_anc[t][2];
-                A.crit_id[2][p] = A.ncell[2] * anc + S.t_k[t];
-                A.crit_key[2][p] = rkey | key_tri(S, R, t);
-            }
-            p++;
+        // ---- critical cells (Alg. 2 l. 10-12), appended with one atomic per warp and
+        // dimension; their order is irrelevant because C_k is sorted by key afterwards.
+        const uint32_t c0 = crit_v ? 1u : 0u, c1 = __popc(st.crit_e), c2 = __popcll(st.crit_t),
+                       c3 = __popc(st.crit_q);
+        if (!__any_sync(0xffffffffu, (c0 | c1 | c2 | c3) != 0u)) continue;
+        const uint64_t rkey = (active && (c0 | c1 | c2 | c3)) ? ((uint64_t)(uint32_t)A.rank[v] << 12) : 0ull;
+        {
+            const int64_t p = warp_append(&A.totals[0], c0);
+            if (c0 && p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
         }
-    }
-    if (D == 3) {
-        int64_t p = (int64_t)s_base[3] + loc[3];
-        uint32_t m = st.crit_q;
-        while (m) {
-            const int q = __ffs(m) - 1;
-            m &= m - 1;
-            if (p < A.cap[3]) {
-                const int64_t anc = v + S.q_anc[q][0] + A.Lx * S.q_anc[q][1] + LxLy * S.q_anc[q][2];
-                A.crit_id[3][p] = A.ncell[3] * anc + S.q_k[q];
-                A.crit_key[3][p] = rkey | key_tet(S, R, q);
+        {
+            int64_t p = warp_append(&A.totals[1], c1);
+            uint32_t m = st.crit_e;
+            while (m) {
+                const int s = __ffs(m) - 1;
+                m &= m - 1;
+                if (p < A.cap[1]) {
+                    const int64_t anc = v + S.e_anc[s][0] + A.Lx * S.e_anc[s][1] + LxLy * S.e_anc[s][2];
+                    A.crit_id[1][p] = A.ncell[1] * anc + S.e_k[s];
+                    A.crit_key[1][p] = rkey | key_edge(R, s);
+                }
+                p++;
             }
-            p++;
+        }
+        {
+            int64_t p = warp_append(&A.totals[2], c2);
+            uint64_t m = st.crit_t;
+            while (m) {
+                const int t = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                if (p < A.cap[2]) {
+                    const int64_t anc = v + S.t_anc[t][0] + A.Lx * S.t_anc[t][1] + LxLy * S.t_anc[t][2];
+                    A.crit_id[2][p] = A.ncell[2] * anc + S.t_k[t];
+                    A.crit_key[2][p] = rkey | key_tri(S, R, t);
+                }
+                p++;
+            }
+        }
+        if (D == 3) {
+            int64_t p = warp_append(&A.totals[3], c3);
+            uint32_t m = st.crit_q;
+            while (m) {
+                const int q = __ffs(m) - 1;
+                m &= m - 1;
+                if (p < A.cap[3]) {
+                    const int64_t anc = v + S.q_anc[q][0] + A.Lx * S.q_anc[q][1] + LxLy * S.q_anc[q][2];
+                    A.crit_id[3][p] = A.ncell[3] * anc + S.q_k[q];
+                    A.crit_key[3][p] = rkey | key_tet(S, R, q);
+                }
+                p++;
+            }
         }
     }
 }
