@@ -141,9 +141,10 @@ dms_status dms_copy(dms_ctx* ctx, void* dst, const void* src, size_t bytes);
  * enable != 0 starts recording (and clears the accumulators); dms_stage_ms waits for
  * the stream and writes the accumulated milliseconds of stages
  * 0 order, 1 gradient (+ compaction), 2 critical sort, 3 D0, 4 D_{d-1},
- * 5 gradient kernel alone, and the number of timed gradient launches in ms_out[6]. */
+ * 5 gradient kernel alone, 6 the number of timed gradient launches,
+ * 7 D0 v-path tracing, 8 D_{d-1} dual tracing, 9 D0 union-find, 10 D_{d-1} union-find. */
 dms_status dms_set_timing(dms_ctx* ctx, int enable);
-dms_status dms_stage_ms(dms_ctx* ctx, double ms_out[7]);
+dms_status dms_stage_ms(dms_ctx* ctx, double ms_out[11]);
 
 /* Number of kernel launches issued by this context so far (bench accounting). */
 int64_t dms_launch_count(const dms_ctx* ctx);

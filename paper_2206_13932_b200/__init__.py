@@ -199,14 +199,15 @@ def dms_set_timing(ctx, enable=True):
     _check(ctx, lib().dms_set_timing(ctx, int(bool(enable))))
 
 
-STAGES = ("order", "gradient", "critical", "d0", "dtop", "gradient_kernel")
+STAGES = ("order", "gradient", "critical", "d0", "dtop", "gradient_kernel", None, "d0_trace", "dtop_trace",
+          "d0_uf", "dtop_uf")
 
 
 def dms_stage_ms(ctx):
     """-> dict stage -> accumulated ms, plus 'gradient_launches'"""
-    out = (ctypes.c_double * 7)()
+    out = (ctypes.c_double * 11)()
     _check(ctx, lib().dms_stage_ms(ctx, out))
-    d = {STAGES[i]: float(out[i]) for i in range(6)}
+    d = {STAGES[i]: float(out[i]) for i in range(11) if STAGES[i]}
     d["gradient_launches"] = int(out[6])
     return d
 

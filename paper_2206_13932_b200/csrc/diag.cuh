@@ -96,34 +96,43 @@ __global__ void k_d0_arcs(Geo3 g, const int64_t* __restrict__ c1, int64_t m, con
 // ---------------------------------------------------------------- dual tracing
 
 // 3D: chase from tetrahedron c (anchored id, or -1 = virtual) to a critical
-// tetrahedron's node, or the virtual node `vnode`
-__device__ int32_t chase_tet(const Geo3& g, const StarTab& S, int64_t c, const int32_t* node_of, int32_t vnode) {
-    while (c >= 0) {
-        const int64_t a = c / 6;
-        const int k = (int)(c % 6);
-        int64_t p[4];
+// tetrahedron's node, or the virtual node `vnode`.  Ids fit in 31 bits (checked at
+// dms_create), so the id arithmetic is 32-bit.
+__device__ int32_t chase_tet(const Geo3& g, const StarTab& S, int64_t c64, const int32_t* node_of, int32_t vnode) {
+    if (c64 < 0) return vnode;
+    uint32_t c = (uint32_t)c64;
+    const uint32_t Lx = (uint32_t)g.Lx, LxLy = (uint32_t)g.Lx * (uint32_t)g.Ly;
+    while (true) {
+        const uint32_t a = c / 6u;
+        const int k = (int)(c - a * 6u);
+        uint32_t p[4];
         p[0] = a;
-        p[1] = a + lin_mask(g, S.chain[3][k][0]);
-        p[2] = a + lin_mask(g, S.chain[3][k][1]);
-        p[3] = a + lin_mask(g, 7);
+        const int m1 = S.chain[3][k][0], m2 = S.chain[3][k][1];
+        p[1] = a + (m1 & 1) + Lx * ((m1 >> 1) & 1) + LxLy * ((m1 >> 2) & 1);
+        p[2] = a + (m2 & 1) + Lx * ((m2 >> 1) & 1) + LxLy * ((m2 >> 2) & 1);
+        p[3] = a + 1 + Lx + LxLy;
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) o[j] = ord_of(__ldg(g.f + p[j]));
         int jx = 0;
-        for (int j = 1; j < 4; j++) if (kless_v(g, p[jx], p[j])) jx = j;
-        const int64_t x = p[jx];
+#pragma unroll
+        for (int j = 1; j < 4; j++)
+            if (o[jx] < o[j] || (o[jx] == o[j] && p[jx] < p[j])) jx = j;
+        const uint32_t x = p[jx];
         const int T = S.q_slot[k][jx];
-        const uint64_t hi = __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * x + 1);
+        const uint64_t hi = __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * (uint64_t)x + 1);
         const int code = (int)((hi >> (8 + 2 * T)) & 3ull);
         if (code == 0) return node_of[c];  // a critical tetrahedron (a maximum)
-        const int tt = S.tet_tri[T][code - 1];      // s' = Pair(c)
+        const int tt = S.tet_tri[T][code - 1];  // s' = Pair(c)
         const int other = S.tri_tet[tt][0] == T ? S.tri_tet[tt][1] : S.tri_tet[tt][0];
-        int cx, cy, cz;
-        coords_of(g, x, cx, cy, cz);
+        const uint32_t cx = x % Lx, cyz = x / Lx;
+        const uint32_t cy = cyz % (uint32_t)g.Ly, cz = cyz / (uint32_t)g.Ly;
         if (other == 255 || !slot_in(g, S, cx, cy, cz, S.tet_a[other]) || !slot_in(g, S, cx, cy, cz, S.tet_b[other]) ||
             !slot_in(g, S, cx, cy, cz, S.tet_c[other]))
             return vnode;  // s' on the boundary: the virtual maximum
-        c = 6 * (x + S.q_anc[other][0] + (int64_t)g.Lx * S.q_anc[other][1] + (int64_t)g.Lx * g.Ly * S.q_anc[other][2]) +
-            S.q_k[other];
+        c = 6u * (uint32_t)((int32_t)x + S.q_anc[other][0] + (int32_t)Lx * S.q_anc[other][1] +
+                            (int32_t)LxLy * S.q_anc[other][2]) + S.q_k[other];
     }
-    return vnode;
 }
 
 // 2D: same over triangles

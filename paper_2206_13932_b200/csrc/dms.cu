@@ -31,27 +31,6 @@ static_assert(sizeof(PairRec) == sizeof(dms_pair), "pair layout");
 
 namespace {
 
-__global__ void k_order_keys(const float* __restrict__ f, int64_t n, uint32_t* __restrict__ keys,
-                             uint32_t* __restrict__ vals, int* err, unsigned long long* kmax) {
-    unsigned long long m = 0;
-    bool nan = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float x = f[i];
-        nan |= is_nan_bits(x);
-        const uint32_t o = ord_of(x);
-        keys[i] = o;
-        vals[i] = (uint32_t)i;
-        const unsigned long long k = ((unsigned long long)o << 32) | (unsigned long long)i;
-        m = k > m ? k : m;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
-        m = y > m ? y : m;
-    }
-    if ((threadIdx.x & 31) == 0) atomicMax(kmax, m);
-    if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
-}
-
 __global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsigned long long* kmax, PairRec* slot) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const StarTab& S = *g.tab;
@@ -115,10 +94,11 @@ struct dms_ctx {
     int64_t npairs[2] = {0, 0};
     int64_t* unp[2] = {nullptr, nullptr};
     int64_t nunp[2] = {0, 0};
+    int64_t cap_pairs[2] = {0, 0}, cap_unp[2] = {0, 0};  // grow-only result buffers
     // state
     bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
     bool timing = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[6];
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[10];
     int64_t launches = 0;
     dms_status sticky = DMS_OK;
     char msg[256] = {0};
@@ -247,12 +227,10 @@ dms_status run_order(dms_ctx* c, int32_t* d_rank) {
     StageTimer tm(c, 0);
     c->rank = d_rank ? d_rank : c->rank_scratch;
     CU(cudaMemsetAsync(c->kmax, 0, sizeof(unsigned long long), c->st));
-    const int64_t n = c->N;
-    k_order_keys<<<std::min<int64_t>(grid_for(n), 148 * 16), kBlock, 0, c->st>>>(c->f, n, c->okeys[0], c->ovals[0],
-                                                                                c->err, c->kmax);
-    c->launches++;
-    radix_sort<uint32_t, uint32_t, 16>(c->okeys[0], c->ovals[0], c->okeys[1], c->ovals[1], n, 0, 32, c->ss, c->st,
-                                       &c->launches, c->rank);
+    // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
+    // (and detects NaN / the highest vertex), the last pass writes rank[index]
+    radix_sort<uint32_t, uint32_t, 16>(c->okeys[0], c->ovals[0], c->okeys[1], c->ovals[1], c->N, 0, 32, c->ss, c->st,
+                                       &c->launches, c->rank, c->f, c->err, c->kmax);
     CU(cudaGetLastError());
     c->have_order = true;
     c->have_grad = c->have_crit = c->have_d[0] = c->have_d[1] = false;
@@ -423,9 +401,12 @@ dms_status emit_unpaired(dms_ctx* c, int which, UFBuf& u, int64_t m, const int64
     int64_t n = 0;
     dms_status s = flag_scan(c, u, m, 1, &n);
     if (s) return s;
-    cudaFree(c->unp[which]);
-    c->unp[which] = nullptr;
-    CU(dalloc(&c->unp[which], n));
+    if (n + 1 > c->cap_unp[which]) {  // grow only: no allocation inside a steady-state step
+        cudaFree(c->unp[which]);
+        c->unp[which] = nullptr;
+        CU(dalloc(&c->unp[which], 2 * n + 1024));
+        c->cap_unp[which] = 2 * n + 1024;
+    }
     c->nunp[which] = n;
     if (n) {
         k_emit_unpaired<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, n, ids, c->unp[which], rev);
@@ -448,16 +429,24 @@ dms_status run_d0(dms_ctx* c) {
     k_node_map<<<grid_for(n0), kBlock, 0, c->st>>>(crit_ids(c, 0), n0, c->node_of0);
     c->launches++;
     if (m) {
+        StageTimer t6(c, 6);
         k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
         c->launches++;
     }
-    s = union_find(c, u, m, n0, true);
+    {
+        StageTimer t8(c, 8);
+        s = union_find(c, u, m, n0, true);
+    }
     if (s) return s;
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
-    cudaFree(c->pairs[0]);
-    CU(dalloc(&c->pairs[0], np + 1));
+    if (np + 1 > c->cap_pairs[0]) {
+        cudaFree(c->pairs[0]);
+        c->pairs[0] = nullptr;
+        CU(dalloc(&c->pairs[0], 2 * np + 1024));
+        c->cap_pairs[0] = 2 * np + 1024;
+    }
     if (np) {
         k_emit_d0<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, 0), crit_ids(c, 1), c->pairs[0]);
         c->launches++;
@@ -488,11 +477,15 @@ dms_status run_dtop(dms_ctx* c) {
     k_node_map<<<grid_for(nd), kBlock, 0, c->st>>>(crit_ids(c, d), nd, c->node_oftop);
     c->launches++;
     if (m) {
+        StageTimer t7(c, 7);
         k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids(c, d - 1), m, c->node_oftop, (int32_t)nd, u.arc_a,
                                                       u.arc_b);
         c->launches++;
     }
-    s = union_find(c, u, m, nd + 1, false);
+    {
+        StageTimer t9(c, 9);
+        s = union_find(c, u, m, nd + 1, false);
+    }
     if (s) return s;
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
@@ -500,8 +493,12 @@ dms_status run_dtop(dms_ctx* c) {
     s = emit_unpaired(c, 1, u, m, crit_ids(c, d - 1), 1);
     if (s) return s;
     const int64_t ninf = d == 1 ? c->nunp[1] : 0;  // Sec. 6: in 1D the unpaired minimum is infinite
-    cudaFree(c->pairs[1]);
-    CU(dalloc(&c->pairs[1], np + ninf + 1));
+    if (np + ninf + 1 > c->cap_pairs[1]) {
+        cudaFree(c->pairs[1]);
+        c->pairs[1] = nullptr;
+        CU(dalloc(&c->pairs[1], 2 * (np + ninf) + 1024));
+        c->cap_pairs[1] = 2 * (np + ninf) + 1024;
+    }
     if (np) {
         // recompute the pair positions (emit_unpaired reused the scan buffers)
         int64_t np2 = 0;
@@ -744,17 +741,17 @@ dms_status dms_set_timing(dms_ctx* c, int enable) {
     return DMS_OK;
 }
 
-dms_status dms_stage_ms(dms_ctx* c, double ms_out[7]) {
+dms_status dms_stage_ms(dms_ctx* c, double ms_out[11]) {
     if (!c || !ms_out) return DMS_ERR_ARG;
     CU(cudaStreamSynchronize(c->st));
-    for (int s = 0; s < 6; s++) {
+    for (int s = 0; s < 10; s++) {
         double t = 0;
         for (auto& p : c->ev[s]) {
             float x = 0;
             CU(cudaEventElapsedTime(&x, p.first, p.second));
             t += x;
         }
-        ms_out[s] = t;
+        ms_out[s < 6 ? s : s + 1] = t;
     }
     ms_out[6] = (double)c->ev[5].size();
     return DMS_OK;

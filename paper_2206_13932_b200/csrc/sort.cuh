@@ -20,17 +20,41 @@ __device__ __forceinline__ uint32_t digit_of(Key k, int shift) {
     return (uint32_t)((k >> shift) & (Key)0xff);
 }
 
-template <typename Key, int ITEMS>
-__global__ void __launch_bounds__(kBlock) k_hist(const Key* __restrict__ keys, int64_t n, int shift,
-                                                 uint32_t* __restrict__ counts, int64_t ntiles) {
+template <typename Key, int ITEMS, bool FROM_F>
+__global__ void __launch_bounds__(kBlock) k_hist(const Key* __restrict__ keys, const float* __restrict__ fin,
+                                                 int64_t n, int shift, uint32_t* __restrict__ counts, int64_t ntiles,
+                                                 int* err, unsigned long long* kmax) {
     __shared__ uint32_t h[kRadix];
     h[threadIdx.x] = 0;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * (kBlock * ITEMS);
+    unsigned long long m = 0;
+    bool nan = false;
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
         int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
-        if (idx < n) atomicAdd(&h[digit_of(keys[idx], shift)], 1u);
+        if (idx < n) {
+            Key kk;
+            if (FROM_F) {
+                const float x = fin[idx];
+                nan |= is_nan_bits(x);
+                const uint32_t o = ord_of(x);
+                kk = (Key)o;
+                const unsigned long long km = ((unsigned long long)o << 32) | (unsigned long long)idx;
+                m = km > m ? km : m;
+            } else {
+                kk = keys[idx];
+            }
+            atomicAdd(&h[digit_of(kk, shift)], 1u);
+        }
+    }
+    if (FROM_F) {  // fused: NaN detection and the highest vertex (f*) for Sec. 6
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+            m = y > m ? y : m;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(kmax, m);
+        if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
     }
     __syncthreads();
     counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
@@ -70,31 +94,50 @@ __global__ void __launch_bounds__(kBlock) k_scan_excl(const uint32_t* __restrict
     }
 }
 
-// Stable scatter. RANK_OUT: write rank_out[val] = position instead of key/val.
-template <typename Key, typename Val, int ITEMS, bool RANK_OUT>
+// Stable scatter of one LSD pass.
+//   FROM_F:   the keys are ord_of(f[i]) and the values the indices i (first pass of the
+//             vertex order: no separate key-extraction pass).
+//   RANK_OUT: write rank_out[val] = position instead of (key, val) (last pass).
+// The tile is ranked in shared memory (warp match + per-warp digit counters, stable),
+// staged digit-sorted in shared memory, and written out as per-digit runs so that
+// consecutive threads store to consecutive global addresses.
+template <typename Key, typename Val, int ITEMS, bool RANK_OUT, bool FROM_F>
 __global__ void __launch_bounds__(kBlock) k_scatter(const Key* __restrict__ kin, const Val* __restrict__ vin,
-                                                    Key* __restrict__ kout, Val* __restrict__ vout,
-                                                    int32_t* __restrict__ rank_out, int64_t n, int shift,
-                                                    const uint32_t* __restrict__ counts_scanned, int64_t ntiles) {
+                                                    const float* __restrict__ fin, Key* __restrict__ kout,
+                                                    Val* __restrict__ vout, int32_t* __restrict__ rank_out, int64_t n,
+                                                    int shift, const uint32_t* __restrict__ counts_scanned,
+                                                    int64_t ntiles) {
     constexpr int NW = kBlock / 32;
+    constexpr int TILE = kBlock * ITEMS;
     __shared__ uint32_t wcnt[NW][kRadix];
     __shared__ uint32_t gbase[kRadix];
+    __shared__ uint32_t tstart[kRadix];
+    __shared__ uint32_t sw[NW + 1];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    Key* sk = reinterpret_cast<Key*>(dyn);
+    Val* sv = reinterpret_cast<Val*>(dyn + sizeof(Key) * TILE);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int w = 0; w < NW; w++) wcnt[w][threadIdx.x] = 0;
     gbase[threadIdx.x] = counts_scanned[(int64_t)threadIdx.x * ntiles + blockIdx.x];
     __syncthreads();
-    const int64_t seg = (int64_t)blockIdx.x * (kBlock * ITEMS) + (int64_t)warp * (32 * ITEMS);
+    const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+    const int64_t seg = tile0 + (int64_t)warp * (32 * ITEMS);
     Key k[ITEMS];
     Val v[ITEMS];
     uint32_t pos[ITEMS];
     uint32_t dg[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
-        int64_t idx = seg + i * 32 + lane;
+        const int64_t idx = seg + i * 32 + lane;
         if (idx < n) {
-            k[i] = kin[idx];
-            v[i] = vin[idx];
+            if (FROM_F) {
+                k[i] = (Key)ord_of(fin[idx]);
+                v[i] = (Val)idx;
+            } else {
+                k[i] = kin[idx];
+                v[i] = vin[idx];
+            }
             dg[i] = digit_of(k[i], shift);
         } else {
             dg[i] = kRadix;  // sentinel, never written
@@ -114,27 +157,41 @@ __global__ void __launch_bounds__(kBlock) k_scatter(const Key* __restrict__ kin,
         pos[i] = b + r;
     }
     __syncthreads();
+    uint32_t dtot;
     {
         uint32_t run = 0;
 #pragma unroll
         for (int w = 0; w < NW; w++) {
-            uint32_t c = wcnt[w][threadIdx.x];
+            const uint32_t c = wcnt[w][threadIdx.x];
             wcnt[w][threadIdx.x] = run;
             run += c;
         }
+        dtot = run;
     }
+    uint32_t tot;
+    const uint32_t ts = block_excl_sum<NW>(dtot, sw, &tot);  // start of digit threadIdx.x in the tile
+    tstart[threadIdx.x] = ts;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
         const uint32_t d = dg[i];
         if (d < kRadix) {
-            const uint32_t p = gbase[d] + wcnt[warp][d] + pos[i];
-            if (RANK_OUT) {
-                rank_out[v[i]] = (int32_t)p;
-            } else {
-                kout[p] = k[i];
-                vout[p] = v[i];
-            }
+            const uint32_t lp = tstart[d] + wcnt[warp][d] + pos[i];
+            sk[lp] = k[i];
+            sv[lp] = v[i];
+        }
+    }
+    __syncthreads();
+    const int tn = (int)((n - tile0) < (int64_t)TILE ? (n - tile0) : (int64_t)TILE);
+    for (int j = threadIdx.x; j < tn; j += kBlock) {
+        const Key kk = sk[j];
+        const uint32_t d = digit_of(kk, shift);
+        const uint32_t p = gbase[d] + (uint32_t)j - tstart[d];
+        if (RANK_OUT) {
+            rank_out[sv[j]] = (int32_t)p;
+        } else {
+            kout[p] = kk;
+            vout[p] = sv[j];
         }
     }
 }
@@ -162,29 +219,45 @@ inline cudaError_t scan_excl(const uint32_t* in, uint32_t* out, int64_t n, SortS
 
 // Sort (keys, vals) by bits [bit0, bit1) of the key.  Buffers a -> b -> a ...; returns
 // 0 if the result is in (ka, va), 1 if in (kb, vb).  With rank_out != nullptr the last
-// pass writes rank_out[val] = position and the return value is meaningless.
+// pass writes rank_out[val] = position and the return value is meaningless.  With
+// f != nullptr the first pass reads the keys as ord_of(f[i]) and the values as i.
 template <typename Key, typename Val, int ITEMS>
 inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, int bit1, SortScratch& s,
-                      cudaStream_t st, int64_t* launches, int32_t* rank_out = nullptr) {
+                      cudaStream_t st, int64_t* launches, int32_t* rank_out = nullptr, const float* f = nullptr,
+                      int* err = nullptr, unsigned long long* kmax = nullptr) {
     if (n <= 0) return 0;
-    const int64_t tiles = ceil_div(n, (int64_t)kBlock * ITEMS);
+    constexpr int TILE = kBlock * ITEMS;
+    constexpr size_t smem = (sizeof(Key) + sizeof(Val)) * TILE;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(k_scatter<Key, Val, ITEMS, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_scatter<Key, Val, ITEMS, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_scatter<Key, Val, ITEMS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_scatter<Key, Val, ITEMS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_done = true;
+    }
+    const int64_t tiles = ceil_div(n, (int64_t)TILE);
     int cur = 0;
     for (int shift = bit0; shift < bit1; shift += 8) {
+        const bool first = shift == bit0 && f != nullptr;
         const bool last = shift + 8 >= bit1;
         Key* ki = cur ? kb : ka;
         Val* vi = cur ? vb : va;
         Key* ko = cur ? ka : kb;
         Val* vo = cur ? va : vb;
-        k_hist<Key, ITEMS><<<(unsigned)tiles, kBlock, 0, st>>>(ki, n, shift, s.counts, tiles);
+        if (first) k_hist<Key, ITEMS, true><<<(unsigned)tiles, kBlock, 0, st>>>(ki, f, n, shift, s.counts, tiles, err, kmax);
+        else k_hist<Key, ITEMS, false><<<(unsigned)tiles, kBlock, 0, st>>>(ki, f, n, shift, s.counts, tiles, err, kmax);
         *launches += 1;
         scan_excl(s.counts, s.counts_scan, tiles * kRadix, s, st, launches);
-        if (last && rank_out) {
-            k_scatter<Key, Val, ITEMS, true><<<(unsigned)tiles, kBlock, 0, st>>>(ki, vi, ko, vo, rank_out, n, shift,
-                                                                               s.counts_scan, tiles);
-        } else {
-            k_scatter<Key, Val, ITEMS, false><<<(unsigned)tiles, kBlock, 0, st>>>(ki, vi, ko, vo, nullptr, n,
-                                                                                shift, s.counts_scan, tiles);
-        }
+        const bool ro = last && rank_out;
+#define DMS_SCATTER(RO, FF)                                                                             \
+    k_scatter<Key, Val, ITEMS, RO, FF><<<(unsigned)tiles, kBlock, smem, st>>>(ki, vi, f, ko, vo, rank_out, n, shift, \
+                                                                          s.counts_scan, tiles)
+        if (ro && first) DMS_SCATTER(true, true);
+        else if (ro) DMS_SCATTER(true, false);
+        else if (first) DMS_SCATTER(false, true);
+        else DMS_SCATTER(false, false);
+#undef DMS_SCATTER
         *launches += 1;
         cur ^= 1;
     }
