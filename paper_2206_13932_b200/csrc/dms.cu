@@ -272,8 +272,18 @@ dms_status launch_gradient(dms_ctx* c) {
 #endif
         const unsigned grid = (unsigned)std::max<int64_t>(
             1, DMS_PERSISTENT ? std::min<int64_t>(need, (int64_t)sms * std::max(per, 1)) : need);
-        if (c->ndim == 3) k_gradient<3><<<grid, kBlockG, 0, c->st>>>(A);
-        else k_gradient<2><<<grid, kBlockG, 0, c->st>>>(A);
+#ifndef DMS_REGROUP
+#define DMS_REGROUP 1
+#endif
+        if (DMS_REGROUP) {
+            const unsigned g2 = (unsigned)ceil_div(c->N, kBlockG);
+            if (c->ndim == 3) k_gradient_rg<3><<<g2, kBlockG, 0, c->st>>>(A);
+            else k_gradient_rg<2><<<g2, kBlockG, 0, c->st>>>(A);
+        } else if (c->ndim == 3) {
+            k_gradient<3><<<grid, kBlockG, 0, c->st>>>(A);
+        } else {
+            k_gradient<2><<<grid, kBlockG, 0, c->st>>>(A);
+        }
     } else {
         k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
     }
