@@ -110,7 +110,10 @@ __device__ __forceinline__ int kfirst(const KMask& m) {
 #ifndef DMS_KEYCACHE
 #define DMS_KEYCACHE 1
 #endif
-constexpr int kBlockG = 128;  // threads per CTA of the (persistent) gradient kernel
+#ifndef DMS_BLOCKG
+#define DMS_BLOCKG 128
+#endif
+constexpr int kBlockG = DMS_BLOCKG;  // threads per CTA of the gradient kernel
 
 // Per-thread key caches in shared memory, laid out [cell][thread] (bank-conflict
 // free): tri slot -> key index, tet slot -> 12-bit key.  Filled once per vertex.
@@ -154,31 +157,35 @@ struct StarState {
     uint64_t tcode_lo, tcode_hi;       // 2 bits per tri slot
     uint64_t qcode;                    // 2 bits per tet slot
     int vcode;                         // edge slot paired with x, -1 = minimum
+    uint64_t U2t;                      // triangles with both edges unclassified
+    uint32_t qc0, qc1;                 // per-tet count of unclassified facets, bit planes
 };
 
+// Called once when edge e becomes classified: triangles of the lower star holding e
+// whose other edge is still unclassified now have exactly one unclassified facet.
+// U2t = triangles whose two edges are both unclassified.
 template <int D>
 __device__ __forceinline__ void push_tris_of_edge(const StarTab& S, const KeyCache& C, StarState& st, int e) {
-    uint64_t cand = S.edge_tri_mask[e] & st.Lt & ~st.cls_t;
-    while (cand) {
-        const int t = __ffsll((long long)cand) - 1;
-        cand &= cand - 1;
-        const int nu = (int)(!((st.cls_e >> S.tri_a[t]) & 1u)) + (int)(!((st.cls_e >> S.tri_b[t]) & 1u));
-        if (nu == 1) kset(st.pq1_t, C.tri(t));
+    const uint64_t et = S.edge_tri_mask[e];
+    uint64_t pushed = et & st.U2t & ~st.cls_t;
+    st.U2t &= ~et;
+    while (pushed) {
+        const int t = __ffsll((long long)pushed) - 1;
+        pushed &= pushed - 1;
+        kset(st.pq1_t, C.tri(t));
     }
 }
 
+// Called once when triangle t becomes classified: decrement the bit-sliced counters
+// (qc1 qc0) of unclassified facets of the lower tets holding t; push those that reach 1.
 template <int D>
 __device__ __forceinline__ void push_tets_of_tri(const StarTab& S, StarState& st, int t) {
     if (D < 3) return;
-    uint32_t cand = S.tri_tet_mask[t] & st.Lq & ~st.cls_q;
-    while (cand) {
-        const int q = __ffs(cand) - 1;
-        cand &= cand - 1;
-        const int nu = (int)(!((st.cls_t >> S.tet_tri[q][0]) & 1ull)) +
-                       (int)(!((st.cls_t >> S.tet_tri[q][1]) & 1ull)) +
-                       (int)(!((st.cls_t >> S.tet_tri[q][2]) & 1ull));
-        if (nu == 1) st.pq1_q |= 1u << q;
-    }
+    const uint32_t M = S.tri_tet_mask[t] & st.Lq;
+    const uint32_t borrow = M & ~st.qc0;
+    st.qc0 ^= M;
+    st.qc1 ^= borrow;
+    st.pq1_q |= M & ~st.cls_q & st.qc0 & ~st.qc1;
 }
 
 __device__ __forceinline__ void set_tcode(StarState& st, int t, uint64_t code) {
@@ -193,6 +200,9 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
                                              int delta, StarState& st) {
     st.vcode = delta;
     st.cls_e = 1u << delta;
+    st.U2t = st.Lt & ~S.edge_tri_mask[delta];
+    st.qc0 = st.Lq;  // every lower tet starts with 3 unclassified facets (0b11)
+    st.qc1 = st.Lq;
     st.pq0_er = ((1u << nlow) - 1u) & ~1u;  // every lower edge but delta (rank 0)
     {
         uint64_t cand = S.edge_tri_mask[delta] & st.Lt;  // cofacets of delta: one unpaired facet each
