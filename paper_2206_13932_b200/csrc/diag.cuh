@@ -95,73 +95,6 @@ __global__ void k_d0_arcs(Geo3 g, const int64_t* __restrict__ c1, int64_t m, con
 
 // ---------------------------------------------------------------- dual tracing
 
-// 3D: chase from tetrahedron c (anchored id, or -1 = virtual) to a critical
-// tetrahedron's node, or the virtual node `vnode`.  Ids fit in 31 bits (checked at
-// dms_create), so the id arithmetic is 32-bit.
-__device__ int32_t chase_tet(const Geo3& g, const StarTab& S, int64_t c64, const int32_t* node_of, int32_t vnode) {
-    if (c64 < 0) return vnode;
-    uint32_t c = (uint32_t)c64;
-    const uint32_t Lx = (uint32_t)g.Lx, LxLy = (uint32_t)g.Lx * (uint32_t)g.Ly;
-    while (true) {
-        const uint32_t a = c / 6u;
-        const int k = (int)(c - a * 6u);
-        uint32_t p[4];
-        p[0] = a;
-        const int m1 = S.chain[3][k][0], m2 = S.chain[3][k][1];
-        p[1] = a + (m1 & 1) + Lx * ((m1 >> 1) & 1) + LxLy * ((m1 >> 2) & 1);
-        p[2] = a + (m2 & 1) + Lx * ((m2 >> 1) & 1) + LxLy * ((m2 >> 2) & 1);
-        p[3] = a + 1 + Lx + LxLy;
-        uint32_t o[4];
-#pragma unroll
-        for (int j = 0; j < 4; j++) o[j] = ord_of(__ldg(g.f + p[j]));
-        int jx = 0;
-#pragma unroll
-        for (int j = 1; j < 4; j++)
-            if (o[jx] < o[j] || (o[jx] == o[j] && p[jx] < p[j])) jx = j;
-        const uint32_t x = p[jx];
-        const int T = S.q_slot[k][jx];
-        const uint64_t hi = __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * (uint64_t)x + 1);
-        const int code = (int)((hi >> (8 + 2 * T)) & 3ull);
-        if (code == 0) return node_of[c];  // a critical tetrahedron (a maximum)
-        const int tt = S.tet_tri[T][code - 1];  // s' = Pair(c)
-        const int other = S.tri_tet[tt][0] == T ? S.tri_tet[tt][1] : S.tri_tet[tt][0];
-        const uint32_t cx = x % Lx, cyz = x / Lx;
-        const uint32_t cy = cyz % (uint32_t)g.Ly, cz = cyz / (uint32_t)g.Ly;
-        if (other == 255 || !slot_in(g, S, cx, cy, cz, S.tet_a[other]) || !slot_in(g, S, cx, cy, cz, S.tet_b[other]) ||
-            !slot_in(g, S, cx, cy, cz, S.tet_c[other]))
-            return vnode;  // s' on the boundary: the virtual maximum
-        c = 6u * (uint32_t)((int32_t)x + S.q_anc[other][0] + (int32_t)Lx * S.q_anc[other][1] +
-                            (int32_t)LxLy * S.q_anc[other][2]) + S.q_k[other];
-    }
-}
-
-// 2D: same over triangles
-__device__ int32_t chase_tri2(const Geo3& g, const StarTab& S, int64_t c, const int32_t* node_of, int32_t vnode) {
-    while (c >= 0) {
-        const int64_t a = c / 2;
-        const int k = (int)(c % 2);
-        int64_t p[3];
-        p[0] = a;
-        p[1] = a + lin_mask(g, S.chain[2][k][0]);
-        p[2] = a + lin_mask(g, 3);
-        int jx = 0;
-        for (int j = 1; j < 3; j++) if (kless_v(g, p[jx], p[j])) jx = j;
-        const int64_t x = p[jx];
-        const int t = S.t_slot[k][jx];
-        const uint32_t w = __ldg(reinterpret_cast<const uint16_t*>(g.grad) + x);
-        const int code = (int)((w >> (3 + 2 * t)) & 3u);
-        if (code == 0) return node_of[c];
-        const int e = code == 1 ? S.tri_a[t] : S.tri_b[t];
-        const int other = S.edge_tri[e][0] == t ? S.edge_tri[e][1] : S.edge_tri[e][0];
-        int cx, cy, cz;
-        coords_of(g, x, cx, cy, cz);
-        if (other == 255 || !slot_in(g, S, cx, cy, cz, S.tri_a[other]) || !slot_in(g, S, cx, cy, cz, S.tri_b[other]))
-            return vnode;
-        c = 2 * (x + S.t_anc[other][0] + (int64_t)g.Lx * S.t_anc[other][1]) + S.t_k[other];
-    }
-    return vnode;
-}
-
 // 1D: edges (a, a+1) have id a
 __device__ int32_t chase_edge1(const Geo3& g, int64_t c, const int32_t* node_of, int32_t vnode) {
     while (c >= 0) {
@@ -176,6 +109,82 @@ __device__ int32_t chase_edge1(const Geo3& g, int64_t c, const int32_t* node_of,
     return vnode;
 }
 
+// Dual chases carrying (x = highest vertex, slot of the current top cell in x's star,
+// ordered f(x), x's gradient word): a hop that stays in St^-(x) needs one f load, a hop
+// that climbs to a higher vertex loads that vertex's gradient word.
+__device__ __forceinline__ bool nb_lower(uint32_t on, uint32_t ox, int s, int ne) {
+    return on < ox || (on == ox && s < (ne >> 1));
+}
+
+__device__ __forceinline__ bool in_grid(const Geo3& g, int x, int y, int z) {
+    return x >= 0 && x < g.Lx && y >= 0 && y < g.Ly && z >= 0 && z < g.Lz;
+}
+
+// 3D: from tetrahedron slot T of x's star up to a critical tetrahedron or VIRTUAL
+__device__ int32_t chase3(const Geo3& g, const StarTab& S, uint32_t x, int T, uint32_t ox, int cx, int cy, int cz,
+                          const int32_t* node_of, int32_t vnode) {
+    const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(g.grad);
+    uint64_t hi = __ldg(gw + 2 * (uint64_t)x + 1);
+    while (true) {
+        const int code = (int)((hi >> (8 + 2 * T)) & 3ull);
+        if (code == 0) {  // critical tetrahedron (a maximum)
+            const int64_t id = 6 * ((int64_t)x + S.q_anc[T][0] + (int64_t)g.Lx * S.q_anc[T][1] +
+                                    (int64_t)g.Lx * g.Ly * S.q_anc[T][2]) + S.q_k[T];
+            return node_of[id];
+        }
+        const int tt = S.tet_tri[T][code - 1];  // s' = Pair(c)
+        const int T2 = S.tri_tet[tt][0] == T ? S.tri_tet[tt][1] : S.tri_tet[tt][0];
+        if (T2 == 255) return vnode;
+        const int s2 = S.tet_a[T2] ^ S.tet_b[T2] ^ S.tet_c[T2] ^ S.tri_a[tt] ^ S.tri_b[tt];
+        const int nx = cx + S.off[s2][0], ny = cy + S.off[s2][1], nz = cz + S.off[s2][2];
+        if (!in_grid(g, nx, ny, nz)) return vnode;  // s' on the boundary: the virtual maximum
+        const uint32_t n2 = x + (uint32_t)S.lin[s2];
+        const uint32_t on = ord_of(__ldg(g.f + n2));
+        if (nb_lower(on, ox, s2, 14)) {  // the other cofacet of s' is still in St^-(x)
+            T = T2;
+            continue;
+        }
+        const int j = S.tet_a[T2] == s2 ? 0 : (S.tet_b[T2] == s2 ? 1 : 2);
+        T = S.q_reslot[T2][j];
+        x = n2;
+        ox = on;
+        cx = nx; cy = ny; cz = nz;
+        hi = __ldg(gw + 2 * (uint64_t)x + 1);
+    }
+}
+
+// 2D: from triangle slot t of x's star up to a critical triangle or VIRTUAL
+__device__ int32_t chase2(const Geo3& g, const StarTab& S, uint32_t x, int t, uint32_t ox, int cx, int cy,
+                          const int32_t* node_of, int32_t vnode) {
+    const uint16_t* gw = reinterpret_cast<const uint16_t*>(g.grad);
+    uint32_t w = __ldg(gw + x);
+    while (true) {
+        const int code = (int)((w >> (3 + 2 * t)) & 3u);
+        if (code == 0) {
+            const int64_t id = 2 * ((int64_t)x + S.t_anc[t][0] + (int64_t)g.Lx * S.t_anc[t][1]) + S.t_k[t];
+            return node_of[id];
+        }
+        const int e = code == 1 ? S.tri_a[t] : S.tri_b[t];
+        const int t2 = S.edge_tri[e][0] == t ? S.edge_tri[e][1] : S.edge_tri[e][0];
+        if (t2 == 255) return vnode;
+        const int s2 = S.tri_a[t2] ^ S.tri_b[t2] ^ e;
+        const int nx = cx + S.off[s2][0], ny = cy + S.off[s2][1];
+        if (!in_grid(g, nx, ny, 0)) return vnode;
+        const uint32_t n2 = x + (uint32_t)S.lin[s2];
+        const uint32_t on = ord_of(__ldg(g.f + n2));
+        if (nb_lower(on, ox, s2, 6)) {
+            t = t2;
+            continue;
+        }
+        const int j = S.tri_a[t2] == s2 ? 0 : 1;
+        t = S.t_reslot[t2][j];
+        x = n2;
+        ox = on;
+        cx = nx; cy = ny;
+        w = __ldg(gw + x);
+    }
+}
+
 // arcs of G_{D_{d-1}}: processing order j = 0.. is DEcreasing lex order (Sec. 5.2)
 __global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ cs, int64_t m, const int32_t* __restrict__ node_of,
                             int32_t vnode, int32_t* __restrict__ arc_a, int32_t* __restrict__ arc_b) {
@@ -184,43 +193,64 @@ __global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ cs, int64_t m, c
     const StarTab& S = *g.tab;
     const int64_t id = cs[m - 1 - j];
     int32_t end[2];
-    if (g.ndim == 3) {
-        const int64_t a = id / 12;
-        const int k = (int)(id % 12);
-        int64_t p[3];
-        p[0] = a;
-        p[1] = a + lin_mask(g, S.chain[2][k][0]);
-        p[2] = a + lin_mask(g, S.chain[2][k][1]);
+    if (g.ndim >= 2) {
+        // the critical (d-1)-simplex, its highest vertex x and its slot in x's star
+        const int nv = g.ndim;  // vertices of a (d-1)-simplex
+        const int64_t a = id / g.ncell[nv - 1];
+        const int k = (int)(id % g.ncell[nv - 1]);
+        uint32_t p[3];
+        uint32_t o[3];
+        p[0] = (uint32_t)a;
+        for (int q = 1; q < nv; q++) p[q] = (uint32_t)(a + lin_mask(g, S.chain[nv - 1][k][q - 1]));
+        for (int q = 0; q < nv; q++) o[q] = ord_of(__ldg(g.f + p[q]));
         int jx = 0;
-        for (int q = 1; q < 3; q++) if (kless_v(g, p[jx], p[q])) jx = q;
-        const int64_t x = p[jx];
-        const int t = S.t_slot[k][jx];
+        for (int q = 1; q < nv; q++)
+            if (o[jx] < o[q] || (o[jx] == o[q] && p[jx] < p[q])) jx = q;
+        const uint32_t x = p[jx], ox = o[jx];
         int cx, cy, cz;
         coords_of(g, x, cx, cy, cz);
-        for (int side = 0; side < 2; side++) {
-            const int T = S.tri_tet[t][side];
-            int64_t c = -1;
-            if (T != 255 && slot_in(g, S, cx, cy, cz, S.tet_a[T]) && slot_in(g, S, cx, cy, cz, S.tet_b[T]) &&
-                slot_in(g, S, cx, cy, cz, S.tet_c[T]))
-                c = 6 * (x + S.q_anc[T][0] + (int64_t)g.Lx * S.q_anc[T][1] + (int64_t)g.Lx * g.Ly * S.q_anc[T][2]) +
-                    S.q_k[T];
-            end[side] = chase_tet(g, S, c, node_of, vnode);
-        }
-    } else if (g.ndim == 2) {
-        const int64_t a = id / 3;
-        const int k = (int)(id % 3);
-        const int64_t p0 = a, p1 = a + lin_mask(g, S.chain[1][k][0]);
-        const int jx = kless_v(g, p0, p1) ? 1 : 0;
-        const int64_t x = jx ? p1 : p0;
-        const int s = S.e_slot[k][jx];
-        int cx, cy, cz;
-        coords_of(g, x, cx, cy, cz);
-        for (int side = 0; side < 2; side++) {
-            const int t = S.edge_tri[s][side];
-            int64_t c = -1;
-            if (t != 255 && slot_in(g, S, cx, cy, cz, S.tri_a[t]) && slot_in(g, S, cx, cy, cz, S.tri_b[t]))
-                c = 2 * (x + S.t_anc[t][0] + (int64_t)g.Lx * S.t_anc[t][1]) + S.t_k[t];
-            end[side] = chase_tri2(g, S, c, node_of, vnode);
+        if (g.ndim == 3) {
+            const int t = S.t_slot[k][jx];
+            for (int side = 0; side < 2; side++) {
+                const int T = S.tri_tet[t][side];
+                int32_t r = vnode;
+                if (T != 255) {
+                    const int s3 = S.tet_a[T] ^ S.tet_b[T] ^ S.tet_c[T] ^ S.tri_a[t] ^ S.tri_b[t];
+                    const int nx = cx + S.off[s3][0], ny = cy + S.off[s3][1], nz = cz + S.off[s3][2];
+                    if (in_grid(g, nx, ny, nz)) {
+                        const uint32_t n3 = x + (uint32_t)S.lin[s3];
+                        const uint32_t on = ord_of(__ldg(g.f + n3));
+                        if (nb_lower(on, ox, s3, 14)) {
+                            r = chase3(g, S, x, T, ox, cx, cy, cz, node_of, vnode);
+                        } else {
+                            const int jj = S.tet_a[T] == s3 ? 0 : (S.tet_b[T] == s3 ? 1 : 2);
+                            r = chase3(g, S, n3, S.q_reslot[T][jj], on, nx, ny, nz, node_of, vnode);
+                        }
+                    }
+                }
+                end[side] = r;
+            }
+        } else {
+            const int e = S.e_slot[k][jx];
+            for (int side = 0; side < 2; side++) {
+                const int t = S.edge_tri[e][side];
+                int32_t r = vnode;
+                if (t != 255) {
+                    const int s3 = S.tri_a[t] ^ S.tri_b[t] ^ e;
+                    const int nx = cx + S.off[s3][0], ny = cy + S.off[s3][1];
+                    if (in_grid(g, nx, ny, 0)) {
+                        const uint32_t n3 = x + (uint32_t)S.lin[s3];
+                        const uint32_t on = ord_of(__ldg(g.f + n3));
+                        if (nb_lower(on, ox, s3, 6)) {
+                            r = chase2(g, S, x, t, ox, cx, cy, node_of, vnode);
+                        } else {
+                            const int jj = S.tri_a[t] == s3 ? 0 : 1;
+                            r = chase2(g, S, n3, S.t_reslot[t][jj], on, nx, ny, node_of, vnode);
+                        }
+                    }
+                }
+                end[side] = r;
+            }
         }
     } else {
         end[0] = chase_edge1(g, id > 0 ? id - 1 : -1, node_of, vnode);

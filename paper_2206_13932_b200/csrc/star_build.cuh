@@ -205,6 +205,31 @@ inline bool build_star_tables(int ndim, const int64_t L[3], StarTab* T) {
         if (rel.size() == 3) { for (int q = 0; q < nq; q++) if (same({T->tet_a[q], T->tet_b[q], T->tet_c[q]})) return q; }
         return -1;
     };
+    // the same cell seen from one of its link vertices
+    std::memset(T->q_reslot, 255, sizeof(T->q_reslot));
+    std::memset(T->t_reslot, 255, sizeof(T->t_reslot));
+    for (int q = 0; q < nq; q++) {
+        const int ls[3] = {T->tet_a[q], T->tet_b[q], T->tet_c[q]};
+        for (int j = 0; j < 3; j++) {
+            std::vector<P3> rel;
+            rel.push_back(sub(zero, nb[ls[j]]));
+            for (int i = 0; i < 3; i++) if (i != j) rel.push_back(sub(nb[ls[i]], nb[ls[j]]));
+            const int r = find_slot(rel);
+            if (r < 0) return false;
+            T->q_reslot[q][j] = (uint8_t)r;
+        }
+    }
+    for (int t = 0; t < nt; t++) {
+        const int ls[2] = {T->tri_a[t], T->tri_b[t]};
+        for (int j = 0; j < 2; j++) {
+            std::vector<P3> rel;
+            rel.push_back(sub(zero, nb[ls[j]]));
+            rel.push_back(sub(nb[ls[1 - j]], nb[ls[j]]));
+            const int r = find_slot(rel);
+            if (r < 0) return false;
+            T->t_reslot[t][j] = (uint8_t)r;
+        }
+    }
     for (int k = 1; k <= ndim; k++) {
         for (int i = 0; i < T->nchain[k]; i++) {
             std::vector<P3> pts{zero};
