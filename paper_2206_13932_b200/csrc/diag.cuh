@@ -75,6 +75,29 @@ __device__ __forceinline__ int64_t descend(const Geo3& g, const StarTab& S, int6
     }
 }
 
+// arc[j] = tmp[perm[j]] (rev: perm[m-1-j]): from tracing order (the spatially coherent
+// emission order of the critical cells) to processing order (sorted, or reversed)
+__global__ void k_permute_arcs(const int32_t* __restrict__ ta, const int32_t* __restrict__ tb,
+                               const uint32_t* __restrict__ perm, int64_t m, int rev, int32_t* __restrict__ arc_a,
+                               int32_t* __restrict__ arc_b) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const uint32_t r = perm[rev ? m - 1 - j : j];
+    arc_a[j] = ta[r];
+    arc_b[j] = tb[r];
+}
+
+__global__ void k_iota(uint32_t* __restrict__ a, int64_t m) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) a[i] = (uint32_t)i;
+}
+
+__global__ void k_gather_ids(const int64_t* __restrict__ src, const uint32_t* __restrict__ perm, int64_t m,
+                             int64_t* __restrict__ dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) dst[i] = src[perm[i]];
+}
+
 __global__ void k_node_map(const int64_t* __restrict__ ids, int64_t m, int32_t* __restrict__ node_of) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) node_of[ids[i]] = (int32_t)i;
@@ -185,13 +208,14 @@ __device__ int32_t chase2(const Geo3& g, const StarTab& S, uint32_t x, int t, ui
     }
 }
 
-// arcs of G_{D_{d-1}}: processing order j = 0.. is DEcreasing lex order (Sec. 5.2)
-__global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ cs, int64_t m, const int32_t* __restrict__ node_of,
+// ends of the arcs of G_{D_{d-1}} for the critical (d-1)-simplices ids[0..m) (in any
+// order; k_permute_arcs puts them in processing order)
+__global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ ids, int64_t m, const int32_t* __restrict__ node_of,
                             int32_t vnode, int32_t* __restrict__ arc_a, int32_t* __restrict__ arc_b) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     const StarTab& S = *g.tab;
-    const int64_t id = cs[m - 1 - j];
+    const int64_t id = ids[j];
     int32_t end[2];
     if (g.ndim >= 2) {
         // the critical (d-1)-simplex, its highest vertex x and its slot in x's star

@@ -75,8 +75,9 @@ struct dms_ctx {
     SortScratch ss;
     // critical records
     int64_t cap[4] = {0, 0, 0, 0};
-    int64_t* cid[2][4] = {};
+    int64_t* cid[2][4] = {};     // [0]: ids in emission order, [1]: ids in lexicographic order
     uint64_t* ckey[2][4] = {};
+    uint32_t* cidx[2][4] = {};   // sort payload: emission index; perm = cidx[cur]
     int cur[4] = {0, 0, 0, 0};
     int64_t ncrit[4] = {0, 0, 0, 0};
     unsigned long long* status = nullptr;
@@ -185,8 +186,10 @@ dms_status alloc_crit(dms_ctx* c) {
         for (int k = 0; k <= c->ndim; k++) {
             cudaFree(c->cid[b][k]);
             cudaFree(c->ckey[b][k]);
+            cudaFree(c->cidx[b][k]);
             CU(dalloc(&c->cid[b][k], c->cap[k]));
             CU(dalloc(&c->ckey[b][k], c->cap[k]));
+            CU(dalloc(&c->cidx[b][k], c->cap[k]));
         }
     return DMS_OK;
 }
@@ -312,6 +315,10 @@ int bits_for(int64_t n) {
     return b;
 }
 
+const int64_t* crit_ids(dms_ctx* c, int k) { return c->cid[1][k]; }            // lexicographic order
+const int64_t* crit_ids_emitted(dms_ctx* c, int k) { return c->cid[0][k]; }    // emission order
+const uint32_t* crit_perm(dms_ctx* c, int k) { return c->cidx[c->cur[k]][k]; }  // sorted pos -> emission idx
+
 dms_status run_critical(dms_ctx* c) {
     if (!c->have_grad) {
         dms_status s = run_gradient(c, nullptr);
@@ -334,15 +341,19 @@ dms_status run_critical(dms_ctx* c) {
     for (int k = 0; k <= c->ndim; k++) c->ncrit[k] = (int64_t)tot[k];
     const int kbits = 12 + bits_for(c->N);
     for (int k = 0; k <= c->ndim; k++) {
-        c->cur[k] = radix_sort<uint64_t, int64_t, 8>(c->ckey[0][k], c->cid[0][k], c->ckey[1][k], c->cid[1][k],
+        k_iota<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cidx[0][k], c->ncrit[k]);
+        c->cur[k] = radix_sort<uint64_t, uint32_t, 8>(c->ckey[0][k], c->cidx[0][k], c->ckey[1][k], c->cidx[1][k],
                                                      c->ncrit[k], 0, kbits, c->ss, c->st, &c->launches);
+        // lexicographically sorted ids = emitted ids gathered through the permutation
+        k_gather_ids<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cid[0][k], crit_perm(c, k), c->ncrit[k],
+                                                                 c->cid[1][k]);
+        c->launches += 2;
     }
     CU(cudaGetLastError());
     c->have_crit = true;
     return DMS_OK;
 }
 
-const int64_t* crit_ids(dms_ctx* c, int k) { return c->cid[c->cur[k]][k]; }
 
 // union-find over arcs (processing order), see diag.cuh
 dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older_is_smaller) {
@@ -440,8 +451,10 @@ dms_status run_d0(dms_ctx* c) {
     c->launches++;
     if (m) {
         StageTimer t6(c, 6);
-        k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
-        c->launches++;
+        // trace in emission order (spatially coherent), then permute into processing order
+        k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, 1), m, c->node_of0, u.ra, u.rb);
+        k_permute_arcs<<<grid_for(m), kBlock, 0, c->st>>>(u.ra, u.rb, crit_perm(c, 1), m, 0, u.arc_a, u.arc_b);
+        c->launches += 2;
     }
     {
         StageTimer t8(c, 8);
@@ -488,9 +501,10 @@ dms_status run_dtop(dms_ctx* c) {
     c->launches++;
     if (m) {
         StageTimer t7(c, 7);
-        k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids(c, d - 1), m, c->node_oftop, (int32_t)nd, u.arc_a,
-                                                      u.arc_b);
-        c->launches++;
+        k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), m, c->node_oftop, (int32_t)nd,
+                                                      u.ra, u.rb);
+        k_permute_arcs<<<grid_for(m), kBlock, 0, c->st>>>(u.ra, u.rb, crit_perm(c, d - 1), m, 1, u.arc_a, u.arc_b);
+        c->launches += 2;
     }
     {
         StageTimer t9(c, 9);
@@ -784,7 +798,7 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->ss.status);
     cudaFree(c->ss.tile_ctr);
     for (int b = 0; b < 2; b++)
-        for (int k = 0; k < 4; k++) { cudaFree(c->cid[b][k]); cudaFree(c->ckey[b][k]); }
+        for (int k = 0; k < 4; k++) { cudaFree(c->cid[b][k]); cudaFree(c->ckey[b][k]); cudaFree(c->cidx[b][k]); }
     cudaFree(c->status);
     cudaFree(c->tile_ctr);
     cudaFree(c->totals);
