@@ -90,6 +90,9 @@ __device__ __forceinline__ uint32_t kidx_key(const StarTab& S, int ki) {
     const int hl = S.hl[ki];
     return ((uint32_t)((hl >> 4) + 1) << 8) | ((uint32_t)((hl & 15) + 1) << 4);
 }
+#ifndef DMS_KEYCACHE
+#define DMS_KEYCACHE 1
+#endif
 struct KMask {  // 128-bit set over triangle key indices (kept in registers)
     uint64_t lo, hi;
 };
@@ -106,10 +109,6 @@ __device__ __forceinline__ int kfirst(const KMask& m) {
     if (m.hi) return 64 + __ffsll((long long)m.hi) - 1;
     return -1;
 }
-
-#ifndef DMS_KEYCACHE
-#define DMS_KEYCACHE 1
-#endif
 #ifndef DMS_BLOCKG
 #define DMS_BLOCKG 128
 #endif

@@ -158,6 +158,7 @@ inline bool build_star_tables(int ndim, const int64_t L[3], StarTab* T) {
         for (int j = 0; j < 3; j++) {
             if (tr[j] < 0) return false;
             T->tet_tri[q][j] = (uint8_t)tr[j];
+            T->tet_tmask[q] |= 1ull << tr[j];
             int t = tr[j];
             if (T->tri_tet[t][0] == 255) T->tri_tet[t][0] = (uint8_t)q;
             else if (T->tri_tet[t][1] == 255) T->tri_tet[t][1] = (uint8_t)q;
