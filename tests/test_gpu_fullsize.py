@@ -125,7 +125,6 @@ def test_full_size(env, cfg):
     got_pairs = got_pairs[np.lexsort((got_pairs[:, 2], got_pairs[:, 1], got_pairs[:, 0]))]
     ref = oracle.gradient_sample(f3, sample, nthreads=NCPU)
     assert np.array_equal(got_pairs, ref.pairs), "gradient vectors on the sampled lower stars"
-    sset = set(sample.tolist())
     for k in range(d + 1):
         mv = kmax(f, simplex_vertices(shape, k, crit[k]))
         mine = np.sort(crit[k][np.isin(mv, sample)])
@@ -159,7 +158,7 @@ def test_full_size(env, cfg):
     assert (fin["birth_value"].view(np.uint32) == f[fin["birth_vertex"]].view(np.uint32)).all()
     assert (fin["death_value"].view(np.uint32) == f[fin["death_vertex"]].view(np.uint32)).all()
     assert np.array_equal(fin["death_vertex"], kmax(f, simplex_vertices(shape, 1, fin["death_id"])))
-    fstar_v = int(np.lexsort((np.arange(N), f))[-1])
+    fstar_v = int(np.nonzero(f == f.max())[0][-1])  # the K-highest vertex: max value, then max index
     assert inf[0]["death_value"].view(np.uint32) == f[fstar_v].view(np.uint32)
 
     # ---- D_{d-1}
