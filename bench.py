@@ -134,6 +134,24 @@ def cpu_oracle_sample(f_full, budget_s=20.0):
                 reps, "x".join(str(min(side, s)) for s in f_full.shape), t_all)}
 
 
+def max_over_ranks(value, dist):
+    """The timing rule for N > 1: every rank times its own replica, the job time is the
+    maximum over ranks (all_reduce MAX; NCCL on the GPU box, gloo in the CPU test)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(n_vertices_per_rank, world, steps, ms_total):
+    """whole-job throughput: vertices processed by all ranks / the (max) job time"""
+    return world * n_vertices_per_rank * steps / (ms_total / 1e3) / 1e6
+
+
 def make_field(cfg, seed):
     from synth import fields
 
@@ -141,20 +159,36 @@ def make_field(cfg, seed):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle, as it stands, on this config's field."""
+    """--impl reference: the CPU oracle, as it stands, timed on the host cores.  Each
+    step is one full front-end run on a fixed crop of this config's field (a bounded
+    sample: the full field would take the oracle tens of minutes)."""
     if rank != 0:
         return
-    f = make_field(args.config, 0)
-    import numpy as np  # noqa: F401
+    import numpy as np
 
-    base = cpu_oracle_sample(f, budget_s=max(10.0, 60.0 / max(1, args.steps + args.warmup)))
+    import oracle
+
+    f = make_field(args.config, 0)
+    side = {3: 96, 2: 1024, 1: 1 << 20}[f.ndim]
+    crop = np.ascontiguousarray(f[tuple(slice(0, min(side, s)) for s in f.shape)])
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.run(crop, nthreads=cores, want_pairs=False)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.run(crop, nthreads=cores, want_pairs=False)
+    dt = time.perf_counter() - t0
+    value = crop.size * args.steps / dt / 1e6
+    sample = "crop %s of the %s field, full front end (order, gradient, C_k, D0, D_{d-1})" % (
+        "x".join(str(x) for x in crop.shape), args.config)
     line = {
-        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (ranked; integer arithmetic)", "data": "synthetic",
-        "config": {"workload": args.config, "desc": CONFIG_DESC[args.config]},
-        "cpu_baseline": base,
-        "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 in, integer arithmetic (oracle)", "data": "synthetic",
+        "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "N": int(f.size)},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -232,13 +266,9 @@ def main():
     launches = ctx.launch_count() - l0
     clk = clocks.stop()
 
-    if dist is not None:
-        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-
+    ms_total = max_over_ranks(ms_total, dist)
     ms_step = ms_total / args.steps
-    value = world * N * args.steps / (ms_total / 1e3) / 1e6
+    value = job_value(N, world, args.steps, ms_total)
 
     counts, _ = dms.dms_critical(ctx.ctx)
     ncrit = counts[: ndim + 1]
@@ -264,6 +294,16 @@ def main():
             if tr:
                 roofline["traffic"] = tr["bytes_per_launch"]
                 roofline["traffic_source"] = tr.get("source")
+                if tr.get("warp_inst_per_launch"):
+                    # the kernel is issue-bound: warp instructions per launch (ncu) over the
+                    # live launch time, against one warp instruction per cycle per SMSP at
+                    # the sampled SM clock
+                    issue_peak = 148 * 4 * (clk.get("sm_mhz") or 1965.0) * 1e6
+                    ach = tr["warp_inst_per_launch"] / (g_ms / 1e3)
+                    roofline["issue"] = {"bound": "alu", "achieved": round(ach / 1e9, 1), "peak": round(issue_peak / 1e9, 1),
+                                         "unit": "G warp-inst/s", "frac": round(ach / issue_peak, 3),
+                                         "lane_efficiency": tr.get("lane_efficiency"),
+                                         "source": tr.get("source")}
         except Exception:
             pass
 
@@ -291,12 +331,8 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ms_e2e = t0.elapsed_time(t1)
-        if dist is not None:
-            t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
-        e2e = {"value": round(world * N * args.steps / (ms_e2e / 1e3) / 1e6, 3), "unit": UNIT,
+        ms_e2e = max_over_ranks(t0.elapsed_time(t1), dist)
+        e2e = {"value": round(job_value(N, world, args.steps, ms_e2e), 3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": round(ms_e2e / args.steps, 3)}
 
