@@ -160,31 +160,46 @@ struct StarState {
     uint32_t qc0, qc1;                 // per-tet count of unclassified facets, bit planes
 };
 
-// Called once when edge e becomes classified: triangles of the lower star holding e
-// whose other edge is still unclassified now have exactly one unclassified facet.
-// U2t = triangles whose two edges are both unclassified.
+// Called once when edge e becomes classified.  Triangles of the lower star holding e:
+//   other edge unclassified (2 -> 1 unclassified facets): pushed to PQone;
+//   other edge classified   (1 -> 0): moved from PQone to PQzero right away.
+// Robins' algorithm would pop such a triangle from PQone later and move it then; PQzero
+// is only popped when PQone is empty, by which time it holds the same cells, so the
+// early move changes no pop.  U2t = triangles whose two edges
+// are both unclassified.
 template <int D>
 __device__ __forceinline__ void push_tris_of_edge(const StarTab& S, const KeyCache& C, StarState& st, int e) {
-    const uint64_t et = S.edge_tri_mask[e];
-    uint64_t pushed = et & st.U2t & ~st.cls_t;
+    const uint64_t et = S.edge_tri_mask[e] & st.Lt & ~st.cls_t;
+    uint64_t pushed = et & st.U2t;
+    uint64_t zeroed = et & ~st.U2t;
     st.U2t &= ~et;
     while (pushed) {
         const int t = __ffsll((long long)pushed) - 1;
         pushed &= pushed - 1;
         kset(st.pq1_t, C.tri(t));
     }
+    while (zeroed) {
+        const int t = __ffsll((long long)zeroed) - 1;
+        zeroed &= zeroed - 1;
+        const int ki = C.tri(t);
+        kclr(st.pq1_t, ki);
+        kset(st.pq0_t, ki);
+    }
 }
 
 // Called once when triangle t becomes classified: decrement the bit-sliced counters
-// (qc1 qc0) of unclassified facets of the lower tets holding t; push those that reach 1.
+// (qc1 qc0) of unclassified facets of the lower tets holding t; those reaching 1 are
+// pushed to PQone, those reaching 0 move from PQone to PQzero (as above).
 template <int D>
 __device__ __forceinline__ void push_tets_of_tri(const StarTab& S, StarState& st, int t) {
     if (D < 3) return;
-    const uint32_t M = S.tri_tet_mask[t] & st.Lq;
+    const uint32_t M = S.tri_tet_mask[t] & st.Lq & ~st.cls_q;
     const uint32_t borrow = M & ~st.qc0;
     st.qc0 ^= M;
     st.qc1 ^= borrow;
-    st.pq1_q |= M & ~st.cls_q & st.qc0 & ~st.qc1;
+    const uint32_t one = M & st.qc0 & ~st.qc1, zero = M & ~st.qc0 & ~st.qc1;
+    st.pq1_q = (st.pq1_q | one) & ~zero;
+    st.pq0_q |= zero;
 }
 
 __device__ __forceinline__ void set_tcode(StarState& st, int t, uint64_t code) {
@@ -213,6 +228,8 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
     }
     while (true) {
         while ((st.pq1_t.lo | st.pq1_t.hi) | st.pq1_q) {
+            // every cell in PQone has exactly one unclassified facet (cells leave PQone
+            // when they reach zero or get classified), so each pop pairs
             const int ki = kfirst(st.pq1_t);
             const uint32_t ktri = ki >= 0 ? kidx_key(S, ki) : 0xffffffffu;
             uint32_t ktet = 0xffffffffu;
@@ -220,11 +237,9 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
             if (ktri < ktet) {
                 kclr(st.pq1_t, ki);
                 const int s = kidx_tri(S, IV, ki);
-                if ((st.cls_t >> s) & 1ull) continue;
-                const int a = S.tri_a[s], b = S.tri_b[s];
-                const bool ua = !((st.cls_e >> a) & 1u), ub = !((st.cls_e >> b) & 1u);
-                if (!ua && !ub) { kset(st.pq0_t, ki); continue; }
-                const int e = ua ? a : b;  // the unique unclassified facet
+                const int a = S.tri_a[s];
+                const bool ua = !((st.cls_e >> a) & 1u);
+                const int e = ua ? a : S.tri_b[s];  // the unique unclassified facet
                 set_tcode(st, s, ua ? 1ull : 2ull);
                 st.cls_e |= 1u << e;
                 st.cls_t |= 1ull << s;
@@ -233,17 +248,16 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
                 push_tris_of_edge<D>(S, C, st, e);  // cofacets of pair(alpha)
             } else if constexpr (D == 3) {
                 st.pq1_q &= ~(1u << q);
-                if ((st.cls_q >> q) & 1u) continue;
-                const int t0 = S.tet_tri[q][0], t1 = S.tet_tri[q][1], t2 = S.tet_tri[q][2];
-                const bool u0 = !((st.cls_t >> t0) & 1ull), u1 = !((st.cls_t >> t1) & 1ull),
-                           u2 = !((st.cls_t >> t2) & 1ull);
-                if (!u0 && !u1 && !u2) { st.pq0_q |= 1u << q; continue; }
+                const int t0 = S.tet_tri[q][0], t1 = S.tet_tri[q][1];
+                const bool u0 = !((st.cls_t >> t0) & 1ull), u1 = !((st.cls_t >> t1) & 1ull);
                 const int j = u0 ? 0 : (u1 ? 1 : 2);
-                const int tt = u0 ? t0 : (u1 ? t1 : t2);
+                const int tt = u0 ? t0 : (u1 ? t1 : S.tet_tri[q][2]);
                 st.qcode |= (uint64_t)(j + 1) << (2 * q);
                 st.cls_t |= 1ull << tt;
                 st.cls_q |= 1u << q;
-                kclr(st.pq0_t, C.tri(tt));
+                const int kt = C.tri(tt);  // tt leaves both queues
+                kclr(st.pq0_t, kt);
+                kclr(st.pq1_t, kt);
                 push_tets_of_tri<D>(S, st, tt);
             }
         }
@@ -258,20 +272,17 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
             const int r = __ffs(st.pq0_er) - 1;
             st.pq0_er &= ~(1u << r);
             const int e = rk(IV, r);
-            if ((st.cls_e >> e) & 1u) continue;
             st.cls_e |= 1u << e;
             st.crit_e |= 1u << e;
             push_tris_of_edge<D>(S, C, st, e);
         } else if (kt < kq) {
             kclr(st.pq0_t, ki);
             const int s = kidx_tri(S, IV, ki);
-            if ((st.cls_t >> s) & 1ull) continue;
             st.cls_t |= 1ull << s;
             st.crit_t |= 1ull << s;
             push_tets_of_tri<D>(S, st, s);
         } else if constexpr (D == 3) {
             st.pq0_q &= ~(1u << q);
-            if ((st.cls_q >> q) & 1u) continue;
             st.cls_q |= 1u << q;
             st.crit_q |= 1u << q;
         }
