@@ -262,31 +262,10 @@ dms_status launch_gradient(dms_ctx* c) {
     A.err = c->err;
     StageTimer tm(c, 5);
     if (c->ndim >= 2) {
-        // persistent grid: as many CTAs as fit on the device, each warp strides over
-        // 32-vertex chunks
-        int dev = 0, sms = 148, per = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (c->ndim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gradient<3>, kBlockG, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gradient<2>, kBlockG, 0);
-        const int64_t need = ceil_div(ceil_div(c->N, 32), kBlockG / 32);
-#ifndef DMS_PERSISTENT
-#define DMS_PERSISTENT 0
-#endif
-        const unsigned grid = (unsigned)std::max<int64_t>(
-            1, DMS_PERSISTENT ? std::min<int64_t>(need, (int64_t)sms * std::max(per, 1)) : need);
-#ifndef DMS_REGROUP
-#define DMS_REGROUP 1
-#endif
-        if (DMS_REGROUP) {
-            const unsigned g2 = (unsigned)ceil_div(c->N, kBlockG);
-            if (c->ndim == 3) k_gradient_rg<3><<<g2, kBlockG, 0, c->st>>>(A);
-            else k_gradient_rg<2><<<g2, kBlockG, 0, c->st>>>(A);
-        } else if (c->ndim == 3) {
-            k_gradient<3><<<grid, kBlockG, 0, c->st>>>(A);
-        } else {
-            k_gradient<2><<<grid, kBlockG, 0, c->st>>>(A);
-        }
+        // one CTA per 128 vertices; the CTA regroups its vertices by expansion work
+        const unsigned g2 = (unsigned)ceil_div(c->N, kBlockG);
+        if (c->ndim == 3) k_gradient_rg<3><<<g2, kBlockG, 0, c->st>>>(A);
+        else k_gradient_rg<2><<<g2, kBlockG, 0, c->st>>>(A);
     } else {
         k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
     }

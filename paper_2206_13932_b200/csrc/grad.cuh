@@ -86,6 +86,17 @@ __device__ __forceinline__ int kidx_tri(const StarTab& S, uint64_t IV, int ki) {
     const int hl = S.hl[ki];
     return S.tri_of[rk(IV, hl >> 4)][rk(IV, hl & 15)];
 }
+// One comparable 16-bit key space for the PQ heads (lexicographic order of the lower
+// star, PAPER.md 1380-1414): triangle (hi,lo) -> (C(hi,2)+lo+1) << 4; tet (hi,mid,lo)
+// -> (C(hi,2)+mid+1) << 4 | (lo+1); edge of rank r >= 1 -> ((C(r,2)+1) << 4) - 1.
+__device__ __forceinline__ uint32_t cmp_tri(int ki) { return (uint32_t)(ki + 1) << 4; }
+__device__ __forceinline__ uint32_t cmp_edge(int r) { return ((uint32_t)((r * (r - 1) >> 1) + 1) << 4) - 1u; }
+__device__ __forceinline__ uint32_t cmp_tet(const StarTab& S, uint64_t R, int q) {
+    int a = rk(R, S.tet_a[q]), b = rk(R, S.tet_b[q]), c = rk(R, S.tet_c[q]);
+    int hi = max(a, max(b, c)), lo = min(a, min(b, c));
+    int mid = a + b + c - hi - lo;
+    return ((uint32_t)((hi * (hi - 1) >> 1) + mid + 1) << 4) | (uint32_t)(lo + 1);
+}
 __device__ __forceinline__ uint32_t kidx_key(const StarTab& S, int ki) {
     const int hl = S.hl[ki];
     return ((uint32_t)((hl >> 4) + 1) << 8) | ((uint32_t)((hl & 15) + 1) << 4);
@@ -117,18 +128,17 @@ constexpr int kBlockG = DMS_BLOCKG;  // threads per CTA of the gradient kernel
 // Per-thread key caches in shared memory, laid out [cell][thread] (bank-conflict
 // free): tri slot -> key index, tet slot -> 12-bit key.  Filled once per vertex.
 struct KeyCache {
-    uint8_t* tki;   // tki[t * kBlockG]
-    uint16_t* qk;   // qk[q * kBlockG]
+    uint8_t* tki;   // tki[t * kBlockG]: tri slot -> key index
+    uint16_t* qk;   // qk[q * kBlockG]: tet slot -> comparable key (cmp_tet)
     uint64_t R;
     const StarTab* S;
     __device__ __forceinline__ int tri(int t) const {
         if (DMS_KEYCACHE) return tki[t * kBlockG];
         return tri_kidx(*S, R, t);
     }
-    __device__ __forceinline__ uint32_t tet(int q) const {
-        if (DMS_KEYCACHE) return qk[q * kBlockG];
-        return key_tet(*S, R, q);
-    }
+    __device__ __forceinline__ uint32_t tet(int q) const { return qk[q * kBlockG]; }
+    uint64_t IV;
+    __device__ __forceinline__ int slot(int ki) const { return kidx_tri(*S, IV, ki); }
 };
 
 // minimum-key member of a tet slot mask: returns slot, key via *k (0xffffffff if empty)
@@ -231,12 +241,12 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
             // every cell in PQone has exactly one unclassified facet (cells leave PQone
             // when they reach zero or get classified), so each pop pairs
             const int ki = kfirst(st.pq1_t);
-            const uint32_t ktri = ki >= 0 ? kidx_key(S, ki) : 0xffffffffu;
+            const uint32_t ktri = ki >= 0 ? cmp_tri(ki) : 0xffffffffu;
             uint32_t ktet = 0xffffffffu;
             const int q = (D == 3 && st.pq1_q) ? tet_min(C, st.pq1_q, &ktet) : -1;
             if (ktri < ktet) {
                 kclr(st.pq1_t, ki);
-                const int s = kidx_tri(S, IV, ki);
+                const int s = C.slot(ki);
                 const int a = S.tri_a[s];
                 const bool ua = !((st.cls_e >> a) & 1u);
                 const int e = ua ? a : S.tri_b[s];  // the unique unclassified facet
@@ -262,9 +272,9 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
             }
         }
         // PQzero: minimum over edges (rank space), triangles (key space), tets
-        const uint32_t ke = st.pq0_er ? ((uint32_t)(__ffs(st.pq0_er)) << 8) : 0xffffffffu;  // (rank+1) << 8
+        const uint32_t ke = st.pq0_er ? cmp_edge(__ffs(st.pq0_er) - 1) : 0xffffffffu;
         const int ki = kfirst(st.pq0_t);
-        const uint32_t kt = ki >= 0 ? kidx_key(S, ki) : 0xffffffffu;
+        const uint32_t kt = ki >= 0 ? cmp_tri(ki) : 0xffffffffu;
         uint32_t kq = 0xffffffffu;
         const int q = (D == 3 && st.pq0_q) ? tet_min(C, st.pq0_q, &kq) : -1;
         if (ke == 0xffffffffu && kt == 0xffffffffu && kq == 0xffffffffu) break;
@@ -277,7 +287,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
             push_tris_of_edge<D>(S, C, st, e);
         } else if (kt < kq) {
             kclr(st.pq0_t, ki);
-            const int s = kidx_tri(S, IV, ki);
+            const int s = C.slot(ki);
             st.cls_t |= 1ull << s;
             st.crit_t |= 1ull << s;
             push_tets_of_tri<D>(S, st, s);
@@ -303,193 +313,6 @@ __device__ __forceinline__ int64_t warp_append(unsigned long long* total, uint32
     if (lane == 31 && tot) base = atomicAdd(total, (unsigned long long)tot);
     base = __shfl_sync(0xffffffffu, base, 31);
     return (int64_t)base + (inc - cnt);
-}
-
-// Persistent kernel: each warp takes 32 consecutive vertices at a time (one per lane).
-template <int D>
-__global__ void __launch_bounds__(kBlockG) k_gradient(GradArgs A) {
-    constexpr int NE = Geo<D>::NE;
-    __shared__ StarTab S;
-    __shared__ uint8_t s_tki[kMaxNT * kBlockG];
-    __shared__ uint16_t s_qk[(D == 3 ? kMaxNQ : 1) * kBlockG];
-    {
-        const int4* src = reinterpret_cast<const int4*>(A.tab);
-        int4* dst = reinterpret_cast<int4*>(&S);
-        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlockG) dst[i] = src[i];
-    }
-    __syncthreads();
-    KeyCache C;
-    C.tki = s_tki + threadIdx.x;
-    C.qk = s_qk + threadIdx.x;
-    C.S = &S;
-    C.R = 0;
-    const int64_t nchunks = (A.N + 31) >> 5;
-    const int64_t nwarps = (int64_t)gridDim.x * (kBlockG / 32);
-    const int LxLy = A.Lx * A.Ly;
-    for (int64_t chunk = ((int64_t)blockIdx.x * kBlockG + threadIdx.x) >> 5; chunk < nchunks; chunk += nwarps) {
-        const int64_t v = chunk * 32 + (threadIdx.x & 31);
-        const bool active = v < A.N;
-        StarState st;
-        st.Le = 0; st.Lq = 0; st.Lt = 0;
-        st.cls_e = st.crit_e = st.pq0_er = 0;
-        st.cls_t = st.crit_t = 0;
-        st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
-        st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
-        st.tcode_lo = st.tcode_hi = st.qcode = 0;
-        st.vcode = -1;
-        uint64_t R = 0, IV = 0;
-        bool crit_v = false;
-        if (active) {
-            const int vv = (int)v;
-            const int cx = vv % A.Lx;
-            const int t = vv / A.Lx;
-            const int cy = t % A.Ly;
-            const int cz = t / A.Ly;
-            const float fx = A.f[v];
-            if (is_nan_bits(fx)) atomicOr(A.err, 1);
-            const uint32_t ox = ord_of(fx);
-            uint32_t o[NE];
-#pragma unroll
-            for (int s = 0; s < NE; s++) {
-                const int dx = off_c<D>(s, 0), dy = off_c<D>(s, 1), dz = off_c<D>(s, 2);
-                bool in = true;
-                if (dx < 0) in &= cx > 0;
-                if (dx > 0) in &= cx < A.Lx - 1;
-                if (dy < 0) in &= cy > 0;
-                if (dy > 0) in &= cy < A.Ly - 1;
-                if (dz < 0) in &= cz > 0;
-                if (dz > 0) in &= cz < A.Lz - 1;
-                o[s] = 0xffffffffu;
-                if (in) {
-                    const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
-                    const bool lower = (os < ox) || (os == ox && s < NE / 2);
-                    if (lower) { o[s] = os; st.Le |= 1u << s; }
-                }
-            }
-            if (st.Le == 0) {
-                crit_v = true;
-            } else {
-                // local ranks among the lower neighbours (non-lower ones hold the 0xffffffff
-                // sentinel, larger than any ordered float, so they never count)
-                int r[NE];
-#pragma unroll
-                for (int s = 0; s < NE; s++) r[s] = 0;
-#pragma unroll
-                for (int s = 0; s < NE; s++)
-#pragma unroll
-                    for (int u = s + 1; u < NE; u++) {
-                        const bool s_lt_u = o[s] <= o[u];  // equal values: the smaller slot first
-                        r[u] += s_lt_u ? 1 : 0;
-                        r[s] += s_lt_u ? 0 : 1;
-                    }
-                int delta = 0;
-#pragma unroll
-                for (int s = 0; s < NE; s++) {
-                    if ((st.Le >> s) & 1u) {
-                        R |= (uint64_t)r[s] << (4 * s);
-                        IV |= (uint64_t)s << (4 * r[s]);
-                        if (r[s] == 0) delta = s;
-                    }
-                }
-                // lower triangles / tets: all their link vertices lower
-                uint64_t ta = 0, tb = 0;
-                uint32_t qa = 0, qb = 0, qc = 0;
-                uint32_t le = st.Le;
-                while (le) {
-                    const int s = __ffs(le) - 1;
-                    le &= le - 1;
-                    ta |= S.tri_amask[s];
-                    tb |= S.tri_bmask[s];
-                    if (D == 3) {
-                        qa |= S.tet_amask[s];
-                        qb |= S.tet_bmask[s];
-                        qc |= S.tet_cmask[s];
-                    }
-                }
-                st.Lt = ta & tb;
-                st.Lq = qa & qb & qc;
-                if (DMS_KEYCACHE) {
-                    uint64_t m = st.Lt;
-                    while (m) {
-                        const int tt = __ffsll((long long)m) - 1;
-                        m &= m - 1;
-                        C.tki[tt * kBlockG] = (uint8_t)tri_kidx(S, R, tt);
-                    }
-                    if (D == 3) {
-                        uint32_t mq = st.Lq;
-                        while (mq) {
-                            const int q = __ffs(mq) - 1;
-                            mq &= mq - 1;
-                            C.qk[q * kBlockG] = (uint16_t)key_tet(S, R, q);
-                        }
-                    }
-                }
-                C.R = R;
-                process_star<D>(S, C, R, IV, __popc(st.Le), delta, st);
-            }
-            // gradient word
-            if (D == 3) {
-                const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
-                const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
-                reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
-            } else {
-                const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
-                reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
-            }
-        }
-        // ---- critical cells (Alg. 2 l. 10-12), appended with one atomic per warp and
-        // dimension; their order is irrelevant because C_k is sorted by key afterwards.
-        const uint32_t c0 = crit_v ? 1u : 0u, c1 = __popc(st.crit_e), c2 = __popcll(st.crit_t),
-                       c3 = __popc(st.crit_q);
-        if (!__any_sync(0xffffffffu, (c0 | c1 | c2 | c3) != 0u)) continue;
-        const uint64_t rkey = (active && (c0 | c1 | c2 | c3)) ? ((uint64_t)(uint32_t)A.rank[v] << 12) : 0ull;
-        {
-            const int64_t p = warp_append(&A.totals[0], c0);
-            if (c0 && p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
-        }
-        {
-            int64_t p = warp_append(&A.totals[1], c1);
-            uint32_t m = st.crit_e;
-            while (m) {
-                const int s = __ffs(m) - 1;
-                m &= m - 1;
-                if (p < A.cap[1]) {
-                    const int64_t anc = v + S.e_anc[s][0] + A.Lx * S.e_anc[s][1] + LxLy * S.e_anc[s][2];
-                    A.crit_id[1][p] = A.ncell[1] * anc + S.e_k[s];
-                    A.crit_key[1][p] = rkey | key_edge(R, s);
-                }
-                p++;
-            }
-        }
-        {
-            int64_t p = warp_append(&A.totals[2], c2);
-            uint64_t m = st.crit_t;
-            while (m) {
-                const int t = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                if (p < A.cap[2]) {
-                    const int64_t anc = v + S.t_anc[t][0] + A.Lx * S.t_anc[t][1] + LxLy * S.t_anc[t][2];
-                    A.crit_id[2][p] = A.ncell[2] * anc + S.t_k[t];
-                    A.crit_key[2][p] = rkey | key_tri(S, R, t);
-                }
-                p++;
-            }
-        }
-        if (D == 3) {
-            int64_t p = warp_append(&A.totals[3], c3);
-            uint32_t m = st.crit_q;
-            while (m) {
-                const int q = __ffs(m) - 1;
-                m &= m - 1;
-                if (p < A.cap[3]) {
-                    const int64_t anc = v + S.q_anc[q][0] + A.Lx * S.q_anc[q][1] + LxLy * S.q_anc[q][2];
-                    A.crit_id[3][p] = A.ncell[3] * anc + S.q_k[q];
-                    A.crit_key[3][p] = rkey | key_tet(S, R, q);
-                }
-                p++;
-            }
-        }
-    }
 }
 
 // ---- regrouped variant: each CTA first builds every lower star's setup state
@@ -589,14 +412,15 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
                 while (m) {
                     const int tt = __ffsll((long long)m) - 1;
                     m &= m - 1;
-                    s_tki[tt * kBlockG + tid] = (uint8_t)tri_kidx(S, R, tt);
+                    const int kix = tri_kidx(S, R, tt);
+                    s_tki[tt * kBlockG + tid] = (uint8_t)kix;
                 }
                 if (D == 3) {
                     uint32_t mq = Lq;
                     while (mq) {
                         const int q = __ffs(mq) - 1;
                         mq &= mq - 1;
-                        s_qk[q * kBlockG + tid] = (uint16_t)key_tet(S, R, q);
+                        s_qk[q * kBlockG + tid] = (uint16_t)cmp_tet(S, R, q);
                     }
                 }
                 w = min(63, __popcll(Lt) + __popc(Lq) + 1);
@@ -647,6 +471,7 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
         KeyCache C;
         C.tki = s_tki + p;
         C.qk = s_qk + p;
+        C.IV = IV;
         C.S = &S;
         C.R = R;
         process_star<D>(S, C, R, IV, __popc(st.Le), (int)((word >> 16) & 15u), st);
