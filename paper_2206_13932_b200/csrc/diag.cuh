@@ -284,6 +284,164 @@ __global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ ids, int64_t m, 
     arc_b[j] = end[1];
 }
 
+// Work-queue version of the dual chases (3D / 2D): a persistent grid; every lane owns
+// one chase (one side of one arc) and walks one hop per iteration; a lane whose chase
+// ended takes the next job (warp-aggregated atomic on a global counter), so long and
+// short paths no longer leave lanes idle.  Jobs: 2 per critical (d-1)-simplex, ids in
+// emission order; results go to out_a / out_b in the same order.
+template <int D>
+struct ChaseState {
+    uint32_t x, ox;
+    int T;       // top-cell slot in x's star
+    int cx, cy, cz;
+    uint64_t w;  // x's gradient word (3D: hi half; 2D: the uint16)
+};
+
+template <int D>
+__device__ __forceinline__ uint64_t load_w(const Geo3& g, uint32_t x) {
+    if (D == 3) return __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * (uint64_t)x + 1);
+    return __ldg(reinterpret_cast<const uint16_t*>(g.grad) + x);
+}
+
+// one hop; returns -2 to continue, else the end node (a maximum's node or vnode)
+template <int D>
+__device__ __forceinline__ int32_t chase_step(const Geo3& g, const StarTab& S, ChaseState<D>& c,
+                                              const int32_t* node_of, int32_t vnode) {
+    constexpr int NE = D == 3 ? 14 : 6;
+    const int T = c.T;
+    const int code = D == 3 ? (int)((c.w >> (8 + 2 * T)) & 3ull) : (int)((c.w >> (3 + 2 * T)) & 3ull);
+    if (code == 0) {  // a critical top cell: a maximum
+        int64_t id;
+        if (D == 3)
+            id = 6 * ((int64_t)c.x + S.q_anc[T][0] + (int64_t)g.Lx * S.q_anc[T][1] + (int64_t)g.Lx * g.Ly * S.q_anc[T][2]) +
+                 S.q_k[T];
+        else
+            id = 2 * ((int64_t)c.x + S.t_anc[T][0] + (int64_t)g.Lx * S.t_anc[T][1]) + S.t_k[T];
+        return node_of[id];
+    }
+    int T2, s2, j;
+    if (D == 3) {
+        const int tt = S.tet_tri[T][code - 1];  // s' = Pair(c)
+        T2 = S.tri_tet[tt][0] == T ? S.tri_tet[tt][1] : S.tri_tet[tt][0];
+        if (T2 == 255) return vnode;
+        s2 = S.tet_a[T2] ^ S.tet_b[T2] ^ S.tet_c[T2] ^ S.tri_a[tt] ^ S.tri_b[tt];
+        j = S.tet_a[T2] == s2 ? 0 : (S.tet_b[T2] == s2 ? 1 : 2);
+    } else {
+        const int e = code == 1 ? S.tri_a[T] : S.tri_b[T];
+        T2 = S.edge_tri[e][0] == T ? S.edge_tri[e][1] : S.edge_tri[e][0];
+        if (T2 == 255) return vnode;
+        s2 = S.tri_a[T2] ^ S.tri_b[T2] ^ e;
+        j = S.tri_a[T2] == s2 ? 0 : 1;
+    }
+    const int nx = c.cx + S.off[s2][0], ny = c.cy + S.off[s2][1], nz = c.cz + S.off[s2][2];
+    if (!in_grid(g, nx, ny, nz)) return vnode;  // s' on the boundary: the virtual maximum
+    const uint32_t n2 = c.x + (uint32_t)S.lin[s2];
+    const uint32_t on = ord_of(__ldg(g.f + n2));
+    if (nb_lower(on, c.ox, s2, NE)) {
+        c.T = T2;  // the other cofacet of s' is still in St^-(x)
+    } else {       // it climbs to n2
+        c.T = D == 3 ? S.q_reslot[T2][j] : S.t_reslot[T2][j];
+        c.x = n2;
+        c.ox = on;
+        c.cx = nx; c.cy = ny; c.cz = nz;
+        c.w = load_w<D>(g, n2);
+    }
+    return -2;
+}
+
+// start of a job: the critical (d-1)-simplex ids[job >> 1], cofacet side job & 1.
+// Returns -2 with c set, or the end node directly.
+template <int D>
+__device__ __forceinline__ int32_t chase_start(const Geo3& g, const StarTab& S, const int64_t* ids, int job,
+                                               ChaseState<D>& c, const int32_t* node_of, int32_t vnode) {
+    constexpr int NE = D == 3 ? 14 : 6;
+    const int64_t id = ids[job >> 1];
+    const int side = job & 1;
+    const int64_t a = id / g.ncell[D - 1];
+    const int k = (int)(id % g.ncell[D - 1]);
+    uint32_t p[3], o[3];
+    p[0] = (uint32_t)a;
+#pragma unroll
+    for (int q = 1; q < D; q++) p[q] = (uint32_t)(a + lin_mask(g, S.chain[D - 1][k][q - 1]));
+#pragma unroll
+    for (int q = 0; q < D; q++) o[q] = ord_of(__ldg(g.f + p[q]));
+    int jx = 0;
+#pragma unroll
+    for (int q = 1; q < D; q++)
+        if (o[jx] < o[q] || (o[jx] == o[q] && p[jx] < p[q])) jx = q;
+    const uint32_t x = p[jx], ox = o[jx];
+    int cx, cy, cz;
+    coords_of(g, x, cx, cy, cz);
+    int T, s3;
+    if (D == 3) {
+        const int t = S.t_slot[k][jx];
+        T = S.tri_tet[t][side];
+        if (T == 255) return vnode;
+        s3 = S.tet_a[T] ^ S.tet_b[T] ^ S.tet_c[T] ^ S.tri_a[t] ^ S.tri_b[t];
+    } else {
+        const int e = S.e_slot[k][jx];
+        T = S.edge_tri[e][side];
+        if (T == 255) return vnode;
+        s3 = S.tri_a[T] ^ S.tri_b[T] ^ e;
+    }
+    const int nx = cx + S.off[s3][0], ny = cy + S.off[s3][1], nz = cz + S.off[s3][2];
+    if (!in_grid(g, nx, ny, nz)) return vnode;
+    const uint32_t n3 = x + (uint32_t)S.lin[s3];
+    const uint32_t on = ord_of(__ldg(g.f + n3));
+    if (nb_lower(on, ox, s3, NE)) {
+        c.x = x; c.ox = ox; c.T = T; c.cx = cx; c.cy = cy; c.cz = cz;
+    } else {
+        int jj;
+        if (D == 3) jj = S.tet_a[T] == s3 ? 0 : (S.tet_b[T] == s3 ? 1 : 2);
+        else jj = S.tri_a[T] == s3 ? 0 : 1;
+        c.T = D == 3 ? S.q_reslot[T][jj] : S.t_reslot[T][jj];
+        c.x = n3; c.ox = on; c.cx = nx; c.cy = ny; c.cz = nz;
+    }
+    c.w = load_w<D>(g, c.x);
+    return -2;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* __restrict__ ids, int njobs,
+                                                       const int32_t* __restrict__ node_of, int32_t vnode,
+                                                       int32_t* __restrict__ out_a, int32_t* __restrict__ out_b,
+                                                       int* job_ctr) {
+    const StarTab& S = *g.tab;
+    const int lane = threadIdx.x & 31;
+    ChaseState<D> c;
+    c.x = c.ox = 0; c.T = 0; c.cx = c.cy = c.cz = 0; c.w = 0;
+    int job = -1;          // current job, -1: none
+    bool done = false;     // the queue is exhausted for this lane
+    while (true) {
+        // lanes without a job take one (warp-aggregated), and may finish at once
+        const bool need = job < 0 && !done;
+        const unsigned nm = __ballot_sync(0xffffffffu, need);
+        if (nm) {
+            int base = 0;
+            if (lane == __ffs(nm) - 1) base = atomicAdd(job_ctr, __popc(nm));
+            base = __shfl_sync(0xffffffffu, base, __ffs(nm) - 1);
+            if (need) {
+                const int jb = base + __popc(nm & lanemask_lt());
+                if (jb >= njobs) {
+                    done = true;
+                } else {
+                    const int32_t r = chase_start<D>(g, S, ids, jb, c, node_of, vnode);
+                    if (r != -2) (jb & 1 ? out_b : out_a)[jb >> 1] = r;
+                    else job = jb;
+                }
+            }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        if (job >= 0) {
+            const int32_t r = chase_step<D>(g, S, c, node_of, vnode);
+            if (r != -2) {
+                (job & 1 ? out_b : out_a)[job >> 1] = r;
+                job = -1;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- union-find
 // Arcs are indexed in processing order; an arc's index is its key.  Nodes are the
 // extrema; older_is_smaller = true for D0 (node = position in ascending C_0), false
@@ -401,8 +559,8 @@ __global__ void k_gather_undecided(const int32_t* out, int64_t m, const uint32_t
 constexpr int kUFTail = 2048;
 
 struct UFArgs {
-    const int32_t* arc_a;
-    const int32_t* arc_b;
+    int32_t* arc_a;  // endpoints are replaced by their current roots every round
+    int32_t* arc_b;
     int32_t* parent;
     uint32_t* best;
     int32_t* ra;
@@ -439,6 +597,8 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
             const int32_t b = uf_find(U.parent, U.arc_b[i]);
             U.ra[i] = a;
             U.rb[i] = b;
+            U.arc_a[i] = a;  // find(old root) == find(endpoint): next round starts here
+            U.arc_b[i] = b;
             if (a == b) { U.out[i] = -1; continue; }
             atomicMin(&U.best[a], (uint32_t)i);
             atomicMin(&U.best[b], (uint32_t)i);

@@ -480,8 +480,21 @@ dms_status run_dtop(dms_ctx* c) {
     c->launches++;
     if (m) {
         StageTimer t7(c, 7);
-        k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), m, c->node_oftop, (int32_t)nd,
-                                                      u.ra, u.rb);
+        if (d == 3) {
+            // persistent work-queue chases, 2 jobs per arc (long ascending paths in 3D)
+            int dev = 0, sms = 148, per = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<3>, kBlock, 0);
+            const unsigned grid = (unsigned)std::max<int64_t>(
+                1, std::min<int64_t>(grid_for(2 * m), (int64_t)sms * std::max(per, 1)));
+            CU(cudaMemsetAsync(c->tile_ctr, 0, sizeof(int), c->st));
+            k_dtop_arcs_q<3><<<grid, kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), (int)(2 * m), c->node_oftop,
+                                                        (int32_t)nd, u.ra, u.rb, c->tile_ctr);
+        } else {
+            k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), m, c->node_oftop, (int32_t)nd,
+                                                          u.ra, u.rb);
+        }
         k_permute_arcs<<<grid_for(m), kBlock, 0, c->st>>>(u.ra, u.rb, crit_perm(c, d - 1), m, 1, u.arc_a, u.arc_b);
         c->launches += 2;
     }
