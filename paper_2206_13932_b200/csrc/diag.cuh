@@ -571,6 +571,7 @@ struct UFArgs {
     int* nlive;   // [2]
     int* status;  // [1]: -1 finished, else the number of undecided arcs left in live[cur]
     int* cur_out; // [1]
+    int* trace;   // [64]: live arcs at the start of each round; [63] = rounds run
     bool older_is_smaller;
     int max_rounds;
 };
@@ -589,6 +590,10 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
         int32_t* live = cur ? U.live1 : U.live0;
         int32_t* nxt = cur ? U.live0 : U.live1;
         const int n = ld_cg_int(&U.nlive[cur]);
+        if (gtid == 0) {
+            if (round < 63) U.trace[round] = n;
+            U.trace[63] = round;
+        }
         if (n <= kUFTail) break;
         // phase 1: roots, cycle arcs, lightest arc of every root
         for (int idx = gtid; idx < n; idx += stride) {

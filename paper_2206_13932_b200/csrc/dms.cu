@@ -49,6 +49,7 @@ struct UFBuf {
     int32_t *arc_a = nullptr, *arc_b = nullptr, *ra = nullptr, *rb = nullptr, *out = nullptr, *list = nullptr;
     int32_t* live2 = nullptr;
     int* nlive = nullptr;  // two device counters
+    int* trace = nullptr;  // [64] union-find round trace
     int32_t* parent = nullptr;
     uint32_t *best = nullptr, *flags = nullptr, *pos = nullptr;
     int64_t cap_arcs = 0, cap_nodes = 0;
@@ -203,6 +204,7 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
             CU(dalloc(p, arcs));
         }
         if (!u.nlive) CU(dalloc(&u.nlive, 4));
+        if (!u.trace) CU(dalloc(&u.trace, 64));
         for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
         u.cap_arcs = arcs;
     }
@@ -360,6 +362,7 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older
     U.nlive = u.nlive;
     U.status = u.nlive + 2;
     U.cur_out = u.nlive + 3;
+    U.trace = u.trace;
     U.older_is_smaller = older_is_smaller;
     U.max_rounds = 4096;
     void* args[] = {&U};
@@ -775,6 +778,13 @@ dms_status dms_stage_ms(dms_ctx* c, double ms_out[11]) {
 
 int64_t dms_launch_count(const dms_ctx* c) { return c ? c->launches : 0; }
 
+// internal diagnostics (not part of include/dms.h): live arcs per union-find round
+int dms_internal_uf_trace(dms_ctx* c, int which, int out[64]) {
+    if (!c || which < 0 || which > 1 || !c->uf[which].trace) return 1;
+    cudaStreamSynchronize(c->st);
+    return cudaMemcpy(out, c->uf[which].trace, 64 * sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+}
+
 const char* dms_last_error(const dms_ctx* c) { return c ? c->msg : "null context"; }
 
 void dms_destroy(dms_ctx* c) {
@@ -803,7 +813,7 @@ void dms_destroy(dms_ctx* c) {
     for (int b = 0; b < 2; b++) {
         UFBuf& u = c->uf[b];
         for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.ra, (void*)u.rb, (void*)u.out, (void*)u.list,
-                        (void*)u.live2, (void*)u.nlive,
+                        (void*)u.live2, (void*)u.nlive, (void*)u.trace,
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
             cudaFree(p);
         cudaFree(c->pairs[b]);
