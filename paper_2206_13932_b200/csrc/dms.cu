@@ -234,7 +234,7 @@ dms_status run_order(dms_ctx* c, int32_t* d_rank) {
     CU(cudaMemsetAsync(c->kmax, 0, sizeof(unsigned long long), c->st));
     // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
     // (and detects NaN / the highest vertex), the last pass writes rank[index]
-    radix_sort<uint32_t, uint32_t, 16>(c->okeys[0], c->ovals[0], c->okeys[1], c->ovals[1], c->N, 0, 32, c->ss, c->st,
+    radix_sort<uint32_t, uint32_t, 12>(c->okeys[0], c->ovals[0], c->okeys[1], c->ovals[1], c->N, 0, 32, c->ss, c->st,
                                        &c->launches, c->rank, c->f, c->err, c->kmax);
     CU(cudaGetLastError());
     c->have_order = true;
