@@ -279,7 +279,7 @@ def main():
     g_ms = stages["gradient_kernel"] / max(1, stages["gradient_launches"])
     g_ach = bmin_grad / (g_ms / 1e3) / 1e9
     roofline = {
-        "kernel": "k_gradient<%d> (lower-star gradient + critical compaction)" % ndim,
+        "kernel": ("k_gradient_rg<%d> (lower-star gradient + critical records)" % ndim) if ndim > 1 else "k_gradient1",
         "bound": "hbm", "achieved": round(g_ach, 1), "peak": peak, "unit": "GB/s",
         "frac": round(g_ach / peak, 4), "traffic": None,
         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(bmin_grad), "ms_per_launch": round(g_ms, 4),

@@ -95,7 +95,9 @@ size_t dms_gradient_bytes(const dms_ctx* ctx);
  * d_grad: caller-owned device buffer of dms_gradient_bytes(ctx) bytes, one packed
  * word per vertex encoding, for every simplex of the vertex's lower star that is the
  * head of a discrete vector, which facet it is paired with (layout: DESIGN.md
- * "Gradient words").  Runs dms_order first if it has not run.  Asynchronous. */
+ * "Gradient words").  Independent of dms_order (it compares values and indices
+ * directly); dms_critical needs both and runs dms_order if it has not run.
+ * Asynchronous. */
 dms_status dms_gradient(dms_ctx* ctx, void* d_grad);
 
 /* Critical simplices C_0..C_d, each sorted by the lexicographic order (Alg. 2 l. 13,
@@ -118,9 +120,9 @@ dms_status dms_diagram_top(dms_ctx* ctx, int mode, const dms_pair** d_pairs, int
  * D_{d-1}.  Ascending lex order; library-owned device int64.  Synchronises. */
 dms_status dms_unpaired_saddles(dms_ctx* ctx, int which, const int64_t** d_ids, int64_t* h_n);
 
-/* Run the whole front end (order, gradient, critical lists, D0, D_{d-1}) on the
- * stream; the host only synchronises to read the critical counts and the union-find
- * progress counters.  Results are read with the calls above afterwards.
+/* Run the whole front end (order, gradient, critical lists, D0, D_{d-1}); the vertex
+ * order runs on an internal second stream concurrently with the gradient and is joined
+ * before the critical sort.  The host synchronises to read the critical and pair counts.  Results are read with the calls above afterwards.
  * d_rank / d_grad may be NULL (library-owned scratch). */
 dms_status dms_run_all(dms_ctx* ctx, int32_t* d_rank, void* d_grad);
 

@@ -87,6 +87,15 @@ __global__ void k_permute_arcs(const int32_t* __restrict__ ta, const int32_t* __
     arc_b[j] = tb[r];
 }
 
+// sort key of a critical cell: x << 12 | G  ->  rank(x) << 12 | G
+__global__ void k_rekey(uint64_t* __restrict__ keys, int64_t m, const int32_t* __restrict__ rank) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        const uint64_t k = keys[i];
+        keys[i] = ((uint64_t)(uint32_t)rank[k >> 12] << 12) | (k & 0xfffull);
+    }
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) a[i] = (uint32_t)i;

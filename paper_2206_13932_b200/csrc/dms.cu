@@ -63,6 +63,9 @@ struct dms_ctx {
     int64_t N = 0;
     const float* f = nullptr;
     cudaStream_t st = nullptr;
+    cudaStream_t st2 = nullptr;          // the vertex order runs here, beside the gradient
+    cudaEvent_t ev_in = nullptr, ev_order = nullptr;
+    bool order_pending = false;          // st must wait ev_order before using ranks
     int64_t ncell[4] = {1, 0, 0, 0};
     StarTab htab;
     StarTab* dtab = nullptr;
@@ -228,7 +231,7 @@ dms_status read_err(dms_ctx* c) {
 
 // ------------------------------------------------------------------ stages
 
-dms_status run_order(dms_ctx* c, int32_t* d_rank) {
+dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank) {
     StageTimer tm(c, 0);
     c->rank = d_rank ? d_rank : c->rank_scratch;
     CU(cudaMemsetAsync(c->kmax, 0, sizeof(unsigned long long), c->st));
@@ -238,7 +241,37 @@ dms_status run_order(dms_ctx* c, int32_t* d_rank) {
                                        &c->launches, c->rank, c->f, c->err, c->kmax);
     CU(cudaGetLastError());
     c->have_order = true;
-    c->have_grad = c->have_crit = c->have_d[0] = c->have_d[1] = false;
+    c->have_crit = c->have_d[0] = c->have_d[1] = false;  // the gradient does not depend on ranks
+    return DMS_OK;
+}
+
+// concurrent = true: the order is enqueued on the second stream after the caller's
+// stream (the field is ready), and the caller's stream waits for it only when ranks are
+// needed (dms_critical's sort keys).  The order is memory-bound and the gradient kernel
+// ALU-bound, so they overlap.
+dms_status run_order(dms_ctx* c, int32_t* d_rank, bool concurrent = false) {
+    if (!concurrent) {
+        c->order_pending = false;
+        return run_order_on_stream(c, d_rank);
+    }
+    CU(cudaEventRecord(c->ev_in, c->st));
+    CU(cudaStreamWaitEvent(c->st2, c->ev_in, 0));
+    cudaStream_t main = c->st;
+    c->st = c->st2;
+    dms_status s = run_order_on_stream(c, d_rank);
+    c->st = main;
+    if (s) return s;
+    CU(cudaEventRecord(c->ev_order, c->st2));
+    c->order_pending = true;
+    return DMS_OK;
+}
+
+dms_status join_order(dms_ctx* c) {
+    if (!c->have_order) return run_order(c, nullptr);
+    if (c->order_pending) {
+        CU(cudaStreamWaitEvent(c->st, c->ev_order, 0));
+        c->order_pending = false;
+    }
     return DMS_OK;
 }
 
@@ -253,7 +286,6 @@ dms_status launch_gradient(dms_ctx* c) {
     A.N = c->N;
     A.tab = c->dtab;
     A.grad = c->grad;
-    A.rank = c->rank;
     for (int k = 0; k < 4; k++) {
         A.crit_id[k] = c->cid[0][k];
         A.crit_key[k] = c->ckey[0][k];
@@ -277,10 +309,6 @@ dms_status launch_gradient(dms_ctx* c) {
 }
 
 dms_status run_gradient(dms_ctx* c, void* d_grad) {
-    if (!c->have_order) {
-        dms_status s = run_order(c, nullptr);
-        if (s) return s;
-    }
     c->grad = d_grad ? d_grad : c->grad_scratch;
     StageTimer tm(c, 1);
     dms_status s = launch_gradient(c);
@@ -305,10 +333,12 @@ dms_status run_critical(dms_ctx* c) {
         dms_status s = run_gradient(c, nullptr);
         if (s) return s;
     }
+    dms_status s = join_order(c);  // ranks (and the NaN flag of the order pass) needed from here
+    if (s) return s;
     StageTimer tm(c, 2);
     unsigned long long tot[4] = {0, 0, 0, 0};
     CU(cudaMemcpyAsync(tot, c->totals, sizeof tot, cudaMemcpyDeviceToHost, c->st));
-    dms_status s = read_err(c);
+    s = read_err(c);
     if (s) return s;
     bool overflow = false;
     for (int k = 0; k <= c->ndim; k++)
@@ -322,7 +352,9 @@ dms_status run_critical(dms_ctx* c) {
     for (int k = 0; k <= c->ndim; k++) c->ncrit[k] = (int64_t)tot[k];
     const int kbits = 12 + bits_for(c->N);
     for (int k = 0; k <= c->ndim; k++) {
+        k_rekey<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->ckey[0][k], c->ncrit[k], c->rank);
         k_iota<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cidx[0][k], c->ncrit[k]);
+        c->launches++;
         c->cur[k] = radix_sort<uint64_t, uint32_t, 8>(c->ckey[0][k], c->cidx[0][k], c->ckey[1][k], c->cidx[1][k],
                                                      c->ncrit[k], 0, kbits, c->ss, c->st, &c->launches);
         // lexicographically sorted ids = emitted ids gathered through the permutation
@@ -583,6 +615,15 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
     CA(dalloc(&c->kmax, 1));
     CA(dalloc(&c->remaining, 1));
     if (cudaMallocHost(&c->h_pinned, 64) != cudaSuccess) return bail(DMS_ERR_OOM);
+    {
+        // the order's (short, memory-bound) kernels get the highest priority so that their
+        // CTAs are scheduled first as the (long, ALU-bound) gradient CTAs retire
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    }
+    if (cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    if (cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     CA(dalloc(&c->node_of0, N));
     CA(dalloc(&c->node_oftop, c->ncell[ndim] * N));
     for (int k = 0; k <= ndim; k++) c->cap[k] = N / 2 + 1024;
@@ -676,7 +717,7 @@ dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, in
 dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     dms_status s = check_sticky(c);
     if (s) return s;
-    if ((s = run_order(c, d_rank))) return s;
+    if ((s = run_order(c, d_rank, true))) return s;  // second stream, overlaps the gradient
     if ((s = run_gradient(c, d_grad))) return s;
     if ((s = run_critical(c))) return s;
     if ((s = run_d0(c))) return s;
@@ -790,7 +831,11 @@ const char* dms_last_error(const dms_ctx* c) { return c ? c->msg : "null context
 void dms_destroy(dms_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->st);
+    if (c->st2) cudaStreamSynchronize(c->st2);
     clear_events(c);
+    if (c->st2) cudaStreamDestroy(c->st2);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
+    if (c->ev_order) cudaEventDestroy(c->ev_order);
     cudaFree(c->dtab);
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);

@@ -48,7 +48,6 @@ struct GradArgs {
     int64_t N;
     const StarTab* tab;
     void* grad;
-    const int32_t* rank;
     int64_t* crit_id[4];
     uint64_t* crit_key[4];
     int64_t cap[4];
@@ -488,7 +487,9 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
     }
     const uint32_t c0 = crit_v ? 1u : 0u, c1 = __popc(st.crit_e), c2 = __popcll(st.crit_t), c3 = __popc(st.crit_q);
     if (!__any_sync(0xffffffffu, (c0 | c1 | c2 | c3) != 0u)) return;
-    const uint64_t rkey = (active && (c0 | c1 | c2 | c3)) ? ((uint64_t)(uint32_t)A.rank[v] << 12) : 0ull;
+    // placeholder sort key x << 12 | G; dms_critical rewrites it to rank(x) << 12 | G
+    // once the vertex order (which runs concurrently on a second stream) is done
+    const uint64_t rkey = (uint64_t)v << 12;
     {
         const int64_t q0 = warp_append(&A.totals[0], c0);
         if (c0 && q0 < A.cap[0]) { A.crit_id[0][q0] = v; A.crit_key[0][q0] = rkey; }
@@ -577,7 +578,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
     }
     __syncthreads();
     if (!active || !(crit_v || crit_e)) return;
-    const uint64_t rkey = (uint64_t)(uint32_t)A.rank[v] << 12;
+    const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_rg
     if (crit_v) {
         const int64_t p = (int64_t)s_base[0] + loc0;
         if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
