@@ -96,6 +96,38 @@ __global__ void k_rekey(uint64_t* __restrict__ keys, int64_t m, const int32_t* _
     }
 }
 
+// inv[perm[p]] = p
+__global__ void k_invert(const uint32_t* __restrict__ perm, int64_t m, uint32_t* __restrict__ inv) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < m) inv[perm[p]] = (uint32_t)p;
+}
+
+// union-find inputs in emission order: arc key = processing index (rev: m-1-sorted
+// position), node age = sorted position (rev: n - sorted position; the virtual node n
+// gets age 0, the oldest)
+__global__ void k_uf_keys(const uint32_t* __restrict__ inv_arcs, int64_t m, int rev, uint32_t* __restrict__ key) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < m) key[e] = rev ? (uint32_t)(m - 1 - inv_arcs[e]) : inv_arcs[e];
+}
+__global__ void k_uf_ages(const uint32_t* __restrict__ inv_nodes, int64_t n, int rev, int32_t* __restrict__ age) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) age[r] = rev ? (int32_t)(n - inv_nodes[r]) : (int32_t)inv_nodes[r];
+    if (rev && r == n) age[n] = 0;
+}
+
+// out in processing order: outp[j] = out[perm[rev ? m-1-j : j]]
+__global__ void k_permute1(const int32_t* __restrict__ out, const uint32_t* __restrict__ perm, int64_t m, int rev,
+                           int32_t* __restrict__ outp) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < m) outp[j] = out[perm[rev ? m - 1 - j : j]];
+}
+
+__global__ void k_gather_keys(const int32_t* __restrict__ list, int64_t n, const uint32_t* __restrict__ key,
+                              uint32_t* __restrict__ out) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) out[j] = key[list[j]];
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) a[i] = (uint32_t)i;
@@ -452,10 +484,11 @@ __global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* _
 }
 
 // ---------------------------------------------------------------- union-find
-// Arcs are indexed in processing order; an arc's index is its key.  Nodes are the
-// extrema; older_is_smaller = true for D0 (node = position in ascending C_0), false
-// for D_{d-1} (node = position in ascending C_d, the virtual node the largest = the
-// oldest).  Hooks always go younger -> older, so a root is its component's oldest node.
+// Arcs and nodes are stored in emission order (spatially coherent, so the rounds hit
+// nearby nodes); every arc carries its key (its processing index: ascending lex order for
+// D0, descending for D_{d-1}) and every node its age (smaller = older; for D_{d-1} the
+// virtual node is the oldest).  Hooks always go younger -> older, so a root is its
+// component's oldest node.
 // out[i]: -2 undecided, -1 unpaired (cycle), >= 0 the node that dies at arc i.
 //
 // A round: every live arc finds its two roots; every root
@@ -486,72 +519,6 @@ __global__ void k_uf_init(int32_t* parent, uint32_t* best, int64_t n, int32_t* o
     if (i < m) { out[i] = -2; live[i] = (int32_t)i; }
 }
 
-__global__ void k_uf_round1(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b,
-                            const int32_t* __restrict__ live, const int* nlive, int32_t* parent, uint32_t* best,
-                            int32_t* ra, int32_t* rb, int32_t* out) {
-    const int n = *nlive;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-        const int32_t i = live[idx];
-        const int32_t a = uf_find(parent, arc_a[i]);
-        const int32_t b = uf_find(parent, arc_b[i]);
-        ra[i] = a;
-        rb[i] = b;
-        if (a == b) { out[i] = -1; continue; }  // the arc closes a cycle: stays unpaired
-        atomicMin(&best[a], (uint32_t)i);
-        atomicMin(&best[b], (uint32_t)i);
-    }
-}
-
-__global__ void k_uf_round2(const int32_t* __restrict__ live, const int* nlive, int32_t* parent, const uint32_t* best,
-                            const int32_t* ra, const int32_t* rb, int32_t* out, bool older_is_smaller) {
-    const int n = *nlive;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-        const int32_t i = live[idx];
-        if (out[i] != -2) continue;
-        const int32_t a = ra[i], b = rb[i];
-        const bool ma = best[a] == (uint32_t)i, mb = best[b] == (uint32_t)i;
-        const bool a_older = older_is_smaller ? (a < b) : (a > b);
-        if (ma && mb) {
-            const int32_t young = a_older ? b : a, old = a_older ? a : b;
-            parent[young] = old;
-            out[i] = young;
-        } else if (ma && !a_older) {
-            parent[a] = b;
-            out[i] = a;
-        } else if (mb && a_older) {
-            parent[b] = a;
-            out[i] = b;
-        }
-    }
-}
-
-__global__ void k_uf_round3(const int32_t* __restrict__ live, const int* nlive, uint32_t* best, const int32_t* ra,
-                            const int32_t* rb, const int32_t* out, int32_t* live_out, int* nlive_out) {
-    const int n = *nlive;
-    const int lane = threadIdx.x & 31;
-    // uniform trip count so the warp-aggregated append can use full-warp intrinsics
-    const int stride = gridDim.x * blockDim.x;
-    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-        const int idx = base + threadIdx.x;
-        bool keep = false;
-        int32_t i = 0;
-        if (idx < n) {
-            i = live[idx];
-            const int32_t o = out[i];
-            if (o != -1) {
-                best[ra[i]] = 0xffffffffu;  // reset this round's candidates
-                best[rb[i]] = 0xffffffffu;
-            }
-            keep = o == -2;
-        }
-        const unsigned mk = __ballot_sync(0xffffffffu, keep);
-        int basepos = 0;
-        if (lane == 0 && mk) basepos = atomicAdd(nlive_out, __popc(mk));
-        basepos = __shfl_sync(0xffffffffu, basepos, 0);
-        if (keep) live_out[basepos + __popc(mk & lanemask_lt())] = i;
-    }
-}
-
 __global__ void k_flag_undecided(const int32_t* out, int64_t m, uint32_t* flags) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) flags[i] = out[i] == -2 ? 1u : 0u;
@@ -570,6 +537,8 @@ constexpr int kUFTail = 2048;
 struct UFArgs {
     int32_t* arc_a;  // endpoints are replaced by their current roots every round
     int32_t* arc_b;
+    const uint32_t* key;  // per arc: its processing index (the arc order of the union-find)
+    const int32_t* age;   // per node: smaller = older
     int32_t* parent;
     uint32_t* best;
     int32_t* ra;
@@ -581,7 +550,6 @@ struct UFArgs {
     int* status;  // [1]: -1 finished, else the number of undecided arcs left in live[cur]
     int* cur_out; // [1]
     int* trace;   // [64]: live arcs at the start of each round; [63] = rounds run
-    bool older_is_smaller;
     int max_rounds;
 };
 
@@ -590,7 +558,7 @@ __device__ __forceinline__ int ld_cg_int(const int* p) { return __ldcg(p); }
 __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ int32_t s_list[kUFTail];
+    __shared__ unsigned long long s_list[kUFTail];
     const int stride = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
@@ -614,8 +582,9 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
             U.arc_a[i] = a;  // find(old root) == find(endpoint): next round starts here
             U.arc_b[i] = b;
             if (a == b) { U.out[i] = -1; continue; }
-            atomicMin(&U.best[a], (uint32_t)i);
-            atomicMin(&U.best[b], (uint32_t)i);
+            const uint32_t ki = U.key[i];
+            atomicMin(&U.best[a], ki);
+            atomicMin(&U.best[b], ki);
         }
         if (gtid == 0) U.nlive[cur ^ 1] = 0;
         grid.sync();
@@ -624,8 +593,9 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
             const int32_t i = live[idx];
             if (U.out[i] != -2) continue;
             const int32_t a = U.ra[i], b = U.rb[i];
-            const bool ma = __ldcg(&U.best[a]) == (uint32_t)i, mb = __ldcg(&U.best[b]) == (uint32_t)i;
-            const bool a_older = U.older_is_smaller ? (a < b) : (a > b);
+            const uint32_t ki = U.key[i];
+            const bool ma = __ldcg(&U.best[a]) == ki, mb = __ldcg(&U.best[b]) == ki;
+            const bool a_older = U.age[a] < U.age[b];
             if (ma && mb) {
                 const int32_t young = a_older ? b : a, old = a_older ? a : b;
                 U.parent[young] = old;
@@ -672,15 +642,16 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
     const int32_t* live = cur ? U.live1 : U.live0;
     int p2 = 1;
     while (p2 < n) p2 <<= 1;
-    for (int j = threadIdx.x; j < p2; j += blockDim.x) s_list[j] = j < n ? live[j] : 0x7fffffff;
+    for (int j = threadIdx.x; j < p2; j += blockDim.x)
+        s_list[j] = j < n ? (((unsigned long long)U.key[live[j]] << 32) | (uint32_t)live[j]) : ~0ull;
     __syncthreads();
-    // bitonic sort (ascending processing order)
+    // bitonic sort by key (ascending processing order)
     for (int k = 2; k <= p2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int t = threadIdx.x; t < p2; t += blockDim.x) {
                 const int o = t ^ j;
                 if (o > t) {
-                    const int32_t x = s_list[t], y = s_list[o];
+                    const unsigned long long x = s_list[t], y = s_list[o];
                     const bool up = (t & k) == 0;
                     if ((x > y) == up) { s_list[t] = y; s_list[o] = x; }
                 }
@@ -690,12 +661,12 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
     }
     if (threadIdx.x == 0) {
         for (int j = 0; j < n; j++) {
-            const int32_t i = s_list[j];
+            const int32_t i = (int32_t)(s_list[j] & 0xffffffffull);
             int32_t a = U.arc_a[i], b = U.arc_b[i];
             while (U.parent[a] != a) a = U.parent[a];
             while (U.parent[b] != b) b = U.parent[b];
             if (a == b) { U.out[i] = -1; continue; }
-            const bool a_older = U.older_is_smaller ? (a < b) : (a > b);
+            const bool a_older = U.age[a] < U.age[b];
             const int32_t young = a_older ? b : a, old = a_older ? a : b;
             U.parent[young] = old;
             U.out[i] = young;
@@ -707,17 +678,15 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
 // sequential Kruskal over the undecided arcs in processing order (the result equals
 // the full sequential union-find: DESIGN.md "Union-find")
 __global__ void k_uf_tail(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b, const int32_t* list,
-                          const uint32_t* n_list_from_scan, const uint32_t* flags_last, int64_t m, int32_t* parent,
-                          int32_t* out, bool older_is_smaller) {
+                          int64_t n, int32_t* parent, int32_t* out, const int32_t* __restrict__ age) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    const int64_t n = (int64_t)n_list_from_scan[0] + flags_last[0];
     for (int64_t j = 0; j < n; j++) {
         const int32_t i = list[j];
         int32_t a = arc_a[i], b = arc_b[i];
         while (parent[a] != a) a = parent[a];
         while (parent[b] != b) b = parent[b];
         if (a == b) { out[i] = -1; continue; }
-        const bool a_older = older_is_smaller ? (a < b) : (a > b);
+        const bool a_older = age[a] < age[b];
         const int32_t young = a_older ? b : a, old = a_older ? a : b;
         parent[young] = old;
         out[i] = young;
@@ -751,13 +720,14 @@ __global__ void k_flag_ge0(const int32_t* out, int64_t m, uint32_t* flags, int w
 }
 
 // D0 pairs (birth = the dying minimum, death = the critical edge), ascending arcs
-__global__ void k_emit_d0(Geo3 g, const int32_t* out, int64_t m, const uint32_t* pos, const int64_t* c0,
+// out: processing order; its values are node (minimum) emission indices into c0e
+__global__ void k_emit_d0(Geo3 g, const int32_t* out, int64_t m, const uint32_t* pos, const int64_t* c0e,
                           const int64_t* c1, PairRec* pairs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m || out[i] < 0) return;
     const StarTab& S = *g.tab;
     PairRec r;
-    r.birth_id = c0[out[i]];
+    r.birth_id = c0e[out[i]];
     r.birth_vertex = (int32_t)r.birth_id;
     r.birth_value = g.f[r.birth_id];
     r.death_id = c1[i];
@@ -770,7 +740,7 @@ __global__ void k_emit_d0(Geo3 g, const int32_t* out, int64_t m, const uint32_t*
 // D_{d-1} pairs (birth = critical (d-1)-simplex, death = the dying maximum), in
 // processing (decreasing) order
 __global__ void k_emit_dtop(Geo3 g, const int32_t* out, int64_t m, const uint32_t* pos, const int64_t* cdm1,
-                            const int64_t* cd, PairRec* pairs) {
+                            const int64_t* cde, PairRec* pairs) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m || out[j] < 0) return;
     const StarTab& S = *g.tab;
@@ -780,7 +750,7 @@ __global__ void k_emit_dtop(Geo3 g, const int32_t* out, int64_t m, const uint32_
     const int64_t bv = max_vertex(g, S, d - 1, r.birth_id);
     r.birth_vertex = (int32_t)bv;
     r.birth_value = g.f[bv];
-    r.death_id = cd[out[j]];
+    r.death_id = cde[out[j]];
     const int64_t dv = max_vertex(g, S, d, r.death_id);
     r.death_vertex = (int32_t)dv;
     r.death_value = g.f[dv];

@@ -48,6 +48,10 @@ __global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsig
 struct UFBuf {
     int32_t *arc_a = nullptr, *arc_b = nullptr, *ra = nullptr, *rb = nullptr, *out = nullptr, *list = nullptr;
     int32_t* live2 = nullptr;
+    int32_t* outp = nullptr;   // out in processing order
+    uint32_t *key = nullptr, *inv_a = nullptr;  // per arc (emission order)
+    int32_t* age = nullptr;                     // per node (emission order)
+    uint32_t* inv_n = nullptr;
     int* nlive = nullptr;  // two device counters
     int* trace = nullptr;  // [64] union-find round trace
     int32_t* parent = nullptr;
@@ -202,7 +206,11 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
     arcs = std::max<int64_t>(arcs, 1);
     nodes = std::max<int64_t>(nodes, 1);
     if (arcs > u.cap_arcs) {
-        for (int32_t** p : {&u.arc_a, &u.arc_b, &u.ra, &u.rb, &u.out, &u.list, &u.live2}) {
+        for (int32_t** p : {&u.arc_a, &u.arc_b, &u.ra, &u.rb, &u.out, &u.list, &u.live2, &u.outp}) {
+            cudaFree(*p);
+            CU(dalloc(p, arcs));
+        }
+        for (uint32_t** p : {&u.key, &u.inv_a}) {
             cudaFree(*p);
             CU(dalloc(p, arcs));
         }
@@ -214,8 +222,12 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
     if (nodes > u.cap_nodes) {
         cudaFree(u.parent);
         cudaFree(u.best);
+        cudaFree(u.age);
+        cudaFree(u.inv_n);
         CU(dalloc(&u.parent, nodes));
         CU(dalloc(&u.best, nodes));
+        CU(dalloc(&u.age, nodes));
+        CU(dalloc(&u.inv_n, nodes));
         u.cap_nodes = nodes;
     }
     return DMS_OK;
@@ -369,7 +381,8 @@ dms_status run_critical(dms_ctx* c) {
 
 
 // union-find over arcs (processing order), see diag.cuh
-dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older_is_smaller) {
+// u.arc_a / u.arc_b / u.key (per arc) and u.age (per node) are in emission order
+dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     const unsigned gi = grid_for(std::max(m, nodes));
     k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.out, u.list, m);
     c->launches++;
@@ -395,7 +408,8 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older
     U.status = u.nlive + 2;
     U.cur_out = u.nlive + 3;
     U.trace = u.trace;
-    U.older_is_smaller = older_is_smaller;
+    U.key = u.key;
+    U.age = u.age;
     U.max_rounds = 4096;
     void* args[] = {&U};
     CU(cudaLaunchCooperativeKernel((void*)k_uf_coop, grid, kBlock, args, 0, c->st));
@@ -405,14 +419,23 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, bool older
     CU(cudaStreamSynchronize(c->st));
     std::memcpy(&st, c->h_pinned, sizeof(int));
     if (st < 0) return DMS_OK;
-    // pathological input (no convergence within max_rounds): sequential tail over
-    // the undecided arcs in processing order
+    // pathological input (no convergence within max_rounds): sequential tail over the
+    // undecided arcs in processing order (gather them, sort by key, then one thread)
     k_flag_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags);
     scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
     k_gather_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, u.list);
-    k_uf_tail<<<1, 32, 0, c->st>>>(u.arc_a, u.arc_b, u.list, u.pos + (m - 1), u.flags + (m - 1), m, u.parent, u.out,
-                                  older_is_smaller);
-    c->launches += 3;
+    uint32_t hp[2];
+    CU(cudaMemcpyAsync(&hp[0], u.pos + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(&hp[1], u.flags + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    const int64_t nl = (int64_t)hp[0] + hp[1];
+    k_gather_keys<<<grid_for(nl), kBlock, 0, c->st>>>(u.list, nl, u.key, u.inv_a);
+    const int where = radix_sort<uint32_t, uint32_t, 12>(u.inv_a, reinterpret_cast<uint32_t*>(u.list), u.flags,
+                                                         reinterpret_cast<uint32_t*>(u.live2), nl, 0, 32, c->ss,
+                                                         c->st, &c->launches);
+    const int32_t* sorted = where ? u.live2 : u.list;
+    k_uf_tail<<<1, 32, 0, c->st>>>(u.arc_a, u.arc_b, sorted, nl, u.parent, u.out, u.age);
+    c->launches += 4;
     CU(cudaGetLastError());
     return DMS_OK;
 }
@@ -450,6 +473,26 @@ dms_status emit_unpaired(dms_ctx* c, int which, UFBuf& u, int64_t m, const int64
     return DMS_OK;
 }
 
+// union-find inputs in emission order: arc keys from the arcs' sort permutation, node
+// ages from the nodes' sort permutation (rev: descending processing order)
+void uf_keys_ages(dms_ctx* c, UFBuf& u, int karcs, int64_t m, int knodes, int64_t n, int rev) {
+    if (m) {
+        k_invert<<<grid_for(m), kBlock, 0, c->st>>>(crit_perm(c, karcs), m, u.inv_a);
+        k_uf_keys<<<grid_for(m), kBlock, 0, c->st>>>(u.inv_a, m, rev, u.key);
+    }
+    if (n) k_invert<<<grid_for(n), kBlock, 0, c->st>>>(crit_perm(c, knodes), n, u.inv_n);
+    k_uf_ages<<<grid_for(n + 1), kBlock, 0, c->st>>>(u.inv_n, n, rev, u.age);
+    c->launches += 5;
+}
+
+// out (emission order) -> processing order, in place (buffer swap)
+void out_to_processing(dms_ctx* c, UFBuf& u, int karcs, int64_t m, int rev) {
+    if (!m) return;
+    k_permute1<<<grid_for(m), kBlock, 0, c->st>>>(u.out, crit_perm(c, karcs), m, rev, u.outp);
+    c->launches++;
+    std::swap(u.out, u.outp);
+}
+
 dms_status run_d0(dms_ctx* c) {
     if (!c->have_crit) {
         dms_status s = run_critical(c);
@@ -461,20 +504,21 @@ dms_status run_d0(dms_ctx* c) {
     dms_status s = alloc_uf(c, u, m, n0);
     if (s) return s;
     Geo3 g = geo(c);
-    k_node_map<<<grid_for(n0), kBlock, 0, c->st>>>(crit_ids(c, 0), n0, c->node_of0);
+    // nodes = minima, numbered in emission (spatial) order
+    k_node_map<<<grid_for(n0), kBlock, 0, c->st>>>(crit_ids_emitted(c, 0), n0, c->node_of0);
     c->launches++;
     if (m) {
         StageTimer t6(c, 6);
-        // trace in emission order (spatially coherent), then permute into processing order
-        k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, 1), m, c->node_of0, u.ra, u.rb);
-        k_permute_arcs<<<grid_for(m), kBlock, 0, c->st>>>(u.ra, u.rb, crit_perm(c, 1), m, 0, u.arc_a, u.arc_b);
-        c->launches += 2;
+        k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
+        c->launches++;
     }
     {
         StageTimer t8(c, 8);
-        s = union_find(c, u, m, n0, true);
+        uf_keys_ages(c, u, 1, m, 0, n0, 0);
+        s = union_find(c, u, m, n0);
+        if (s) return s;
+        out_to_processing(c, u, 1, m, 0);
     }
-    if (s) return s;
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
@@ -485,10 +529,11 @@ dms_status run_d0(dms_ctx* c) {
         c->cap_pairs[0] = 2 * np + 1024;
     }
     if (np) {
-        k_emit_d0<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, 0), crit_ids(c, 1), c->pairs[0]);
+        k_emit_d0<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids_emitted(c, 0), crit_ids(c, 1),
+                                                    c->pairs[0]);
         c->launches++;
     }
-    // Sec. 6: the global minimum (oldest node, position 0 of C_0) never dies
+    // Sec. 6: the global minimum (the oldest node, first of C_0) never dies
     k_emit_inf_k<<<1, 32, 0, c->st>>>(g, 0, crit_ids(c, 0), c->kmax, c->pairs[0] + np);
     c->launches++;
     c->npairs[0] = np + 1;
@@ -511,7 +556,8 @@ dms_status run_dtop(dms_ctx* c) {
     dms_status s = alloc_uf(c, u, m, nd + 1);
     if (s) return s;
     Geo3 g = geo(c);
-    k_node_map<<<grid_for(nd), kBlock, 0, c->st>>>(crit_ids(c, d), nd, c->node_oftop);
+    // nodes = critical d-simplices in emission order, plus the virtual maximum nd
+    k_node_map<<<grid_for(nd), kBlock, 0, c->st>>>(crit_ids_emitted(c, d), nd, c->node_oftop);
     c->launches++;
     if (m) {
         StageTimer t7(c, 7);
@@ -525,19 +571,20 @@ dms_status run_dtop(dms_ctx* c) {
                 1, std::min<int64_t>(grid_for(2 * m), (int64_t)sms * std::max(per, 1)));
             CU(cudaMemsetAsync(c->tile_ctr, 0, sizeof(int), c->st));
             k_dtop_arcs_q<3><<<grid, kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), (int)(2 * m), c->node_oftop,
-                                                        (int32_t)nd, u.ra, u.rb, c->tile_ctr);
+                                                        (int32_t)nd, u.arc_a, u.arc_b, c->tile_ctr);
         } else {
             k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), m, c->node_oftop, (int32_t)nd,
-                                                          u.ra, u.rb);
+                                                          u.arc_a, u.arc_b);
         }
-        k_permute_arcs<<<grid_for(m), kBlock, 0, c->st>>>(u.ra, u.rb, crit_perm(c, d - 1), m, 1, u.arc_a, u.arc_b);
-        c->launches += 2;
+        c->launches++;
     }
     {
         StageTimer t9(c, 9);
-        s = union_find(c, u, m, nd + 1, false);
+        uf_keys_ages(c, u, d - 1, m, d, nd, 1);
+        s = union_find(c, u, m, nd + 1);
+        if (s) return s;
+        out_to_processing(c, u, d - 1, m, 1);
     }
-    if (s) return s;
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
@@ -555,8 +602,8 @@ dms_status run_dtop(dms_ctx* c) {
         int64_t np2 = 0;
         s = flag_scan(c, u, m, 0, &np2);
         if (s) return s;
-        k_emit_dtop<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, d - 1), crit_ids(c, d),
-                                                      c->pairs[1]);
+        k_emit_dtop<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, d - 1),
+                                                      crit_ids_emitted(c, d), c->pairs[1]);
         c->launches++;
     }
     for (int64_t i = 0; i < ninf; i++) {
@@ -858,7 +905,8 @@ void dms_destroy(dms_ctx* c) {
     for (int b = 0; b < 2; b++) {
         UFBuf& u = c->uf[b];
         for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.ra, (void*)u.rb, (void*)u.out, (void*)u.list,
-                        (void*)u.live2, (void*)u.nlive, (void*)u.trace,
+                        (void*)u.live2, (void*)u.nlive, (void*)u.trace, (void*)u.outp, (void*)u.key,
+                        (void*)u.inv_a, (void*)u.age, (void*)u.inv_n,
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
             cudaFree(p);
         cudaFree(c->pairs[b]);
