@@ -513,9 +513,10 @@ __device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t a) {
     }
 }
 
-__global__ void k_uf_init(int32_t* parent, uint32_t* best, int64_t n, int32_t* out, int32_t* live, int64_t m) {
+__global__ void k_uf_init(int32_t* parent, unsigned long long* best, int64_t n, int32_t* out, int32_t* live,
+                          int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) { parent[i] = (int32_t)i; best[i] = 0xffffffffu; }
+    if (i < n) { parent[i] = (int32_t)i; best[i] = ~0ull; }
     if (i < m) { out[i] = -2; live[i] = (int32_t)i; }
 }
 
@@ -540,7 +541,7 @@ struct UFArgs {
     const uint32_t* key;  // per arc: its processing index (the arc order of the union-find)
     const int32_t* age;   // per node: smaller = older
     int32_t* parent;
-    uint32_t* best;
+    unsigned long long* best;  // per root: round tag << 32 | lightest arc key (see best_tag)
     int32_t* ra;
     int32_t* rb;
     int32_t* out;
@@ -549,11 +550,42 @@ struct UFArgs {
     int* nlive;   // [2]
     int* status;  // [1]: -1 finished, else the number of undecided arcs left in live[cur]
     int* cur_out; // [1]
-    int* trace;   // [64]: live arcs at the start of each round; [63] = rounds run
+    int* trace;   // [64]: live arcs at the start of each round; [63] = rounds run; [128..]:
+                  // 64 u64 round start timestamps
     int max_rounds;
+    int agg;
 };
 
 __device__ __forceinline__ int ld_cg_int(const int* p) { return __ldcg(p); }
+// The lightest outgoing arc of every root, per round: best[r] = tag(round) << 32 | key
+// with tags decreasing over the rounds, so a value left from an earlier round is always
+// larger than any of this round's (no reset pass).  All lanes of the warp call it
+// (active or not): lanes hitting the same root pre-reduce with match/redux and only
+// the leader touches memory, and only if the stored value is larger -- the roots of
+// the big components otherwise take one same-address atomic per incident arc.
+__device__ __forceinline__ unsigned long long best_tag(int round) {
+    return (unsigned long long)(0x7fffffffu - (uint32_t)round) << 32;
+}
+__device__ __forceinline__ void best_min(unsigned long long* best, int32_t r, uint32_t key, unsigned long long tag,
+                                         bool active, int agg) {
+    if (agg == 0) {
+        if (active) atomicMin(best + r, tag | key);
+        return;
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const unsigned peers = __match_any_sync(act, r);
+    const uint32_t kmin = __reduce_min_sync(peers, key);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) {
+        const unsigned long long v = tag | kmin;
+        if (agg == 1 || __ldcg(best + r) > v) atomicMin(best + r, v);
+    }
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
     namespace cg = cooperative_groups;
@@ -568,23 +600,33 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
         int32_t* nxt = cur ? U.live0 : U.live1;
         const int n = ld_cg_int(&U.nlive[cur]);
         if (gtid == 0) {
-            if (round < 63) U.trace[round] = n;
+            if (round < 63) {
+                U.trace[round] = n;
+                reinterpret_cast<unsigned long long*>(U.trace + 128)[round] = globaltimer();
+            }
             U.trace[63] = round;
         }
         if (n <= kUFTail) break;
         // phase 1: roots, cycle arcs, lightest arc of every root
-        for (int idx = gtid; idx < n; idx += stride) {
-            const int32_t i = live[idx];
-            const int32_t a = uf_find(U.parent, U.arc_a[i]);
-            const int32_t b = uf_find(U.parent, U.arc_b[i]);
-            U.ra[i] = a;
-            U.rb[i] = b;
-            U.arc_a[i] = a;  // find(old root) == find(endpoint): next round starts here
-            U.arc_b[i] = b;
-            if (a == b) { U.out[i] = -1; continue; }
-            const uint32_t ki = U.key[i];
-            atomicMin(&U.best[a], ki);
-            atomicMin(&U.best[b], ki);
+        const unsigned long long tag = best_tag(round);
+        for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+            const int idx = base + threadIdx.x;
+            int32_t a = 0, b = 0;
+            uint32_t ki = 0;
+            bool act = false;
+            if (idx < n) {
+                const int32_t i = live[idx];
+                a = uf_find(U.parent, U.arc_a[i]);
+                b = uf_find(U.parent, U.arc_b[i]);
+                U.ra[i] = a;
+                U.rb[i] = b;
+                U.arc_a[i] = a;  // find(old root) == find(endpoint): next round starts here
+                U.arc_b[i] = b;
+                if (a == b) U.out[i] = -1;
+                else { act = true; ki = U.key[i]; }
+            }
+            best_min(U.best, a, ki, tag, act, U.agg);
+            best_min(U.best, b, ki, tag, act, U.agg);
         }
         if (gtid == 0) U.nlive[cur ^ 1] = 0;
         grid.sync();
@@ -594,7 +636,7 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
             if (U.out[i] != -2) continue;
             const int32_t a = U.ra[i], b = U.rb[i];
             const uint32_t ki = U.key[i];
-            const bool ma = __ldcg(&U.best[a]) == ki, mb = __ldcg(&U.best[b]) == ki;
+            const bool ma = __ldcg(&U.best[a]) == (tag | ki), mb = __ldcg(&U.best[b]) == (tag | ki);
             const bool a_older = U.age[a] < U.age[b];
             if (ma && mb) {
                 const int32_t young = a_older ? b : a, old = a_older ? a : b;
@@ -609,19 +651,14 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
             }
         }
         grid.sync();
-        // phase 3: reset the candidates, compact the undecided arcs
+        // phase 3: compact the undecided arcs
         for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
             const int idx = base + threadIdx.x;
             bool keep = false;
             int32_t i = 0;
             if (idx < n) {
                 i = live[idx];
-                const int32_t o = U.out[i];
-                if (o != -1) {
-                    U.best[U.ra[i]] = 0xffffffffu;
-                    U.best[U.rb[i]] = 0xffffffffu;
-                }
-                keep = o == -2;
+                keep = U.out[i] == -2;
             }
             const unsigned mk = __ballot_sync(0xffffffffu, keep);
             int bp = 0;

@@ -55,7 +55,8 @@ struct UFBuf {
     int* nlive = nullptr;  // two device counters
     int* trace = nullptr;  // [64] union-find round trace
     int32_t* parent = nullptr;
-    uint32_t *best = nullptr, *flags = nullptr, *pos = nullptr;
+    unsigned long long* best = nullptr;
+    uint32_t *flags = nullptr, *pos = nullptr;
     int64_t cap_arcs = 0, cap_nodes = 0;
 };
 
@@ -214,8 +215,8 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
             cudaFree(*p);
             CU(dalloc(p, arcs));
         }
-        if (!u.nlive) CU(dalloc(&u.nlive, 4));
-        if (!u.trace) CU(dalloc(&u.trace, 64));
+        if (!u.nlive) CU(dalloc(&u.nlive, 8));
+        if (!u.trace) CU(dalloc(&u.trace, 128 + 128));
         for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
         u.cap_arcs = arcs;
     }
@@ -411,6 +412,10 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     U.key = u.key;
     U.age = u.age;
     U.max_rounds = 4096;
+    // same-address contention on best[] comes with arc-dense graphs (3D: ~4 arcs per node,
+    // the big components collect most arcs): pre-reduce per warp there (measured)
+    static const int agg_env = getenv("DMS_AGG") ? atoi(getenv("DMS_AGG")) : -1;
+    U.agg = agg_env >= 0 ? agg_env : ((double)m > 3.0 * (double)nodes ? 2 : 0);
     void* args[] = {&U};
     CU(cudaLaunchCooperativeKernel((void*)k_uf_coop, grid, kBlock, args, 0, c->st));
     c->launches++;
@@ -867,6 +872,12 @@ dms_status dms_stage_ms(dms_ctx* c, double ms_out[11]) {
 int64_t dms_launch_count(const dms_ctx* c) { return c ? c->launches : 0; }
 
 // internal diagnostics (not part of include/dms.h): live arcs per union-find round
+int dms_internal_uf_trace2(dms_ctx* c, int which, int out[64], unsigned long long t[64]) {
+    if (!c || which < 0 || which > 1 || !c->uf[which].trace) return 1;
+    cudaStreamSynchronize(c->st);
+    if (cudaMemcpy(out, c->uf[which].trace, 64 * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+    return cudaMemcpy(t, c->uf[which].trace + 128, 64 * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+}
 int dms_internal_uf_trace(dms_ctx* c, int which, int out[64]) {
     if (!c || which < 0 || which > 1 || !c->uf[which].trace) return 1;
     cudaStreamSynchronize(c->st);
