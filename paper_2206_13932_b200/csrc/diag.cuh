@@ -513,11 +513,16 @@ __device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t a) {
     }
 }
 
-__global__ void k_uf_init(int32_t* parent, unsigned long long* best, int64_t n, int32_t* out, int32_t* live,
-                          int64_t m) {
+// parent/best for the nodes; out = -2 (undecided) and the first live list of arc
+// records {endpoint a, endpoint b, key, arc} for the arcs
+__global__ void k_uf_init(int32_t* parent, unsigned long long* best, int64_t n, const int32_t* arc_a,
+                          const int32_t* arc_b, const uint32_t* key, int64_t m, int32_t* out, int4* rec) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) { parent[i] = (int32_t)i; best[i] = ~0ull; }
-    if (i < m) { out[i] = -2; live[i] = (int32_t)i; }
+    if (i < m) {
+        out[i] = -2;
+        rec[i] = make_int4(arc_a[i], arc_b[i], (int)key[i], (int)i);
+    }
 }
 
 __global__ void k_flag_undecided(const int32_t* out, int64_t m, uint32_t* flags) {
@@ -534,24 +539,20 @@ __global__ void k_gather_undecided(const int32_t* out, int64_t m, const uint32_t
 // phases, no host round trip), then block 0 sorts the (few) undecided arcs and runs
 // the sequential elder-rule union-find over them in processing order.
 constexpr int kUFTail = 2048;
+constexpr int kUFTile = 1024;  // records per CTA tile in pass A (kUFTile * 16 B == kUFTail * 8 B)
 
 struct UFArgs {
-    int32_t* arc_a;  // endpoints are replaced by their current roots every round
-    int32_t* arc_b;
     const uint32_t* key;  // per arc: its processing index (the arc order of the union-find)
     const int32_t* age;   // per node: smaller = older
     int32_t* parent;
     unsigned long long* best;  // per root: round tag << 32 | lightest arc key (see best_tag)
-    int32_t* ra;
-    int32_t* rb;
     int32_t* out;
-    int32_t* live0;
-    int32_t* live1;
+    int4* rec0;   // live arc records {a, b, key, arc}; a, b = roots as of the last find
+    int4* rec1;
     int* nlive;   // [2]
-    int* status;  // [1]: -1 finished, else the number of undecided arcs left in live[cur]
+    int* status;  // [1]: -1 finished, else the number of undecided arcs left
     int* cur_out; // [1]
-    int* trace;   // [64]: live arcs at the start of each round; [63] = rounds run; [128..]:
-                  // 64 u64 round start timestamps
+    int* trace;   // [64]: live arcs of each round; [63] = rounds run; [128..]: 64 u64 timestamps
     int max_rounds;
     int agg;
 };
@@ -590,97 +591,109 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ unsigned long long s_list[kUFTail];
+    __shared__ int4 s_rec[kUFTile];  // pass A staging; the tail's sort list after the rounds
+    __shared__ int s_cnt, s_base;
+    unsigned long long* s_list = reinterpret_cast<unsigned long long*>(s_rec);
     const int stride = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     int cur = 0;
+    bool done = false;
     for (int round = 0; round < U.max_rounds; round++) {
-        int32_t* live = cur ? U.live1 : U.live0;
-        int32_t* nxt = cur ? U.live0 : U.live1;
+        const int4* live = cur ? U.rec1 : U.rec0;
+        int4* nxt = cur ? U.rec0 : U.rec1;
         const int n = ld_cg_int(&U.nlive[cur]);
+        // pass A: roots of the arcs still undecided (records marked a = -1 were decided
+        // last round), cycle arcs (same root: final, unpaired), lightest arc of every
+        // root; the survivors are compacted into the next list with their roots
+        const unsigned long long tag = best_tag(round);
+        // tiles of kUFTile records per CTA: survivors gather in shared memory and leave
+        // with one global atomic per tile (a per-warp atomic on the single list counter
+        // serialises: measured 2/3 of the stall samples on 1D)
+        // (a tile is K * kBlock records, K <= 4 chosen so that small rounds still spread
+        // over the whole grid)
+        const int K = min(kUFTile / kBlock, max(1, (n + stride - 1) / stride));
+        for (int tile = blockIdx.x * K * kBlock; tile < n; tile += gridDim.x * K * kBlock) {
+            if (threadIdx.x == 0) s_cnt = 0;
+            __syncthreads();
+            for (int k = 0; k < K; k++) {
+                const int idx = tile + k * kBlock + threadIdx.x;
+                int4 r = make_int4(0, 0, 0, 0);
+                bool act = false;
+                if (idx < n) {
+                    r = live[idx];
+                    if (r.x >= 0) {
+                        r.x = uf_find(U.parent, r.x);
+                        r.y = uf_find(U.parent, r.y);
+                        if (r.x == r.y) U.out[r.w] = -1;
+                        else act = true;
+                    }
+                }
+                best_min(U.best, r.x, (uint32_t)r.z, tag, act, U.agg);
+                best_min(U.best, r.y, (uint32_t)r.z, tag, act, U.agg);
+                const unsigned mk = __ballot_sync(0xffffffffu, act);
+                int bp = 0;
+                if (lane == 0 && mk) bp = atomicAdd(&s_cnt, __popc(mk));
+                bp = __shfl_sync(0xffffffffu, bp, 0);
+                if (act) s_rec[bp + __popc(mk & lanemask_lt())] = r;
+            }
+            __syncthreads();
+            const int cnt = s_cnt;
+            if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&U.nlive[cur ^ 1], cnt);
+            __syncthreads();
+            for (int j = threadIdx.x; j < cnt; j += kBlock) nxt[s_base + j] = s_rec[j];
+            __syncthreads();
+        }
+        grid.sync();
+        cur ^= 1;  // the survivors' list
+        const int m2 = ld_cg_int(&U.nlive[cur]);
         if (gtid == 0) {
             if (round < 63) {
-                U.trace[round] = n;
+                U.trace[round] = m2;
                 reinterpret_cast<unsigned long long*>(U.trace + 128)[round] = globaltimer();
             }
             U.trace[63] = round;
+            U.nlive[cur ^ 1] = 0;  // the list just consumed becomes the next round's output
         }
-        if (n <= kUFTail) break;
-        // phase 1: roots, cycle arcs, lightest arc of every root
-        const unsigned long long tag = best_tag(round);
-        for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-            const int idx = base + threadIdx.x;
-            int32_t a = 0, b = 0;
-            uint32_t ki = 0;
-            bool act = false;
-            if (idx < n) {
-                const int32_t i = live[idx];
-                a = uf_find(U.parent, U.arc_a[i]);
-                b = uf_find(U.parent, U.arc_b[i]);
-                U.ra[i] = a;
-                U.rb[i] = b;
-                U.arc_a[i] = a;  // find(old root) == find(endpoint): next round starts here
-                U.arc_b[i] = b;
-                if (a == b) U.out[i] = -1;
-                else { act = true; ki = U.key[i]; }
-            }
-            best_min(U.best, a, ki, tag, act, U.agg);
-            best_min(U.best, b, ki, tag, act, U.agg);
-        }
-        if (gtid == 0) U.nlive[cur ^ 1] = 0;
-        grid.sync();
-        // phase 2: mutual minimum, or a younger root dying at its lightest arc
-        for (int idx = gtid; idx < n; idx += stride) {
-            const int32_t i = live[idx];
-            if (U.out[i] != -2) continue;
-            const int32_t a = U.ra[i], b = U.rb[i];
-            const uint32_t ki = U.key[i];
-            const bool ma = __ldcg(&U.best[a]) == (tag | ki), mb = __ldcg(&U.best[b]) == (tag | ki);
-            const bool a_older = U.age[a] < U.age[b];
+        if (m2 <= kUFTail) { done = true; break; }
+        // pass B: mutual minimum, or a younger root dying at its lightest arc
+        int4* sur = cur ? U.rec1 : U.rec0;
+        for (int idx = gtid; idx < m2; idx += stride) {
+            const int4 r = sur[idx];
+            const unsigned long long kt = tag | (uint32_t)r.z;
+            const bool ma = __ldcg(&U.best[r.x]) == kt, mb = __ldcg(&U.best[r.y]) == kt;
+            if (!ma && !mb) continue;
+            const bool a_older = U.age[r.x] < U.age[r.y];
+            int32_t young = -1;
             if (ma && mb) {
-                const int32_t young = a_older ? b : a, old = a_older ? a : b;
-                U.parent[young] = old;
-                U.out[i] = young;
+                young = a_older ? r.y : r.x;
+                U.parent[young] = a_older ? r.x : r.y;
             } else if (ma && !a_older) {
-                U.parent[a] = b;
-                U.out[i] = a;
+                young = r.x;
+                U.parent[r.x] = r.y;
             } else if (mb && a_older) {
-                U.parent[b] = a;
-                U.out[i] = b;
+                young = r.y;
+                U.parent[r.y] = r.x;
+            }
+            if (young >= 0) {
+                U.out[r.w] = young;
+                sur[idx].x = -1;
             }
         }
         grid.sync();
-        // phase 3: compact the undecided arcs
-        for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-            const int idx = base + threadIdx.x;
-            bool keep = false;
-            int32_t i = 0;
-            if (idx < n) {
-                i = live[idx];
-                keep = U.out[i] == -2;
-            }
-            const unsigned mk = __ballot_sync(0xffffffffu, keep);
-            int bp = 0;
-            if (lane == 0 && mk) bp = atomicAdd(&U.nlive[cur ^ 1], __popc(mk));
-            bp = __shfl_sync(0xffffffffu, bp, 0);
-            if (keep) nxt[bp + __popc(mk & lanemask_lt())] = i;
-        }
-        grid.sync();
-        cur ^= 1;
     }
     if (blockIdx.x != 0) return;
     const int n = ld_cg_int(&U.nlive[cur]);
     if (threadIdx.x == 0) *U.cur_out = cur;
-    if (n > kUFTail) {  // did not converge within max_rounds: the host finishes the tail
-        if (threadIdx.x == 0) *U.status = n;
+    if (!done) {  // did not converge within max_rounds: the host finishes the tail
+        if (threadIdx.x == 0) *U.status = n > 0 ? n : 1;
         return;
     }
-    const int32_t* live = cur ? U.live1 : U.live0;
+    const int4* live = cur ? U.rec1 : U.rec0;
     int p2 = 1;
     while (p2 < n) p2 <<= 1;
     for (int j = threadIdx.x; j < p2; j += blockDim.x)
-        s_list[j] = j < n ? (((unsigned long long)U.key[live[j]] << 32) | (uint32_t)live[j]) : ~0ull;
+        s_list[j] = j < n ? (((unsigned long long)(uint32_t)live[j].z << 32) | (uint32_t)j) : ~0ull;
     __syncthreads();
     // bitonic sort by key (ascending processing order)
     for (int k = 2; k <= p2; k <<= 1) {
@@ -698,15 +711,15 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
     }
     if (threadIdx.x == 0) {
         for (int j = 0; j < n; j++) {
-            const int32_t i = (int32_t)(s_list[j] & 0xffffffffull);
-            int32_t a = U.arc_a[i], b = U.arc_b[i];
+            const int4 r = live[(int)(s_list[j] & 0xffffffffull)];
+            int32_t a = r.x, b = r.y;
             while (U.parent[a] != a) a = U.parent[a];
             while (U.parent[b] != b) b = U.parent[b];
-            if (a == b) { U.out[i] = -1; continue; }
+            if (a == b) { U.out[r.w] = -1; continue; }
             const bool a_older = U.age[a] < U.age[b];
             const int32_t young = a_older ? b : a, old = a_older ? a : b;
             U.parent[young] = old;
-            U.out[i] = young;
+            U.out[r.w] = young;
         }
         *U.status = -1;
     }

@@ -46,7 +46,8 @@ __global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsig
 }
 
 struct UFBuf {
-    int32_t *arc_a = nullptr, *arc_b = nullptr, *ra = nullptr, *rb = nullptr, *out = nullptr, *list = nullptr;
+    int32_t *arc_a = nullptr, *arc_b = nullptr, *out = nullptr, *list = nullptr;
+    int4 *rec0 = nullptr, *rec1 = nullptr;  // union-find live arc records
     int32_t* live2 = nullptr;
     int32_t* outp = nullptr;   // out in processing order
     uint32_t *key = nullptr, *inv_a = nullptr;  // per arc (emission order)
@@ -207,7 +208,11 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
     arcs = std::max<int64_t>(arcs, 1);
     nodes = std::max<int64_t>(nodes, 1);
     if (arcs > u.cap_arcs) {
-        for (int32_t** p : {&u.arc_a, &u.arc_b, &u.ra, &u.rb, &u.out, &u.list, &u.live2, &u.outp}) {
+        for (int4** p : {&u.rec0, &u.rec1}) {
+            cudaFree(*p);
+            CU(dalloc(p, arcs));
+        }
+        for (int32_t** p : {&u.arc_a, &u.arc_b, &u.out, &u.list, &u.live2, &u.outp}) {
             cudaFree(*p);
             CU(dalloc(p, arcs));
         }
@@ -385,7 +390,7 @@ dms_status run_critical(dms_ctx* c) {
 // u.arc_a / u.arc_b / u.key (per arc) and u.age (per node) are in emission order
 dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     const unsigned gi = grid_for(std::max(m, nodes));
-    k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.out, u.list, m);
+    k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.arc_a, u.arc_b, u.key, m, u.out, u.rec0);
     c->launches++;
     if (m == 0) return DMS_OK;
     int hm[4] = {(int)m, 0, 0, 0};  // nlive[2], status, cur
@@ -396,15 +401,11 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_uf_coop, kBlock, 0);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(m), (int64_t)sms * std::max(per, 1)));
     UFArgs U;
-    U.arc_a = u.arc_a;
-    U.arc_b = u.arc_b;
     U.parent = u.parent;
     U.best = u.best;
-    U.ra = u.ra;
-    U.rb = u.rb;
     U.out = u.out;
-    U.live0 = u.list;
-    U.live1 = u.live2;
+    U.rec0 = u.rec0;
+    U.rec1 = u.rec1;
     U.nlive = u.nlive;
     U.status = u.nlive + 2;
     U.cur_out = u.nlive + 3;
@@ -915,7 +916,7 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->node_oftop);
     for (int b = 0; b < 2; b++) {
         UFBuf& u = c->uf[b];
-        for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.ra, (void*)u.rb, (void*)u.out, (void*)u.list,
+        for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.rec0, (void*)u.rec1, (void*)u.out, (void*)u.list,
                         (void*)u.live2, (void*)u.nlive, (void*)u.trace, (void*)u.outp, (void*)u.key,
                         (void*)u.inv_a, (void*)u.age, (void*)u.inv_n,
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
