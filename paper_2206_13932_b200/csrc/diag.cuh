@@ -453,24 +453,33 @@ __global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* _
     c.x = c.ox = 0; c.T = 0; c.cx = c.cy = c.cz = 0; c.w = 0;
     int job = -1;          // current job, -1: none
     bool done = false;     // the queue is exhausted for this lane
+    // jobs come from the global queue in warp-private batches (one atomic per batch: a
+    // per-refill atomic on the single queue counter serialises across the whole grid)
+    constexpr int kBatch = 32;
+    int b_next = 0, b_end = 0;  // warp-uniform: the batch's unassigned jobs [b_next, b_end)
+    bool exhausted = false;
     while (true) {
-        // lanes without a job take one (warp-aggregated), and may finish at once
         const bool need = job < 0 && !done;
         const unsigned nm = __ballot_sync(0xffffffffu, need);
         if (nm) {
-            int base = 0;
-            if (lane == __ffs(nm) - 1) base = atomicAdd(job_ctr, __popc(nm));
-            base = __shfl_sync(0xffffffffu, base, __ffs(nm) - 1);
+            if (b_next >= b_end && !exhausted) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(job_ctr, kBatch);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base >= njobs) exhausted = true;
+                else { b_next = base; b_end = min(base + kBatch, njobs); }
+            }
             if (need) {
-                const int jb = base + __popc(nm & lanemask_lt());
-                if (jb >= njobs) {
-                    done = true;
-                } else {
+                const int jb = b_next + __popc(nm & lanemask_lt());
+                if (jb < b_end) {
                     const int32_t r = chase_start<D>(g, S, ids, jb, c, node_of, vnode);
                     if (r != -2) (jb & 1 ? out_b : out_a)[jb >> 1] = r;
                     else job = jb;
+                } else if (exhausted) {
+                    done = true;
                 }
             }
+            b_next = min(b_end, b_next + __popc(nm));
         }
         if (__all_sync(0xffffffffu, done)) break;
         if (job >= 0) {
