@@ -442,11 +442,34 @@ __device__ __forceinline__ int32_t chase_start(const Geo3& g, const StarTab& S, 
     return -2;
 }
 
+#ifdef DMS_CHASE_STATS  // diagnostics build only: histogram of hops per chase (log2 bins), [63] = total
+__device__ unsigned long long g_chase_hist[64];
+#endif
+// anchored id of the top cell in slot T of x's star
 template <int D>
+__device__ __forceinline__ int64_t top_id(const Geo3& g, const StarTab& S, uint32_t x, int T) {
+    if (D == 3)
+        return 6 * ((int64_t)x + S.q_anc[T][0] + (int64_t)g.Lx * S.q_anc[T][1] + (int64_t)g.Lx * g.Ly * S.q_anc[T][2]) +
+               S.q_k[T];
+    return 2 * ((int64_t)x + S.t_anc[T][0] + (int64_t)g.Lx * S.t_anc[T][1]) + S.t_k[T];
+}
+
+// Ascending dual chases, 2 jobs per critical (d-1)-simplex (one per cofacet side),
+// from a work queue.  MEMO: ascending paths merge (they drain into few maxima), so
+// the top cell a chase enters when it climbs to a new vertex is stamped (generation
+// << 24 | job + 1); a chase that climbs into a cell stamped in this generation by
+// another job stops there and records "same end as that job" (res[job] = -3 - other);
+// k_resolve_joins follows these links.  Paths are acyclic, so the links are too.  Two
+// merged paths climb into the same cells from then on, so stamping at climbs only
+// loses at most one climb of sharing; plain loads/stores suffice (a lost race only
+// loses a merge: any stamp seen is a cell that job really entered).  Without MEMO the
+// ends go to out_a/out_b.
+template <int D, bool MEMO>
 __global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* __restrict__ ids, int njobs,
                                                        const int32_t* __restrict__ node_of, int32_t vnode,
                                                        int32_t* __restrict__ out_a, int32_t* __restrict__ out_b,
-                                                       int* job_ctr) {
+                                                       int* job_ctr, uint32_t* mark, uint32_t gen,
+                                                       int32_t* __restrict__ res) {
     const StarTab& S = *g.tab;
     const int lane = threadIdx.x & 31;
     ChaseState<D> c;
@@ -458,6 +481,9 @@ __global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* _
     constexpr int kBatch = 32;
     int b_next = 0, b_end = 0;  // warp-uniform: the batch's unassigned jobs [b_next, b_end)
     bool exhausted = false;
+#ifdef DMS_CHASE_STATS
+    int hops = 0;
+#endif
     while (true) {
         const bool need = job < 0 && !done;
         const unsigned nm = __ballot_sync(0xffffffffu, need);
@@ -473,8 +499,15 @@ __global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* _
                 const int jb = b_next + __popc(nm & lanemask_lt());
                 if (jb < b_end) {
                     const int32_t r = chase_start<D>(g, S, ids, jb, c, node_of, vnode);
-                    if (r != -2) (jb & 1 ? out_b : out_a)[jb >> 1] = r;
-                    else job = jb;
+                    if (r != -2) {
+                        if (MEMO) res[jb] = r;
+                        else (jb & 1 ? out_b : out_a)[jb >> 1] = r;
+                    } else {
+                        job = jb;
+                    }
+#ifdef DMS_CHASE_STATS
+                    hops = 0;
+#endif
                 } else if (exhausted) {
                     done = true;
                 }
@@ -483,13 +516,38 @@ __global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* _
         }
         if (__all_sync(0xffffffffu, done)) break;
         if (job >= 0) {
-            const int32_t r = chase_step<D>(g, S, c, node_of, vnode);
+            const uint32_t x0 = c.x;
+            int32_t r = chase_step<D>(g, S, c, node_of, vnode);
+            if (MEMO && r == -2 && c.x != x0) {  // stamps at climbs only (see above)
+                uint32_t* mp = mark + top_id<D>(g, S, c.x, c.T);
+                const uint32_t old = __ldcg(mp);
+                if ((old >> 24) == gen) r = -3 - (int32_t)((old & 0xffffffu) - 1u);  // joins that job
+                else __stcg(mp, (gen << 24) | (uint32_t)(job + 1));
+            }
+#ifdef DMS_CHASE_STATS
+            hops++;
+#endif
             if (r != -2) {
-                (job & 1 ? out_b : out_a)[job >> 1] = r;
+                if (MEMO) res[job] = r;
+                else (job & 1 ? out_b : out_a)[job >> 1] = r;
                 job = -1;
+#ifdef DMS_CHASE_STATS
+                atomicAdd(&g_chase_hist[min(62, 31 - __clz(hops))], 1ull);
+                atomicAdd(&g_chase_hist[63], (unsigned long long)hops);
+#endif
             }
         }
     }
+}
+
+// ends of the memoised chases: follow the join links to a job that reached an end
+__global__ void k_resolve_joins(const int32_t* __restrict__ res, int njobs, int32_t* __restrict__ out_a,
+                                int32_t* __restrict__ out_b) {
+    const int jb = blockIdx.x * blockDim.x + threadIdx.x;
+    if (jb >= njobs) return;
+    int32_t v = res[jb];
+    while (v < 0) v = __ldg(res + (-3 - v));
+    (jb & 1 ? out_b : out_a)[jb >> 1] = v;
 }
 
 // ---------------------------------------------------------------- union-find

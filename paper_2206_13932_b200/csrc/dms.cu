@@ -93,6 +93,8 @@ struct dms_ctx {
     unsigned long long* status = nullptr;
     int64_t status_words = 0;
     int* tile_ctr = nullptr;
+    uint32_t* chase_mark = nullptr;  // D_{d-1} chase stamps, one per top cell
+    uint32_t chase_gen = 0;
     unsigned long long* totals = nullptr;
     int* err = nullptr;
     unsigned long long* kmax = nullptr;
@@ -567,17 +569,49 @@ dms_status run_dtop(dms_ctx* c) {
     c->launches++;
     if (m) {
         StageTimer t7(c, 7);
-        if (d == 3) {
-            // persistent work-queue chases, 2 jobs per arc (long ascending paths in 3D)
+        if (d >= 2) {
+            // persistent work-queue chases, 2 jobs per arc (ascending paths of very uneven
+            // length), memoised where the job ids fit the 24-bit stamps
+            static const int memo_env = getenv("DMS_MEMO") ? atoi(getenv("DMS_MEMO")) : 1;
+            const bool memo = memo_env && 2 * m + 1 < (1 << 24);
             int dev = 0, sms = 148, per = 1;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<3>, kBlock, 0);
+            if (d == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<3, true>, kBlock, 0);
+            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<2, true>, kBlock, 0);
             const unsigned grid = (unsigned)std::max<int64_t>(
                 1, std::min<int64_t>(grid_for(2 * m), (int64_t)sms * std::max(per, 1)));
             CU(cudaMemsetAsync(c->tile_ctr, 0, sizeof(int), c->st));
-            k_dtop_arcs_q<3><<<grid, kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), (int)(2 * m), c->node_oftop,
-                                                        (int32_t)nd, u.arc_a, u.arc_b, c->tile_ctr);
+            const int64_t* ids = crit_ids_emitted(c, d - 1);
+            if (memo) {
+                const int64_t ncells = c->N * (d == 3 ? 6 : 2);
+                if (!c->chase_mark) {
+                    CU(dalloc(&c->chase_mark, ncells));
+                    CU(cudaMemsetAsync(c->chase_mark, 0, ncells * sizeof(uint32_t), c->st));
+                    c->chase_gen = 0;
+                }
+                if (++c->chase_gen == 256) {  // stamps wrap: clear them
+                    CU(cudaMemsetAsync(c->chase_mark, 0, ncells * sizeof(uint32_t), c->st));
+                    c->chase_gen = 1;
+                }
+                int32_t* res = reinterpret_cast<int32_t*>(u.rec0);  // 2m int32 (rec0: 4m, free until the union-find)
+                if (d == 3)
+                    k_dtop_arcs_q<3, true><<<grid, kBlock, 0, c->st>>>(g, ids, (int)(2 * m), c->node_oftop, (int32_t)nd,
+                                                                      u.arc_a, u.arc_b, c->tile_ctr, c->chase_mark,
+                                                                      c->chase_gen, res);
+                else
+                    k_dtop_arcs_q<2, true><<<grid, kBlock, 0, c->st>>>(g, ids, (int)(2 * m), c->node_oftop, (int32_t)nd,
+                                                                      u.arc_a, u.arc_b, c->tile_ctr, c->chase_mark,
+                                                                      c->chase_gen, res);
+                k_resolve_joins<<<grid_for(2 * m), kBlock, 0, c->st>>>(res, (int)(2 * m), u.arc_a, u.arc_b);
+                c->launches++;
+            } else if (d == 3) {
+                k_dtop_arcs_q<3, false><<<grid, kBlock, 0, c->st>>>(g, ids, (int)(2 * m), c->node_oftop, (int32_t)nd,
+                                                                    u.arc_a, u.arc_b, c->tile_ctr, nullptr, 0, nullptr);
+            } else {
+                k_dtop_arcs_q<2, false><<<grid, kBlock, 0, c->st>>>(g, ids, (int)(2 * m), c->node_oftop, (int32_t)nd,
+                                                                    u.arc_a, u.arc_b, c->tile_ctr, nullptr, 0, nullptr);
+            }
         } else {
             k_dtop_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, d - 1), m, c->node_oftop, (int32_t)nd,
                                                           u.arc_a, u.arc_b);
@@ -873,6 +907,15 @@ dms_status dms_stage_ms(dms_ctx* c, double ms_out[11]) {
 int64_t dms_launch_count(const dms_ctx* c) { return c ? c->launches : 0; }
 
 // internal diagnostics (not part of include/dms.h): live arcs per union-find round
+#ifdef DMS_CHASE_STATS
+int dms_internal_chase_stats(unsigned long long out[64], int reset) {
+    if (reset) {
+        unsigned long long z[64] = {0};
+        return cudaMemcpyToSymbol(g_chase_hist, z, sizeof z) == cudaSuccess ? 0 : 1;
+    }
+    return cudaMemcpyFromSymbol(out, g_chase_hist, 64 * 8) == cudaSuccess ? 0 : 1;
+}
+#endif
 int dms_internal_uf_trace2(dms_ctx* c, int which, int out[64], unsigned long long t[64]) {
     if (!c || which < 0 || which > 1 || !c->uf[which].trace) return 1;
     cudaStreamSynchronize(c->st);
@@ -907,6 +950,7 @@ void dms_destroy(dms_ctx* c) {
         for (int k = 0; k < 4; k++) { cudaFree(c->cid[b][k]); cudaFree(c->ckey[b][k]); cudaFree(c->cidx[b][k]); }
     cudaFree(c->status);
     cudaFree(c->tile_ctr);
+    cudaFree(c->chase_mark);
     cudaFree(c->totals);
     cudaFree(c->err);
     cudaFree(c->kmax);
