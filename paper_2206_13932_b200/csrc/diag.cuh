@@ -360,20 +360,10 @@ __device__ __forceinline__ int32_t chase_step(const Geo3& g, const StarTab& S, C
             id = 2 * ((int64_t)c.x + S.t_anc[T][0] + (int64_t)g.Lx * S.t_anc[T][1]) + S.t_k[T];
         return node_of[id];
     }
-    int T2, s2, j;
-    if (D == 3) {
-        const int tt = S.tet_tri[T][code - 1];  // s' = Pair(c)
-        T2 = S.tri_tet[tt][0] == T ? S.tri_tet[tt][1] : S.tri_tet[tt][0];
-        if (T2 == 255) return vnode;
-        s2 = S.tet_a[T2] ^ S.tet_b[T2] ^ S.tet_c[T2] ^ S.tri_a[tt] ^ S.tri_b[tt];
-        j = S.tet_a[T2] == s2 ? 0 : (S.tet_b[T2] == s2 ? 1 : 2);
-    } else {
-        const int e = code == 1 ? S.tri_a[T] : S.tri_b[T];
-        T2 = S.edge_tri[e][0] == T ? S.edge_tri[e][1] : S.edge_tri[e][0];
-        if (T2 == 255) return vnode;
-        s2 = S.tri_a[T2] ^ S.tri_b[T2] ^ e;
-        j = S.tri_a[T2] == s2 ? 0 : 1;
-    }
+    const uint32_t e = D == 3 ? S.q_next[T][code - 1] : S.t_next[T][code - 1];
+    const int T2 = (int)(e & 255u);
+    if (T2 == 255) return vnode;
+    const int s2 = (int)((e >> 8) & 255u);
     const int nx = c.cx + S.off[s2][0], ny = c.cy + S.off[s2][1], nz = c.cz + S.off[s2][2];
     if (!in_grid(g, nx, ny, nz)) return vnode;  // s' on the boundary: the virtual maximum
     const uint32_t n2 = c.x + (uint32_t)S.lin[s2];
@@ -381,7 +371,7 @@ __device__ __forceinline__ int32_t chase_step(const Geo3& g, const StarTab& S, C
     if (nb_lower(on, c.ox, s2, NE)) {
         c.T = T2;  // the other cofacet of s' is still in St^-(x)
     } else {       // it climbs to n2
-        c.T = D == 3 ? S.q_reslot[T2][j] : S.t_reslot[T2][j];
+        c.T = (int)(e >> 16);
         c.x = n2;
         c.ox = on;
         c.cx = nx; c.cy = ny; c.cz = nz;
@@ -470,7 +460,15 @@ __global__ void __launch_bounds__(kBlock) k_dtop_arcs_q(Geo3 g, const int64_t* _
                                                        int32_t* __restrict__ out_a, int32_t* __restrict__ out_b,
                                                        int* job_ctr, uint32_t* mark, uint32_t gen,
                                                        int32_t* __restrict__ res) {
-    const StarTab& S = *g.tab;
+    // star tables: shared memory in 2D, L1-cached global in 3D (measured)
+    __shared__ StarTab S_sh;
+    if (D == 2) {
+        const int4* src = reinterpret_cast<const int4*>(g.tab);
+        int4* dst = reinterpret_cast<int4*>(&S_sh);
+        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+    }
+    const StarTab& S = D == 2 ? S_sh : *g.tab;
     const int lane = threadIdx.x & 31;
     ChaseState<D> c;
     c.x = c.ox = 0; c.T = 0; c.cx = c.cy = c.cz = 0; c.w = 0;
