@@ -313,13 +313,20 @@ def main():
         f_pin = torch.from_numpy(f_host).pin_memory()
         h2d = f_pin.numel() * 4
 
+        # pinned destinations for the diagrams (grown on demand, outside the timed steps)
+        pin_out = [torch.empty(0, dtype=torch.uint8).pin_memory() for _ in range(2)]
+
         def e2e_step():
-            f_dev.copy_(f_pin, non_blocking=True)
-            step()
-            a = ctx.diagram0()
-            b = ctx.diagram_top()
+            # the public host-input call: the upload overlaps the gradient slab by slab
+            ctx.run_all_host(f_pin, rank_buf, grad_buf)
+            a = ctx.diagram0(out=pin_out[0])
+            b = ctx.diagram_top(out=pin_out[1])
             return a.nbytes + b.nbytes
 
+        ctx.run_all(rank_buf, grad_buf)
+        for k, fn in enumerate((dms.dms_diagram0, dms.dms_diagram_top)):
+            need = fn(ctx.ctx)[1] * dms.PAIR_DTYPE.itemsize  # same field every step
+            pin_out[k] = torch.empty(need + (1 << 20), dtype=torch.uint8).pin_memory()
         d2h = e2e_step()
         torch.cuda.synchronize()
         barrier()

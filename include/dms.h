@@ -126,6 +126,16 @@ dms_status dms_unpaired_saddles(dms_ctx* ctx, int which, const int64_t** d_ids, 
  * d_rank / d_grad may be NULL (library-owned scratch). */
 dms_status dms_run_all(dms_ctx* ctx, int32_t* d_rank, void* d_grad);
 
+/* dms_run_all with the field supplied in HOST memory: h_f (N float32, x-fastest, the
+ * layout of dms_create) is uploaded into the device field buffer given to dms_create
+ * (which this call overwrites) in slabs of whole planes, and the gradient of each slab
+ * starts as soon as the slab and its upper halo plane are on the device, so the
+ * host-to-device transfer overlaps the gradient; the vertex order follows the upload
+ * on the internal second stream.  h_f should be page-locked (cudaHostAlloc /
+ * torch pin_memory) for the copies to be asynchronous; the caller keeps it unchanged
+ * until the next synchronising call.  Same results and errors as dms_run_all. */
+dms_status dms_run_all_host(dms_ctx* ctx, const float* h_f, int32_t* d_rank, void* d_grad);
+
 /* Wait for the stream and report a pending device-side error (NaN, overflow). */
 dms_status dms_sync(dms_ctx* ctx);
 

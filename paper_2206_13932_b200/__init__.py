@@ -53,6 +53,7 @@ ABI_SYMBOLS = [
     "dms_diagram_top",
     "dms_unpaired_saddles",
     "dms_run_all",
+    "dms_run_all_host",
     "dms_sync",
     "dms_decode_pairs",
     "dms_copy",
@@ -94,6 +95,7 @@ def lib():
     L.dms_diagram_top.argtypes = [p, i32, P(p), P(i64)]
     L.dms_unpaired_saddles.argtypes = [p, i32, P(p), P(i64)]
     L.dms_run_all.argtypes = [p, p, p]
+    L.dms_run_all_host.argtypes = [p, p, p, p]
     L.dms_sync.argtypes = [p]
     L.dms_decode_pairs.argtypes = [p, i32, p, i64, i64, p, i64]
     L.dms_decode_pairs.restype = i64
@@ -107,7 +109,8 @@ def lib():
     L.dms_destroy.argtypes = [p]
     L.dms_destroy.restype = None
     for name in ("dms_create", "dms_order", "dms_gradient", "dms_critical", "dms_diagram0", "dms_diagram_top",
-                 "dms_unpaired_saddles", "dms_run_all", "dms_sync", "dms_copy", "dms_set_timing", "dms_stage_ms"):
+                 "dms_unpaired_saddles", "dms_run_all", "dms_run_all_host", "dms_sync", "dms_copy", "dms_set_timing",
+                 "dms_stage_ms"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -189,6 +192,13 @@ def dms_unpaired_saddles(ctx, which):
 def dms_run_all(ctx, rank=None, grad=None):
     _check(ctx, lib().dms_run_all(ctx, ctypes.c_void_p(rank.data_ptr() if rank is not None else 0),
                                   ctypes.c_void_p(grad.data_ptr() if grad is not None else 0)))
+
+
+def dms_run_all_host(ctx, f_host, rank=None, grad=None):
+    """f_host: a CPU float32 tensor (pinned for an overlapped upload), N elements."""
+    _check(ctx, lib().dms_run_all_host(ctx, ctypes.c_void_p(f_host.data_ptr()),
+                                       ctypes.c_void_p(rank.data_ptr() if rank is not None else 0),
+                                       ctypes.c_void_p(grad.data_ptr() if grad is not None else 0)))
 
 
 def dms_sync(ctx):
@@ -279,6 +289,14 @@ class DMS:
     def run_all(self, rank=None, grad=None):
         dms_run_all(self.ctx, rank, grad)
 
+    def run_all_host(self, f_host, rank=None, grad=None):
+        """run_all with the field uploaded from host memory (overwrites the device field)."""
+        if f_host.device.type != "cpu" or f_host.dtype != self.torch.float32 or f_host.numel() != self.f.numel():
+            raise ValueError("f_host must be a CPU float32 tensor with the field's size")
+        if not f_host.is_contiguous():
+            raise ValueError("f_host must be contiguous")
+        dms_run_all_host(self.ctx, f_host, rank, grad)
+
     def critical(self):
         """-> list of int64 CUDA tensors C_0..C_d (lexicographically sorted)."""
         t = self.torch
@@ -291,17 +309,25 @@ class DMS:
             out.append(a)
         return out
 
-    def _pairs(self, p, n):
-        a = np.empty(n, dtype=PAIR_DTYPE)
+    def _pairs(self, p, n, out=None):
+        nbytes = n * PAIR_DTYPE.itemsize
+        if out is None:
+            a = np.empty(n, dtype=PAIR_DTYPE)
+        else:  # caller's (pinned) CPU uint8 tensor: a view of its first n records
+            if out.device.type != "cpu" or out.dtype != self.torch.uint8 or out.numel() < nbytes:
+                raise ValueError("out must be a CPU uint8 tensor of at least %d bytes" % nbytes)
+            a = out.numpy()[:nbytes].view(PAIR_DTYPE)
         if n:
-            self._copy(a.ctypes.data, p, n * PAIR_DTYPE.itemsize)
+            self._copy(a.ctypes.data, p, nbytes)
         return a
 
-    def diagram0(self) -> np.ndarray:
-        return self._pairs(*dms_diagram0(self.ctx))
+    def diagram0(self, out=None) -> np.ndarray:
+        """D0 as a structured array (PAIR_DTYPE); out: optional pinned CPU uint8 tensor
+        to copy into (the result is then a view of it)."""
+        return self._pairs(*dms_diagram0(self.ctx), out=out)
 
-    def diagram_top(self, mode=0) -> np.ndarray:
-        return self._pairs(*dms_diagram_top(self.ctx, mode))
+    def diagram_top(self, mode=0, out=None) -> np.ndarray:
+        return self._pairs(*dms_diagram_top(self.ctx, mode), out=out)
 
     def unpaired_saddles(self, which) -> np.ndarray:
         p, n = dms_unpaired_saddles(self.ctx, which)

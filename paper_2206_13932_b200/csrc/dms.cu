@@ -71,6 +71,7 @@ struct dms_ctx {
     cudaStream_t st = nullptr;
     cudaStream_t st2 = nullptr;          // the vertex order runs here, beside the gradient
     cudaEvent_t ev_in = nullptr, ev_order = nullptr;
+    cudaEvent_t ev_slab[8] = {};  // dms_run_all_host: upload slabs
     bool order_pending = false;          // st must wait ev_order before using ranks
     int64_t ncell[4] = {1, 0, 0, 0};
     StarTab htab;
@@ -295,10 +296,15 @@ dms_status join_order(dms_ctx* c) {
     return DMS_OK;
 }
 
-dms_status launch_gradient(dms_ctx* c) {
-    const int64_t ntiles = ceil_div(c->N, kBlock);
-    CU(cudaMemsetAsync(c->totals, 0, 4 * sizeof(unsigned long long), c->st));
+// one gradient launch over the vertices [v0, v1) (the record counters are zeroed by the
+// first launch of a pass, v0 == 0)
+dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
+    const int64_t ntiles = ceil_div(v1 - v0, kBlock);
+    if (v0 == 0) CU(cudaMemsetAsync(c->totals, 0, 4 * sizeof(unsigned long long), c->st));
+    if (v1 <= v0) return DMS_OK;
     GradArgs A;
+    A.v0 = v0;
+    A.v1 = v1;
     A.f = c->f;
     A.Lx = (int32_t)c->L[0];
     A.Ly = (int32_t)c->L[1];
@@ -317,7 +323,7 @@ dms_status launch_gradient(dms_ctx* c) {
     StageTimer tm(c, 5);
     if (c->ndim >= 2) {
         // one CTA per 128 vertices; the CTA regroups its vertices by expansion work
-        const unsigned g2 = (unsigned)ceil_div(c->N, kBlockG);
+        const unsigned g2 = (unsigned)ceil_div(v1 - v0, kBlockG);
         if (c->ndim == 3) k_gradient_rg<3><<<g2, kBlockG, 0, c->st>>>(A);
         else k_gradient_rg<2><<<g2, kBlockG, 0, c->st>>>(A);
     } else {
@@ -331,7 +337,7 @@ dms_status launch_gradient(dms_ctx* c) {
 dms_status run_gradient(dms_ctx* c, void* d_grad) {
     c->grad = d_grad ? d_grad : c->grad_scratch;
     StageTimer tm(c, 1);
-    dms_status s = launch_gradient(c);
+    dms_status s = launch_gradient(c, 0, c->N);
     if (s) return s;
     c->have_grad = true;
     c->have_crit = c->have_d[0] = c->have_d[1] = false;
@@ -366,7 +372,7 @@ dms_status run_critical(dms_ctx* c) {
     if (overflow) {  // rare: grow the record buffers and recompute
         s = alloc_crit(c);
         if (s) return s;
-        s = launch_gradient(c);
+        s = launch_gradient(c, 0, c->N);
         if (s) return s;
     }
     for (int k = 0; k <= c->ndim; k++) c->ncrit[k] = (int64_t)tot[k];
@@ -812,6 +818,56 @@ dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     return DMS_OK;
 }
 
+dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void* d_grad) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!h_f) return DMS_ERR_ARG;
+    // Upload in K slabs of whole planes (z in 3D, y in 2D, runs in 1D) on the second
+    // stream; the gradient of slab i starts once slab i+1 (its upper halo plane) is in,
+    // so the transfer hides behind the ALU-bound gradient.  The vertex order (which
+    // needs every value) follows the last slab on the same stream.
+    constexpr int K = 8;
+    for (int i = 0; i < K; i++)
+        if (!c->ev_slab[i]) CU(cudaEventCreateWithFlags(&c->ev_slab[i], cudaEventDisableTiming));
+    const int64_t plane = c->ndim == 3 ? c->L[0] * c->L[1] : (c->ndim == 2 ? c->L[0] : 1);
+    const int64_t nplanes = c->N / plane;
+    int64_t b[K + 1];
+    for (int i = 0; i <= K; i++) b[i] = plane * (nplanes * i / K);
+    CU(cudaEventRecord(c->ev_in, c->st));  // earlier work on the field is done
+    CU(cudaStreamWaitEvent(c->st2, c->ev_in, 0));
+    float* fdev = const_cast<float*>(c->f);
+    for (int i = 0; i < K; i++) {
+        if (b[i + 1] > b[i])
+            CU(cudaMemcpyAsync(fdev + b[i], h_f + b[i], (size_t)(b[i + 1] - b[i]) * sizeof(float),
+                               cudaMemcpyHostToDevice, c->st2));
+        CU(cudaEventRecord(c->ev_slab[i], c->st2));
+    }
+    // the vertex order on the second stream, after the last slab
+    {
+        cudaStream_t main = c->st;
+        c->st = c->st2;
+        s = run_order_on_stream(c, d_rank);
+        c->st = main;
+        if (s) return s;
+        CU(cudaEventRecord(c->ev_order, c->st2));
+        c->order_pending = true;
+    }
+    c->grad = d_grad ? d_grad : c->grad_scratch;
+    {
+        StageTimer tm(c, 1);
+        for (int i = 0; i < K; i++) {
+            CU(cudaStreamWaitEvent(c->st, c->ev_slab[std::min(i + 1, K - 1)], 0));
+            if ((s = launch_gradient(c, b[i], b[i + 1]))) return s;
+        }
+    }
+    c->have_grad = true;
+    c->have_crit = c->have_d[0] = c->have_d[1] = false;
+    if ((s = run_critical(c))) return s;
+    if ((s = run_d0(c))) return s;
+    if ((s = run_dtop(c))) return s;
+    return DMS_OK;
+}
+
 dms_status dms_sync(dms_ctx* c) {
     dms_status s = check_sticky(c);
     if (s) return s;
@@ -938,6 +994,8 @@ void dms_destroy(dms_ctx* c) {
     if (c->st2) cudaStreamDestroy(c->st2);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_order) cudaEventDestroy(c->ev_order);
+    for (cudaEvent_t e : c->ev_slab)
+        if (e) cudaEventDestroy(e);
     cudaFree(c->dtab);
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);

@@ -46,6 +46,7 @@ struct GradArgs {
     const float* f;
     int32_t Lx, Ly, Lz;
     int64_t N;
+    int64_t v0, v1;  // this launch's vertex range [v0, v1)
     const StarTab* tab;
     void* grad;
     int64_t* crit_id[4];
@@ -339,11 +340,11 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
     const int tid = threadIdx.x;
     // ---- phase A: setup of this thread's own vertex
     {
-        const int64_t v = (int64_t)blockIdx.x * kBlockG + tid;
+        const int64_t v = A.v0 + (int64_t)blockIdx.x * kBlockG + tid;
         uint32_t Le = 0, Lq = 0, word = 0;
         uint64_t Lt = 0, R = 0, IV = 0;
         int w = 0;
-        if (v < A.N) {
+        if (v < A.v1) {
             const int vv = (int)v;
             const int cx = vv % A.Lx;
             const int t = vv / A.Lx;
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
     }
     // ---- phase C: expansion of a (work-sorted) vertex of this CTA
     const int p = s_perm[tid];
-    const int64_t v = (int64_t)blockIdx.x * kBlockG + p;
+    const int64_t v = A.v0 + (int64_t)blockIdx.x * kBlockG + p;
     const uint32_t word = s_Le[p];
     const bool active = (word >> 24) & 1u;
     StarState st;
@@ -545,8 +546,8 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
 __global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
     __shared__ uint32_t sw[2][kBlock / 32 + 1];
     __shared__ unsigned long long s_base[2];
-    const int64_t v = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    const bool active = v < A.N;
+    const int64_t v = A.v0 + (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const bool active = v < A.v1;
     bool crit_v = false, crit_e = false;
     int crit_slot = 0;
     if (active) {

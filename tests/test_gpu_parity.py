@@ -151,3 +151,30 @@ def test_deterministic_repeat(env):
     for key in ("rank", "grad"):
         assert np.array_equal(a[key], b[key])
     assert a["d0"].tobytes() == b["d0"].tobytes() and a["dtop"].tobytes() == b["dtop"].tobytes()
+
+
+@pytest.mark.parametrize("name,shape", [("c1", (32, 32, 32)), ("c1", (4, 5, 6)), ("c4", (40, 48, 64)),
+                                        ("c5a", (300, 257)), ("c5b", (100003,)), ("c5b", (5,))])
+def test_run_all_host_matches_device_input(env, name, shape):
+    """dms_run_all_host (slab-pipelined upload from pinned host memory) gives exactly the
+    results of dms_run_all on the same field already on the device, including fields
+    with fewer planes than upload slabs; the device buffer starts with other values."""
+    torch, dms = env
+    f = np.ascontiguousarray(fields.make(name, seed=3, shape=shape))
+    ref = gpu_run(env, f)
+    dev = torch.full(f.shape, 7.0, dtype=torch.float32, device="cuda")
+    d = dms.DMS(dev)
+    rank = torch.empty(f.size, dtype=torch.int32, device="cuda")
+    grad = torch.empty(dms.dms_gradient_bytes(d.ctx), dtype=torch.uint8, device="cuda")
+    for _ in range(2):  # twice: the second upload overwrites a field the first run used
+        d.run_all_host(torch.from_numpy(f).pin_memory(), rank, grad)
+        assert np.array_equal(dev.cpu().numpy(), f)
+        assert np.array_equal(rank.cpu().numpy(), ref["rank"])
+        assert np.array_equal(grad.cpu().numpy(), ref["grad"])
+        for k in range(f.ndim + 1):
+            assert np.array_equal(d.critical()[k].cpu().numpy(), ref["crit"][k])
+        assert d.diagram0().tobytes() == ref["d0"].tobytes()
+        assert d.diagram_top().tobytes() == ref["dtop"].tobytes()
+        assert np.array_equal(d.unpaired_saddles(0), ref["un0"])
+        assert np.array_equal(d.unpaired_saddles(1), ref["untop"])
+    d.close()
