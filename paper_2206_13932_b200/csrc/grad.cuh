@@ -107,15 +107,21 @@ __device__ __forceinline__ uint32_t kidx_key(const StarTab& S, int ki) {
 struct KMask {  // 128-bit set over triangle key indices (kept in registers)
     uint64_t lo, hi;
 };
+// W (wide): key indices may reach 90 (3D); without W they stay below 64 (2D: < 15) and
+// the queue is one 64-bit word.
+template <bool W>
 __device__ __forceinline__ void kset(KMask& m, int ki) {
-    if (ki < 64) m.lo |= 1ull << ki;
+    if (!W || ki < 64) m.lo |= 1ull << ki;
     else m.hi |= 1ull << (ki - 64);
 }
+template <bool W>
 __device__ __forceinline__ void kclr(KMask& m, int ki) {
-    if (ki < 64) m.lo &= ~(1ull << ki);
+    if (!W || ki < 64) m.lo &= ~(1ull << ki);
     else m.hi &= ~(1ull << (ki - 64));
 }
+template <bool W>
 __device__ __forceinline__ int kfirst(const KMask& m) {
+    if (!W) return __ffsll((long long)m.lo) - 1;
     if (m.lo) return __ffsll((long long)m.lo) - 1;
     if (m.hi) return 64 + __ffsll((long long)m.hi) - 1;
     return -1;
@@ -177,7 +183,7 @@ struct StarState {
 // is only popped when PQone is empty, by which time it holds the same cells, so the
 // early move changes no pop.  U2t = triangles whose two edges
 // are both unclassified.
-template <int D>
+template <int D, bool W>
 __device__ __forceinline__ void push_tris_of_edge(const StarTab& S, const KeyCache& C, StarState& st, int e) {
     const uint64_t et = S.edge_tri_mask[e] & st.Lt & ~st.cls_t;
     uint64_t pushed = et & st.U2t;
@@ -186,14 +192,14 @@ __device__ __forceinline__ void push_tris_of_edge(const StarTab& S, const KeyCac
     while (pushed) {
         const int t = __ffsll((long long)pushed) - 1;
         pushed &= pushed - 1;
-        kset(st.pq1_t, C.tri(t));
+        kset<W>(st.pq1_t, C.tri(t));
     }
     while (zeroed) {
         const int t = __ffsll((long long)zeroed) - 1;
         zeroed &= zeroed - 1;
         const int ki = C.tri(t);
-        kclr(st.pq1_t, ki);
-        kset(st.pq0_t, ki);
+        kclr<W>(st.pq1_t, ki);
+        kset<W>(st.pq0_t, ki);
     }
 }
 
@@ -219,7 +225,7 @@ __device__ __forceinline__ void set_tcode(StarState& st, int t, uint64_t code) {
 
 // ProcessLowerStars on one lower star (Robins et al., as pinned in DESIGN.md Z1).
 // R: slot -> local rank, IV: local rank -> slot (4 bits each).
-template <int D>
+template <int D, bool W>
 __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C, uint64_t R, uint64_t IV, int nlow,
                                              int delta, StarState& st) {
     st.vcode = delta;
@@ -233,19 +239,19 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
         while (cand) {
             const int t = __ffsll((long long)cand) - 1;
             cand &= cand - 1;
-            kset(st.pq1_t, C.tri(t));
+            kset<W>(st.pq1_t, C.tri(t));
         }
     }
     while (true) {
-        while ((st.pq1_t.lo | st.pq1_t.hi) | st.pq1_q) {
+        while ((st.pq1_t.lo | (W ? st.pq1_t.hi : 0ull)) | st.pq1_q) {
             // every cell in PQone has exactly one unclassified facet (cells leave PQone
             // when they reach zero or get classified), so each pop pairs
-            const int ki = kfirst(st.pq1_t);
+            const int ki = kfirst<W>(st.pq1_t);
             const uint32_t ktri = ki >= 0 ? cmp_tri(ki) : 0xffffffffu;
             uint32_t ktet = 0xffffffffu;
             const int q = (D == 3 && st.pq1_q) ? tet_min(C, st.pq1_q, &ktet) : -1;
             if (ktri < ktet) {
-                kclr(st.pq1_t, ki);
+                kclr<W>(st.pq1_t, ki);
                 const int s = C.slot(ki);
                 const int a = S.tri_a[s];
                 const bool ua = !((st.cls_e >> a) & 1u);
@@ -255,7 +261,7 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
                 st.cls_t |= 1ull << s;
                 st.pq0_er &= ~(1u << rk(R, e));
                 push_tets_of_tri<D>(S, st, s);      // cofacets of alpha
-                push_tris_of_edge<D>(S, C, st, e);  // cofacets of pair(alpha)
+                push_tris_of_edge<D, W>(S, C, st, e);  // cofacets of pair(alpha)
             } else if constexpr (D == 3) {
                 st.pq1_q &= ~(1u << q);
                 const int t0 = S.tet_tri[q][0], t1 = S.tet_tri[q][1];
@@ -266,14 +272,14 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
                 st.cls_t |= 1ull << tt;
                 st.cls_q |= 1u << q;
                 const int kt = C.tri(tt);  // tt leaves both queues
-                kclr(st.pq0_t, kt);
-                kclr(st.pq1_t, kt);
+                kclr<W>(st.pq0_t, kt);
+                kclr<W>(st.pq1_t, kt);
                 push_tets_of_tri<D>(S, st, tt);
             }
         }
         // PQzero: minimum over edges (rank space), triangles (key space), tets
         const uint32_t ke = st.pq0_er ? cmp_edge(__ffs(st.pq0_er) - 1) : 0xffffffffu;
-        const int ki = kfirst(st.pq0_t);
+        const int ki = kfirst<W>(st.pq0_t);
         const uint32_t kt = ki >= 0 ? cmp_tri(ki) : 0xffffffffu;
         uint32_t kq = 0xffffffffu;
         const int q = (D == 3 && st.pq0_q) ? tet_min(C, st.pq0_q, &kq) : -1;
@@ -284,9 +290,9 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
             const int e = rk(IV, r);
             st.cls_e |= 1u << e;
             st.crit_e |= 1u << e;
-            push_tris_of_edge<D>(S, C, st, e);
+            push_tris_of_edge<D, W>(S, C, st, e);
         } else if (kt < kq) {
-            kclr(st.pq0_t, ki);
+            kclr<W>(st.pq0_t, ki);
             const int s = C.slot(ki);
             st.cls_t |= 1ull << s;
             st.crit_t |= 1ull << s;
@@ -474,7 +480,9 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
         C.IV = IV;
         C.S = &S;
         C.R = R;
-        process_star<D>(S, C, R, IV, __popc(st.Le), (int)((word >> 16) & 15u), st);
+        // 2D key indices stay below C(6,2) = 15: one-word queues.  (3D keeps the two-word
+        // form for every star: a narrow/wide split per star cost 15 % in 3D.)
+        process_star<D, D == 3>(S, C, R, IV, __popc(st.Le), (int)((word >> 16) & 15u), st);
     }
     if (active) {
         if (D == 3) {
