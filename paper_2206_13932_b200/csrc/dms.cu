@@ -54,11 +54,21 @@ struct UFBuf {
     int32_t* age = nullptr;                     // per node (emission order)
     uint32_t* inv_n = nullptr;
     int* nlive = nullptr;  // two device counters
+    int* h_status = nullptr;  // pinned: the union-find's convergence status
     int* trace = nullptr;  // [64] union-find round trace
     int32_t* parent = nullptr;
     unsigned long long* best = nullptr;
     uint32_t *flags = nullptr, *pos = nullptr;
     int64_t cap_arcs = 0, cap_nodes = 0;
+};
+
+// a second issue lane (stream + scan scratch + pinned scratch): D0 runs on it beside
+// D_{d-1} (PAPER.md 1124: the two diagrams are computed concurrently)
+struct Lane {
+    cudaStream_t st = nullptr;
+    SortScratch ss;
+    int* tile_ctr = nullptr;
+    unsigned long long* h_pinned = nullptr;
 };
 
 }  // namespace
@@ -72,6 +82,10 @@ struct dms_ctx {
     cudaStream_t st2 = nullptr;          // the vertex order runs here, beside the gradient
     cudaEvent_t ev_in = nullptr, ev_order = nullptr;
     cudaEvent_t ev_slab[8] = {};  // dms_run_all_host: upload slabs
+    Lane lane3;                   // D0's lane when the diagrams run concurrently
+    cudaEvent_t ev_crit = nullptr, ev_d0 = nullptr;
+    bool half = false;            // concurrent diagrams: persistent / cooperative grids use half the GPU
+    cudaEvent_t t_diag[2] = {};   // stage timers spanning issue .. finish
     bool order_pending = false;          // st must wait ev_order before using ranks
     int64_t ncell[4] = {1, 0, 0, 0};
     StarTab htab;
@@ -137,6 +151,36 @@ struct StageTimer {
         } else {
             cudaEventDestroy(a);
         }
+    }
+};
+
+cudaEvent_t stage_begin(dms_ctx* c) {
+    cudaEvent_t a = nullptr;
+    if (c->timing && cudaEventCreate(&a) == cudaSuccess) cudaEventRecord(a, c->st);
+    return a;
+}
+void stage_end(dms_ctx* c, int stage, cudaEvent_t a) {
+    if (!a) return;
+    cudaEvent_t b = nullptr;
+    if (cudaEventCreate(&b) == cudaSuccess) {
+        cudaEventRecord(b, c->st);
+        c->ev[stage].emplace_back(a, b);
+    } else {
+        cudaEventDestroy(a);
+    }
+}
+
+// swaps the context's issue resources with a lane's for a scope
+struct LaneSwap {
+    dms_ctx* c;
+    Lane& L;
+    LaneSwap(dms_ctx* c_, Lane& l) : c(c_), L(l) { swap(); }
+    ~LaneSwap() { swap(); }
+    void swap() {
+        std::swap(c->st, L.st);
+        std::swap(c->ss, L.ss);
+        std::swap(c->tile_ctr, L.tile_ctr);
+        std::swap(c->h_pinned, L.h_pinned);
     }
 };
 
@@ -224,6 +268,7 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
             CU(dalloc(p, arcs));
         }
         if (!u.nlive) CU(dalloc(&u.nlive, 8));
+        if (!u.h_status && cudaMallocHost(&u.h_status, sizeof(int)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
         if (!u.trace) CU(dalloc(&u.trace, 128 + 128));
         for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
         u.cap_arcs = arcs;
@@ -396,7 +441,8 @@ dms_status run_critical(dms_ctx* c) {
 
 // union-find over arcs (processing order), see diag.cuh
 // u.arc_a / u.arc_b / u.key (per arc) and u.age (per node) are in emission order
-dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
+// issue: init + the cooperative rounds; the convergence status lands in pinned memory
+dms_status uf_issue(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     const unsigned gi = grid_for(std::max(m, nodes));
     k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.arc_a, u.arc_b, u.key, m, u.out, u.rec0);
     c->launches++;
@@ -407,7 +453,8 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_uf_coop, kBlock, 0);
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(m), (int64_t)sms * std::max(per, 1)));
+    const int64_t resident = (int64_t)sms * std::max(per, 1) / (c->half ? 2 : 1);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(m), resident));
     UFArgs U;
     U.parent = u.parent;
     U.best = u.best;
@@ -428,11 +475,16 @@ dms_status union_find(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     void* args[] = {&U};
     CU(cudaLaunchCooperativeKernel((void*)k_uf_coop, grid, kBlock, args, 0, c->st));
     c->launches++;
-    int st = -1;
-    CU(cudaMemcpyAsync(c->h_pinned, u.nlive + 2, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(u.h_status, u.nlive + 2, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    return DMS_OK;
+}
+
+// finish: wait for the rounds; a pathological input that did not converge within
+// max_rounds gets the sequential tail here
+dms_status uf_finish(dms_ctx* c, UFBuf& u, int64_t m) {
+    if (m == 0) return DMS_OK;
     CU(cudaStreamSynchronize(c->st));
-    std::memcpy(&st, c->h_pinned, sizeof(int));
-    if (st < 0) return DMS_OK;
+    if (*u.h_status < 0) return DMS_OK;
     // pathological input (no convergence within max_rounds): sequential tail over the
     // undecided arcs in processing order (gather them, sort by key, then one thread)
     k_flag_undecided<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags);
@@ -507,12 +559,8 @@ void out_to_processing(dms_ctx* c, UFBuf& u, int karcs, int64_t m, int rev) {
     std::swap(u.out, u.outp);
 }
 
-dms_status run_d0(dms_ctx* c) {
-    if (!c->have_crit) {
-        dms_status s = run_critical(c);
-        if (s) return s;
-    }
-    StageTimer tm(c, 3);
+dms_status d0_issue(dms_ctx* c) {
+    c->t_diag[0] = stage_begin(c);
     UFBuf& u = c->uf[0];
     const int64_t m = c->ncrit[1], n0 = c->ncrit[0];
     dms_status s = alloc_uf(c, u, m, n0);
@@ -529,10 +577,19 @@ dms_status run_d0(dms_ctx* c) {
     {
         StageTimer t8(c, 8);
         uf_keys_ages(c, u, 1, m, 0, n0, 0);
-        s = union_find(c, u, m, n0);
+        s = uf_issue(c, u, m, n0);
         if (s) return s;
-        out_to_processing(c, u, 1, m, 0);
     }
+    return DMS_OK;
+}
+
+dms_status d0_finish(dms_ctx* c) {
+    UFBuf& u = c->uf[0];
+    const int64_t m = c->ncrit[1];
+    Geo3 g = geo(c);
+    dms_status s = uf_finish(c, u, m);
+    if (s) return s;
+    out_to_processing(c, u, 1, m, 0);
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
@@ -554,16 +611,14 @@ dms_status run_d0(dms_ctx* c) {
     s = emit_unpaired(c, 0, u, m, crit_ids(c, 1), 0);
     if (s) return s;
     CU(cudaGetLastError());
+    stage_end(c, 3, c->t_diag[0]);
+    c->t_diag[0] = nullptr;
     c->have_d[0] = true;
     return DMS_OK;
 }
 
-dms_status run_dtop(dms_ctx* c) {
-    if (!c->have_crit) {
-        dms_status s = run_critical(c);
-        if (s) return s;
-    }
-    StageTimer tm(c, 4);
+dms_status dtop_issue(dms_ctx* c) {
+    c->t_diag[1] = stage_begin(c);
     const int d = c->ndim;
     UFBuf& u = c->uf[1];
     const int64_t m = c->ncrit[d - 1], nd = c->ncrit[d];
@@ -586,7 +641,7 @@ dms_status run_dtop(dms_ctx* c) {
             if (d == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<3, true>, kBlock, 0);
             else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<2, true>, kBlock, 0);
             const unsigned grid = (unsigned)std::max<int64_t>(
-                1, std::min<int64_t>(grid_for(2 * m), (int64_t)sms * std::max(per, 1)));
+                1, std::min<int64_t>(grid_for(2 * m), (int64_t)sms * std::max(per, 1) / (c->half ? 2 : 1)));
             CU(cudaMemsetAsync(c->tile_ctr, 0, sizeof(int), c->st));
             const int64_t* ids = crit_ids_emitted(c, d - 1);
             if (memo) {
@@ -627,10 +682,20 @@ dms_status run_dtop(dms_ctx* c) {
     {
         StageTimer t9(c, 9);
         uf_keys_ages(c, u, d - 1, m, d, nd, 1);
-        s = union_find(c, u, m, nd + 1);
+        s = uf_issue(c, u, m, nd + 1);
         if (s) return s;
-        out_to_processing(c, u, d - 1, m, 1);
     }
+    return DMS_OK;
+}
+
+dms_status dtop_finish(dms_ctx* c) {
+    const int d = c->ndim;
+    UFBuf& u = c->uf[1];
+    const int64_t m = c->ncrit[d - 1];
+    Geo3 g = geo(c);
+    dms_status s = uf_finish(c, u, m);
+    if (s) return s;
+    out_to_processing(c, u, d - 1, m, 1);
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
@@ -658,7 +723,58 @@ dms_status run_dtop(dms_ctx* c) {
     }
     c->npairs[1] = np + ninf;
     CU(cudaGetLastError());
+    stage_end(c, 4, c->t_diag[1]);
+    c->t_diag[1] = nullptr;
     c->have_d[1] = true;
+    return DMS_OK;
+}
+
+dms_status run_d0(dms_ctx* c) {
+    if (!c->have_crit) {
+        dms_status s = run_critical(c);
+        if (s) return s;
+    }
+    dms_status s = d0_issue(c);
+    return s ? s : d0_finish(c);
+}
+
+dms_status run_dtop(dms_ctx* c) {
+    if (!c->have_crit) {
+        dms_status s = run_critical(c);
+        if (s) return s;
+    }
+    dms_status s = dtop_issue(c);
+    return s ? s : dtop_finish(c);
+}
+
+// D0 on the second lane beside D_{d-1} (both only read the gradient and the critical
+// lists): issue both, then finish both, so the host's count reads for one overlap the
+// other's kernels; persistent and cooperative grids take half the GPU each (two
+// cooperative grids must be co-resident together).
+dms_status run_diagrams(dms_ctx* c) {
+    static const int conc_env = getenv("DMS_CONCURRENT") ? atoi(getenv("DMS_CONCURRENT")) : 1;
+    if (!conc_env || !c->lane3.st) {
+        dms_status s = run_d0(c);
+        return s ? s : run_dtop(c);
+    }
+    CU(cudaEventRecord(c->ev_crit, c->st));
+    CU(cudaStreamWaitEvent(c->lane3.st, c->ev_crit, 0));
+    c->half = true;
+    dms_status s;
+    {
+        LaneSwap ls(c, c->lane3);
+        s = d0_issue(c);
+    }
+    if (!s) s = dtop_issue(c);
+    if (!s) {
+        LaneSwap ls(c, c->lane3);
+        s = d0_finish(c);
+    }
+    if (!s) s = dtop_finish(c);
+    c->half = false;
+    if (s) return s;
+    CU(cudaEventRecord(c->ev_d0, c->lane3.st));  // the caller's stream sees D0's results
+    CU(cudaStreamWaitEvent(c->st, c->ev_d0, 0));
     return DMS_OK;
 }
 
@@ -715,6 +831,19 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         if (cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi) != cudaSuccess) return bail(DMS_ERR_CUDA);
     }
+    {
+        Lane& L = c->lane3;
+        if (cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking) != cudaSuccess) return bail(DMS_ERR_CUDA);
+        CA(dalloc(&L.ss.counts, max_tiles * kRadix));
+        CA(dalloc(&L.ss.counts_scan, max_tiles * kRadix));
+        CA(dalloc(&L.ss.status, ceil_div(std::max<int64_t>(max_tiles * kRadix, N), (int64_t)kBlock * kScanItems) + 1));
+        CA(dalloc(&L.ss.tile_ctr, 1));
+        L.ss.max_tiles = max_tiles;
+        CA(dalloc(&L.tile_ctr, 1));
+        if (cudaMallocHost(&L.h_pinned, 64) != cudaSuccess) return bail(DMS_ERR_OOM);
+    }
+    if (cudaEventCreateWithFlags(&c->ev_crit, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    if (cudaEventCreateWithFlags(&c->ev_d0, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     CA(dalloc(&c->node_of0, N));
@@ -813,8 +942,7 @@ dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     if ((s = run_order(c, d_rank, true))) return s;  // second stream, overlaps the gradient
     if ((s = run_gradient(c, d_grad))) return s;
     if ((s = run_critical(c))) return s;
-    if ((s = run_d0(c))) return s;
-    if ((s = run_dtop(c))) return s;
+    if ((s = run_diagrams(c))) return s;
     return DMS_OK;
 }
 
@@ -863,8 +991,7 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
     c->have_grad = true;
     c->have_crit = c->have_d[0] = c->have_d[1] = false;
     if ((s = run_critical(c))) return s;
-    if ((s = run_d0(c))) return s;
-    if ((s = run_dtop(c))) return s;
+    if ((s = run_diagrams(c))) return s;
     return DMS_OK;
 }
 
@@ -990,8 +1117,23 @@ void dms_destroy(dms_ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->st);
     if (c->st2) cudaStreamSynchronize(c->st2);
+    if (c->lane3.st) cudaStreamSynchronize(c->lane3.st);
     clear_events(c);
     if (c->st2) cudaStreamDestroy(c->st2);
+    {
+        Lane& L = c->lane3;
+        if (L.st) cudaStreamDestroy(L.st);
+        cudaFree(L.ss.counts);
+        cudaFree(L.ss.counts_scan);
+        cudaFree(L.ss.status);
+        cudaFree(L.ss.tile_ctr);
+        cudaFree(L.tile_ctr);
+        if (L.h_pinned) cudaFreeHost(L.h_pinned);
+    }
+    for (cudaEvent_t e : {c->ev_crit, c->ev_d0})
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->t_diag)
+        if (e) cudaEventDestroy(e);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_order) cudaEventDestroy(c->ev_order);
     for (cudaEvent_t e : c->ev_slab)
@@ -1023,6 +1165,7 @@ void dms_destroy(dms_ctx* c) {
                         (void*)u.inv_a, (void*)u.age, (void*)u.inv_n,
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
             cudaFree(p);
+        if (u.h_status) cudaFreeHost(u.h_status);
         cudaFree(c->pairs[b]);
         cudaFree(c->unp[b]);
     }
