@@ -590,6 +590,16 @@ __global__ void k_uf_init(int32_t* parent, unsigned long long* best, int64_t n, 
     }
 }
 
+// the arc records in processing (key) order for the batched rounds: src[j] = the arc
+// with key j (perm: processing index -> emission index; rev: D_{d-1}'s descending order)
+__global__ void k_uf_src(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b,
+                         const uint32_t* __restrict__ perm, int64_t m, int rev, int4* __restrict__ src) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const int64_t i = perm[rev ? m - 1 - j : j];
+    src[j] = make_int4(arc_a[i], arc_b[i], (int)j, (int)i);
+}
+
 __global__ void k_flag_undecided(const int32_t* out, int64_t m, uint32_t* flags) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) flags[i] = out[i] == -2 ? 1u : 0u;
@@ -620,6 +630,15 @@ struct UFArgs {
     int* trace;   // [64]: live arcs of each round; [63] = rounds run; [128..]: 64 u64 timestamps
     int max_rounds;
     int agg;
+    // batches (dense graphs): src = all arc records in processing (key) order; the rounds
+    // start with an empty live list and reveal `batch` more records of src whenever the
+    // live list has shrunk to batch / 4 or less.  Every arc is still decided only after all
+    // lighter arcs are present, so the decisions are the sequential ones;
+    // cycle arcs die in the first round after their batch is revealed instead of riding
+    // along through every round.  batch = 0: everything is live from the start.
+    const int4* src;
+    int nsrc;
+    int batch;
 };
 
 __device__ __forceinline__ int ld_cg_int(const int* p) { return __ldcg(p); }
@@ -664,10 +683,16 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
     const int lane = threadIdx.x & 31;
     int cur = 0;
     bool done = false;
+    int rv = U.batch ? 0 : U.nsrc;  // records of src revealed so far
     for (int round = 0; round < U.max_rounds; round++) {
         const int4* live = cur ? U.rec1 : U.rec0;
         int4* nxt = cur ? U.rec0 : U.rec1;
-        const int n = ld_cg_int(&U.nlive[cur]);
+        const int nl = ld_cg_int(&U.nlive[cur]);
+        int add = 0;  // this round also takes src[rv .. rv + add)
+        if (rv < U.nsrc && nl <= U.batch / 4) {
+            add = min(U.batch, U.nsrc - rv);
+        }
+        const int n = nl + add;
         // pass A: roots of the arcs still undecided (records marked a = -1 were decided
         // last round), cycle arcs (same root: final, unpaired), lightest arc of every
         // root; the survivors are compacted into the next list with their roots
@@ -686,7 +711,7 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
                 int4 r = make_int4(0, 0, 0, 0);
                 bool act = false;
                 if (idx < n) {
-                    r = live[idx];
+                    r = idx < nl ? live[idx] : U.src[rv + (idx - nl)];
                     if (r.x >= 0) {
                         r.x = uf_find(U.parent, r.x);
                         r.y = uf_find(U.parent, r.y);
@@ -711,6 +736,7 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
         }
         grid.sync();
         cur ^= 1;  // the survivors' list
+        rv += add;
         const int m2 = ld_cg_int(&U.nlive[cur]);
         if (gtid == 0) {
             if (round < 63) {
@@ -720,7 +746,11 @@ __global__ void __launch_bounds__(kBlock) k_uf_coop(UFArgs U) {
             U.trace[63] = round;
             U.nlive[cur ^ 1] = 0;  // the list just consumed becomes the next round's output
         }
-        if (m2 <= kUFTail) { done = true; break; }
+        if (m2 <= kUFTail && rv == U.nsrc) { done = true; break; }
+        if (m2 == 0) {  // nothing to decide this round: reveal more next round
+            grid.sync();  // (the counter reset above must land before the next appends)
+            continue;
+        }
         // pass B: mutual minimum, or a younger root dying at its lightest arc
         int4* sur = cur ? U.rec1 : U.rec0;
         for (int idx = gtid; idx < m2; idx += stride) {

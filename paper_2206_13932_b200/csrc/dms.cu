@@ -48,6 +48,7 @@ __global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsig
 struct UFBuf {
     int32_t *arc_a = nullptr, *arc_b = nullptr, *out = nullptr, *list = nullptr;
     int4 *rec0 = nullptr, *rec1 = nullptr;  // union-find live arc records
+    int4* rsrc = nullptr;                    // all arc records in key order (batched rounds)
     int32_t* live2 = nullptr;
     int32_t* outp = nullptr;   // out in processing order
     uint32_t *key = nullptr, *inv_a = nullptr;  // per arc (emission order)
@@ -255,7 +256,7 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
     arcs = std::max<int64_t>(arcs, 1);
     nodes = std::max<int64_t>(nodes, 1);
     if (arcs > u.cap_arcs) {
-        for (int4** p : {&u.rec0, &u.rec1}) {
+        for (int4** p : {&u.rec0, &u.rec1, &u.rsrc}) {
             cudaFree(*p);
             CU(dalloc(p, arcs));
         }
@@ -442,7 +443,7 @@ dms_status run_critical(dms_ctx* c) {
 // union-find over arcs (processing order), see diag.cuh
 // u.arc_a / u.arc_b / u.key (per arc) and u.age (per node) are in emission order
 // issue: init + the cooperative rounds; the convergence status lands in pinned memory
-dms_status uf_issue(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
+dms_status uf_issue(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, int karcs, int rev) {
     const unsigned gi = grid_for(std::max(m, nodes));
     k_uf_init<<<gi, kBlock, 0, c->st>>>(u.parent, u.best, nodes, u.arc_a, u.arc_b, u.key, m, u.out, u.rec0);
     c->launches++;
@@ -471,7 +472,20 @@ dms_status uf_issue(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes) {
     // same-address contention on best[] comes with arc-dense graphs (3D: ~4 arcs per node,
     // the big components collect most arcs): pre-reduce per warp there (measured)
     static const int agg_env = getenv("DMS_AGG") ? atoi(getenv("DMS_AGG")) : -1;
-    U.agg = agg_env >= 0 ? agg_env : ((double)m > 3.0 * (double)nodes ? 2 : 0);
+    const bool dense = (double)m > 3.0 * (double)nodes;
+    U.agg = agg_env >= 0 ? agg_env : (dense ? 2 : 0);
+    // dense graphs (most arcs close cycles): reveal the arcs in key-ordered batches
+    static const int batch_env = getenv("DMS_UFBATCH") ? atoi(getenv("DMS_UFBATCH")) : -1;
+    const int nb = batch_env >= 0 ? batch_env : (dense ? 16 : 0);  // (sweep: DESIGN.md 8b)
+    U.src = u.rsrc;
+    U.nsrc = (int)m;
+    U.batch = nb > 0 ? (int)std::max<int64_t>(kUFTail, (m + nb - 1) / nb) : 0;
+    if (U.batch) {
+        k_uf_src<<<grid_for(m), kBlock, 0, c->st>>>(u.arc_a, u.arc_b, crit_perm(c, karcs), m, rev, u.rsrc);
+        c->launches++;
+        int hz[2] = {0, 0};  // the live list starts empty
+        CU(cudaMemcpyAsync(u.nlive, hz, sizeof hz, cudaMemcpyHostToDevice, c->st));
+    }
     void* args[] = {&U};
     CU(cudaLaunchCooperativeKernel((void*)k_uf_coop, grid, kBlock, args, 0, c->st));
     c->launches++;
@@ -577,7 +591,7 @@ dms_status d0_issue(dms_ctx* c) {
     {
         StageTimer t8(c, 8);
         uf_keys_ages(c, u, 1, m, 0, n0, 0);
-        s = uf_issue(c, u, m, n0);
+        s = uf_issue(c, u, m, n0, 1, 0);
         if (s) return s;
     }
     return DMS_OK;
@@ -682,7 +696,7 @@ dms_status dtop_issue(dms_ctx* c) {
     {
         StageTimer t9(c, 9);
         uf_keys_ages(c, u, d - 1, m, d, nd, 1);
-        s = uf_issue(c, u, m, nd + 1);
+        s = uf_issue(c, u, m, nd + 1, d - 1, 1);
         if (s) return s;
     }
     return DMS_OK;
@@ -1160,7 +1174,7 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->node_oftop);
     for (int b = 0; b < 2; b++) {
         UFBuf& u = c->uf[b];
-        for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.rec0, (void*)u.rec1, (void*)u.out, (void*)u.list,
+        for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.rec0, (void*)u.rec1, (void*)u.rsrc, (void*)u.out, (void*)u.list,
                         (void*)u.live2, (void*)u.nlive, (void*)u.trace, (void*)u.outp, (void*)u.key,
                         (void*)u.inv_a, (void*)u.age, (void*)u.inv_n,
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})

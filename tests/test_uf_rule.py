@@ -29,11 +29,14 @@ def sequential(n, arcs, older_is_smaller=True):
     return out
 
 
-def rounds(n, arcs, older_is_smaller=True, max_rounds=100000):
+def rounds(n, arcs, older_is_smaller=True, max_rounds=100000, batch=0):
+    """batch > 0: the arcs (listed in processing order) are revealed in key-ordered
+    batches whenever at most batch // 4 are live (diag.cuh UFArgs::batch)."""
     m = len(arcs)
     parent = list(range(n))
     out = [-2] * m
-    live = list(range(m))
+    live = [] if batch else list(range(m))
+    rv = 0 if batch else m
 
     def find(a):
         while parent[a] != a:
@@ -41,8 +44,12 @@ def rounds(n, arcs, older_is_smaller=True, max_rounds=100000):
         return a
 
     nrounds = 0
-    while live and nrounds < max_rounds:
+    while (live or rv < m) and nrounds < max_rounds:
         nrounds += 1
+        if rv < m and len(live) <= batch // 4:
+            add = min(batch, m - rv)
+            live = live + list(range(rv, rv + add))
+            rv += add
         best = {}
         ra, rb = {}, {}
         for i in live:
@@ -129,3 +136,24 @@ def test_round_counts_are_small():
     _, r1 = rounds(3000, path_graph(rng, 3000))
     _, r2 = rounds(3000, giant_basin(rng, 3000))
     assert r1 < 200 and r2 < 60, (r1, r2)
+
+
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("batch", [1, 4, 9, 64])
+def test_batched_rounds_equal_sequential(seed, batch):
+    """Revealing the arcs in key-ordered batches (dense graphs, diag.cuh) keeps every
+    decision of the sequential elder-rule union-find."""
+    rng = np.random.default_rng(1000 + seed)
+    kind = seed % 3
+    if kind == 0:
+        n = int(rng.integers(2, 80))
+        arcs = random_graph(rng, n, int(rng.integers(1, 5 * n)))
+    elif kind == 1:
+        n = int(rng.integers(3, 200))
+        arcs = path_graph(rng, n)
+    else:
+        n = int(rng.integers(2, 200))
+        arcs = giant_basin(rng, n)
+    older = bool(seed % 2)
+    got, _ = rounds(n, arcs, older, batch=batch)
+    assert got == sequential(n, arcs, older)
