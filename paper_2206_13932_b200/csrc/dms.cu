@@ -110,6 +110,9 @@ struct dms_ctx {
     int64_t status_words = 0;
     int* tile_ctr = nullptr;
     uint32_t* chase_mark = nullptr;  // D_{d-1} chase stamps, one per top cell
+    uint32_t* lut2 = nullptr;        // 2D: ProcessLowerStars result per star pattern
+    int sms = 148;                   // multiprocessors of the context's device
+    Lut2Off lut2off;
     uint32_t chase_gen = 0;
     unsigned long long* totals = nullptr;
     int* err = nullptr;
@@ -370,7 +373,11 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     if (c->ndim >= 2) {
         // one CTA per 128 vertices; the CTA regroups its vertices by expansion work
         const unsigned g2 = (unsigned)ceil_div(v1 - v0, kBlockG);
+        static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
         if (c->ndim == 3) k_gradient_rg<3><<<g2, kBlockG, 0, c->st>>>(A);
+        else if (c->lut2 && lut_env)
+            k_gradient_lut2<<<(unsigned)std::min<int64_t>(ceil_div(v1 - v0, kBlock), c->sms * 8), kBlock, 0, c->st>>>(
+                A, c->lut2, c->lut2off);
         else k_gradient_rg<2><<<g2, kBlockG, 0, c->st>>>(A);
     } else {
         k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
@@ -864,6 +871,22 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
     CA(dalloc(&c->node_oftop, c->ncell[ndim] * N));
     for (int k = 0; k <= ndim; k++) c->cap[k] = N / 2 + 1024;
     if (alloc_crit(c) != DMS_OK) return bail(DMS_ERR_OOM);
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (ndim == 2) {  // 2D: the ProcessLowerStars table of all 1957 star patterns
+        int acc = 0;
+        for (int L = 0; L < 64; L++) {
+            c->lut2off.off[L] = (uint16_t)acc;
+            acc += fact_small(__builtin_popcount(L));
+        }
+        if (acc != kLut2) return bail(DMS_ERR_INVARIANT);
+        CA(dalloc(&c->lut2, kLut2));
+        k_build_lut2<<<(unsigned)ceil_div(kLut2, kBlockG), kBlockG, 0, c->st>>>(c->dtab, c->lut2off, c->lut2);
+        if (cudaGetLastError() != cudaSuccess) return bail(DMS_ERR_CUDA);
+    }
     if (cudaMemsetAsync(c->err, 0, sizeof(int), c->st) != cudaSuccess) return bail(DMS_ERR_CUDA);
 #undef CA
     *out = c;
@@ -1165,6 +1188,7 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->status);
     cudaFree(c->tile_ctr);
     cudaFree(c->chase_mark);
+    cudaFree(c->lut2);
     cudaFree(c->totals);
     cudaFree(c->err);
     cudaFree(c->kmax);

@@ -547,6 +547,247 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
     }
 }
 
+// ---- 2D by table lookup.  A 2D lower star is determined by its lower mask Le (6 bits)
+// and the order of its <= 6 lower neighbours, i.e. one of sum_k C(6,k) k! = 1957
+// patterns; ProcessLowerStars's result (gradient word + critical edges / triangles)
+// depends only on that pattern.  k_build_lut2 runs the same process_star<2> on every
+// pattern once per context; the per-vertex kernel then only ranks its neighbours and
+// looks the result up.  Pattern index: lut2_off[Le] + Lehmer code of the ranks of the
+// lower slots taken in slot order (c_i = later lower slots ranked below slot i).
+constexpr int kLut2 = 1957;
+struct Lut2Off {
+    uint16_t off[64];
+};
+__host__ __device__ inline int fact_small(int k) {
+    int f = 1;
+    for (int i = 2; i <= k; i++) f *= i;
+    return f;
+}
+// entry: bits 0-14 gradient word, 16-21 critical edge slots, 22-27 critical tri slots
+__global__ void __launch_bounds__(kBlockG) k_build_lut2(const StarTab* __restrict__ tab, Lut2Off offs,
+                                                          uint32_t* __restrict__ lut) {
+    __shared__ StarTab S;
+    __shared__ uint8_t s_tki[Geo<2>::NT * kBlockG];
+    __shared__ uint16_t s_qk[kBlockG];
+    {
+        const int4* src = reinterpret_cast<const int4*>(tab);
+        int4* dst = reinterpret_cast<int4*>(&S);
+        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlockG) dst[i] = src[i];
+    }
+    __syncthreads();
+    const int tid = threadIdx.x;
+    const int pidx = blockIdx.x * kBlockG + tid;
+    if (pidx >= kLut2) return;
+    int Le = 0;
+    while (Le < 63 && offs.off[Le + 1] <= pidx) Le++;
+    const int k = __popc(Le);
+    int q = pidx - offs.off[Le];
+    // decode the Lehmer code into the ranks of the lower slots (in slot order)
+    int avail = (1 << k) - 1, rk_of[6];
+    for (int i = 0; i < k; i++) {
+        const int f = fact_small(k - 1 - i);
+        int c = q / f;
+        q -= c * f;
+        int r = 0;  // the c-th smallest rank still available
+        for (int t = avail; ; t &= t - 1) {
+            const int b = __ffs(t) - 1;
+            if (c-- == 0) { r = b; break; }
+        }
+        avail &= ~(1 << r);
+        rk_of[i] = r;
+    }
+    uint64_t R = 0, IV = 0;
+    int delta = 0;
+    for (int s = 0, i = 0; s < 6; s++)
+        if ((Le >> s) & 1) {
+            R |= (uint64_t)rk_of[i] << (4 * s);
+            IV |= (uint64_t)s << (4 * rk_of[i]);
+            if (rk_of[i] == 0) delta = s;
+            i++;
+        }
+    uint64_t ta = 0, tb = 0;
+    for (int s = 0; s < 6; s++)
+        if ((Le >> s) & 1) { ta |= S.tri_amask[s]; tb |= S.tri_bmask[s]; }
+    StarState st;
+    st.Le = (uint32_t)Le;
+    st.Lt = ta & tb;
+    st.Lq = 0;
+    st.cls_e = st.crit_e = st.pq0_er = 0;
+    st.cls_t = st.crit_t = 0;
+    st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
+    st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
+    st.tcode_lo = st.tcode_hi = st.qcode = 0;
+    st.vcode = -1;
+    uint32_t word;
+    if (Le) {
+        for (uint64_t m = st.Lt; m; m &= m - 1) {
+            const int tt = __ffsll((long long)m) - 1;
+            s_tki[tt * kBlockG + tid] = (uint8_t)tri_kidx(S, R, tt);
+        }
+        KeyCache C;
+        C.tki = s_tki + tid;
+        C.qk = s_qk + tid;
+        C.IV = IV;
+        C.S = &S;
+        C.R = R;
+        process_star<2, false>(S, C, R, IV, k, delta, st);
+        word = (uint32_t)st.vcode | ((uint32_t)st.tcode_lo << 3);
+    } else {
+        word = 7u;  // a minimum
+    }
+    lut[pidx] = word | (st.crit_e << 16) | ((uint32_t)st.crit_t << 22);
+}
+
+constexpr uint32_t kLutCap = 512;  // records per dimension buffered per CTA (>= 2 x 256: one iteration adds <= 256 x 2)
+// write a CTA's buffered records of dimension k and empty the buffer (all threads call)
+__device__ __forceinline__ void lut_flush(const GradArgs& A, int k, const int64_t* ids, const uint64_t* keys,
+                                          uint32_t* s_n, unsigned long long* s_base) {
+    __syncthreads();
+    const uint32_t n = s_n[k];
+    if (threadIdx.x == 0) *s_base = atomicAdd(&A.totals[k], (unsigned long long)n);
+    __syncthreads();
+    const int64_t base = (int64_t)*s_base;
+    for (uint32_t j = threadIdx.x; j < n; j += kBlock)
+        if (base + j < A.cap[k]) {
+            A.crit_id[k][base + j] = ids[j];
+            A.crit_key[k][base + j] = keys[j];
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) s_n[k] = 0;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBlock) k_gradient_lut2(GradArgs A, const uint32_t* __restrict__ lut,
+                                                           Lut2Off offs) {
+    // persistent grid: the 7.8 KB table is staged into shared memory once per CTA; the
+    // critical records collect in per-CTA shared buffers and leave with one counter
+    // atomic per flush (a per-warp atomic on the three record counters serialised: 88 %
+    // of the stall samples)
+    __shared__ uint32_t s_lut[kLut2];
+    __shared__ uint16_t s_off[64];
+    __shared__ int64_t s_id[3][kLutCap];
+    __shared__ uint64_t s_key[3][kLutCap];
+    __shared__ uint32_t s_n[3];
+    __shared__ uint32_t s_sw[kBlock / 32 + 1];
+    __shared__ unsigned long long s_base;
+    for (int i = threadIdx.x; i < kLut2; i += kBlock) s_lut[i] = lut[i];
+    if (threadIdx.x < 64) s_off[threadIdx.x] = offs.off[threadIdx.x];
+    if (threadIdx.x < 3) s_n[threadIdx.x] = 0;
+    __syncthreads();
+    const StarTab& S = *A.tab;  // (anchors of critical cells only)
+    const int Lx = A.Lx;
+    for (int64_t base = A.v0 + (int64_t)blockIdx.x * kBlock; base < A.v1; base += (int64_t)gridDim.x * kBlock) {
+        const int64_t v = base + threadIdx.x;
+        const bool active = v < A.v1;
+        uint32_t e = 0, Le = 0;
+        uint64_t R = 0;
+        if (active) {
+            const int vv = (int)v;
+            const int cx = vv % Lx, cy = vv / Lx;
+            const float fx = A.f[v];
+            if (is_nan_bits(fx)) atomicOr(A.err, 1);
+            const uint32_t ox = ord_of(fx);
+            uint32_t o[6];
+#pragma unroll
+            for (int s = 0; s < 6; s++) {
+                const int dx = kOff2[s][0], dy = kOff2[s][1];
+                bool in = true;
+                if (dx < 0) in &= cx > 0;
+                if (dx > 0) in &= cx < Lx - 1;
+                if (dy < 0) in &= cy > 0;
+                if (dy > 0) in &= cy < A.Ly - 1;
+                o[s] = 0xffffffffu;
+                if (in) {
+                    const uint32_t os = ord_of(__ldg(A.f + v + dx + Lx * dy));
+                    if ((os < ox) || (os == ox && s < 3)) { o[s] = os; Le |= 1u << s; }
+                }
+            }
+            int r[6], later[6];
+#pragma unroll
+            for (int s = 0; s < 6; s++) r[s] = later[s] = 0;
+#pragma unroll
+            for (int s = 0; s < 6; s++)
+#pragma unroll
+                for (int u = s + 1; u < 6; u++) {
+                    const bool s_lt_u = o[s] <= o[u];  // equal values: the smaller slot first
+                    r[u] += s_lt_u ? 1 : 0;
+                    r[s] += s_lt_u ? 0 : 1;
+                    later[s] += s_lt_u ? 0 : 1;
+                }
+            const int k = __popc(Le);
+            int idx = s_off[Le], pos = 0;
+            constexpr uint64_t kFact = 0x781806020101ull;  // 0! .. 5! in bytes (no local-memory table)
+#pragma unroll
+            for (int s = 0; s < 6; s++)
+                if ((Le >> s) & 1u) {
+                    R |= (uint64_t)r[s] << (4 * s);
+                    idx += later[s] * (int)((kFact >> (8 * (k - 1 - pos))) & 0xffull);
+                    pos++;
+                }
+            e = s_lut[idx];
+            reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(e & 0x7fffu);
+        }
+        const bool crit_v = active && Le == 0;
+        const uint32_t crit_e = (e >> 16) & 63u, crit_t = (e >> 22) & 63u;
+        // one block scan of the three counts packed in 10/11/11-bit fields (sums <= 256,
+        // <= 6 x 256, <= 6 x 256 per iteration)
+        const uint32_t packed = (crit_v ? 1u : 0u) | ((uint32_t)__popc(crit_e) << 10) | ((uint32_t)__popc(crit_t) << 21);
+        uint32_t ptot;
+        const uint32_t pex = block_excl_sum<kBlock / 32>(packed, s_sw, &ptot);
+        if (ptot == 0) continue;
+        const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_rg
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const int sh = k == 0 ? 0 : (k == 1 ? 10 : 21);
+            const uint32_t msk = k == 0 ? 1023u : 2047u;
+            const uint32_t tot = (ptot >> sh) & msk, ex = (pex >> sh) & msk;
+            if (tot == 0) continue;
+            if (s_n[k] + tot > kLutCap) lut_flush(A, k, s_id[k], s_key[k], s_n, &s_base);
+            // (more than a buffer in one iteration cannot happen on 2D stars -- <= 2
+            // critical edges and <= 1 critical triangle each -- but is handled: straight
+            // to global memory)
+            const bool direct = tot > kLutCap;
+            if (direct) {
+                if (threadIdx.x == 0) s_base = atomicAdd(&A.totals[k], (unsigned long long)tot);
+                __syncthreads();
+            }
+            int64_t at = direct ? (int64_t)s_base + ex : (int64_t)(s_n[k] + ex);
+            int64_t* ids = direct ? A.crit_id[k] : s_id[k];
+            uint64_t* keys = direct ? A.crit_key[k] : s_key[k];
+            const int64_t lim = direct ? A.cap[k] : (int64_t)kLutCap;
+            if (k == 0 && crit_v && at < lim) { ids[at] = v; keys[at] = rkey; }
+            if (k == 1)
+                for (uint32_t m = crit_e; m; m &= m - 1, at++) {
+                    const int sl = __ffs(m) - 1;
+                    const int64_t anc = v + S.e_anc[sl][0] + Lx * S.e_anc[sl][1];
+                    if (at < lim) {
+                        ids[at] = A.ncell[1] * anc + S.e_k[sl];
+                        keys[at] = rkey | key_edge(R, sl);
+                    }
+                }
+            if (k == 2)
+                for (uint32_t m = crit_t; m; m &= m - 1, at++) {
+                    const int t = __ffs(m) - 1;
+                    const int64_t anc = v + S.t_anc[t][0] + Lx * S.t_anc[t][1];
+                    if (at < lim) {
+                        ids[at] = A.ncell[2] * anc + S.t_k[t];
+                        keys[at] = rkey | key_tri(S, R, t);
+                    }
+                }
+            if (direct) __syncthreads();  // s_base is reused
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            const int sh = threadIdx.x == 0 ? 0 : (threadIdx.x == 1 ? 10 : 21);
+            const uint32_t tot = (ptot >> sh) & (threadIdx.x == 0 ? 1023u : 2047u);
+            if (tot <= kLutCap) s_n[threadIdx.x] += tot;
+        }
+        __syncthreads();
+    }
+    for (int k = 0; k < 3; k++)
+        if (s_n[k]) lut_flush(A, k, s_id[k], s_key[k], s_n, &s_base);
+}
+
 // 1D: the lower star of x holds at most two edges; ProcessLowerStars reduces to:
 // no lower neighbour -> minimum; otherwise pair x with the edge to the lower (in K)
 // lower neighbour; a second lower edge is critical (SURVEY App. B closed form, which
