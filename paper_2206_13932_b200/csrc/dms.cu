@@ -371,10 +371,12 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     A.err = c->err;
     StageTimer tm(c, 5);
     if (c->ndim >= 2) {
-        // one CTA per 128 vertices; the CTA regroups its vertices by expansion work
+        // (2D fallback without the table: one CTA per 128 vertices, regrouped by work)
         const unsigned g2 = (unsigned)ceil_div(v1 - v0, kBlockG);
         static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
-        if (c->ndim == 3) k_gradient_rg<3><<<g2, kBlockG, 0, c->st>>>(A);
+        // 3D: pools of 8 x 128 vertices per CTA, expanded in work order
+        if (c->ndim == 3)
+            k_gradient_pool<3, 8><<<(unsigned)ceil_div(v1 - v0, 8 * kBlockG), kBlockG, 0, c->st>>>(A);
         else if (c->lut2 && lut_env)
             k_gradient_lut2<<<(unsigned)std::min<int64_t>(ceil_div(v1 - v0, kBlock), c->sms * 8), kBlock, 0, c->st>>>(
                 A, c->lut2, c->lut2off);

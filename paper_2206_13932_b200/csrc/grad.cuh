@@ -547,6 +547,234 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
     }
 }
 
+// ---- pooled variant: a CTA of 128 threads takes P x 128 consecutive vertices; phase A
+// ranks the neighbours of all of them (compact state: local ranks + lower mask), the
+// pool is counting-sorted by the work estimate |Lt| + |Lq|, and phase C expands the
+// stars in P rounds of 128 in sorted order (warps of near-equal work).  The key caches
+// are rebuilt per expanded star in the thread's own shared-memory column.
+template <int D, int P, int MINB = 1>
+__global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
+    constexpr int NE = Geo<D>::NE;
+    constexpr int POOL = P * kBlockG;
+    __shared__ StarTab S;
+    __shared__ uint8_t s_tki[kMaxNT * kBlockG];
+    __shared__ uint16_t s_qk[(D == 3 ? kMaxNQ : 1) * kBlockG];
+    __shared__ uint64_t s_R[POOL];
+    __shared__ uint32_t s_W[POOL];
+    __shared__ uint8_t s_w[POOL];
+    __shared__ uint16_t s_perm[POOL];
+    __shared__ int s_hist[64];
+    {
+        const int4* src = reinterpret_cast<const int4*>(A.tab);
+        int4* dst = reinterpret_cast<int4*>(&S);
+        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlockG) dst[i] = src[i];
+    }
+    if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+    __syncthreads();
+    const int LxLy = A.Lx * A.Ly;
+    const int tid = threadIdx.x;
+    const int64_t pool0 = A.v0 + (int64_t)blockIdx.x * POOL;
+    // ---- phase A
+#pragma unroll 1
+    for (int k = 0; k < P; k++) {
+        const int slot = k * kBlockG + tid;
+        const int64_t v = pool0 + slot;
+        uint32_t Le = 0, word = 0;
+        uint64_t R = 0;
+        int w = 0;
+        if (v < A.v1) {
+            const int vv = (int)v;
+            const int cx = vv % A.Lx;
+            const int t = vv / A.Lx;
+            const int cy = t % A.Ly;
+            const int cz = t / A.Ly;
+            const float fx = A.f[v];
+            if (is_nan_bits(fx)) atomicOr(A.err, 1);
+            const uint32_t ox = ord_of(fx);
+            uint32_t o[NE];
+#pragma unroll
+            for (int s = 0; s < NE; s++) {
+                const int dx = off_c<D>(s, 0), dy = off_c<D>(s, 1), dz = off_c<D>(s, 2);
+                bool in = true;
+                if (dx < 0) in &= cx > 0;
+                if (dx > 0) in &= cx < A.Lx - 1;
+                if (dy < 0) in &= cy > 0;
+                if (dy > 0) in &= cy < A.Ly - 1;
+                if (dz < 0) in &= cz > 0;
+                if (dz > 0) in &= cz < A.Lz - 1;
+                o[s] = 0xffffffffu;
+                if (in) {
+                    const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
+                    const bool lower = (os < ox) || (os == ox && s < NE / 2);
+                    if (lower) { o[s] = os; Le |= 1u << s; }
+                }
+            }
+            int delta = 0;
+            if (Le) {
+                int r[NE];
+#pragma unroll
+                for (int s = 0; s < NE; s++) r[s] = 0;
+#pragma unroll
+                for (int s = 0; s < NE; s++)
+#pragma unroll
+                    for (int u = s + 1; u < NE; u++) {
+                        const bool s_lt_u = o[s] <= o[u];  // equal values: the smaller slot first
+                        r[u] += s_lt_u ? 1 : 0;
+                        r[s] += s_lt_u ? 0 : 1;
+                    }
+#pragma unroll
+                for (int s = 0; s < NE; s++) {
+                    if ((Le >> s) & 1u) {
+                        R |= (uint64_t)r[s] << (4 * s);
+                        if (r[s] == 0) delta = s;
+                    }
+                }
+                uint64_t ta = 0, tb = 0;
+                uint32_t qa = 0, qb = 0, qc = 0;
+                for (uint32_t le = Le; le; le &= le - 1) {
+                    const int s = __ffs(le) - 1;
+                    ta |= S.tri_amask[s];
+                    tb |= S.tri_bmask[s];
+                    if (D == 3) {
+                        qa |= S.tet_amask[s];
+                        qb |= S.tet_bmask[s];
+                        qc |= S.tet_cmask[s];
+                    }
+                }
+                w = min(63, __popcll(ta & tb) + __popc(qa & qb & qc) + 1);
+            }
+            word = Le | ((uint32_t)delta << 16) | (1u << 24);  // bit 24: active
+        }
+        s_R[slot] = R;
+        s_W[slot] = word;
+        s_w[slot] = (uint8_t)w;
+        atomicAdd(&s_hist[w], 1);
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 64-bin work histogram
+        const int a0 = s_hist[2 * tid], a1 = s_hist[2 * tid + 1];
+        int inc = a0 + a1;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o2);
+            if (tid >= o2) inc += y;
+        }
+        const int ex = inc - a0 - a1;
+        s_hist[2 * tid] = ex;
+        s_hist[2 * tid + 1] = ex + a0;
+    }
+    __syncthreads();
+    for (int k = 0; k < P; k++) {
+        const int slot = k * kBlockG + tid;
+        s_perm[atomicAdd(&s_hist[s_w[slot]], 1)] = (uint16_t)slot;
+    }
+    __syncthreads();
+    // ---- phase C: P rounds of 128 stars in work order
+#pragma unroll 1
+    for (int round = 0; round < P; round++) {
+        const int p = s_perm[round * kBlockG + tid];
+        const int64_t v = pool0 + p;
+        const uint32_t word = s_W[p];
+        const bool active = (word >> 24) & 1u;
+        const uint64_t R = s_R[p];
+        StarState st;
+        st.Le = word & 0xffffu;
+        st.cls_e = st.crit_e = st.pq0_er = 0;
+        st.cls_t = st.crit_t = 0;
+        st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
+        st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
+        st.tcode_lo = st.tcode_hi = st.qcode = 0;
+        st.vcode = -1;
+        st.Lt = 0;
+        st.Lq = 0;
+        uint64_t IV = 0;
+        const bool crit_v = active && st.Le == 0;
+        if (active && st.Le) {
+            uint64_t ta = 0, tb = 0;
+            uint32_t qa = 0, qb = 0, qc = 0;
+            for (uint32_t le = st.Le; le; le &= le - 1) {
+                const int s = __ffs(le) - 1;
+                IV |= (uint64_t)s << (4 * rk(R, s));
+                ta |= S.tri_amask[s];
+                tb |= S.tri_bmask[s];
+                if (D == 3) {
+                    qa |= S.tet_amask[s];
+                    qb |= S.tet_bmask[s];
+                    qc |= S.tet_cmask[s];
+                }
+            }
+            st.Lt = ta & tb;
+            st.Lq = qa & qb & qc;
+            for (uint64_t m = st.Lt; m; m &= m - 1) {
+                const int tt = __ffsll((long long)m) - 1;
+                s_tki[tt * kBlockG + tid] = (uint8_t)tri_kidx(S, R, tt);
+            }
+            if (D == 3)
+                for (uint32_t mq = st.Lq; mq; mq &= mq - 1) {
+                    const int q = __ffs(mq) - 1;
+                    s_qk[q * kBlockG + tid] = (uint16_t)cmp_tet(S, R, q);
+                }
+            KeyCache C;
+            C.tki = s_tki + tid;
+            C.qk = s_qk + tid;
+            C.IV = IV;
+            C.S = &S;
+            C.R = R;
+            process_star<D, D == 3>(S, C, R, IV, __popc(st.Le), (int)((word >> 16) & 15u), st);
+        }
+        if (active) {
+            if (D == 3) {
+                const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
+                const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
+                reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
+            } else {
+                const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
+                reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
+            }
+        }
+        const uint32_t c0 = crit_v ? 1u : 0u, c1 = __popc(st.crit_e), c2 = __popcll(st.crit_t), c3 = __popc(st.crit_q);
+        if (!__any_sync(0xffffffffu, (c0 | c1 | c2 | c3) != 0u)) continue;
+        const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_rg
+        {
+            const int64_t q0 = warp_append(&A.totals[0], c0);
+            if (c0 && q0 < A.cap[0]) { A.crit_id[0][q0] = v; A.crit_key[0][q0] = rkey; }
+        }
+        {
+            int64_t q1 = warp_append(&A.totals[1], c1);
+            for (uint32_t m = st.crit_e; m; m &= m - 1, q1++) {
+                const int s = __ffs(m) - 1;
+                if (q1 < A.cap[1]) {
+                    const int64_t anc = v + S.e_anc[s][0] + A.Lx * S.e_anc[s][1] + LxLy * S.e_anc[s][2];
+                    A.crit_id[1][q1] = A.ncell[1] * anc + S.e_k[s];
+                    A.crit_key[1][q1] = rkey | key_edge(R, s);
+                }
+            }
+        }
+        {
+            int64_t q2 = warp_append(&A.totals[2], c2);
+            for (uint64_t m = st.crit_t; m; m &= m - 1, q2++) {
+                const int t = __ffsll((long long)m) - 1;
+                if (q2 < A.cap[2]) {
+                    const int64_t anc = v + S.t_anc[t][0] + A.Lx * S.t_anc[t][1] + LxLy * S.t_anc[t][2];
+                    A.crit_id[2][q2] = A.ncell[2] * anc + S.t_k[t];
+                    A.crit_key[2][q2] = rkey | key_tri(S, R, t);
+                }
+            }
+        }
+        if (D == 3) {
+            int64_t q3 = warp_append(&A.totals[3], c3);
+            for (uint32_t m = st.crit_q; m; m &= m - 1, q3++) {
+                const int q = __ffs(m) - 1;
+                if (q3 < A.cap[3]) {
+                    const int64_t anc = v + S.q_anc[q][0] + A.Lx * S.q_anc[q][1] + LxLy * S.q_anc[q][2];
+                    A.crit_id[3][q3] = A.ncell[3] * anc + S.q_k[q];
+                    A.crit_key[3][q3] = rkey | key_tet(S, R, q);
+                }
+            }
+        }
+    }
+}
+
 // ---- 2D by table lookup.  A 2D lower star is determined by its lower mask Le (6 bits)
 // and the order of its <= 6 lower neighbours, i.e. one of sum_k C(6,k) k! = 1957
 // patterns; ProcessLowerStars's result (gradient word + critical edges / triangles)
