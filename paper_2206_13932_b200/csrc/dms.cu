@@ -477,7 +477,10 @@ dms_status uf_issue(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, int karcs, i
     U.trace = u.trace;
     U.key = u.key;
     U.age = u.age;
-    U.max_rounds = 4096;
+    // DMS_UF_MAX_ROUNDS (tests only): cap the parallel rounds to exercise the sequential
+    // fallback tail that a pathological input would take
+    static const int rounds_env = getenv("DMS_UF_MAX_ROUNDS") ? atoi(getenv("DMS_UF_MAX_ROUNDS")) : 4096;
+    U.max_rounds = std::max(1, rounds_env);
     // same-address contention on best[] comes with arc-dense graphs (3D: ~4 arcs per node,
     // the big components collect most arcs): pre-reduce per warp there (measured)
     static const int agg_env = getenv("DMS_AGG") ? atoi(getenv("DMS_AGG")) : -1;

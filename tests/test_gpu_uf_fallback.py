@@ -1,0 +1,42 @@
+"""GPU: the union-find's sequential fallback (taken when the parallel rounds do not
+converge within max_rounds) gives the same bit-exact diagrams as the oracle.  The round
+cap is forced through DMS_UF_MAX_ROUNDS in a subprocess (the library reads it once)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, paper_2206_13932_b200 as dms
+from synth import fields
+for name, shape in [("c1", (20, 24, 28)), ("c4", (40, 40, 40)), ("c5a", (200, 190)), ("c5b", (30001,))]:
+    f = np.ascontiguousarray(fields.make(name, seed=5, shape=shape))
+    ref = oracle.run(f)
+    d = dms.DMS(torch.from_numpy(f).cuda())
+    d.run_all()
+    assert d.diagram0().tobytes() == ref.d0.tobytes(), (name, "D0")
+    assert d.diagram_top().tobytes() == ref.dtop.tobytes(), (name, "Dtop")
+    assert np.array_equal(d.unpaired_saddles(0), ref.unpaired0), (name, "un0")
+    assert np.array_equal(d.unpaired_saddles(1), ref.unpaired_top), (name, "untop")
+    d.close()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("rounds", ["1", "3"])
+def test_union_find_fallback_tail(rounds):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, DMS_UF_MAX_ROUNDS=rounds)
+    r = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
