@@ -874,7 +874,10 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
     if (cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     CA(dalloc(&c->node_of0, N));
     CA(dalloc(&c->node_oftop, c->ncell[ndim] * N));
-    for (int k = 0; k <= ndim; k++) c->cap[k] = N / 2 + 1024;
+    // DMS_CRIT_CAP (tests only): a small initial record capacity exercises the overflow
+    // path (grow the buffers, recompute the gradient)
+    static const int64_t cap_env = getenv("DMS_CRIT_CAP") ? atoll(getenv("DMS_CRIT_CAP")) : -1;
+    for (int k = 0; k <= ndim; k++) c->cap[k] = cap_env >= 0 ? cap_env : N / 2 + 1024;
     if (alloc_crit(c) != DMS_OK) return bail(DMS_ERR_OOM);
     {
         int dev = 0;

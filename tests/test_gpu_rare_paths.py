@@ -1,6 +1,8 @@
-"""GPU: the union-find's sequential fallback (taken when the parallel rounds do not
-converge within max_rounds) gives the same bit-exact diagrams as the oracle.  The round
-cap is forced through DMS_UF_MAX_ROUNDS in a subprocess (the library reads it once)."""
+"""GPU: rarely taken paths stay bit-exact against the oracle -- the union-find's
+sequential fallback (taken when the parallel rounds do not converge within max_rounds)
+and the critical-record overflow path (buffers grown, gradient recomputed).  They are
+forced through DMS_UF_MAX_ROUNDS / DMS_CRIT_CAP in a subprocess (the library reads them
+once)."""
 from __future__ import annotations
 
 import os
@@ -27,6 +29,8 @@ for name, shape in [("c1", (20, 24, 28)), ("c4", (40, 40, 40)), ("c5a", (200, 19
     assert d.diagram_top().tobytes() == ref.dtop.tobytes(), (name, "Dtop")
     assert np.array_equal(d.unpaired_saddles(0), ref.unpaired0), (name, "un0")
     assert np.array_equal(d.unpaired_saddles(1), ref.unpaired_top), (name, "untop")
+    for k in range(f.ndim + 1):
+        assert np.array_equal(d.critical()[k].cpu().numpy(), ref.crit[k]), (name, "C", k)
     d.close()
 print("ok")
 """
@@ -38,5 +42,14 @@ def test_union_find_fallback_tail(rounds):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     env = dict(os.environ, DMS_UF_MAX_ROUNDS=rounds)
+    r = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_critical_record_overflow():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, DMS_CRIT_CAP="7")
     r = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
