@@ -178,3 +178,18 @@ def test_run_all_host_matches_device_input(env, name, shape):
         assert np.array_equal(d.unpaired_saddles(0), ref["un0"])
         assert np.array_equal(d.unpaired_saddles(1), ref["untop"])
     d.close()
+
+
+def test_chase_stamps_wrap_around(env):
+    """The memoised D_{d-1} chases stamp cells with an 8-bit generation that wraps every
+    255 runs (the stamps are then cleared): 260 runs of one context stay exact."""
+    torch, dms = env
+    for name, shape in [("c4", (24, 20, 18)), ("c5a", (60, 50))]:
+        f = np.ascontiguousarray(fields.make(name, seed=11, shape=shape))
+        ref = oracle.run(f)
+        d = dms.DMS(torch.from_numpy(f).cuda())
+        for i in range(260):
+            d.run_all()
+            if i in (0, 254, 255, 259):
+                assert d.diagram_top().tobytes() == ref.dtop.tobytes(), (name, i)
+        d.close()
