@@ -307,7 +307,10 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank) {
     CU(cudaMemsetAsync(c->kmax, 0, sizeof(unsigned long long), c->st));
     // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
     // (and detects NaN / the highest vertex), the last pass writes rank[index]
-    radix_sort<uint32_t, uint32_t, 12>(c->okeys[0], c->ovals[0], c->okeys[1], c->ovals[1], c->N, 0, 32, c->ss, c->st,
+#ifndef DMS_ORDER_ITEMS
+#define DMS_ORDER_ITEMS 12
+#endif
+    radix_sort<uint32_t, uint32_t, DMS_ORDER_ITEMS>(c->okeys[0], c->ovals[0], c->okeys[1], c->ovals[1], c->N, 0, 32, c->ss, c->st,
                                        &c->launches, c->rank, c->f, c->err, c->kmax);
     CU(cudaGetLastError());
     c->have_order = true;
@@ -984,7 +987,8 @@ dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, in
 dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     dms_status s = check_sticky(c);
     if (s) return s;
-    if ((s = run_order(c, d_rank, true))) return s;  // second stream, overlaps the gradient
+    static const int oseq_env = getenv("DMS_ORDER_SEQ") ? atoi(getenv("DMS_ORDER_SEQ")) : 0;
+    if ((s = run_order(c, d_rank, !oseq_env))) return s;  // second stream, overlaps the gradient
     if ((s = run_gradient(c, d_grad))) return s;
     if ((s = run_critical(c))) return s;
     if ((s = run_diagrams(c))) return s;
