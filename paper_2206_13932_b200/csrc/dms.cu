@@ -439,8 +439,12 @@ dms_status run_critical(dms_ctx* c) {
         k_rekey<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->ckey[0][k], c->ncrit[k], c->rank);
         k_iota<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cidx[0][k], c->ncrit[k]);
         c->launches++;
+        // the low 12 bits (G) only order cells of one star: C_0 holds at most one cell per
+        // star (x itself), and in 1D so does C_1 (the second lower edge), so their keys
+        // sort on the rank bits alone (one 8-bit pass fewer)
+        const int bit0 = (k == 0 || c->ndim == 1) ? 12 : 0;
         c->cur[k] = radix_sort<uint64_t, uint32_t, 8>(c->ckey[0][k], c->cidx[0][k], c->ckey[1][k], c->cidx[1][k],
-                                                     c->ncrit[k], 0, kbits, c->ss, c->st, &c->launches);
+                                                     c->ncrit[k], bit0, kbits, c->ss, c->st, &c->launches);
         // lexicographically sorted ids = emitted ids gathered through the permutation
         k_gather_ids<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cid[0][k], crit_perm(c, k), c->ncrit[k],
                                                                  c->cid[1][k]);
