@@ -441,8 +441,9 @@ dms_status run_critical(dms_ctx* c) {
         c->launches++;
         // the low 12 bits (G) only order cells of one star: C_0 holds at most one cell per
         // star (x itself), and in 1D so does C_1 (the second lower edge), so their keys
-        // sort on the rank bits alone (one 8-bit pass fewer)
-        const int bit0 = (k == 0 || c->ndim == 1) ? 12 : 0;
+        // sort on the rank bits alone; edge keys have G's low 8 bits zero, triangle keys
+        // its low 4 (key_edge / key_tri) -- fewer 8-bit passes
+        const int bit0 = (k == 0 || c->ndim == 1) ? 12 : (k == 1 ? 8 : (k == 2 ? 4 : 0));
         c->cur[k] = radix_sort<uint64_t, uint32_t, 8>(c->ckey[0][k], c->cidx[0][k], c->ckey[1][k], c->cidx[1][k],
                                                      c->ncrit[k], bit0, kbits, c->ss, c->st, &c->launches);
         // lexicographically sorted ids = emitted ids gathered through the permutation
