@@ -675,7 +675,7 @@ dms_status dtop_issue(dms_ctx* c) {
             if (d == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<3, true>, kBlock, 0);
             else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dtop_arcs_q<2, true>, kBlock, 0);
             const unsigned grid = (unsigned)std::max<int64_t>(
-                1, std::min<int64_t>(grid_for(2 * m), (int64_t)sms * std::max(per, 1) / (c->half ? 2 : 1)));
+                1, std::min<int64_t>(grid_for(2 * m), (int64_t)sms * std::max(per, 1)));
             CU(cudaMemsetAsync(c->tile_ctr, 0, sizeof(int), c->st));
             const int64_t* ids = crit_ids_emitted(c, d - 1);
             if (memo) {
@@ -783,8 +783,9 @@ dms_status run_dtop(dms_ctx* c) {
 
 // D0 on the second lane beside D_{d-1} (both only read the gradient and the critical
 // lists): issue both, then finish both, so the host's count reads for one overlap the
-// other's kernels; persistent and cooperative grids take half the GPU each (two
-// cooperative grids must be co-resident together).
+// other's kernels; the cooperative union-find grids take half the GPU each (two
+// cooperative grids must be co-resident together); the persistent chase grid stays
+// full (it never waits on other work, and halving it measured slower).
 dms_status run_diagrams(dms_ctx* c) {
     static const int conc_env = getenv("DMS_CONCURRENT") ? atoi(getenv("DMS_CONCURRENT")) : 1;
     if (!conc_env || !c->lane3.st) {
