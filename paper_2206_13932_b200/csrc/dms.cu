@@ -85,7 +85,7 @@ struct dms_ctx {
     cudaEvent_t ev_slab[8] = {};  // dms_run_all_host: upload slabs
     Lane lane3;                   // D0's lane when the diagrams run concurrently
     cudaEvent_t ev_crit = nullptr, ev_d0 = nullptr;
-    bool half = false;            // concurrent diagrams: persistent / cooperative grids use half the GPU
+    bool half = false;            // concurrent diagrams: the cooperative union-find grids use half the GPU
     cudaEvent_t t_diag[2] = {};   // stage timers spanning issue .. finish
     bool order_pending = false;          // st must wait ev_order before using ranks
     int64_t ncell[4] = {1, 0, 0, 0};
