@@ -96,22 +96,17 @@ __global__ void k_rekey(uint64_t* __restrict__ keys, int64_t m, const int32_t* _
     }
 }
 
-// inv[perm[p]] = p
-__global__ void k_invert(const uint32_t* __restrict__ perm, int64_t m, uint32_t* __restrict__ inv) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < m) inv[perm[p]] = (uint32_t)p;
-}
-
-// union-find inputs in emission order: arc key = processing index (rev: m-1-sorted
+// union-find inputs in emission order, scattered straight from the sort permutations
+// (perm: sorted position -> emission index): arc key = processing index (rev: m-1-sorted
 // position), node age = sorted position (rev: n - sorted position; the virtual node n
 // gets age 0, the oldest)
-__global__ void k_uf_keys(const uint32_t* __restrict__ inv_arcs, int64_t m, int rev, uint32_t* __restrict__ key) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < m) key[e] = rev ? (uint32_t)(m - 1 - inv_arcs[e]) : inv_arcs[e];
+__global__ void k_uf_keys(const uint32_t* __restrict__ perm, int64_t m, int rev, uint32_t* __restrict__ key) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < m) key[perm[p]] = rev ? (uint32_t)(m - 1 - p) : (uint32_t)p;
 }
-__global__ void k_uf_ages(const uint32_t* __restrict__ inv_nodes, int64_t n, int rev, int32_t* __restrict__ age) {
+__global__ void k_uf_ages(const uint32_t* __restrict__ perm, int64_t n, int rev, int32_t* __restrict__ age) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) age[r] = rev ? (int32_t)(n - inv_nodes[r]) : (int32_t)inv_nodes[r];
+    if (r < n) age[perm[r]] = rev ? (int32_t)(n - r) : (int32_t)r;
     if (rev && r == n) age[n] = 0;
 }
 

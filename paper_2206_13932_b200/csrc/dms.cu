@@ -53,7 +53,6 @@ struct UFBuf {
     int32_t* outp = nullptr;   // out in processing order
     uint32_t *key = nullptr, *inv_a = nullptr;  // per arc (emission order)
     int32_t* age = nullptr;                     // per node (emission order)
-    uint32_t* inv_n = nullptr;
     int* nlive = nullptr;  // two device counters
     int* h_status = nullptr;  // pinned: the union-find's convergence status
     int* trace = nullptr;  // [64] union-find round trace
@@ -281,11 +280,9 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
         cudaFree(u.parent);
         cudaFree(u.best);
         cudaFree(u.age);
-        cudaFree(u.inv_n);
         CU(dalloc(&u.parent, nodes));
         CU(dalloc(&u.best, nodes));
         CU(dalloc(&u.age, nodes));
-        CU(dalloc(&u.inv_n, nodes));
         u.cap_nodes = nodes;
     }
     return DMS_OK;
@@ -576,13 +573,9 @@ dms_status emit_unpaired(dms_ctx* c, int which, UFBuf& u, int64_t m, const int64
 // union-find inputs in emission order: arc keys from the arcs' sort permutation, node
 // ages from the nodes' sort permutation (rev: descending processing order)
 void uf_keys_ages(dms_ctx* c, UFBuf& u, int karcs, int64_t m, int knodes, int64_t n, int rev) {
-    if (m) {
-        k_invert<<<grid_for(m), kBlock, 0, c->st>>>(crit_perm(c, karcs), m, u.inv_a);
-        k_uf_keys<<<grid_for(m), kBlock, 0, c->st>>>(u.inv_a, m, rev, u.key);
-    }
-    if (n) k_invert<<<grid_for(n), kBlock, 0, c->st>>>(crit_perm(c, knodes), n, u.inv_n);
-    k_uf_ages<<<grid_for(n + 1), kBlock, 0, c->st>>>(u.inv_n, n, rev, u.age);
-    c->launches += 5;
+    if (m) k_uf_keys<<<grid_for(m), kBlock, 0, c->st>>>(crit_perm(c, karcs), m, rev, u.key);
+    k_uf_ages<<<grid_for(n + 1), kBlock, 0, c->st>>>(crit_perm(c, knodes), n, rev, u.age);
+    c->launches += 2;
 }
 
 // out (emission order) -> processing order, in place (buffer swap)
@@ -1218,7 +1211,7 @@ void dms_destroy(dms_ctx* c) {
         UFBuf& u = c->uf[b];
         for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.rec0, (void*)u.rec1, (void*)u.rsrc, (void*)u.out, (void*)u.list,
                         (void*)u.live2, (void*)u.nlive, (void*)u.trace, (void*)u.outp, (void*)u.key,
-                        (void*)u.inv_a, (void*)u.age, (void*)u.inv_n,
+                        (void*)u.inv_a, (void*)u.age,
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
             cudaFree(p);
         if (u.h_status) cudaFreeHost(u.h_status);
