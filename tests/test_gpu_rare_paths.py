@@ -53,3 +53,19 @@ def test_critical_record_overflow():
     env = dict(os.environ, DMS_CRIT_CAP="7")
     r = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("knobs", [
+    {"DMS_CONCURRENT": "0", "DMS_ORDER_SEQ": "1"},
+    {"DMS_LUT2": "0", "DMS_MEMO": "0"},
+    {"DMS_AGG": "0", "DMS_UFBATCH": "0"},
+    {"DMS_AGG": "1", "DMS_UFBATCH": "4"},
+])
+def test_knobs_keep_results(knobs):
+    """Every A/B knob of DESIGN.md 8c leaves the results bit-exact."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, **knobs)
+    r = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
