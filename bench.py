@@ -279,7 +279,9 @@ def main():
     g_ms = stages["gradient_kernel"] / max(1, stages["gradient_launches"])
     g_ach = bmin_grad / (g_ms / 1e3) / 1e9
     roofline = {
-        "kernel": ("k_gradient_rg<%d> (lower-star gradient + critical records)" % ndim) if ndim > 1 else "k_gradient1",
+        "kernel": {3: "k_gradient_pool<3,8> (lower-star gradient + critical records)",
+                   2: "k_gradient_lut2 (2D lower-star gradient by table lookup + critical records)",
+                   1: "k_gradient1 (1D lower-star gradient + critical records)"}[ndim],
         "bound": "hbm", "achieved": round(g_ach, 1), "peak": peak, "unit": "GB/s",
         "frac": round(g_ach / peak, 4), "traffic": None,
         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(bmin_grad), "ms_per_launch": round(g_ms, 4),
