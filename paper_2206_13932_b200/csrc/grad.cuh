@@ -109,13 +109,32 @@ struct KMask {  // 128-bit set over triangle key indices (kept in registers)
 };
 // W (wide): key indices may reach 90 (3D); without W they stay below 64 (2D: < 15) and
 // the queue is one 64-bit word.
+#ifndef DMS_KMASK_PTX
+#define DMS_KMASK_PTX 1  // branch-free key masks (c4 gradient 41.56 -> 41.15 ms)
+#endif
+// 1 << s for s in [0, 64), 0 for s >= 64 (PTX clamps 64-bit shift amounts to 64)
+__device__ __forceinline__ uint64_t bit_or_zero(uint32_t s) {
+    uint64_t r;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(1ull), "r"(s));
+    return r;
+}
 template <bool W>
 __device__ __forceinline__ void kset(KMask& m, int ki) {
+    if (W && DMS_KMASK_PTX) {
+        m.lo |= bit_or_zero((uint32_t)ki);
+        m.hi |= bit_or_zero((uint32_t)(ki - 64));
+        return;
+    }
     if (!W || ki < 64) m.lo |= 1ull << ki;
     else m.hi |= 1ull << (ki - 64);
 }
 template <bool W>
 __device__ __forceinline__ void kclr(KMask& m, int ki) {
+    if (W && DMS_KMASK_PTX) {
+        m.lo &= ~bit_or_zero((uint32_t)ki);
+        m.hi &= ~bit_or_zero((uint32_t)(ki - 64));
+        return;
+    }
     if (!W || ki < 64) m.lo &= ~(1ull << ki);
     else m.hi &= ~(1ull << (ki - 64));
 }
