@@ -75,18 +75,6 @@ __device__ __forceinline__ int64_t descend(const Geo3& g, const StarTab& S, int6
     }
 }
 
-// arc[j] = tmp[perm[j]] (rev: perm[m-1-j]): from tracing order (the spatially coherent
-// emission order of the critical cells) to processing order (sorted, or reversed)
-__global__ void k_permute_arcs(const int32_t* __restrict__ ta, const int32_t* __restrict__ tb,
-                               const uint32_t* __restrict__ perm, int64_t m, int rev, int32_t* __restrict__ arc_a,
-                               int32_t* __restrict__ arc_b) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= m) return;
-    const uint32_t r = perm[rev ? m - 1 - j : j];
-    arc_a[j] = ta[r];
-    arc_b[j] = tb[r];
-}
-
 // sort key of a critical cell: x << 12 | G  ->  rank(x) << 12 | G
 __global__ void k_rekey(uint64_t* __restrict__ keys, int64_t m, const int32_t* __restrict__ rank) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -168,9 +156,7 @@ __device__ int32_t chase_edge1(const Geo3& g, int64_t c, const int32_t* node_of,
     return vnode;
 }
 
-// Dual chases carrying (x = highest vertex, slot of the current top cell in x's star,
-// ordered f(x), x's gradient word): a hop that stays in St^-(x) needs one f load, a hop
-// that climbs to a higher vertex loads that vertex's gradient word.
+// neighbour slot s of a star is lower than its centre (ordered values, index tie-break)
 __device__ __forceinline__ bool nb_lower(uint32_t on, uint32_t ox, int s, int ne) {
     return on < ox || (on == ox && s < (ne >> 1));
 }
@@ -179,151 +165,24 @@ __device__ __forceinline__ bool in_grid(const Geo3& g, int x, int y, int z) {
     return x >= 0 && x < g.Lx && y >= 0 && y < g.Ly && z >= 0 && z < g.Lz;
 }
 
-// 3D: from tetrahedron slot T of x's star up to a critical tetrahedron or VIRTUAL
-__device__ int32_t chase3(const Geo3& g, const StarTab& S, uint32_t x, int T, uint32_t ox, int cx, int cy, int cz,
-                          const int32_t* node_of, int32_t vnode) {
-    const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(g.grad);
-    uint64_t hi = __ldg(gw + 2 * (uint64_t)x + 1);
-    while (true) {
-        const int code = (int)((hi >> (8 + 2 * T)) & 3ull);
-        if (code == 0) {  // critical tetrahedron (a maximum)
-            const int64_t id = 6 * ((int64_t)x + S.q_anc[T][0] + (int64_t)g.Lx * S.q_anc[T][1] +
-                                    (int64_t)g.Lx * g.Ly * S.q_anc[T][2]) + S.q_k[T];
-            return node_of[id];
-        }
-        const int tt = S.tet_tri[T][code - 1];  // s' = Pair(c)
-        const int T2 = S.tri_tet[tt][0] == T ? S.tri_tet[tt][1] : S.tri_tet[tt][0];
-        if (T2 == 255) return vnode;
-        const int s2 = S.tet_a[T2] ^ S.tet_b[T2] ^ S.tet_c[T2] ^ S.tri_a[tt] ^ S.tri_b[tt];
-        const int nx = cx + S.off[s2][0], ny = cy + S.off[s2][1], nz = cz + S.off[s2][2];
-        if (!in_grid(g, nx, ny, nz)) return vnode;  // s' on the boundary: the virtual maximum
-        const uint32_t n2 = x + (uint32_t)S.lin[s2];
-        const uint32_t on = ord_of(__ldg(g.f + n2));
-        if (nb_lower(on, ox, s2, 14)) {  // the other cofacet of s' is still in St^-(x)
-            T = T2;
-            continue;
-        }
-        const int j = S.tet_a[T2] == s2 ? 0 : (S.tet_b[T2] == s2 ? 1 : 2);
-        T = S.q_reslot[T2][j];
-        x = n2;
-        ox = on;
-        cx = nx; cy = ny; cz = nz;
-        hi = __ldg(gw + 2 * (uint64_t)x + 1);
-    }
-}
-
-// 2D: from triangle slot t of x's star up to a critical triangle or VIRTUAL
-__device__ int32_t chase2(const Geo3& g, const StarTab& S, uint32_t x, int t, uint32_t ox, int cx, int cy,
-                          const int32_t* node_of, int32_t vnode) {
-    const uint16_t* gw = reinterpret_cast<const uint16_t*>(g.grad);
-    uint32_t w = __ldg(gw + x);
-    while (true) {
-        const int code = (int)((w >> (3 + 2 * t)) & 3u);
-        if (code == 0) {
-            const int64_t id = 2 * ((int64_t)x + S.t_anc[t][0] + (int64_t)g.Lx * S.t_anc[t][1]) + S.t_k[t];
-            return node_of[id];
-        }
-        const int e = code == 1 ? S.tri_a[t] : S.tri_b[t];
-        const int t2 = S.edge_tri[e][0] == t ? S.edge_tri[e][1] : S.edge_tri[e][0];
-        if (t2 == 255) return vnode;
-        const int s2 = S.tri_a[t2] ^ S.tri_b[t2] ^ e;
-        const int nx = cx + S.off[s2][0], ny = cy + S.off[s2][1];
-        if (!in_grid(g, nx, ny, 0)) return vnode;
-        const uint32_t n2 = x + (uint32_t)S.lin[s2];
-        const uint32_t on = ord_of(__ldg(g.f + n2));
-        if (nb_lower(on, ox, s2, 6)) {
-            t = t2;
-            continue;
-        }
-        const int j = S.tri_a[t2] == s2 ? 0 : 1;
-        t = S.t_reslot[t2][j];
-        x = n2;
-        ox = on;
-        cx = nx; cy = ny;
-        w = __ldg(gw + x);
-    }
-}
-
-// ends of the arcs of G_{D_{d-1}} for the critical (d-1)-simplices ids[0..m) (in any
-// order; k_permute_arcs puts them in processing order)
+// 1D: the arcs of G_{D_{d-1}} for the critical vertices ids[0..m) (the (d-1)-simplices):
+// both edges of a critical vertex chase up to a critical edge (a maximum) or VIRTUAL
+// (2D / 3D use the work-queue kernel below)
 __global__ void k_dtop_arcs(Geo3 g, const int64_t* __restrict__ ids, int64_t m, const int32_t* __restrict__ node_of,
                             int32_t vnode, int32_t* __restrict__ arc_a, int32_t* __restrict__ arc_b) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
-    const StarTab& S = *g.tab;
     const int64_t id = ids[j];
-    int32_t end[2];
-    if (g.ndim >= 2) {
-        // the critical (d-1)-simplex, its highest vertex x and its slot in x's star
-        const int nv = g.ndim;  // vertices of a (d-1)-simplex
-        const int64_t a = id / g.ncell[nv - 1];
-        const int k = (int)(id % g.ncell[nv - 1]);
-        uint32_t p[3];
-        uint32_t o[3];
-        p[0] = (uint32_t)a;
-        for (int q = 1; q < nv; q++) p[q] = (uint32_t)(a + lin_mask(g, S.chain[nv - 1][k][q - 1]));
-        for (int q = 0; q < nv; q++) o[q] = ord_of(__ldg(g.f + p[q]));
-        int jx = 0;
-        for (int q = 1; q < nv; q++)
-            if (o[jx] < o[q] || (o[jx] == o[q] && p[jx] < p[q])) jx = q;
-        const uint32_t x = p[jx], ox = o[jx];
-        int cx, cy, cz;
-        coords_of(g, x, cx, cy, cz);
-        if (g.ndim == 3) {
-            const int t = S.t_slot[k][jx];
-            for (int side = 0; side < 2; side++) {
-                const int T = S.tri_tet[t][side];
-                int32_t r = vnode;
-                if (T != 255) {
-                    const int s3 = S.tet_a[T] ^ S.tet_b[T] ^ S.tet_c[T] ^ S.tri_a[t] ^ S.tri_b[t];
-                    const int nx = cx + S.off[s3][0], ny = cy + S.off[s3][1], nz = cz + S.off[s3][2];
-                    if (in_grid(g, nx, ny, nz)) {
-                        const uint32_t n3 = x + (uint32_t)S.lin[s3];
-                        const uint32_t on = ord_of(__ldg(g.f + n3));
-                        if (nb_lower(on, ox, s3, 14)) {
-                            r = chase3(g, S, x, T, ox, cx, cy, cz, node_of, vnode);
-                        } else {
-                            const int jj = S.tet_a[T] == s3 ? 0 : (S.tet_b[T] == s3 ? 1 : 2);
-                            r = chase3(g, S, n3, S.q_reslot[T][jj], on, nx, ny, nz, node_of, vnode);
-                        }
-                    }
-                }
-                end[side] = r;
-            }
-        } else {
-            const int e = S.e_slot[k][jx];
-            for (int side = 0; side < 2; side++) {
-                const int t = S.edge_tri[e][side];
-                int32_t r = vnode;
-                if (t != 255) {
-                    const int s3 = S.tri_a[t] ^ S.tri_b[t] ^ e;
-                    const int nx = cx + S.off[s3][0], ny = cy + S.off[s3][1];
-                    if (in_grid(g, nx, ny, 0)) {
-                        const uint32_t n3 = x + (uint32_t)S.lin[s3];
-                        const uint32_t on = ord_of(__ldg(g.f + n3));
-                        if (nb_lower(on, ox, s3, 6)) {
-                            r = chase2(g, S, x, t, ox, cx, cy, node_of, vnode);
-                        } else {
-                            const int jj = S.tri_a[t] == s3 ? 0 : 1;
-                            r = chase2(g, S, n3, S.t_reslot[t][jj], on, nx, ny, node_of, vnode);
-                        }
-                    }
-                }
-                end[side] = r;
-            }
-        }
-    } else {
-        end[0] = chase_edge1(g, id > 0 ? id - 1 : -1, node_of, vnode);
-        end[1] = chase_edge1(g, id < g.N - 1 ? id : -1, node_of, vnode);
-    }
-    arc_a[j] = end[0];
-    arc_b[j] = end[1];
+    arc_a[j] = chase_edge1(g, id > 0 ? id - 1 : -1, node_of, vnode);
+    arc_b[j] = chase_edge1(g, id < g.N - 1 ? id : -1, node_of, vnode);
 }
 
-// Work-queue version of the dual chases (3D / 2D): a persistent grid; every lane owns
-// one chase (one side of one arc) and walks one hop per iteration; a lane whose chase
-// ended takes the next job (warp-aggregated atomic on a global counter), so long and
-// short paths no longer leave lanes idle.  Jobs: 2 per critical (d-1)-simplex, ids in
+// Work-queue dual chases (3D / 2D): a persistent grid; every lane owns one chase (one
+// side of one arc) and walks one hop per iteration, carrying (x = highest vertex, slot
+// of the current top cell in x's star, ordered f(x), x's gradient word): a hop that stays
+// in St^-(x) needs one f load, a hop that climbs loads the new vertex's gradient word.
+// A lane whose chase ended takes the next job from a warp-private batch, so long and
+// short paths do not leave lanes idle.  Jobs: 2 per critical (d-1)-simplex, ids in
 // emission order; results go to out_a / out_b in the same order.
 template <int D>
 struct ChaseState {
@@ -895,23 +754,6 @@ __global__ void k_emit_dtop(Geo3 g, const int32_t* out, int64_t m, const uint32_
     r.death_vertex = (int32_t)dv;
     r.death_value = g.f[dv];
     pairs[pos[j]] = r;
-}
-
-// an infinite class record (Sec. 6): (f(sigma), f*), death_id = -1
-__global__ void k_emit_inf(Geo3 g, int dim, const int64_t* id_ptr, const unsigned int* fmax_ord, PairRec* slot) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const StarTab& S = *g.tab;
-    PairRec r;
-    r.birth_id = *id_ptr;
-    const int64_t bv = max_vertex(g, S, dim, r.birth_id);
-    r.birth_vertex = (int32_t)bv;
-    r.birth_value = g.f[bv];
-    r.death_id = -1;
-    r.death_vertex = -1;
-    const uint32_t o = *fmax_ord;
-    const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
-    r.death_value = __uint_as_float(u);
-    *slot = r;
 }
 
 // unpaired saddles, in ascending lex order.  rev: the arcs are in decreasing order.
