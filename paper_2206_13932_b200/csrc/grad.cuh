@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
 
 // ---- pooled variant: a CTA of 128 threads takes P x 128 consecutive vertices; phase A
 // ranks the neighbours of all of them (compact state: local ranks + lower mask), the
-// pool is counting-sorted by the work estimate |Lt| + |Lq|, and phase C expands the
+// pool is counting-sorted by the work estimate |Le| + |Lt| + |Lq|, and phase C expands the
 // stars in P rounds of 128 in sorted order (warps of near-equal work).  The key caches
 // are rebuilt per expanded star in the thread's own shared-memory column.
 template <int D, int P, int MINB = 1>
