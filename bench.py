@@ -278,36 +278,43 @@ def main():
     peak, peak_kind = load_peaks()
     g_ms = stages["gradient_kernel"] / max(1, stages["gradient_launches"])
     g_ach = bmin_grad / (g_ms / 1e3) / 1e9
-    roofline = {
-        "kernel": {3: "k_gradient_pool<3,8> (lower-star gradient + critical records)",
+    kernel_name = {3: "k_gradient_pool<3,8> (lower-star gradient + critical records)",
                    2: "k_gradient_lut2 (2D lower-star gradient by table lookup + critical records)",
-                   1: "k_gradient1 (1D lower-star gradient + critical records)"}[ndim],
+                   1: "k_gradient1 (1D lower-star gradient + critical records)"}[ndim]
+    hbm = {
         "bound": "hbm", "achieved": round(g_ach, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(g_ach / peak, 4), "traffic": None,
-        "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(bmin_grad), "ms_per_launch": round(g_ms, 4),
+        "frac": round(g_ach / peak, 4), "peak_kind": peak_kind,
+        "algorithmic_bytes_per_launch": int(bmin_grad),
         "end_to_end_frac_of_hbm": round(bmin_e2e / (ms_step / 1e3) / 1e9 / peak, 4),
         "end_to_end_frac_of_8TBps": round(bmin_e2e / (ms_step / 1e3) / 8e12, 4),
     }
+    roofline = dict(kernel=kernel_name, **{k: hbm[k] for k in ("bound", "achieved", "peak", "unit", "frac")},
+                    traffic=None, peak_kind=peak_kind, ms_per_launch=round(g_ms, 4))
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    tr = None
     if os.path.exists(prof):
         try:
             with open(prof) as fh:
                 tr = json.load(fh).get(args.config)
-            if tr:
-                roofline["traffic"] = tr["bytes_per_launch"]
-                roofline["traffic_source"] = tr.get("source")
-                if tr.get("warp_inst_per_launch"):
-                    # the kernel is issue-bound: warp instructions per launch (ncu) over the
-                    # live launch time, against one warp instruction per cycle per SMSP at
-                    # the sampled SM clock
-                    issue_peak = 148 * 4 * (clk.get("sm_mhz") or 1965.0) * 1e6
-                    ach = tr["warp_inst_per_launch"] / (g_ms / 1e3)
-                    roofline["issue"] = {"bound": "alu", "achieved": round(ach / 1e9, 1), "peak": round(issue_peak / 1e9, 1),
-                                         "unit": "G warp-inst/s", "frac": round(ach / issue_peak, 3),
-                                         "lane_efficiency": tr.get("lane_efficiency"),
-                                         "source": tr.get("source")}
         except Exception:
-            pass
+            tr = None
+    if tr:
+        roofline["traffic"] = tr["bytes_per_launch"]
+        roofline["traffic_source"] = tr.get("source")
+        if tr.get("warp_inst_per_launch"):
+            # The kernel is bound by integer issue (ncu: ALU pipe ~89 % busy, DRAM < 1 %), so
+            # its roofline is the issue rate: warp instructions per
+            # launch (ncu, fixed for the input) over the live launch time, against one warp
+            # instruction per cycle per SMSP, 148 SMs x 4 SMSPs, at the sampled SM clock.
+            # The north star's HBM fraction stays in roofline["hbm"].
+            issue_peak = 148 * 4 * (clk.get("sm_mhz") or 1965.0) * 1e6
+            ach = tr["warp_inst_per_launch"] / (g_ms / 1e3)
+            roofline.update({"bound": "alu", "achieved": round(ach / 1e9, 1), "peak": round(issue_peak / 1e9, 1),
+                             "unit": "G warp-inst/s", "frac": round(ach / issue_peak, 3),
+                             "peak_kind": "derived: 148 SMs x 4 SMSPs x 1 warp-instruction/cycle x sampled SM clock",
+                             "lane_efficiency": tr.get("lane_efficiency"),
+                             "alu_pipe_pct_ncu": tr.get("alu_pipe_pct")})
+    roofline["hbm"] = hbm
 
     # end to end through the public API: pinned host input -> device, run, diagrams back
     e2e = None
