@@ -376,8 +376,6 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     A.err = c->err;
     StageTimer tm(c, 5);
     if (c->ndim >= 2) {
-        // (2D fallback without the table: one CTA per 128 vertices, regrouped by work)
-        const unsigned g2 = (unsigned)ceil_div(v1 - v0, kBlockG);
         static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
         // 3D: pools of 8 x 128 vertices per CTA, expanded in work order
         if (c->ndim == 3)
@@ -385,7 +383,7 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
         else if (c->lut2 && lut_env)
             k_gradient_lut2<<<(unsigned)std::min<int64_t>(ceil_div(v1 - v0, kBlock), c->sms * 8), kBlock, 0, c->st>>>(
                 A, c->lut2, c->lut2off);
-        else k_gradient_rg<2><<<g2, kBlockG, 0, c->st>>>(A);
+        else k_gradient_pool<2, 8><<<(unsigned)ceil_div(v1 - v0, 8 * kBlockG), kBlockG, 0, c->st>>>(A);
     } else {
         k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
     }

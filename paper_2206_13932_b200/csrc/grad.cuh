@@ -1,18 +1,21 @@
 // grad.cuh -- lower-star discrete gradient + critical-simplex compaction (sm_100a).
 //
-// One thread per vertex x runs Robins et al.'s ProcessLowerStars (the "expansions"
-// of PAPER.md 1965-1971, 272-276; Alg. 2 l. 2, PAPER.md 330-333) on St^-(x)
-// (PAPER.md 1443-1451), with:
+// One thread per star St^-(x) (PAPER.md 1443-1451) runs Robins et al.'s
+// ProcessLowerStars (the "expansions" of PAPER.md 1965-1971, 272-276; Alg. 2 l. 2,
+// PAPER.md 330-333), with:
 //   * the lower neighbours relabelled by local rank r in [0,14) (4 bits each, packed
 //     in one 64-bit register), so the lexicographic key G of a star cell
 //     (PAPER.md 1380-1414: decreasing vertex sequence, face before coface) is the
 //     12-bit integer (r_a+1)<<8 | (r_b+1)<<4 | (r_c+1) (absent vertices = 0);
 //   * the two priority queues (PQzero / PQone) and the classification state as bit
-//     masks over the star's edge / triangle / tetrahedron slots; popping the minimum
-//     scans the (few) members of a queue.
-// The critical cells of every lower star (Alg. 2 l. 10-12) are written compactly
-// with a single-pass decoupled look-back scan over CTAs (dynamic tile ids), each as an
-// (anchored id, sort key) record; sort key = rank(x) << 12 | G.
+//     masks over the star's edge / triangle / tetrahedron slots (triangles keyed by
+//     C(hi,2)+lo, so a pop is a find-first-set);
+//   * 3D: k_gradient_pool -- a CTA ranks the neighbours of a pool of 1024 vertices and
+//     expands the stars in work order (warps of near-equal work); 2D: k_gradient_lut2 --
+//     the result of every one of the 1957 2D star patterns is tabulated once per
+//     context (k_build_lut2, the same process_star) and looked up; 1D: k_gradient1.
+// The critical cells of every lower star (Alg. 2 l. 10-12) are appended as (anchored
+// id, sort key) records; the sort key rank(x) << 12 | G gives the lexicographic order.
 //
 // Gradient words:
 //   3D uint64 lo : 2-bit code of tri slots 0..31 (1: paired with edge tri_a, 2: tri_b)
@@ -340,232 +343,6 @@ __device__ __forceinline__ int64_t warp_append(unsigned long long* total, uint32
     return (int64_t)base + (inc - cnt);
 }
 
-// ---- regrouped variant: each CTA first builds every lower star's setup state
-// (masks, local ranks, key caches) for its 128 vertices, then sorts the vertices by an
-// estimate of the expansion work (|Lt| + |Lq|) so that the lanes of a warp run lower
-// stars of similar size, which cuts the idle lanes of the data-dependent loop.
-template <int D>
-__global__ void __launch_bounds__(kBlockG) k_gradient_rg(GradArgs A) {
-    constexpr int NE = Geo<D>::NE;
-    __shared__ StarTab S;
-    __shared__ uint8_t s_tki[kMaxNT * kBlockG];
-    __shared__ uint16_t s_qk[(D == 3 ? kMaxNQ : 1) * kBlockG];
-    __shared__ uint64_t s_R[kBlockG], s_IV[kBlockG], s_Lt[kBlockG];
-    __shared__ uint32_t s_Le[kBlockG], s_Lq[kBlockG];
-    __shared__ int s_hist[64];
-    __shared__ uint8_t s_perm[kBlockG];
-    {
-        const int4* src = reinterpret_cast<const int4*>(A.tab);
-        int4* dst = reinterpret_cast<int4*>(&S);
-        for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlockG) dst[i] = src[i];
-    }
-    if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
-    __syncthreads();
-    const int LxLy = A.Lx * A.Ly;
-    const int tid = threadIdx.x;
-    // ---- phase A: setup of this thread's own vertex
-    {
-        const int64_t v = A.v0 + (int64_t)blockIdx.x * kBlockG + tid;
-        uint32_t Le = 0, Lq = 0, word = 0;
-        uint64_t Lt = 0, R = 0, IV = 0;
-        int w = 0;
-        if (v < A.v1) {
-            const int vv = (int)v;
-            const int cx = vv % A.Lx;
-            const int t = vv / A.Lx;
-            const int cy = t % A.Ly;
-            const int cz = t / A.Ly;
-            const float fx = A.f[v];
-            if (is_nan_bits(fx)) atomicOr(A.err, 1);
-            const uint32_t ox = ord_of(fx);
-            uint32_t o[NE];
-#pragma unroll
-            for (int s = 0; s < NE; s++) {
-                const int dx = off_c<D>(s, 0), dy = off_c<D>(s, 1), dz = off_c<D>(s, 2);
-                bool in = true;
-                if (dx < 0) in &= cx > 0;
-                if (dx > 0) in &= cx < A.Lx - 1;
-                if (dy < 0) in &= cy > 0;
-                if (dy > 0) in &= cy < A.Ly - 1;
-                if (dz < 0) in &= cz > 0;
-                if (dz > 0) in &= cz < A.Lz - 1;
-                o[s] = 0xffffffffu;
-                if (in) {
-                    const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
-                    const bool lower = (os < ox) || (os == ox && s < NE / 2);
-                    if (lower) { o[s] = os; Le |= 1u << s; }
-                }
-            }
-            int delta = 0;
-            if (Le) {
-                int r[NE];
-#pragma unroll
-                for (int s = 0; s < NE; s++) r[s] = 0;
-#pragma unroll
-                for (int s = 0; s < NE; s++)
-#pragma unroll
-                    for (int u = s + 1; u < NE; u++) {
-                        const bool s_lt_u = o[s] <= o[u];  // equal values: the smaller slot first
-                        r[u] += s_lt_u ? 1 : 0;
-                        r[s] += s_lt_u ? 0 : 1;
-                    }
-#pragma unroll
-                for (int s = 0; s < NE; s++) {
-                    if ((Le >> s) & 1u) {
-                        R |= (uint64_t)r[s] << (4 * s);
-                        IV |= (uint64_t)s << (4 * r[s]);
-                        if (r[s] == 0) delta = s;
-                    }
-                }
-                uint64_t ta = 0, tb = 0;
-                uint32_t qa = 0, qb = 0, qc = 0;
-                uint32_t le = Le;
-                while (le) {
-                    const int s = __ffs(le) - 1;
-                    le &= le - 1;
-                    ta |= S.tri_amask[s];
-                    tb |= S.tri_bmask[s];
-                    if (D == 3) {
-                        qa |= S.tet_amask[s];
-                        qb |= S.tet_bmask[s];
-                        qc |= S.tet_cmask[s];
-                    }
-                }
-                Lt = ta & tb;
-                Lq = qa & qb & qc;
-                uint64_t m = Lt;
-                while (m) {
-                    const int tt = __ffsll((long long)m) - 1;
-                    m &= m - 1;
-                    const int kix = tri_kidx(S, R, tt);
-                    s_tki[tt * kBlockG + tid] = (uint8_t)kix;
-                }
-                if (D == 3) {
-                    uint32_t mq = Lq;
-                    while (mq) {
-                        const int q = __ffs(mq) - 1;
-                        mq &= mq - 1;
-                        s_qk[q * kBlockG + tid] = (uint16_t)cmp_tet(S, R, q);
-                    }
-                }
-                w = min(63, __popcll(Lt) + __popc(Lq) + 1);
-            }
-            word = Le | ((uint32_t)delta << 16) | (1u << 24);  // bit 24: active
-        }
-        s_R[tid] = R;
-        s_IV[tid] = IV;
-        s_Lt[tid] = Lt;
-        s_Le[tid] = word;
-        s_Lq[tid] = Lq;
-        atomicAdd(&s_hist[w], 1);
-        __syncthreads();
-        if (tid < 32) {  // exclusive scan of the 64-bin work histogram
-            const int a0 = s_hist[2 * tid], a1 = s_hist[2 * tid + 1];
-            int inc = a0 + a1;
-#pragma unroll
-            for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, inc, o2);
-                if (tid >= o2) inc += y;
-            }
-            const int ex = inc - a0 - a1;
-            s_hist[2 * tid] = ex;
-            s_hist[2 * tid + 1] = ex + a0;
-        }
-        __syncthreads();
-        s_perm[atomicAdd(&s_hist[w], 1)] = (uint8_t)tid;
-        __syncthreads();
-    }
-    // ---- phase C: expansion of a (work-sorted) vertex of this CTA
-    const int p = s_perm[tid];
-    const int64_t v = A.v0 + (int64_t)blockIdx.x * kBlockG + p;
-    const uint32_t word = s_Le[p];
-    const bool active = (word >> 24) & 1u;
-    StarState st;
-    st.Le = word & 0xffffu;
-    st.Lq = s_Lq[p];
-    st.Lt = s_Lt[p];
-    st.cls_e = st.crit_e = st.pq0_er = 0;
-    st.cls_t = st.crit_t = 0;
-    st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
-    st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
-    st.tcode_lo = st.tcode_hi = st.qcode = 0;
-    st.vcode = -1;
-    const uint64_t R = s_R[p], IV = s_IV[p];
-    const bool crit_v = active && st.Le == 0;
-    if (active && st.Le) {
-        KeyCache C;
-        C.tki = s_tki + p;
-        C.qk = s_qk + p;
-        C.IV = IV;
-        C.S = &S;
-        C.R = R;
-        // 2D key indices stay below C(6,2) = 15: one-word queues.  (3D keeps the two-word
-        // form for every star: a narrow/wide split per star cost 15 % in 3D.)
-        process_star<D, D == 3>(S, C, R, IV, __popc(st.Le), (int)((word >> 16) & 15u), st);
-    }
-    if (active) {
-        if (D == 3) {
-            const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
-            const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
-            reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
-        } else {
-            const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
-            reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
-        }
-    }
-    const uint32_t c0 = crit_v ? 1u : 0u, c1 = __popc(st.crit_e), c2 = __popcll(st.crit_t), c3 = __popc(st.crit_q);
-    if (!__any_sync(0xffffffffu, (c0 | c1 | c2 | c3) != 0u)) return;
-    // placeholder sort key x << 12 | G; dms_critical rewrites it to rank(x) << 12 | G
-    // once the vertex order (which runs concurrently on a second stream) is done
-    const uint64_t rkey = (uint64_t)v << 12;
-    {
-        const int64_t q0 = warp_append(&A.totals[0], c0);
-        if (c0 && q0 < A.cap[0]) { A.crit_id[0][q0] = v; A.crit_key[0][q0] = rkey; }
-    }
-    {
-        int64_t q1 = warp_append(&A.totals[1], c1);
-        uint32_t m = st.crit_e;
-        while (m) {
-            const int s = __ffs(m) - 1;
-            m &= m - 1;
-            if (q1 < A.cap[1]) {
-                const int64_t anc = v + S.e_anc[s][0] + A.Lx * S.e_anc[s][1] + LxLy * S.e_anc[s][2];
-                A.crit_id[1][q1] = A.ncell[1] * anc + S.e_k[s];
-                A.crit_key[1][q1] = rkey | key_edge(R, s);
-            }
-            q1++;
-        }
-    }
-    {
-        int64_t q2 = warp_append(&A.totals[2], c2);
-        uint64_t m = st.crit_t;
-        while (m) {
-            const int t = __ffsll((long long)m) - 1;
-            m &= m - 1;
-            if (q2 < A.cap[2]) {
-                const int64_t anc = v + S.t_anc[t][0] + A.Lx * S.t_anc[t][1] + LxLy * S.t_anc[t][2];
-                A.crit_id[2][q2] = A.ncell[2] * anc + S.t_k[t];
-                A.crit_key[2][q2] = rkey | key_tri(S, R, t);
-            }
-            q2++;
-        }
-    }
-    if (D == 3) {
-        int64_t q3 = warp_append(&A.totals[3], c3);
-        uint32_t m = st.crit_q;
-        while (m) {
-            const int q = __ffs(m) - 1;
-            m &= m - 1;
-            if (q3 < A.cap[3]) {
-                const int64_t anc = v + S.q_anc[q][0] + A.Lx * S.q_anc[q][1] + LxLy * S.q_anc[q][2];
-                A.crit_id[3][q3] = A.ncell[3] * anc + S.q_k[q];
-                A.crit_key[3][q3] = rkey | key_tet(S, R, q);
-            }
-            q3++;
-        }
-    }
-}
-
 // ---- pooled variant: a CTA of 128 threads takes P x 128 consecutive vertices; phase A
 // ranks the neighbours of all of them (compact state: local ranks + lower mask), the
 // pool is counting-sorted by the work estimate |Le| + |Lt| + |Lq|, and phase C expands the
@@ -755,7 +532,9 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
         }
         const uint32_t c0 = crit_v ? 1u : 0u, c1 = __popc(st.crit_e), c2 = __popcll(st.crit_t), c3 = __popc(st.crit_q);
         if (!__any_sync(0xffffffffu, (c0 | c1 | c2 | c3) != 0u)) continue;
-        const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_rg
+        // placeholder sort key x << 12 | G; dms_critical rewrites it to rank(x) << 12 | G
+        // once the vertex order (which runs concurrently on a second stream) is done
+        const uint64_t rkey = (uint64_t)v << 12;
         {
             const int64_t q0 = warp_append(&A.totals[0], c0);
             if (c0 && q0 < A.cap[0]) { A.crit_id[0][q0] = v; A.crit_key[0][q0] = rkey; }
@@ -984,7 +763,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient_lut2(GradArgs A, const uint
         uint32_t ptot;
         const uint32_t pex = block_excl_sum<kBlock / 32>(packed, s_sw, &ptot);
         if (ptot == 0) continue;
-        const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_rg
+        const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_pool
 #pragma unroll
         for (int k = 0; k < 3; k++) {
             const int sh = k == 0 ? 0 : (k == 1 ? 10 : 21);
@@ -1077,7 +856,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
     }
     __syncthreads();
     if (!active || !(crit_v || crit_e)) return;
-    const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_rg
+    const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_pool
     if (crit_v) {
         const int64_t p = (int64_t)s_base[0] + loc0;
         if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
