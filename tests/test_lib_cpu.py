@@ -118,3 +118,18 @@ def test_no_cpu_fallback_without_device(dms):
         pytest.skip("has a GPU")
     with pytest.raises(TypeError):
         dms.dms_create(torch.zeros(4, 4))
+
+
+@pytest.mark.parametrize("dims,ndim", [((1 << 16, 1 << 15, 1), 2), ((800, 800, 800), 3), ((720, 720, 720), 3),
+                                       ((1 << 31,), 1)])
+def test_too_large_rejected_before_any_device_work(dms, dims, ndim):
+    """Size limits (include/dms.h DMS_ERR_TOO_LARGE): N < 2^31 and C_d * N < 2^31 (int32
+    vertex and top-cell indexing).  Checked before the library touches the device, so it
+    runs without a GPU (the device pointer is never dereferenced)."""
+    import ctypes
+
+    L = dms.lib()
+    arr = (ctypes.c_int64 * 3)(*(list(dims) + [1] * (3 - len(dims))))
+    out = ctypes.c_void_p()
+    st = L.dms_create(arr, ndim, ctypes.c_void_p(0x1000), None, ctypes.byref(out))
+    assert st == 4 and not out.value  # DMS_ERR_TOO_LARGE, no context
