@@ -366,6 +366,10 @@ def main():
                        "l2": "input (%d MB) larger than L2; no flush" % (N * 4 >> 20),
                        "parallelism": "replicas" if world > 1 else "single"},
             "stages_ms_per_step": {k: round(v / args.steps, 4) for k, v in stages.items() if k != "gradient_launches"},
+            # per stage as throughput: N / t_stage; stages on the concurrent
+            # streams overlap, so these do not add up to the step
+            "stages_mvertices_per_s": {k: round(N / (v / args.steps) / 1e3, 1) for k, v in stages.items()
+                                       if k in ("order", "gradient", "critical", "d0", "dtop") and v > 0},
             "counts": {"critical": ncrit, "d0_pairs": nd0, "dtop_pairs": ndt},
             "roofline": roofline,
             "cpu_baseline": cpu_base,
