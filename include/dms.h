@@ -36,8 +36,17 @@
  *   dms_diagram_top, dms_sync) as DMS_ERR_NAN.  CUDA errors -> DMS_ERR_CUDA
  *   (sticky: later calls on the same context return DMS_ERR_STATE).
  *
- * Synchronisation
- *   Only calls returning host counts (h_count, h_n) synchronise the stream.
+ * Synchronisation and threads
+ *   Only calls returning host counts (h_count, h_n) synchronise the stream (and
+ *   dms_run_all / dms_run_all_host, which read the critical and pair counts).  The
+ *   library also uses two internal streams of its own (the vertex order; D0 beside
+ *   D_{d-1}); their work is joined into the caller's stream before a call returns.
+ *   A context is not thread-safe: calls on one context must not overlap; distinct
+ *   contexts are independent.
+ *
+ * Size limits
+ *   N < 2^31 and (top cells per vertex) * N < 2^31, checked by dms_create
+ *   (DMS_ERR_TOO_LARGE) before any device work; the largest 3D cube is about 710^3.
  */
 #ifndef DMS_H
 #define DMS_H
