@@ -1,12 +1,15 @@
 // dms.cu -- C-ABI entry points (include/dms.h) and host orchestration.
 //
-// One context = one field on one stream.  The pipeline (Fig. 4 overview,
-// 1236-1332, restricted to the front end):
-//   order    k_order_keys + radix sort -> rank                     (Sec. 2.1, 7.1)
-//   gradient k_gradient<D> (+ fused critical compaction)          (Sec. 2.6, Alg. 2)
-//   critical radix sort of each C_k by lexicographic key           (Alg. 2 l. 13)
+// One context = one field on the caller's stream (plus two internal streams).  The
+// pipeline (Fig. 4 overview, 1236-1332, restricted to the front end):
+//   order    radix sort of (ordered f, index) -> rank, on the      (Sec. 2.1, 7.1)
+//            second stream beside the gradient
+//   gradient k_gradient_pool<3> / k_gradient_lut2 / k_gradient1     (Sec. 2.6, Alg. 2)
+//            (+ appended critical records)
+//   critical radix sort of each C_k by its lexicographic key       (Alg. 2 l. 13)
 //   D0       node map, k_d0_arcs, union-find rounds, emission      (Sec. 5.1, 6)
-//   D_{d-1}  node map, k_dtop_arcs, union-find rounds, emission    (Sec. 5.2, 6)
+//   D_{d-1}  node map, memoised work-queue chases, union-find      (Sec. 5.2, 6)
+//            rounds, emission; D0 runs on a third stream beside it (Sec. 7.2)
 #include <cuda_runtime.h>
 
 #include <algorithm>
