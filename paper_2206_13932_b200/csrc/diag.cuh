@@ -1,14 +1,15 @@
 // diag.cuh -- extremum diagrams D0 and D_{d-1} (Sec. 5) on sm_100a.
 //
 // D0 (Sec. 5.1, PAPER.md 2481-2685):
-//   (a)+(b) k_d0_arcs: for every critical edge (sorted, Alg. 2), follow the two
+//   (a)+(b) k_d0_arcs: for every critical edge (in emission order), follow the two
 //           descending v-paths (vertex -> paired edge -> other vertex) from its
 //           vertices to minima.  The paired edge of a vertex is its steepest-descent
 //           edge, so this is root finding in the steepest-descent forest.  Arc =
-//           (node of minimum a, node of minimum b); nodes = positions in sorted C_0.
+//           (node of minimum a, node of minimum b); nodes = emission positions in C_0,
+//           arc keys = positions in the sorted C_1, node ages = positions in sorted C_0.
 //   (c)+(d) union-find over the arcs in increasing lexicographic order with the
-//           Elder rule, done as parallel mutual-minimum contraction rounds (DESIGN.md
-//           "Union-find"), finished by a sequential tail kernel.
+//           Elder rule, done as parallel contraction rounds in one cooperative kernel
+//           (DESIGN.md "Union-find"), finished by a sequential tail in the same kernel.
 // D_{d-1} (Sec. 5.2, PAPER.md 2690-2825): the same on the dual gradient: stable sets
 //   of the critical (d-1)-simplices, followed through the d-simplices (d-simplex ->
 //   its paired facet -> the other cofacet of that facet), a virtual maximum on the
