@@ -30,6 +30,7 @@ struct Geo3 {
     const float* f;
     const void* grad;
     const StarTab* tab;
+    const ChaseTab* ctab;  // dual-chase transitions
 };
 
 __device__ __forceinline__ int64_t lin_mask(const Geo3& g, int m) {
@@ -215,7 +216,7 @@ __device__ __forceinline__ int32_t chase_step(const Geo3& g, const StarTab& S, C
             id = 2 * ((int64_t)c.x + S.t_anc[T][0] + (int64_t)g.Lx * S.t_anc[T][1]) + S.t_k[T];
         return node_of[id];
     }
-    const uint32_t e = D == 3 ? S.q_next[T][code - 1] : S.t_next[T][code - 1];
+    const uint32_t e = D == 3 ? g.ctab->q_next[T][code - 1] : g.ctab->t_next[T][code - 1];
     const int T2 = (int)(e & 255u);
     if (T2 == 255) return vnode;
     const int s2 = (int)((e >> 8) & 255u);

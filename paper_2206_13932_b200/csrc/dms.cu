@@ -98,6 +98,7 @@ struct dms_ctx {
     int64_t ncell[4] = {1, 0, 0, 0};
     StarTab htab;
     StarTab* dtab = nullptr;
+    ChaseTab* dctab = nullptr;  // dual-chase transitions (device)
     // caller or scratch buffers
     int32_t* rank = nullptr;
     void* grad = nullptr;
@@ -240,6 +241,7 @@ Geo3 geo(const dms_ctx* c) {
     g.f = c->f;
     g.grad = c->grad;
     g.tab = c->dtab;
+    g.ctab = c->dctab;
     return g;
 }
 
@@ -843,6 +845,12 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
 #define CA(call) do { if ((call) != cudaSuccess) return bail(DMS_ERR_OOM); } while (0)
     CA(dalloc(&c->dtab, 1));
     if (cudaMemcpy(c->dtab, &c->htab, sizeof(StarTab), cudaMemcpyHostToDevice) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    {
+        ChaseTab ct;
+        build_chase_tables(c->htab, &ct);
+        CA(dalloc(&c->dctab, 1));
+        if (cudaMemcpy(c->dctab, &ct, sizeof(ChaseTab), cudaMemcpyHostToDevice) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    }
     CA(dalloc(&c->rank_scratch, N));
     CA(cudaMalloc(&c->grad_scratch, dms_gradient_bytes(c)));
     for (int b = 0; b < 2; b++) { CA(dalloc(&c->okeys[b], N)); CA(dalloc(&c->ovals[b], N)); }
@@ -1194,6 +1202,7 @@ void dms_destroy(dms_ctx* c) {
     for (cudaEvent_t e : c->ev_slab)
         if (e) cudaEventDestroy(e);
     cudaFree(c->dtab);
+    cudaFree(c->dctab);
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);
     for (int b = 0; b < 2; b++) { cudaFree(c->okeys[b]); cudaFree(c->ovals[b]); }

@@ -356,8 +356,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
     __shared__ uint8_t s_tki[kMaxNT * kBlockG];
     __shared__ uint16_t s_qk[(D == 3 ? kMaxNQ : 1) * kBlockG];
     __shared__ uint64_t s_R[POOL];
-    __shared__ uint32_t s_W[POOL];
-    __shared__ uint8_t s_w[POOL];
+    __shared__ uint32_t s_W[POOL];  // Le | delta << 16 | active << 24 | work << 25
     __shared__ uint16_t s_perm[POOL];
     __shared__ int s_hist[64];
     {
@@ -444,8 +443,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             word = Le | ((uint32_t)delta << 16) | (1u << 24);  // bit 24: active
         }
         s_R[slot] = R;
-        s_W[slot] = word;
-        s_w[slot] = (uint8_t)w;
+        s_W[slot] = word | ((uint32_t)w << 25);
         atomicAdd(&s_hist[w], 1);
     }
     __syncthreads();
@@ -464,7 +462,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
     __syncthreads();
     for (int k = 0; k < P; k++) {
         const int slot = k * kBlockG + tid;
-        s_perm[atomicAdd(&s_hist[s_w[slot]], 1)] = (uint16_t)slot;
+        s_perm[atomicAdd(&s_hist[s_W[slot] >> 25], 1)] = (uint16_t)slot;
     }
     __syncthreads();
     // ---- phase C: P rounds of 128 stars in work order

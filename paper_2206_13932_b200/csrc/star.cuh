@@ -38,8 +38,6 @@ struct alignas(16) StarTab {
     uint64_t tet_tmask[kMaxNQ];       // the 3 triangle slots of a tet slot, as a mask
     uint8_t q_reslot[kMaxNQ][3];      // tet slot T seen from its link vertex j (a,b,c) -> slot there
     uint8_t t_reslot[kMaxNT][2];      // tri slot t seen from its link vertex j (a,b) -> slot there
-    uint32_t q_next[kMaxNQ][3];       // dual-chase transition: T2 | s2 << 8 | T2 seen from s2 << 16
-    uint32_t t_next[kMaxNT][2];       // (2D: triangles); T2 = 255: no other cofacet
     // anchored ids of star cells: anchor offset from x and chain index
     int8_t e_anc[kMaxNE][3];  uint8_t e_k[kMaxNE];
     int8_t t_anc[kMaxNT][3];  uint8_t t_k[kMaxNT];
@@ -53,7 +51,17 @@ struct alignas(16) StarTab {
     int nchain[4];
 };
 
+// One-lookup transitions of the ascending dual chase (diag.cuh chase_step), kept out of
+// StarTab so the gradient kernels' shared-memory copy stays small: top cell T paired
+// with its facet #c -> T2 | s2 << 8 | (T2 seen from s2) << 16 (T2 = 255: no other
+// cofacet of that facet in this star).
+struct alignas(16) ChaseTab {
+    uint32_t q_next[kMaxNQ][3];  // 3D: tetrahedra
+    uint32_t t_next[kMaxNT][2];  // 2D: triangles
+};
+
 // Build the tables for a grid (host).  Returns false if something is inconsistent.
 bool build_star_tables(int ndim, const int64_t L[3], StarTab* T);
+inline void build_chase_tables(const StarTab& T, ChaseTab* C);
 
 }  // namespace dms

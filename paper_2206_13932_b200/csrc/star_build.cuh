@@ -231,33 +231,6 @@ inline bool build_star_tables(int ndim, const int64_t L[3], StarTab* T) {
             T->t_reslot[t][j] = (uint8_t)r;
         }
     }
-    // one-lookup transitions of the ascending dual chase (diag.cuh chase_step): top cell
-    // T paired with its facet #c -> the other cofacet T2 of that facet in this star
-    // (255: none), the slot s2 of T2's vertex off the facet, and T2 seen from s2
-    std::memset(T->q_next, 255, sizeof(T->q_next));
-    std::memset(T->t_next, 255, sizeof(T->t_next));
-    if (ndim == 3) {
-        for (int q = 0; q < nq; q++)
-            for (int c = 0; c < 3; c++) {
-                const int tt = T->tet_tri[q][c];
-                const int T2 = T->tri_tet[tt][0] == q ? T->tri_tet[tt][1] : T->tri_tet[tt][0];
-                if (T2 == 255) { T->q_next[q][c] = 0xffffffu; continue; }
-                const int s2 = T->tet_a[T2] ^ T->tet_b[T2] ^ T->tet_c[T2] ^ T->tri_a[tt] ^ T->tri_b[tt];
-                const int j = T->tet_a[T2] == s2 ? 0 : (T->tet_b[T2] == s2 ? 1 : 2);
-                T->q_next[q][c] = (uint32_t)T2 | ((uint32_t)s2 << 8) | ((uint32_t)T->q_reslot[T2][j] << 16);
-            }
-    }
-    if (ndim == 2) {
-        for (int t = 0; t < nt; t++)
-            for (int c = 0; c < 2; c++) {
-                const int e = c == 0 ? T->tri_a[t] : T->tri_b[t];
-                const int T2 = T->edge_tri[e][0] == t ? T->edge_tri[e][1] : T->edge_tri[e][0];
-                if (T2 == 255) { T->t_next[t][c] = 0xffffffu; continue; }
-                const int s2 = T->tri_a[T2] ^ T->tri_b[T2] ^ e;
-                const int j = T->tri_a[T2] == s2 ? 0 : 1;
-                T->t_next[t][c] = (uint32_t)T2 | ((uint32_t)s2 << 8) | ((uint32_t)T->t_reslot[T2][j] << 16);
-            }
-    }
     for (int k = 1; k <= ndim; k++) {
         for (int i = 0; i < T->nchain[k]; i++) {
             std::vector<P3> pts{zero};
@@ -275,6 +248,38 @@ inline bool build_star_tables(int ndim, const int64_t L[3], StarTab* T) {
         }
     }
     return true;
+}
+
+
+// the dual-chase transition table (see star.cuh ChaseTab)
+inline void build_chase_tables(const StarTab& T, ChaseTab* C) {
+    // one-lookup transitions of the ascending dual chase (diag.cuh chase_step): top cell
+    // T paired with its facet #c -> the other cofacet T2 of that facet in this star
+    // (255: none), the slot s2 of T2's vertex off the facet, and T2 seen from s2
+    std::memset(C->q_next, 255, sizeof(C->q_next));
+    std::memset(C->t_next, 255, sizeof(C->t_next));
+    if (T.ndim == 3) {
+        for (int q = 0; q < T.nq; q++)
+            for (int c = 0; c < 3; c++) {
+                const int tt = T.tet_tri[q][c];
+                const int T2 = T.tri_tet[tt][0] == q ? T.tri_tet[tt][1] : T.tri_tet[tt][0];
+                if (T2 == 255) { C->q_next[q][c] = 0xffffffu; continue; }
+                const int s2 = T.tet_a[T2] ^ T.tet_b[T2] ^ T.tet_c[T2] ^ T.tri_a[tt] ^ T.tri_b[tt];
+                const int j = T.tet_a[T2] == s2 ? 0 : (T.tet_b[T2] == s2 ? 1 : 2);
+                C->q_next[q][c] = (uint32_t)T2 | ((uint32_t)s2 << 8) | ((uint32_t)T.q_reslot[T2][j] << 16);
+            }
+    }
+    if (T.ndim == 2) {
+        for (int t = 0; t < T.nt; t++)
+            for (int c = 0; c < 2; c++) {
+                const int e = c == 0 ? T.tri_a[t] : T.tri_b[t];
+                const int T2 = T.edge_tri[e][0] == t ? T.edge_tri[e][1] : T.edge_tri[e][0];
+                if (T2 == 255) { C->t_next[t][c] = 0xffffffu; continue; }
+                const int s2 = T.tri_a[T2] ^ T.tri_b[T2] ^ e;
+                const int j = T.tri_a[T2] == s2 ? 0 : 1;
+                C->t_next[t][c] = (uint32_t)T2 | ((uint32_t)s2 << 8) | ((uint32_t)T.t_reslot[T2][j] << 16);
+            }
+    }
 }
 
 }  // namespace dms
