@@ -83,7 +83,7 @@ def env():
 @pytest.mark.parametrize("cfg", CFGS)
 def test_full_size(env, cfg):
     torch, dms = env
-    f3 = fields.make(cfg)
+    f3 = fields.make(cfg, seed=int(os.environ.get("DMS_FULLSIZE_SEED", "0")))
     shape = f3.shape
     d = f3.ndim
     f = f3.ravel()
