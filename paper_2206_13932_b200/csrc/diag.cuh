@@ -469,8 +469,12 @@ __global__ void k_gather_undecided(const int32_t* out, int64_t m, const uint32_t
 // All union-find rounds in one cooperative launch (grid-wide barriers between the
 // phases, no host round trip), then block 0 sorts the (few) undecided arcs and runs
 // the sequential elder-rule union-find over them in processing order.
-constexpr int kUFTail = 2048;
-constexpr int kUFTile = 1024;  // records per CTA tile in pass A (kUFTile * 16 B == kUFTail * 8 B)
+#ifndef DMS_UFTAIL
+#define DMS_UFTAIL 128  // sequential-tail threshold (sweep 2048..64: smaller is slightly faster; 1D most)
+#endif
+constexpr int kUFTail = DMS_UFTAIL;
+constexpr int kUFTile = 1024;  // records per CTA tile in pass A (its 16 KB also hold the tail's sort list)
+static_assert(kUFTail * 8 <= kUFTile * 16, "the tail's sort list aliases the pass-A staging");
 
 struct UFArgs {
     const uint32_t* key;  // per arc: its processing index (the arc order of the union-find)
