@@ -25,11 +25,13 @@ __global__ void __launch_bounds__(kBlock) k_hist(const Key* __restrict__ keys, c
                                                  int64_t n, int shift, uint32_t* __restrict__ counts, int64_t ntiles,
                                                  int* err, unsigned long long* kmax) {
     __shared__ uint32_t h[kRadix];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * (kBlock * ITEMS);
     unsigned long long m = 0;
     bool nan = false;
+    // tile-strided (a small persistent grid leaves room beside the gradient kernel)
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = tile * (kBlock * ITEMS);
 #pragma unroll
     for (int i = 0; i < ITEMS; i++) {
         int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
@@ -48,6 +50,10 @@ __global__ void __launch_bounds__(kBlock) k_hist(const Key* __restrict__ keys, c
             atomicAdd(&h[digit_of(kk, shift)], 1u);
         }
     }
+    __syncthreads();
+    counts[(int64_t)threadIdx.x * ntiles + tile] = h[threadIdx.x];
+    __syncthreads();
+    }
     if (FROM_F) {  // fused: NaN detection and the highest vertex (f*) for Sec. 6
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
@@ -56,8 +62,6 @@ __global__ void __launch_bounds__(kBlock) k_hist(const Key* __restrict__ keys, c
         if ((threadIdx.x & 31) == 0) atomicMax(kmax, m);
         if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
     }
-    __syncthreads();
-    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
 // Exclusive scan of n uint32 (single pass, decoupled look-back). status[ntiles] and
@@ -120,11 +124,12 @@ __global__ void __launch_bounds__(kBlock, DMS_SCATTER_MINB) k_scatter(const Key*
     Key* sk = reinterpret_cast<Key*>(dyn);
     Val* sv = reinterpret_cast<Val*>(dyn + sizeof(Key) * TILE);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {  // tile-strided (see k_hist)
 #pragma unroll
     for (int w = 0; w < NW; w++) wcnt[w][threadIdx.x] = 0;
-    gbase[threadIdx.x] = counts_scanned[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+    gbase[threadIdx.x] = counts_scanned[(int64_t)threadIdx.x * ntiles + tile];
     __syncthreads();
-    const int64_t tile0 = (int64_t)blockIdx.x * TILE;
+    const int64_t tile0 = tile * TILE;
     const int64_t seg = tile0 + (int64_t)warp * (32 * ITEMS);
     Key k[ITEMS];
     Val v[ITEMS];
@@ -197,6 +202,8 @@ __global__ void __launch_bounds__(kBlock, DMS_SCATTER_MINB) k_scatter(const Key*
             vout[p] = sv[j];
         }
     }
+    __syncthreads();
+    }
 }
 
 struct SortScratch {
@@ -227,7 +234,7 @@ inline cudaError_t scan_excl(const uint32_t* in, uint32_t* out, int64_t n, SortS
 template <typename Key, typename Val, int ITEMS>
 inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, int bit1, SortScratch& s,
                       cudaStream_t st, int64_t* launches, int32_t* rank_out = nullptr, const float* f = nullptr,
-                      int* err = nullptr, unsigned long long* kmax = nullptr) {
+                      int* err = nullptr, unsigned long long* kmax = nullptr, int64_t grid_cap = 0) {
     if (n <= 0) return 0;
     constexpr int TILE = kBlock * ITEMS;
     constexpr size_t smem = (sizeof(Key) + sizeof(Val)) * TILE;
@@ -240,6 +247,8 @@ inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, i
         attr_done = true;
     }
     const int64_t tiles = ceil_div(n, (int64_t)TILE);
+    // grid_cap > 0: a small tile-strided grid (leaves SM room for a concurrent kernel)
+    const unsigned grid = (unsigned)(grid_cap > 0 ? std::min<int64_t>(tiles, grid_cap) : tiles);
     int cur = 0;
     for (int shift = bit0; shift < bit1; shift += 8) {
         const bool first = shift == bit0 && f != nullptr;
@@ -248,13 +257,13 @@ inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, i
         Val* vi = cur ? vb : va;
         Key* ko = cur ? ka : kb;
         Val* vo = cur ? va : vb;
-        if (first) k_hist<Key, ITEMS, true><<<(unsigned)tiles, kBlock, 0, st>>>(ki, f, n, shift, s.counts, tiles, err, kmax);
-        else k_hist<Key, ITEMS, false><<<(unsigned)tiles, kBlock, 0, st>>>(ki, f, n, shift, s.counts, tiles, err, kmax);
+        if (first) k_hist<Key, ITEMS, true><<<grid, kBlock, 0, st>>>(ki, f, n, shift, s.counts, tiles, err, kmax);
+        else k_hist<Key, ITEMS, false><<<grid, kBlock, 0, st>>>(ki, f, n, shift, s.counts, tiles, err, kmax);
         *launches += 1;
         scan_excl(s.counts, s.counts_scan, tiles * kRadix, s, st, launches);
         const bool ro = last && rank_out;
 #define DMS_SCATTER(RO, FF)                                                                             \
-    k_scatter<Key, Val, ITEMS, RO, FF><<<(unsigned)tiles, kBlock, smem, st>>>(ki, vi, f, ko, vo, rank_out, n, shift, \
+    k_scatter<Key, Val, ITEMS, RO, FF><<<grid, kBlock, smem, st>>>(ki, vi, f, ko, vo, rank_out, n, shift, \
                                                                           s.counts_scan, tiles)
         if (ro && first) DMS_SCATTER(true, true);
         else if (ro) DMS_SCATTER(true, false);
