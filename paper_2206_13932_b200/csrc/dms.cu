@@ -397,7 +397,7 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
                 A, c->lut2, c->lut2off);
         else k_gradient_pool<2, 8><<<(unsigned)ceil_div(v1 - v0, 8 * kBlockG), kBlockG, 0, c->st>>>(A);
     } else {
-        k_gradient1<<<(unsigned)ntiles, kBlock, 0, c->st>>>(A);
+        k_gradient1<<<(unsigned)ceil_div(v1 - v0, (int64_t)kBlock * kG1), kBlock, 0, c->st>>>(A);
     }
     c->launches++;
     CU(cudaGetLastError());

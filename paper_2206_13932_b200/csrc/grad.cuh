@@ -818,52 +818,70 @@ __global__ void __launch_bounds__(kBlock) k_gradient_lut2(GradArgs A, const uint
 // no lower neighbour -> minimum; otherwise pair x with the edge to the lower (in K)
 // lower neighbour; a second lower edge is critical (SURVEY App. B closed form, which
 // the oracle's generic expansion reproduces).
+constexpr int kG1 = 4;  // 1D: vertices per thread
 __global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
-    __shared__ uint32_t sw[2][kBlock / 32 + 1];
+    __shared__ uint32_t sw[kBlock / 32 + 1];
     __shared__ unsigned long long s_base[2];
-    const int64_t v = A.v0 + (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    const bool active = v < A.v1;
-    bool crit_v = false, crit_e = false;
-    int crit_slot = 0;
-    if (active) {
-        const float fx = A.f[v];
-        if (is_nan_bits(fx)) atomicOr(A.err, 1);
-        const uint32_t ox = ord_of(fx);
-        uint32_t ol = 0xffffffffu, orr = 0xffffffffu;
-        bool ll = false, lr = false;
-        if (v > 0) { ol = ord_of(A.f[v - 1]); ll = ol <= ox; }        // left index smaller: ties lower
-        if (v < A.N - 1) { orr = ord_of(A.f[v + 1]); lr = orr < ox; }  // right index larger
+    const int64_t v0 = A.v0 + ((int64_t)blockIdx.x * kBlock + threadIdx.x) * kG1;
+    // f[v0-1 .. v0+kG1] (absent neighbours never lower)
+    uint32_t o[kG1 + 2];
+    bool nan = false;
+#pragma unroll
+    for (int i = 0; i < kG1 + 2; i++) {
+        const int64_t u = v0 - 1 + i;
+        o[i] = 0xffffffffu;
+        if (u >= 0 && u < A.N) {  // (neighbours past v1 exist: the next slab is uploaded first)
+            const float x = __ldg(A.f + u);
+            nan |= (i > 0 && i <= kG1 && u < A.v1) && is_nan_bits(x);
+            o[i] = ord_of(x);
+        }
+    }
+    if (nan) atomicOr(A.err, 1);
+    uint32_t cv = 0, ce = 0, cslot = 0, n0 = 0, n1 = 0;  // bit i: vertex v0+i critical / crit edge / its slot
+#pragma unroll
+    for (int i = 0; i < kG1; i++) {
+        const int64_t v = v0 + i;
+        if (v >= A.v1) continue;
+        const uint32_t ox = o[i + 1], ol = o[i], orr = o[i + 2];
+        const bool ll = v > 0 && ol <= ox;          // left index smaller: ties lower
+        const bool lr = v < A.N - 1 && orr < ox;    // right index larger
         uint8_t code;
-        if (!ll && !lr) { code = 3; crit_v = true; }
+        if (!ll && !lr) { code = 3; cv |= 1u << i; n0++; }
         else if (ll && !lr) code = 0;
         else if (!ll && lr) code = 1;
         else {
             const bool left_lower = ol <= orr;  // K(v-1) < K(v+1)
             code = left_lower ? 0 : 1;
-            crit_e = true;
-            crit_slot = left_lower ? 1 : 0;
+            ce |= 1u << i;
+            n1++;
+            if (!left_lower) cslot |= 1u << i;  // the critical (higher) edge is the left one
         }
         reinterpret_cast<uint8_t*>(A.grad)[v] = code;
     }
-    uint32_t tot0, tot1;
-    const uint32_t loc0 = block_excl_sum<kBlock / 32>(crit_v ? 1u : 0u, sw[0], &tot0);
-    const uint32_t loc1 = block_excl_sum<kBlock / 32>(crit_e ? 1u : 0u, sw[1], &tot1);
+    // record positions: one packed block scan (counts <= 4 per thread each), one counter
+    // atomic per dimension per CTA
+    uint32_t tot;
+    const uint32_t ex = block_excl_sum<kBlock / 32>(n0 | (n1 << 16), sw, &tot);
     if (threadIdx.x < 2) {
-        const uint32_t t = threadIdx.x ? tot1 : tot0;
+        const uint32_t t = threadIdx.x ? (tot >> 16) : (tot & 0xffffu);
         s_base[threadIdx.x] = t ? atomicAdd(&A.totals[threadIdx.x], (unsigned long long)t) : 0ull;
     }
     __syncthreads();
-    if (!active || !(crit_v || crit_e)) return;
-    const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_pool
-    if (crit_v) {
-        const int64_t p = (int64_t)s_base[0] + loc0;
-        if (p < A.cap[0]) { A.crit_id[0][p] = v; A.crit_key[0][p] = rkey; }
-    }
-    if (crit_e) {
-        const int64_t p = (int64_t)s_base[1] + loc1;
-        if (p < A.cap[1]) {
-            A.crit_id[1][p] = crit_slot == 0 ? v - 1 : v;  // edge (a, a+1) has id a
-            A.crit_key[1][p] = rkey | (2u << 8);            // the higher of the two lower edges
+    int64_t p0 = (int64_t)s_base[0] + (ex & 0xffffu), p1 = (int64_t)s_base[1] + (ex >> 16);
+#pragma unroll
+    for (int i = 0; i < kG1; i++) {
+        const int64_t v = v0 + i;
+        const uint64_t rkey = (uint64_t)v << 12;  // placeholder, see k_gradient_pool
+        if ((cv >> i) & 1u) {
+            if (p0 < A.cap[0]) { A.crit_id[0][p0] = v; A.crit_key[0][p0] = rkey; }
+            p0++;
+        }
+        if ((ce >> i) & 1u) {
+            if (p1 < A.cap[1]) {
+                A.crit_id[1][p1] = ((cslot >> i) & 1u) ? v - 1 : v;  // edge (a, a+1) has id a
+                A.crit_key[1][p1] = rkey | (2u << 8);                  // the higher of the two lower edges
+            }
+            p1++;
         }
     }
 }
