@@ -193,3 +193,18 @@ def test_chase_stamps_wrap_around(env):
             if i in (0, 254, 255, 259):
                 assert d.diagram_top().tobytes() == ref.dtop.tobytes(), (name, i)
         d.close()
+
+
+def test_run_all_host_pageable_input(env):
+    """dms_run_all_host also accepts pageable host memory (the copies then stage through
+    the driver): same results."""
+    torch, dms = env
+    f = np.ascontiguousarray(fields.make("c4", seed=4, shape=(30, 26, 22)))
+    ref = gpu_run(env, f)
+    d = dms.DMS(torch.zeros(f.shape, dtype=torch.float32, device="cuda"))
+    d.run_all_host(torch.from_numpy(f))  # not pinned
+    assert d.diagram0().tobytes() == ref["d0"].tobytes()
+    assert d.diagram_top().tobytes() == ref["dtop"].tobytes()
+    for k in range(f.ndim + 1):
+        assert np.array_equal(d.critical()[k].cpu().numpy(), ref["crit"][k])
+    d.close()
