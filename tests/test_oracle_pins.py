@@ -8,6 +8,9 @@ from __future__ import annotations
 
 import itertools
 
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -28,12 +31,17 @@ def sqdist_field(shape, sign):
 
 # ------------------------------------------------------------------ O1 order
 
-@pytest.mark.parametrize(
-    "vals,expect",
-    [([0, 3, 1, 2], [0, 3, 1, 2]), ([1, 1, 1], [0, 1, 2]), ([5, -1], [1, 0])],
-)
-def test_ranks_spec_examples(vals, expect):
-    assert list(oracle.ranks(np.array(vals, np.float32))) == expect
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden(name):
+    with open(os.path.join(GOLDEN, name)) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("case", golden("spec_ranks.json")["cases"])
+def test_ranks_spec_examples(case):  # tests/golden/spec_ranks.json: S:117-119
+    assert list(oracle.ranks(np.array(case["values"], np.float32))) == case["ranks"]
 
 
 def test_ranks_equal_numpy_stable_argsort():
@@ -225,23 +233,24 @@ def test_gradient_constant_and_elevation():
 # ------------------------------------------------------------------ hand-built fields
 
 def test_spec_path_example():
-    # [0,2,1,3] -> criticals {v0, v2, e(v1,v2)}, D0 {(1,2)}, inf 0
-    f = np.array([0, 2, 1, 3], np.float32)
+    g = golden("spec_path_1d.json")
+    f = np.array(g["field"], np.float32)
     res = oracle.run(f)
-    assert list(res.crit[0]) == [0, 2]
-    assert ids_to_sets(f.shape, 1, res.crit[1]) == [frozenset((1, 2))]
-    d0 = [(float(p["birth_value"]), float(p["death_value"]), int(p["death_id"]) < 0) for p in res.d0]
-    assert d0 == [(1.0, 2.0, False), (0.0, 3.0, True)]
+    assert list(res.crit[0]) == g["crit0"]
+    assert ids_to_sets(f.shape, 1, res.crit[1]) == [frozenset(s) for s in g["crit1_vertex_sets"]]
+    d0 = [[float(p["birth_value"]), float(p["death_value"]), int(p["death_id"]) < 0] for p in res.d0]
+    assert d0 == g["d0"]
 
 
 def test_1d_example_table():
-    f = np.array([0, 2, 1, 3, 1.5, 4, 0.5, 5, 2.5], np.float32)
+    g = golden("hand_1d_table.json")
+    f = np.array(g["field"], np.float32)
     res = oracle.run(f)
-    assert [len(c) for c in res.crit] == [5, 4]
+    assert [len(c) for c in res.crit] == g["crit_counts"]
     fin = sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] >= 0)
-    assert fin == [(0.5, 4.0), (1.0, 2.0), (1.5, 3.0), (2.5, 5.0)]
+    assert fin == [tuple(x) for x in g["d0_finite"]]
     inf = [(float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] < 0]
-    assert inf == [(0.0, 5.0)]
+    assert inf == [tuple(x) for x in g["d0_infinite"]]
     # 1D: D_{d-1} = D0 (duality), including the infinite class
     top = sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.dtop)
     assert top == sorted(fin + inf)
@@ -249,29 +258,27 @@ def test_1d_example_table():
 
 @pytest.mark.parametrize("d", [2, 3])
 def test_negative_paraboloid(d):
+    g = golden("paraboloids.json")["neg"][str(d)]
     f = sqdist_field((5,) * d, -1)
     res = oracle.run(f)
-    if d == 2:
-        assert [len(c) for c in res.crit] == [4, 4, 1]
-        assert sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] >= 0) == [(-8.0, -4.0)] * 3
-        assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.dtop] == [(-4.0, 0.0)]
-    else:
-        assert [len(c) for c in res.crit] == [8, 12, 6, 1]
-        assert sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] >= 0) == [(-12.0, -8.0)] * 7
-        assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.dtop] == [(-4.0, 0.0)]
-        # |D1| = |C1| - |D0 finite| = |C2| - |D2|
-        assert len(res.crit[1]) - 7 == len(res.crit[2]) - len(res.dtop) == 5
+    assert [len(c) for c in res.crit] == g["crit_counts"]
+    fin = sorted((float(p["birth_value"]), float(p["death_value"])) for p in res.d0 if p["death_id"] >= 0)
+    assert fin == [tuple(x) for x in g["d0_finite"]]
+    assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.dtop] == [tuple(x) for x in g["dtop"]]
+    if d == 3:  # |D1| = |C1| - |D0 finite| = |C2| - |D2|
+        assert len(res.crit[1]) - len(fin) == len(res.crit[2]) - len(res.dtop) == g["d1_count"]
     inf = [p for p in res.d0 if p["death_id"] < 0]
     assert len(inf) == 1 and float(inf[0]["birth_value"]) == -4.0 * d and float(inf[0]["death_value"]) == 0.0
 
 
 @pytest.mark.parametrize("d", [2, 3])
 def test_bowl(d):
+    g = golden("paraboloids.json")["bowl"][str(d)]
     f = sqdist_field((5,) * d, +1)
     res = oracle.run(f)
-    assert [len(c) for c in res.crit] == [1] + [0] * d
+    assert [len(c) for c in res.crit] == g["crit_counts"]
     assert len(res.dtop) == 0
-    assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.d0] == [(0.0, 4.0 * d)]
+    assert [(float(p["birth_value"]), float(p["death_value"])) for p in res.d0] == [tuple(x) for x in g["d0"]]
 
 
 # ------------------------------------------------------------------ O5 / O6 vs brute force
