@@ -741,24 +741,24 @@ dms_status dtop_finish(dms_ctx* c) {
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
-    s = emit_unpaired(c, 1, u, m, crit_ids(c, d - 1), 1);
-    if (s) return s;
-    const int64_t ninf = d == 1 ? c->nunp[1] : 0;  // Sec. 6: in 1D the unpaired minimum is infinite
-    if (np + ninf + 1 > c->cap_pairs[1]) {
+    // pairs first (their positions are in the scan buffers), then the unpaired list
+    // (which rescans); in 1D the unpaired minima (<= m - np) follow the pairs as infinite
+    // classes
+    const int64_t need = (d == 1 ? m : np) + 1;
+    if (need > c->cap_pairs[1]) {
         cudaFree(c->pairs[1]);
         c->pairs[1] = nullptr;
-        CU(dalloc(&c->pairs[1], 2 * (np + ninf) + 1024));
-        c->cap_pairs[1] = 2 * (np + ninf) + 1024;
+        CU(dalloc(&c->pairs[1], 2 * need + 1024));
+        c->cap_pairs[1] = 2 * need + 1024;
     }
     if (np) {
-        // recompute the pair positions (emit_unpaired reused the scan buffers)
-        int64_t np2 = 0;
-        s = flag_scan(c, u, m, 0, &np2);
-        if (s) return s;
         k_emit_dtop<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, d - 1),
                                                       crit_ids_emitted(c, d), c->pairs[1]);
         c->launches++;
     }
+    s = emit_unpaired(c, 1, u, m, crit_ids(c, d - 1), 1);
+    if (s) return s;
+    const int64_t ninf = d == 1 ? c->nunp[1] : 0;  // Sec. 6: in 1D the unpaired minimum is infinite
     for (int64_t i = 0; i < ninf; i++) {
         k_emit_inf_k<<<1, 32, 0, c->st>>>(g, 0, c->unp[1] + i, c->kmax, c->pairs[1] + np + i);
         c->launches++;
