@@ -31,6 +31,7 @@ struct Geo3 {
     const void* grad;
     const StarTab* tab;
     const ChaseTab* ctab;  // dual-chase transitions
+    const unsigned long long* cw;  // 3D, optional: chase word per vertex = tet codes | lower mask << 48
 };
 
 __device__ __forceinline__ int64_t lin_mask(const Geo3& g, int m) {
@@ -194,10 +195,19 @@ struct ChaseState {
     uint64_t w;  // x's gradient word (3D: hi half; 2D: the uint16)
 };
 
+// 3D with chase words: w = tet codes (bits 0-47) | lower mask (bits 48-61), so a hop that
+// stays in St^-(x) reads nothing and a climb reads one 8-byte word.  Otherwise w = the
+// gradient word (3D hi half, tet codes at bit 8; 2D the uint16).
 template <int D>
 __device__ __forceinline__ uint64_t load_w(const Geo3& g, uint32_t x) {
+    if (D == 3 && g.cw) return __ldg(g.cw + x);
     if (D == 3) return __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * (uint64_t)x + 1);
     return __ldg(reinterpret_cast<const uint16_t*>(g.grad) + x);
+}
+template <int D>
+__device__ __forceinline__ int top_code(const Geo3& g, uint64_t w, int T) {
+    if (D == 3) return (int)((w >> ((g.cw ? 0 : 8) + 2 * T)) & 3ull);
+    return (int)((w >> (3 + 2 * T)) & 3ull);
 }
 
 // one hop; returns -2 to continue, else the end node (a maximum's node or vnode)
@@ -206,7 +216,7 @@ __device__ __forceinline__ int32_t chase_step(const Geo3& g, const StarTab& S, C
                                               const int32_t* node_of, int32_t vnode) {
     constexpr int NE = D == 3 ? 14 : 6;
     const int T = c.T;
-    const int code = D == 3 ? (int)((c.w >> (8 + 2 * T)) & 3ull) : (int)((c.w >> (3 + 2 * T)) & 3ull);
+    const int code = top_code<D>(g, c.w, T);
     if (code == 0) {  // a critical top cell: a maximum
         int64_t id;
         if (D == 3)
@@ -223,8 +233,15 @@ __device__ __forceinline__ int32_t chase_step(const Geo3& g, const StarTab& S, C
     const int nx = c.cx + S.off[s2][0], ny = c.cy + S.off[s2][1], nz = c.cz + S.off[s2][2];
     if (!in_grid(g, nx, ny, nz)) return vnode;  // s' on the boundary: the virtual maximum
     const uint32_t n2 = c.x + (uint32_t)S.lin[s2];
-    const uint32_t on = ord_of(__ldg(g.f + n2));
-    if (nb_lower(on, c.ox, s2, NE)) {
+    bool stay;
+    uint32_t on = 0;
+    if (D == 3 && g.cw) {
+        stay = (c.w >> (48 + s2)) & 1ull;  // s2 in x's lower mask
+    } else {
+        on = ord_of(__ldg(g.f + n2));
+        stay = nb_lower(on, c.ox, s2, NE);
+    }
+    if (stay) {
         c.T = T2;  // the other cofacet of s' is still in St^-(x)
     } else {       // it climbs to n2
         c.T = (int)(e >> 16);
@@ -274,8 +291,17 @@ __device__ __forceinline__ int32_t chase_start(const Geo3& g, const StarTab& S, 
     const int nx = cx + S.off[s3][0], ny = cy + S.off[s3][1], nz = cz + S.off[s3][2];
     if (!in_grid(g, nx, ny, nz)) return vnode;
     const uint32_t n3 = x + (uint32_t)S.lin[s3];
-    const uint32_t on = ord_of(__ldg(g.f + n3));
-    if (nb_lower(on, ox, s3, NE)) {
+    bool stay;
+    uint32_t on = 0;
+    uint64_t wx = 0;
+    if (D == 3 && g.cw) {
+        wx = __ldg(g.cw + x);
+        stay = (wx >> (48 + s3)) & 1ull;
+    } else {
+        on = ord_of(__ldg(g.f + n3));
+        stay = nb_lower(on, ox, s3, NE);
+    }
+    if (stay) {
         c.x = x; c.ox = ox; c.T = T; c.cx = cx; c.cy = cy; c.cz = cz;
     } else {
         int jj;
@@ -284,7 +310,7 @@ __device__ __forceinline__ int32_t chase_start(const Geo3& g, const StarTab& S, 
         c.T = D == 3 ? S.q_reslot[T][jj] : S.t_reslot[T][jj];
         c.x = n3; c.ox = on; c.cx = nx; c.cy = ny; c.cz = nz;
     }
-    c.w = load_w<D>(g, c.x);
+    c.w = (D == 3 && g.cw && c.x == x) ? wx : load_w<D>(g, c.x);
     return -2;
 }
 

@@ -119,6 +119,7 @@ struct dms_ctx {
     int* tile_ctr = nullptr;
     uint32_t* chase_mark = nullptr;  // D_{d-1} chase stamps, one per top cell
     uint32_t* lut2 = nullptr;        // 2D: ProcessLowerStars result per star pattern
+    unsigned long long* cw = nullptr;  // 3D: chase words (tet codes | lower mask << 48)
     int sms = 148;                   // multiprocessors of the context's device
     Lut2Off lut2off;
     uint32_t chase_gen = 0;
@@ -242,6 +243,7 @@ Geo3 geo(const dms_ctx* c) {
     g.grad = c->grad;
     g.tab = c->dtab;
     g.ctab = c->dctab;
+    g.cw = c->cw;
     return g;
 }
 
@@ -386,6 +388,7 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     }
     A.totals = c->totals;
     A.err = c->err;
+    A.cw = c->cw;
     StageTimer tm(c, 5);
     if (c->ndim >= 2) {
         static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
@@ -907,6 +910,10 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    {  // 3D: the dual chases read one packed word per vertex (DMS_CHASEWORD=0: the gradient words)
+        static const int cw_env = getenv("DMS_CHASEWORD") ? atoi(getenv("DMS_CHASEWORD")) : 1;
+        if (ndim == 3 && cw_env) CA(dalloc(&c->cw, N));
+    }
     if (ndim == 2) {  // 2D: the ProcessLowerStars table of all 1957 star patterns
         int acc = 0;
         for (int L = 0; L < 64; L++) {
@@ -1223,6 +1230,7 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->tile_ctr);
     cudaFree(c->chase_mark);
     cudaFree(c->lut2);
+    cudaFree(c->cw);
     cudaFree(c->totals);
     cudaFree(c->err);
     cudaFree(c->kmax);

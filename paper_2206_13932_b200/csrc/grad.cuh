@@ -57,6 +57,7 @@ struct GradArgs {
     int64_t cap[4];
     int64_t ncell[4];
     unsigned long long* totals;  // [4], zeroed: running record counts
+    unsigned long long* cw;      // 3D, optional: chase words (tet codes | lower mask << 48)
     int* err;                    // bit 0: NaN seen
 };
 
@@ -523,6 +524,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
                 const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
                 reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
+                if (A.cw) A.cw[v] = st.qcode | ((uint64_t)st.Le << 48);
             } else {
                 const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
                 reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
