@@ -32,6 +32,7 @@ struct Geo3 {
     const StarTab* tab;
     const ChaseTab* ctab;  // dual-chase transitions
     const unsigned long long* cw;  // 3D, optional: chase word per vertex = tet codes | lower mask << 48
+    const uint32_t* cw2;           // 2D, optional: chase word = triangle codes | lower mask << 12
 };
 
 __device__ __forceinline__ int64_t lin_mask(const Geo3& g, int m) {
@@ -202,12 +203,22 @@ template <int D>
 __device__ __forceinline__ uint64_t load_w(const Geo3& g, uint32_t x) {
     if (D == 3 && g.cw) return __ldg(g.cw + x);
     if (D == 3) return __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * (uint64_t)x + 1);
+    if (g.cw2) return __ldg(g.cw2 + x);
     return __ldg(reinterpret_cast<const uint16_t*>(g.grad) + x);
 }
 template <int D>
 __device__ __forceinline__ int top_code(const Geo3& g, uint64_t w, int T) {
     if (D == 3) return (int)((w >> ((g.cw ? 0 : 8) + 2 * T)) & 3ull);
-    return (int)((w >> (3 + 2 * T)) & 3ull);
+    return (int)((w >> ((g.cw2 ? 0 : 3) + 2 * T)) & 3ull);
+}
+// chase word present: is neighbour slot s in the lower mask of the word's vertex
+template <int D>
+__device__ __forceinline__ bool has_cw(const Geo3& g) {
+    return D == 3 ? g.cw != nullptr : g.cw2 != nullptr;
+}
+template <int D>
+__device__ __forceinline__ bool cw_lower(uint64_t w, int s) {
+    return (w >> ((D == 3 ? 48 : 12) + s)) & 1ull;
 }
 
 // one hop; returns -2 to continue, else the end node (a maximum's node or vnode)
@@ -235,8 +246,8 @@ __device__ __forceinline__ int32_t chase_step(const Geo3& g, const StarTab& S, C
     const uint32_t n2 = c.x + (uint32_t)S.lin[s2];
     bool stay;
     uint32_t on = 0;
-    if (D == 3 && g.cw) {
-        stay = (c.w >> (48 + s2)) & 1ull;  // s2 in x's lower mask
+    if (has_cw<D>(g)) {
+        stay = cw_lower<D>(c.w, s2);  // s2 in x's lower mask
     } else {
         on = ord_of(__ldg(g.f + n2));
         stay = nb_lower(on, c.ox, s2, NE);
@@ -294,9 +305,9 @@ __device__ __forceinline__ int32_t chase_start(const Geo3& g, const StarTab& S, 
     bool stay;
     uint32_t on = 0;
     uint64_t wx = 0;
-    if (D == 3 && g.cw) {
-        wx = __ldg(g.cw + x);
-        stay = (wx >> (48 + s3)) & 1ull;
+    if (has_cw<D>(g)) {
+        wx = load_w<D>(g, x);
+        stay = cw_lower<D>(wx, s3);
     } else {
         on = ord_of(__ldg(g.f + n3));
         stay = nb_lower(on, ox, s3, NE);
@@ -310,7 +321,7 @@ __device__ __forceinline__ int32_t chase_start(const Geo3& g, const StarTab& S, 
         c.T = D == 3 ? S.q_reslot[T][jj] : S.t_reslot[T][jj];
         c.x = n3; c.ox = on; c.cx = nx; c.cy = ny; c.cz = nz;
     }
-    c.w = (D == 3 && g.cw && c.x == x) ? wx : load_w<D>(g, c.x);
+    c.w = (has_cw<D>(g) && c.x == x) ? wx : load_w<D>(g, c.x);
     return -2;
 }
 
