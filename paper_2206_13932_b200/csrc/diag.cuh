@@ -33,6 +33,7 @@ struct Geo3 {
     const ChaseTab* ctab;  // dual-chase transitions
     const unsigned long long* cw;  // 3D, optional: chase word per vertex = tet codes | lower mask << 48
     const uint32_t* cw2;           // 2D, optional: chase word = triangle codes | lower mask << 12
+    const uint8_t* vc;             // 2D / 3D, optional: vertex codes (the D0 descent), 1 byte each
 };
 
 __device__ __forceinline__ int64_t lin_mask(const Geo3& g, int m) {
@@ -46,6 +47,10 @@ __device__ __forceinline__ bool kless_v(const Geo3& g, int64_t u, int64_t v) {
 
 // vertex code of v (edge slot paired with v), -1 if v is a minimum
 __device__ __forceinline__ int vcode_of(const Geo3& g, int64_t v) {
+    if (g.vc) {  // compact copy: 8-16x denser than the gradient words
+        const int c = (int)__ldg(g.vc + v);
+        return c == (g.ndim == 3 ? 15 : 7) ? -1 : c;
+    }
     if (g.ndim == 3) {
         int c = (int)((__ldg(reinterpret_cast<const uint32_t*>(g.grad) + 4 * v + 3) >> 24) & 15u);
         return c == 15 ? -1 : c;

@@ -121,6 +121,7 @@ struct dms_ctx {
     uint32_t* lut2 = nullptr;        // 2D: ProcessLowerStars result per star pattern
     unsigned long long* cw = nullptr;  // 3D: chase words (tet codes | lower mask << 48)
     uint32_t* cw2 = nullptr;           // 2D: chase words (triangle codes | lower mask << 12)
+    uint8_t* vc = nullptr;             // 2D / 3D: vertex codes (D0 descent)
     int sms = 148;                   // multiprocessors of the context's device
     Lut2Off lut2off;
     uint32_t chase_gen = 0;
@@ -246,6 +247,7 @@ Geo3 geo(const dms_ctx* c) {
     g.ctab = c->dctab;
     g.cw = c->cw;
     g.cw2 = c->cw2;
+    g.vc = c->vc;
     return g;
 }
 
@@ -392,6 +394,7 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     A.err = c->err;
     A.cw = c->cw;
     A.cw2 = c->cw2;
+    A.vc = c->vc;
     StageTimer tm(c, 5);
     if (c->ndim >= 2) {
         static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
@@ -917,6 +920,8 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
         static const int cw_env = getenv("DMS_CHASEWORD") ? atoi(getenv("DMS_CHASEWORD")) : 1;
         if (ndim == 3 && cw_env) CA(dalloc(&c->cw, N));
         if (ndim == 2 && cw_env) CA(dalloc(&c->cw2, N));
+        static const int vc_env = getenv("DMS_VCODES") ? atoi(getenv("DMS_VCODES")) : 1;
+        if (ndim >= 2 && vc_env) CA(dalloc(&c->vc, N));
     }
     if (ndim == 2) {  // 2D: the ProcessLowerStars table of all 1957 star patterns
         int acc = 0;
@@ -1236,6 +1241,7 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->lut2);
     cudaFree(c->cw);
     cudaFree(c->cw2);
+    cudaFree(c->vc);
     cudaFree(c->totals);
     cudaFree(c->err);
     cudaFree(c->kmax);

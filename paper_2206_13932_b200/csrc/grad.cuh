@@ -59,6 +59,7 @@ struct GradArgs {
     unsigned long long* totals;  // [4], zeroed: running record counts
     unsigned long long* cw;      // 3D, optional: chase words (tet codes | lower mask << 48)
     uint32_t* cw2;               // 2D, optional: chase words (triangle codes | lower mask << 12)
+    uint8_t* vc;                 // 2D / 3D, optional: vertex codes (15 / 7 = minimum), for the D0 descent
     int* err;                    // bit 0: NaN seen
 };
 
@@ -526,10 +527,12 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
                 reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
                 if (A.cw) A.cw[v] = st.qcode | ((uint64_t)st.Le << 48);
+                if (A.vc) A.vc[v] = (uint8_t)vc;
             } else {
                 const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
                 reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));
                 if (A.cw2) A.cw2[v] = ((uint32_t)st.tcode_lo & 0xfffu) | (st.Le << 12);
+                if (A.vc) A.vc[v] = (uint8_t)vc;
             }
         }
         const uint32_t c0 = crit_v ? 1u : 0u, c1 = __popc(st.crit_e), c2 = __popcll(st.crit_t), c3 = __popc(st.crit_q);
@@ -757,6 +760,7 @@ __global__ void __launch_bounds__(kBlock) k_gradient_lut2(GradArgs A, const uint
             e = s_lut[idx];
             reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(e & 0x7fffu);
             if (A.cw2) A.cw2[v] = ((e >> 3) & 0xfffu) | (Le << 12);
+            if (A.vc) A.vc[v] = (uint8_t)(e & 7u);
         }
         const bool crit_v = active && Le == 0;
         const uint32_t crit_e = (e >> 16) & 63u, crit_t = (e >> 22) & 63u;
