@@ -813,4 +813,15 @@ __global__ void k_emit_unpaired(const int32_t* out, int64_t m, const uint32_t* p
     list[rev ? n - 1 - pos[j] : pos[j]] = id;
 }
 
+// same, with the count taken on the device (n = exclusive-scan end + last flag), so the
+// host does not wait for it
+__global__ void k_emit_unpaired_dev(const int32_t* out, int64_t m, const uint32_t* pos, const uint32_t* flags,
+                                    const int64_t* ids, int64_t* list, int rev) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m || out[j] != -1) return;
+    const int64_t n = (int64_t)__ldg(pos + m - 1) + __ldg(flags + m - 1);
+    const int64_t id = rev ? ids[m - 1 - j] : ids[j];
+    list[rev ? n - 1 - pos[j] : pos[j]] = id;
+}
+
 }  // namespace dms

@@ -58,6 +58,7 @@ struct UFBuf {
     int32_t* age = nullptr;                     // per node (emission order)
     int* nlive = nullptr;  // two device counters
     int* h_status = nullptr;  // pinned: the union-find's convergence status
+    uint32_t* h_cnt = nullptr;  // pinned: last scan position + last flag (unpaired count)
     int* trace = nullptr;  // [64] union-find round trace
     int32_t* parent = nullptr;
     unsigned long long* best = nullptr;
@@ -137,6 +138,7 @@ struct dms_ctx {
     int64_t npairs[2] = {0, 0};
     int64_t* unp[2] = {nullptr, nullptr};
     int64_t nunp[2] = {0, 0};
+    bool nunp_async[2] = {false, false};  // nunp still in the pinned slot of uf[which]
     int64_t cap_pairs[2] = {0, 0}, cap_unp[2] = {0, 0};  // grow-only result buffers
     // state
     bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
@@ -288,6 +290,7 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
         }
         if (!u.nlive) CU(dalloc(&u.nlive, 8));
         if (!u.h_status && cudaMallocHost(&u.h_status, sizeof(int)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
+        if (!u.h_cnt && cudaMallocHost(&u.h_cnt, 2 * sizeof(uint32_t)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
         if (!u.trace) CU(dalloc(&u.trace, 128 + 128));
         for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
         u.cap_arcs = arcs;
@@ -576,7 +579,28 @@ dms_status flag_scan(dms_ctx* c, UFBuf& u, int64_t m, int want_unpaired, int64_t
     return DMS_OK;
 }
 
-dms_status emit_unpaired(dms_ctx* c, int which, UFBuf& u, int64_t m, const int64_t* ids, int rev) {
+// async: the count stays on the device (read after the next synchronisation, see
+// unpaired_count), so the host does not wait here
+dms_status emit_unpaired(dms_ctx* c, int which, UFBuf& u, int64_t m, const int64_t* ids, int rev,
+                         bool async = false) {
+    c->nunp_async[which] = false;
+    if (async && m > 0) {
+        k_flag_ge0<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags, 1);
+        c->launches++;
+        scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
+        if (m + 1 > c->cap_unp[which]) {  // grow only: capacity for every arc
+            cudaFree(c->unp[which]);
+            c->unp[which] = nullptr;
+            CU(dalloc(&c->unp[which], 2 * m + 1024));
+            c->cap_unp[which] = 2 * m + 1024;
+        }
+        k_emit_unpaired_dev<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.pos, u.flags, ids, c->unp[which], rev);
+        c->launches++;
+        CU(cudaMemcpyAsync(&u.h_cnt[0], u.pos + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaMemcpyAsync(&u.h_cnt[1], u.flags + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+        c->nunp_async[which] = true;
+        return DMS_OK;
+    }
     int64_t n = 0;
     dms_status s = flag_scan(c, u, m, 1, &n);
     if (s) return s;
@@ -659,7 +683,7 @@ dms_status d0_finish(dms_ctx* c) {
     k_emit_inf_k<<<1, 32, 0, c->st>>>(g, 0, crit_ids(c, 0), c->kmax, c->pairs[0] + np);
     c->launches++;
     c->npairs[0] = np + 1;
-    s = emit_unpaired(c, 0, u, m, crit_ids(c, 1), 0);
+    s = emit_unpaired(c, 0, u, m, crit_ids(c, 1), 0, true);
     if (s) return s;
     CU(cudaGetLastError());
     stage_end(c, 3, c->t_diag[0]);
@@ -765,7 +789,7 @@ dms_status dtop_finish(dms_ctx* c) {
                                                       crit_ids_emitted(c, d), c->pairs[1]);
         c->launches++;
     }
-    s = emit_unpaired(c, 1, u, m, crit_ids(c, d - 1), 1);
+    s = emit_unpaired(c, 1, u, m, crit_ids(c, d - 1), 1, d >= 2);  // 1D needs the count here
     if (s) return s;
     const int64_t ninf = d == 1 ? c->nunp[1] : 0;  // Sec. 6: in 1D the unpaired minimum is infinite
     for (int64_t i = 0; i < ninf; i++) {
@@ -1006,6 +1030,15 @@ dms_status dms_diagram_top(dms_ctx* c, int mode, const dms_pair** d_pairs, int64
     return DMS_OK;
 }
 
+// the unpaired count, after the caller's stream has been synchronised
+static int64_t unpaired_count(dms_ctx* c, int which) {
+    if (c->nunp_async[which]) {
+        c->nunp[which] = (int64_t)c->uf[which].h_cnt[0] + c->uf[which].h_cnt[1];
+        c->nunp_async[which] = false;
+    }
+    return c->nunp[which];
+}
+
 dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, int64_t* h_n) {
     dms_status s = check_sticky(c);
     if (s) return s;
@@ -1016,7 +1049,7 @@ dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, in
     }
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
     *d_ids = c->unp[which];
-    *h_n = c->nunp[which];
+    *h_n = unpaired_count(c, which);
     return DMS_OK;
 }
 
@@ -1257,6 +1290,7 @@ void dms_destroy(dms_ctx* c) {
                         (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
             cudaFree(p);
         if (u.h_status) cudaFreeHost(u.h_status);
+        if (u.h_cnt) cudaFreeHost(u.h_cnt);
         cudaFree(c->pairs[b]);
         cudaFree(c->unp[b]);
     }
