@@ -48,6 +48,24 @@ __global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsig
     *slot = r;
 }
 
+// the infinite class with its slot after the np finite pairs, np read on the device from
+// the pair scan (np = scan end + last flag)
+__global__ void k_emit_inf_dev(Geo3 g, int dim, const int64_t* id_ptr, const unsigned long long* kmax, PairRec* base,
+                               const uint32_t* pos, const uint32_t* flags, int64_t m) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t np = (int64_t)pos[m - 1] + flags[m - 1];
+    const StarTab& S = *g.tab;
+    PairRec r;
+    r.birth_id = *id_ptr;
+    const int64_t bv = max_vertex(g, S, dim, r.birth_id);
+    r.birth_vertex = (int32_t)bv;
+    r.birth_value = g.f[bv];
+    r.death_id = -1;
+    r.death_vertex = -1;
+    r.death_value = g.f[(int64_t)(*kmax & 0xffffffffull)];
+    base[np] = r;
+}
+
 struct UFBuf {
     int32_t *arc_a = nullptr, *arc_b = nullptr, *out = nullptr, *list = nullptr;
     int4 *rec0 = nullptr, *rec1 = nullptr;  // union-find live arc records
@@ -58,7 +76,8 @@ struct UFBuf {
     int32_t* age = nullptr;                     // per node (emission order)
     int* nlive = nullptr;  // two device counters
     int* h_status = nullptr;  // pinned: the union-find's convergence status
-    uint32_t* h_cnt = nullptr;  // pinned: last scan position + last flag (unpaired count)
+    uint32_t* h_cnt = nullptr;  // pinned: [0..1] last scan position + last flag of the unpaired
+                                //   scan, [2..3] the same for the pair scan
     int* trace = nullptr;  // [64] union-find round trace
     int32_t* parent = nullptr;
     unsigned long long* best = nullptr;
@@ -139,6 +158,7 @@ struct dms_ctx {
     int64_t* unp[2] = {nullptr, nullptr};
     int64_t nunp[2] = {0, 0};
     bool nunp_async[2] = {false, false};  // nunp still in the pinned slot of uf[which]
+    int npairs_async[2] = {0, 0};         // > 0: npairs = pinned pair count + (this - 1) infinite records
     int64_t cap_pairs[2] = {0, 0}, cap_unp[2] = {0, 0};  // grow-only result buffers
     // state
     bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
@@ -290,7 +310,7 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
         }
         if (!u.nlive) CU(dalloc(&u.nlive, 8));
         if (!u.h_status && cudaMallocHost(&u.h_status, sizeof(int)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
-        if (!u.h_cnt && cudaMallocHost(&u.h_cnt, 2 * sizeof(uint32_t)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
+        if (!u.h_cnt && cudaMallocHost(&u.h_cnt, 4 * sizeof(uint32_t)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
         if (!u.trace) CU(dalloc(&u.trace, 128 + 128));
         for (uint32_t** p : {&u.flags, &u.pos}) { cudaFree(*p); CU(dalloc(p, arcs)); }
         u.cap_arcs = arcs;
@@ -665,6 +685,33 @@ dms_status d0_finish(dms_ctx* c) {
     dms_status s = uf_finish(c, u, m);
     if (s) return s;
     out_to_processing(c, u, 1, m, 0);
+    c->npairs_async[0] = 0;
+    if (m > 0) {  // no host wait: pair count read on the device, and by the host after the next sync
+        k_flag_ge0<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags, 0);
+        c->launches++;
+        scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
+        if (m + 1 > c->cap_pairs[0]) {
+            cudaFree(c->pairs[0]);
+            c->pairs[0] = nullptr;
+            CU(dalloc(&c->pairs[0], 2 * m + 1024));
+            c->cap_pairs[0] = 2 * m + 1024;
+        }
+        k_emit_d0<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids_emitted(c, 0), crit_ids(c, 1),
+                                                    c->pairs[0]);
+        // Sec. 6: the global minimum (the oldest node, first of C_0) never dies
+        k_emit_inf_dev<<<1, 32, 0, c->st>>>(g, 0, crit_ids(c, 0), c->kmax, c->pairs[0], u.pos, u.flags, m);
+        c->launches += 2;
+        CU(cudaMemcpyAsync(&u.h_cnt[2], u.pos + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaMemcpyAsync(&u.h_cnt[3], u.flags + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+        c->npairs_async[0] = 2;  // np + the infinite class
+        s = emit_unpaired(c, 0, u, m, crit_ids(c, 1), 0, true);
+        if (s) return s;
+        CU(cudaGetLastError());
+        stage_end(c, 3, c->t_diag[0]);
+        c->t_diag[0] = nullptr;
+        c->have_d[0] = true;
+        return DMS_OK;
+    }
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
@@ -771,6 +818,31 @@ dms_status dtop_finish(dms_ctx* c) {
     dms_status s = uf_finish(c, u, m);
     if (s) return s;
     out_to_processing(c, u, d - 1, m, 1);
+    c->npairs_async[1] = 0;
+    if (d >= 2 && m > 0) {  // no host wait (no infinite records for d >= 2, Sec. 6)
+        k_flag_ge0<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, u.flags, 0);
+        c->launches++;
+        scan_excl(u.flags, u.pos, m, c->ss, c->st, &c->launches);
+        if (m + 1 > c->cap_pairs[1]) {
+            cudaFree(c->pairs[1]);
+            c->pairs[1] = nullptr;
+            CU(dalloc(&c->pairs[1], 2 * m + 1024));
+            c->cap_pairs[1] = 2 * m + 1024;
+        }
+        k_emit_dtop<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, d - 1),
+                                                      crit_ids_emitted(c, d), c->pairs[1]);
+        c->launches++;
+        CU(cudaMemcpyAsync(&u.h_cnt[2], u.pos + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaMemcpyAsync(&u.h_cnt[3], u.flags + (m - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+        c->npairs_async[1] = 1;  // np, no infinite records
+        s = emit_unpaired(c, 1, u, m, crit_ids(c, d - 1), 1, true);
+        if (s) return s;
+        CU(cudaGetLastError());
+        stage_end(c, 4, c->t_diag[1]);
+        c->t_diag[1] = nullptr;
+        c->have_d[1] = true;
+        return DMS_OK;
+    }
     int64_t np = 0;
     s = flag_scan(c, u, m, 0, &np);
     if (s) return s;
@@ -855,6 +927,24 @@ dms_status run_diagrams(dms_ctx* c) {
 }
 
 }  // namespace
+
+// counts left on the device by the asynchronous emissions, read once the caller's stream
+// has been synchronised
+static int64_t pair_count(dms_ctx* c, int which) {
+    if (c->npairs_async[which] > 0) {
+        c->npairs[which] = (int64_t)c->uf[which].h_cnt[2] + c->uf[which].h_cnt[3] + c->npairs_async[which] - 1;
+        c->npairs_async[which] = 0;
+    }
+    return c->npairs[which];
+}
+
+static int64_t unpaired_count(dms_ctx* c, int which) {
+    if (c->nunp_async[which]) {
+        c->nunp[which] = (int64_t)c->uf[which].h_cnt[0] + c->uf[which].h_cnt[1];
+        c->nunp_async[which] = false;
+    }
+    return c->nunp[which];
+}
 
 // ====================================================================== C ABI
 
@@ -1010,7 +1100,7 @@ dms_status dms_diagram0(dms_ctx* c, const dms_pair** d_pairs, int64_t* h_n) {
     }
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
     *d_pairs = reinterpret_cast<const dms_pair*>(c->pairs[0]);
-    *h_n = c->npairs[0];
+    *h_n = pair_count(c, 0);
     return DMS_OK;
 }
 
@@ -1026,19 +1116,11 @@ dms_status dms_diagram_top(dms_ctx* c, int mode, const dms_pair** d_pairs, int64
     }
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
     *d_pairs = reinterpret_cast<const dms_pair*>(c->pairs[1]);
-    *h_n = c->npairs[1];
+    *h_n = pair_count(c, 1);
     return DMS_OK;
 }
 
 // the unpaired count, after the caller's stream has been synchronised
-static int64_t unpaired_count(dms_ctx* c, int which) {
-    if (c->nunp_async[which]) {
-        c->nunp[which] = (int64_t)c->uf[which].h_cnt[0] + c->uf[which].h_cnt[1];
-        c->nunp_async[which] = false;
-    }
-    return c->nunp[which];
-}
-
 dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, int64_t* h_n) {
     dms_status s = check_sticky(c);
     if (s) return s;
