@@ -38,7 +38,8 @@
  *
  * Synchronisation and threads
  *   Only calls returning host counts (h_count, h_n) synchronise the stream (and
- *   dms_run_all / dms_run_all_host, which read the critical and pair counts).  The
+ *   dms_run_all / dms_run_all_host, which wait for the critical counts and for each
+ *   union-find's convergence flag).  The
  *   library also uses two internal streams of its own (the vertex order; D0 beside
  *   D_{d-1}); their work is joined into the caller's stream before a call returns.
  *   A context is not thread-safe: calls on one context must not overlap; distinct
