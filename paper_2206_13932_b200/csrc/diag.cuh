@@ -742,7 +742,7 @@ __global__ void k_uf_tail(const int32_t* __restrict__ arc_a, const int32_t* __re
 
 // ---------------------------------------------------------------- emission
 
-struct PairRec {
+struct alignas(16) PairRec {  // 32 B, two 16-byte stores per record
     int64_t birth_id, death_id;
     int32_t birth_vertex, death_vertex;
     float birth_value, death_value;

@@ -422,8 +422,11 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     if (c->ndim >= 2) {
         static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
         // 3D: pools of 8 x 128 vertices per CTA, expanded in work order
+        // DMS_GRAD_PAD: unused dynamic shared memory per 3D gradient CTA (bytes), to leave
+        // SM room for the order's kernels beside it (A/B knob, default 0)
+        static const int pad_env = getenv("DMS_GRAD_PAD") ? atoi(getenv("DMS_GRAD_PAD")) : 0;
         if (c->ndim == 3)
-            k_gradient_pool<3, 8><<<(unsigned)ceil_div(v1 - v0, 8 * kBlockG), kBlockG, 0, c->st>>>(A);
+            k_gradient_pool<3, 8><<<(unsigned)ceil_div(v1 - v0, 8 * kBlockG), kBlockG, (size_t)pad_env, c->st>>>(A);
         else if (c->lut2 && lut_env)
             k_gradient_lut2<<<(unsigned)std::min<int64_t>(ceil_div(v1 - v0, kBlock), c->sms * 8), kBlock, 0, c->st>>>(
                 A, c->lut2, c->lut2off);
