@@ -120,6 +120,14 @@ __global__ void k_gather_keys(const int32_t* __restrict__ list, int64_t n, const
     if (j < n) out[j] = key[list[j]];
 }
 
+// keys that sort on the rank bits alone (one cell per star): the 32-bit rank of the
+// highest vertex (keys are x << 12 | G before the rekey)
+__global__ void k_rekey32(const uint64_t* __restrict__ keys, int64_t m, const int32_t* __restrict__ rank,
+                          uint32_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) out[i] = (uint32_t)rank[keys[i] >> 12];
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) a[i] = (uint32_t)i;

@@ -482,9 +482,24 @@ dms_status run_critical(dms_ctx* c) {
     }
     for (int k = 0; k <= c->ndim; k++) c->ncrit[k] = (int64_t)tot[k];
     const int kbits = 12 + bits_for(c->N);
+    static const int k32_env = getenv("DMS_CRIT_KEY32") ? atoi(getenv("DMS_CRIT_KEY32")) : 1;
     for (int k = 0; k <= c->ndim; k++) {
-        k_rekey<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->ckey[0][k], c->ncrit[k], c->rank);
         k_iota<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cidx[0][k], c->ncrit[k]);
+        c->launches++;
+        if ((k == 0 || c->ndim == 1) && k32_env) {
+            // one cell per star (see below): sort 32-bit ranks, half the key bytes per pass;
+            // the keys go to the second buffer (ka), the first one is the ping-pong buffer
+            uint32_t* ka = reinterpret_cast<uint32_t*>(c->ckey[1][k]);
+            uint32_t* kb = reinterpret_cast<uint32_t*>(c->ckey[0][k]);
+            k_rekey32<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->ckey[0][k], c->ncrit[k], c->rank, ka);
+            c->cur[k] = radix_sort<uint32_t, uint32_t, DMS_ORDER_ITEMS>(ka, c->cidx[0][k], kb, c->cidx[1][k], c->ncrit[k], 0,
+                                                                        bits_for(c->N), c->ss, c->st, &c->launches);
+            k_gather_ids<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cid[0][k], crit_perm(c, k), c->ncrit[k],
+                                                                     c->cid[1][k]);
+            c->launches += 2;
+            continue;
+        }
+        k_rekey<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->ckey[0][k], c->ncrit[k], c->rank);
         c->launches++;
         // the low 12 bits (G) only order cells of one star: C_0 holds at most one cell per
         // star (x itself), and in 1D so does C_1 (the second lower edge), so their keys
@@ -496,7 +511,7 @@ dms_status run_critical(dms_ctx* c) {
         // lexicographically sorted ids = emitted ids gathered through the permutation
         k_gather_ids<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cid[0][k], crit_perm(c, k), c->ncrit[k],
                                                                  c->cid[1][k]);
-        c->launches += 2;
+        c->launches++;
     }
     CU(cudaGetLastError());
     c->have_crit = true;
