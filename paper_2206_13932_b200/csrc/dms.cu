@@ -342,11 +342,14 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     c->rank = d_rank ? d_rank : c->rank_scratch;
     CU(cudaMemsetAsync(c->kmax, 0, sizeof(unsigned long long), c->st));
     // Beside the (long, ALU-bound) 3D gradient the order's histogram / scatter passes run
-    // on a tile-strided grid of 2 CTAs per SM, leaving the rest of every SM to gradient
+    // on a tile-strided grid of 1-2 CTAs per SM, leaving the rest of every SM to gradient
     // CTAs (c4: 46.6 -> 45.3 ms; in 1D / 2D the order is the longer branch and keeps the
     // full grid).  DMS_ORDER_CTAS overrides (0: full grid).
     static const int octas_env = getenv("DMS_ORDER_CTAS") ? atoi(getenv("DMS_ORDER_CTAS")) : -1;
-    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? 2 : 0);
+    // 1 CTA per SM on large fields, where the gradient runs long enough to hide the slower
+    // order (c4: 2 -> 1 CTA, 44.38 -> 42.62 ms); 2 below 2^25 vertices, where the order
+    // would become the longer branch (c3 9.07 vs 9.11, c2 1.76 vs 1.80 ms)
+    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? (c->N > (1 << 25) ? 1 : 2) : 0);
     const int64_t order_cap = octas > 0 ? (int64_t)c->sms * octas : 0;
     // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
     // (and detects NaN / the highest vertex), the last pass writes rank[index]
