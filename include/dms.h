@@ -94,7 +94,10 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
 
 /* Vertex order (PAPER.md 1368-1372; Sec. 7.1 "global sort"): d_rank[v] = number of
  * vertices u with K(u) < K(v), i.e. a key-value radix sort of (value, index).
- * d_rank: caller-owned device int32[N].  Asynchronous. */
+ * d_rank: caller-owned device int32[N]; it must stay valid until the next
+ * dms_gradient / dms_run_all* call has been synchronised (the critical sort keys read
+ * it).  Clears the context's NaN flag first (the flag describes the current field).
+ * Asynchronous. */
 dms_status dms_order(dms_ctx* ctx, int32_t* d_rank);
 
 /* Bytes of the packed gradient: 3D 16 B/vertex, 2D 2 B/vertex, 1D 1 B/vertex. */
@@ -107,7 +110,10 @@ size_t dms_gradient_bytes(const dms_ctx* ctx);
  * head of a discrete vector, which facet it is paired with (layout: DESIGN.md
  * "Gradient words").  Independent of dms_order (it compares values and indices
  * directly); dms_critical needs both and runs dms_order if it has not run.
- * Asynchronous. */
+ * Each gradient pass consumes the order computed since the previous pass: calling
+ * dms_gradient again without a new dms_order (a changed field) makes the next call
+ * that needs ranks recompute the order into a library-owned buffer.  A gradient pass
+ * not preceded by dms_order clears the NaN flag.  Asynchronous. */
 dms_status dms_gradient(dms_ctx* ctx, void* d_grad);
 
 /* Critical simplices C_0..C_d, each sorted by the lexicographic order (Alg. 2 l. 13,

@@ -161,6 +161,7 @@ struct dms_ctx {
     int npairs_async[2] = {0, 0};         // > 0: npairs = pinned pair count + (this - 1) infinite records
     int64_t cap_pairs[2] = {0, 0}, cap_unp[2] = {0, 0};  // grow-only result buffers
     // state
+    bool order_fresh = false;  // an order computed since the last gradient pass
     bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[10];
@@ -327,6 +328,14 @@ dms_status alloc_uf(dms_ctx* c, UFBuf& u, int64_t arcs, int64_t nodes) {
     return DMS_OK;
 }
 
+// The NaN flag describes the field of the current pass: every entry point that reads f
+// (dms_order, dms_gradient, dms_run_all, dms_run_all_host) clears it on the caller's
+// stream first, so a clean field after a NaN field gives DMS_OK.
+dms_status clear_err(dms_ctx* c) {
+    CU(cudaMemsetAsync(c->err, 0, sizeof(int), c->st));
+    return DMS_OK;
+}
+
 dms_status read_err(dms_ctx* c) {
     int e = 0;
     CU(cudaMemcpyAsync(&e, c->err, sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -366,6 +375,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
                                                         c->st, &c->launches, c->rank, c->f, c->err, c->kmax, order_cap);
     CU(cudaGetLastError());
     c->have_order = true;
+    c->order_fresh = true;
     c->have_crit = c->have_d[0] = c->have_d[1] = false;  // the gradient does not depend on ranks
     return DMS_OK;
 }
@@ -434,7 +444,11 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
         // DMS_GRAD_PAD: unused dynamic shared memory per 3D gradient CTA (bytes), to leave
         // SM room for the order's kernels beside it (A/B knob, default 0)
         static const int pad_env = getenv("DMS_GRAD_PAD") ? atoi(getenv("DMS_GRAD_PAD")) : 0;
-        if (c->ndim == 3)
+        // DMS_GRAD_FAST=0: the queue-driven expansion instead of the closed form (A/B)
+        static const int fast_env = getenv("DMS_GRAD_FAST") ? atoi(getenv("DMS_GRAD_FAST")) : 1;
+        if (c->ndim == 3 && fast_env)
+            k_gradient_pool<3, 8, 1, true><<<(unsigned)ceil_div(v1 - v0, 8 * kBlockG), kBlockG, (size_t)pad_env, c->st>>>(A);
+        else if (c->ndim == 3)
             k_gradient_pool<3, 8><<<(unsigned)ceil_div(v1 - v0, 8 * kBlockG), kBlockG, (size_t)pad_env, c->st>>>(A);
         else if (c->lut2 && lut_env)
             k_gradient_lut2<<<(unsigned)std::min<int64_t>(ceil_div(v1 - v0, kBlock), c->sms * 8), kBlock, 0, c->st>>>(
@@ -449,6 +463,11 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
 }
 
 dms_status run_gradient(dms_ctx* c, void* d_grad) {
+    // each gradient pass consumes the order computed since the previous one; a second
+    // gradient pass without a new dms_order means a new field, so the order (ranks,
+    // f*) is recomputed lazily into the library's own buffer
+    if (!c->order_fresh) c->have_order = false;
+    c->order_fresh = false;
     c->grad = d_grad ? d_grad : c->grad_scratch;
     StageTimer tm(c, 1);
     dms_status s = launch_gradient(c, 0, c->N);
@@ -1091,6 +1110,7 @@ dms_status dms_order(dms_ctx* c, int32_t* d_rank) {
     dms_status s = check_sticky(c);
     if (s) return s;
     if (!d_rank) return DMS_ERR_ARG;
+    if ((s = clear_err(c))) return s;
     return run_order(c, d_rank);
 }
 
@@ -1098,6 +1118,7 @@ dms_status dms_gradient(dms_ctx* c, void* d_grad) {
     dms_status s = check_sticky(c);
     if (s) return s;
     if (!d_grad) return DMS_ERR_ARG;
+    if (!c->order_fresh && (s = clear_err(c))) return s;  // (after dms_order: one flag for the pass)
     return run_gradient(c, d_grad);
 }
 
@@ -1166,6 +1187,7 @@ dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     dms_status s = check_sticky(c);
     if (s) return s;
     static const int oseq_env = getenv("DMS_ORDER_SEQ") ? atoi(getenv("DMS_ORDER_SEQ")) : 0;
+    if ((s = clear_err(c))) return s;
     if ((s = run_order(c, d_rank, !oseq_env))) return s;  // second stream, overlaps the gradient
     if ((s = run_gradient(c, d_grad))) return s;
     if ((s = run_critical(c))) return s;
@@ -1189,6 +1211,7 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
     const int64_t nplanes = c->N / plane;
     int64_t b[kSlabs + 1];
     for (int i = 0; i <= K; i++) b[i] = plane * (nplanes * i / K);
+    if ((s = clear_err(c))) return s;
     CU(cudaEventRecord(c->ev_in, c->st));  // earlier work on the field is done
     CU(cudaStreamWaitEvent(c->st2, c->ev_in, 0));
     float* fdev = const_cast<float*>(c->f);
@@ -1217,6 +1240,7 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
         }
     }
     c->have_grad = true;
+    c->order_fresh = false;
     c->have_crit = c->have_d[0] = c->have_d[1] = false;
     if ((s = run_critical(c))) return s;
     if ((s = run_diagrams(c))) return s;

@@ -330,6 +330,157 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
     }
 }
 
+// ---- ProcessLowerStars in closed form (3D).  DESIGN.md "Gradient (3D)" gives the
+// argument; in short, read St^-(x) as the cone over its lower link L (a subcomplex of
+// the 14-vertex link sphere, Lk^-(x), PAPER.md 1443-1477): star edge (x,u) <-> link
+// vertex u, star triangle (x,u,w) <-> link edge uw, star tet <-> link triangle, x <->
+// the empty cell; the lexicographic keys (PAPER.md 1380-1414) become the keys of L's
+// cells under the local ranks.  Then Robins' queues (Z1) do exactly this:
+//   (1) link vertices are absorbed by Prim's algorithm from the lowest vertex of each
+//       component of L (edge candidates never depend on triangles), so the vertex <->
+//       edge pairs are the unique minimum spanning forest T of L's graph under the keys
+//       (max rank, min rank), each vertex paired with the forest edge towards its
+//       component's lowest vertex; the lowest vertex of every component but the first
+//       is critical (a critical star edge, the canonical rule O3(iv));
+//   (2) the triangles then pair with the non-forest edges by peeling: a triangle with
+//       exactly one unclassified edge takes it (the minimum-key such triangle first --
+//       only the full sphere, an interior maximum, depends on that order); when none
+//       is left, the minimum-key unclassified edge is critical (a hole of L) and
+//       peeling resumes; a triangle left over is critical (the sphere's 2-cycle).
+// Kruskal in key order builds T (union-find over ranks packed in nibbles), a traversal
+// from the component roots orients it.  The result equals process_star() on every
+// star (tests/test_gpu_*: every gradient vector against the oracle).
+__device__ __forceinline__ int nib4(uint64_t P, int i) { return (int)((P >> (4 * i)) & 15ull); }
+__device__ __forceinline__ uint64_t setnib4(uint64_t P, int i, int v) {
+    return (P & ~(15ull << (4 * i))) | ((uint64_t)v << (4 * i));
+}
+__device__ __forceinline__ int uf_find4(uint64_t P, int j) {
+    int p = nib4(P, j);
+    while (p != j) { j = p; p = nib4(P, j); }
+    return j;
+}
+// re-test the unclassified link triangles in nb after an edge of theirs was classified:
+// ready <=> exactly one unclassified edge left (none left: not ready, ends critical)
+__device__ __forceinline__ uint32_t retest_ready(const StarTab& S, uint32_t nb, uint64_t U, uint32_t ready) {
+    for (; nb; nb &= nb - 1) {
+        const int q = __ffs(nb) - 1;
+        const uint32_t b = 1u << q;
+        ready = (__popcll(S.tet_tmask[q] & U) == 1) ? (ready | b) : (ready & ~b);
+    }
+    return ready;
+}
+__device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, uint64_t IV, int n, StarState& st) {
+    const int s0 = nib4(IV, 0);  // delta = (x, lowest lower neighbour)
+    st.vcode = s0;
+    // (1) minimum spanning forest of L by Kruskal: link vertices in rank order, each
+    // with its edges to lower-ranked link vertices in rank order
+    uint64_t P = 0, T = 0;
+    uint32_t done = 1u << s0, crit_e = 0;
+#pragma unroll 1
+    for (int k = 1; k < n; k++) {
+        const int s = nib4(IV, k);
+        uint32_t nm = S.adj[s] & done;
+        done |= 1u << s;
+        if (!nm) {  // no lower-ranked neighbour yet: a new root (may merge later)
+            P = setnib4(P, k, k);
+            continue;
+        }
+        uint32_t MR = 0;
+        do {
+            MR |= 1u << nib4(R, __ffs(nm) - 1);
+            nm &= nm - 1;
+        } while (nm);
+        int j = __ffs(MR) - 1;
+        MR &= MR - 1;
+        int cr = uf_find4(P, j);
+        T |= 1ull << S.tri_of[s][nib4(IV, j)];
+        while (MR) {
+            j = __ffs(MR) - 1;
+            MR &= MR - 1;
+            const int rj = uf_find4(P, j);
+            if (rj != cr) {
+                T |= 1ull << S.tri_of[s][nib4(IV, j)];
+                if (rj < cr) { P = setnib4(P, cr, rj); cr = rj; }
+                else P = setnib4(P, rj, cr);
+            }
+        }
+        P = setnib4(P, k, cr);
+    }
+    // the roots left are the components' lowest vertices: all but rank 0 are critical
+    for (int k = 1; k < n; k++)
+        if (nib4(P, k) == k) crit_e |= 1u << nib4(IV, k);
+    st.crit_e = crit_e;
+    // orient T away from the roots: the star triangle of forest edge (u, w), w the
+    // child, pairs with the star edge (x, w)
+    {
+        uint32_t fr = crit_e | (1u << s0);
+        uint64_t Trem = T;
+#pragma unroll 1
+        while (Trem && fr) {
+            const int u = __ffs(fr) - 1;
+            fr &= fr - 1;
+            uint64_t te = S.edge_tri_mask[u] & Trem;
+            Trem &= ~te;
+            while (te) {
+                const int t = __ffsll((long long)te) - 1;
+                te &= te - 1;
+                const int a = S.tri_a[t];
+                const bool ca = a != u;
+                set_tcode(st, t, ca ? 1ull : 2ull);
+                fr |= 1u << (ca ? a : (int)S.tri_b[t]);
+            }
+        }
+    }
+    // (2) peel the link triangles against the non-forest edges U
+    uint64_t U = st.Lt & ~T;
+    if (!st.Lq && !U) return;
+    const bool ordered = st.Le == 0x3fffu;  // the full sphere: peeling order matters
+    uint32_t ready = 0, clsq = 0;
+    for (uint32_t m = st.Lq; m; m &= m - 1) {
+        const int q = __ffs(m) - 1;
+        if (__popcll(S.tet_tmask[q] & U) == 1) ready |= 1u << q;
+    }
+    uint64_t crit_t = 0;
+#pragma unroll 1
+    while (true) {
+#pragma unroll 1
+        while (ready) {
+            int q = __ffs(ready) - 1;
+            if (ordered && (ready & (ready - 1))) {
+                uint32_t best = cmp_tet(S, R, q);
+                for (uint32_t m = ready & (ready - 1); m; m &= m - 1) {
+                    const int q2 = __ffs(m) - 1;
+                    const uint32_t k2 = cmp_tet(S, R, q2);
+                    if (k2 < best) { best = k2; q = q2; }
+                }
+            }
+            ready &= ~(1u << q);
+            const int e = __ffsll((long long)(S.tet_tmask[q] & U)) - 1;
+            const int j = (e == S.tet_tri[q][0]) ? 0 : ((e == S.tet_tri[q][1]) ? 1 : 2);
+            st.qcode |= (uint64_t)(j + 1) << (2 * q);
+            clsq |= 1u << q;
+            U &= ~(1ull << e);
+            ready = retest_ready(S, S.tri_tet_mask[e] & st.Lq & ~clsq, U, ready);
+        }
+        if (!U) break;
+        // a hole of L: the minimum-key unclassified edge is critical
+        int e = __ffsll((long long)U) - 1;
+        {
+            uint32_t best = key_tri(S, R, e);
+            for (uint64_t m = U & (U - 1); m; m &= m - 1) {
+                const int e2 = __ffsll((long long)m) - 1;
+                const uint32_t k2 = key_tri(S, R, e2);
+                if (k2 < best) { best = k2; e = e2; }
+            }
+        }
+        crit_t |= 1ull << e;
+        U &= ~(1ull << e);
+        ready = retest_ready(S, S.tri_tet_mask[e] & st.Lq & ~clsq, U, ready);
+    }
+    st.crit_t = crit_t;
+    st.crit_q = st.Lq & ~clsq;
+}
+
 // warp-level append of `cnt` records per lane: returns this lane's first position
 __device__ __forceinline__ int64_t warp_append(unsigned long long* total, uint32_t cnt) {
     const int lane = threadIdx.x & 31;
@@ -351,13 +502,14 @@ __device__ __forceinline__ int64_t warp_append(unsigned long long* total, uint32
 // pool is counting-sorted by the work estimate |Le| + |Lt| + |Lq|, and phase C expands the
 // stars in P rounds of 128 in sorted order (warps of near-equal work).  The key caches
 // are rebuilt per expanded star in the thread's own shared-memory column.
-template <int D, int P, int MINB = 1>
+template <int D, int P, int MINB = 1, bool FAST = false>
 __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
+    static_assert(!FAST || D == 3, "closed-form expansion is 3D");
     constexpr int NE = Geo<D>::NE;
     constexpr int POOL = P * kBlockG;
     __shared__ StarTab S;
-    __shared__ uint8_t s_tki[kMaxNT * kBlockG];
-    __shared__ uint16_t s_qk[(D == 3 ? kMaxNQ : 1) * kBlockG];
+    __shared__ uint8_t s_tki[FAST ? 1 : kMaxNT * kBlockG];
+    __shared__ uint16_t s_qk[(D == 3 && !FAST ? kMaxNQ : 1) * kBlockG];
     __shared__ uint64_t s_R[POOL];
     __shared__ uint32_t s_W[POOL];  // Le | delta << 16 | active << 24 | work << 25
     __shared__ uint16_t s_perm[POOL];
@@ -427,6 +579,9 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                         if (r[s] == 0) delta = s;
                     }
                 }
+                if (FAST) {
+                    w = __popc(Le);  // the closed form's loops run over the lower link
+                } else {
                 uint64_t ta = 0, tb = 0;
                 uint32_t qa = 0, qb = 0, qc = 0;
                 for (uint32_t le = Le; le; le &= le - 1) {
@@ -442,6 +597,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 // work estimate: lower-star cells besides x (= 2 pops + 1 - #critical);
                 // (|Lt| + |Lq| + 1 or tet-weighted forms measured 0.5-1.3 % slower)
                 w = min(63, __popc(Le) + __popcll(ta & tb) + __popc(qa & qb & qc));
+                }
             }
             word = Le | ((uint32_t)delta << 16) | (1u << 24);  // bit 24: active
         }
@@ -504,6 +660,9 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             }
             st.Lt = ta & tb;
             st.Lq = qa & qb & qc;
+            if constexpr (FAST) {
+                process_star_fast(S, R, IV, __popc(st.Le), st);
+            } else {
             for (uint64_t m = st.Lt; m; m &= m - 1) {
                 const int tt = __ffsll((long long)m) - 1;
                 s_tki[tt * kBlockG + tid] = (uint8_t)tri_kidx(S, R, tt);
@@ -520,6 +679,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             C.S = &S;
             C.R = R;
             process_star<D, D == 3>(S, C, R, IV, __popc(st.Le), (int)((word >> 16) & 15u), st);
+            }
         }
         if (active) {
             if (D == 3) {

@@ -36,6 +36,7 @@ struct alignas(16) StarTab {
     uint8_t tri_of[kMaxNE][kMaxNE];   // (slot a, slot b) -> tri slot (255: not a triangle)
     uint8_t hl[96];                   // triangle key index C(hi,2)+lo -> hi << 4 | lo
     uint64_t tet_tmask[kMaxNQ];       // the 3 triangle slots of a tet slot, as a mask
+    uint16_t adj[kMaxNE];             // link adjacency: slots u with (x, n_s, n_u) a triangle
     uint8_t q_reslot[kMaxNQ][3];      // tet slot T seen from its link vertex j (a,b,c) -> slot there
     uint8_t t_reslot[kMaxNT][2];      // tri slot t seen from its link vertex j (a,b) -> slot there
     // anchored ids of star cells: anchor offset from x and chain index

@@ -130,6 +130,8 @@ inline bool build_star_tables(int ndim, const int64_t L[3], StarTab* T) {
     for (int t = 0; t < nt; t++) {
         T->tri_of[T->tri_a[t]][T->tri_b[t]] = (uint8_t)t;
         T->tri_of[T->tri_b[t]][T->tri_a[t]] = (uint8_t)t;
+        T->adj[T->tri_a[t]] |= (uint16_t)(1u << T->tri_b[t]);
+        T->adj[T->tri_b[t]] |= (uint16_t)(1u << T->tri_a[t]);
     }
     for (int hi = 1; hi < kMaxNE; hi++)
         for (int lo = 0; lo < hi; lo++) T->hl[hi * (hi - 1) / 2 + lo] = (uint8_t)(hi << 4 | lo);
