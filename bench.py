@@ -107,31 +107,73 @@ def algorithmic_bytes(N, ndim, ncrit, npairs):
     return e2e, grad_kernel
 
 
-def cpu_oracle_sample(f_full, budget_s=20.0):
-    """The oracle (as it stands) on a bounded crop of the same field, on the host cores."""
-    import numpy as np
+def host_cpu_info():
+    """lscpu model name, physical cores and logical CPUs of the host the oracle runs on."""
+    info = {"logical_cpus": os.cpu_count() or 1}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        cps, sk = kv.get("Core(s) per socket"), kv.get("Socket(s)")
+        if cps and sk and cps.isdigit() and sk.isdigit():
+            info["physical_cores"] = int(cps) * int(sk)
+    except Exception:
+        pass
+    return info
 
+
+ORACLE_STAGES = ("nan_scan_fstar", "gradient", "critical_sort", "d0", "dtop")
+
+
+def oracle_timed(crop, nthreads):
+    """One timed oracle pass over `crop`: the vertex order (orc_ranks) and the
+    rest of the front end (orc_run: gradient, C_k, D0, D_{d-1}), per stage in ms."""
     import oracle
+
+    t0 = time.perf_counter()
+    oracle.ranks(crop)
+    t_order = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    r = oracle.run(crop, nthreads=nthreads, want_pairs=False)
+    t_run = (time.perf_counter() - t0) * 1e3
+    stages = {"order": round(t_order, 2)}
+    stages.update({k: round(float(v), 2) for k, v in zip(ORACLE_STAGES, r.ms[:5])})
+    return t_order + t_run, stages
+
+
+def cpu_oracle_sample(f_full, budget_s=24.0):
+    """The oracle (as it stands, never tuned) on a bounded crop of the same field, on the
+    host cores, 1 thread and all cores; each setting is one pass of the
+    whole front end including the vertex order, with per-stage times.  The crop grows
+    until the all-core pass takes >= 1/4 of the budget (the 1-thread pass then fits)."""
+    import numpy as np
 
     cores = os.cpu_count() or 1
     d = f_full.ndim
-    side = {3: 48, 2: 512, 1: 1 << 18}[d]
-    t_all, nv = 0.0, 0
-    reps = 0
-    while t_all < budget_s and reps < 8:
-        sl = tuple(slice(0, min(side, s)) for s in f_full.shape)
-        crop = np.ascontiguousarray(f_full[sl])
-        t0 = time.perf_counter()
-        oracle.run(crop, nthreads=cores, want_pairs=False)
-        t_all += time.perf_counter() - t0
-        nv += crop.size
-        reps += 1
-        if t_all > budget_s / 2 and reps >= 1:
+    side = {3: 32, 2: 256, 1: 1 << 16}[d]
+    while True:
+        crop = np.ascontiguousarray(f_full[tuple(slice(0, min(side, s)) for s in f_full.shape)])
+        t_all, st_all = oracle_timed(crop, cores)
+        grown = tuple(min(int(side * (1.26 if d == 3 else (1.41 if d == 2 else 2))), s) for s in f_full.shape)
+        if t_all >= budget_s * 250 or grown == tuple(min(side, s) for s in f_full.shape):
             break
-        side = int(side * (1.5 if d == 3 else 2))
-    return {"value": nv / t_all / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "%d run(s) of the full front end on crops of the same field (up to %s), %.1f s" % (
-                reps, "x".join(str(min(side, s)) for s in f_full.shape), t_all)}
+        side = max(grown)
+    t_one, st_one = oracle_timed(crop, 1)
+    n = crop.size
+    return {"value": round(n / (t_all / 1e3) / 1e6, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "one pass of the full front end (order, gradient, C_k, D0, D_{d-1}) on the crop %s of "
+                      "the same field, all %d host threads; per-stage ms below" % (
+                          "x".join(str(x) for x in crop.shape), cores),
+            "one_thread": {"value": round(n / (t_one / 1e3) / 1e6, 4), "unit": UNIT, "stages_ms": st_one},
+            "all_cores": {"value": round(n / (t_all / 1e3) / 1e6, 4), "unit": UNIT, "threads": cores,
+                          "stages_ms": st_all},
+            "host": host_cpu_info(),
+            "note": "the oracle fans out only the per-vertex gradient over threads (the paper's "
+                    "parallel structure, P:1121-1124); order, C_k sort and the union-finds are sequential"}
 
 
 def max_over_ranks(value, dist):
@@ -160,34 +202,36 @@ def make_field(cfg, seed):
 
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle, as it stands, timed on the host cores.  Each
-    step is one full front-end run on a fixed crop of this config's field (a bounded
-    sample: the full field would take the oracle tens of minutes)."""
+    step is one full front-end pass (order + gradient + C_k + D0 + D_{d-1}) on a fixed
+    crop of this config's field (a bounded sample: the whole c4 field takes the oracle
+    ~9 min on 8 cores, tests/golden/fullsize_c4.json)."""
     if rank != 0:
         return
     import numpy as np
-
-    import oracle
 
     f = make_field(args.config, 0)
     side = {3: 96, 2: 1024, 1: 1 << 20}[f.ndim]
     crop = np.ascontiguousarray(f[tuple(slice(0, min(side, s)) for s in f.shape)])
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
-        oracle.run(crop, nthreads=cores, want_pairs=False)
-    t0 = time.perf_counter()
+        oracle_timed(crop, cores)
+    dt, per = 0.0, {}
     for _ in range(args.steps):
-        oracle.run(crop, nthreads=cores, want_pairs=False)
-    dt = time.perf_counter() - t0
+        t, st = oracle_timed(crop, cores)
+        dt += t / 1e3
+        for k, v in st.items():
+            per[k] = per.get(k, 0.0) + v / args.steps
     value = crop.size * args.steps / dt / 1e6
-    sample = "crop %s of the %s field, full front end (order, gradient, C_k, D0, D_{d-1})" % (
-        "x".join(str(x) for x in crop.shape), args.config)
+    sample = "crop %s of the %s field, full front end (order, gradient, C_k, D0, D_{d-1}), %d threads" % (
+        "x".join(str(x) for x in crop.shape), args.config, cores)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 in, integer arithmetic (oracle)", "data": "synthetic",
         "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "N": int(f.size)},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                         "stages_ms_per_step": {k: round(v, 2) for k, v in per.items()}, "host": host_cpu_info()},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -278,18 +322,29 @@ def main():
     peak, peak_kind = load_peaks()
     g_ms = stages["gradient_kernel"] / max(1, stages["gradient_launches"])
     g_ach = bmin_grad / (g_ms / 1e3) / 1e9
-    kernel_name = {3: "k_gradient_pool<3,8> (lower-star gradient + critical records)",
+    kernel_name = {3: "k_gradient_pool<3,8,1,true> (closed-form lower-star gradient + critical records)",
                    2: "k_gradient_lut2 (2D lower-star gradient by table lookup + critical records)",
                    1: "k_gradient1 (1D lower-star gradient + critical records)"}[ndim]
-    hbm = {
-        "bound": "hbm", "achieved": round(g_ach, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(g_ach / peak, 4), "peak_kind": peak_kind,
-        "algorithmic_bytes_per_launch": int(bmin_grad),
-        "end_to_end_frac_of_hbm": round(bmin_e2e / (ms_step / 1e3) / 1e9 / peak, 4),
-        "end_to_end_frac_of_8TBps": round(bmin_e2e / (ms_step / 1e3) / 8e12, 4),
+    # roofline: the dominant kernel's ALGORITHMIC bytes per launch
+    # (N (4 + G_w) + 8 sum|C_k|) over its average launch time (CUDA events on the
+    # library's stream, inside the timed region) against the measured HBM peak
+    roofline = {"kernel": kernel_name, "bound": "hbm", "achieved": round(g_ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(g_ach / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                "ms_per_launch": round(g_ms, 4), "algorithmic_bytes_per_launch": int(bmin_grad)}
+    # per-stage and end-to-end fractions of the HBM roofline (SURVEY 8(d) per-stage minima:
+    # a1 8 B/v; a2+a3 (4 + G_w) B/v + 8 sum|C_k|; a4-a8 32 B per output pair)
+    def frac(nbytes, ms):
+        return round(nbytes / (ms / 1e3) / 1e9 / peak, 5) if ms and ms > 0 else None
+
+    st_ms = {k: v / args.steps for k, v in stages.items() if k != "gradient_launches"}
+    roofline["stages"] = {
+        "a1_order": frac(8.0 * N, st_ms.get("order")),
+        "a2_a3_gradient_critical": frac(bmin_grad, st_ms.get("gradient", 0) + st_ms.get("critical", 0)),
+        "a4_a8_diagrams": frac(32.0 * (nd0 + ndt), max(st_ms.get("d0", 0), st_ms.get("dtop", 0))),
+        "end_to_end": frac(bmin_e2e, ms_step),
+        "end_to_end_of_8TBps": round(bmin_e2e / (ms_step / 1e3) / 8e12, 5),
+        "note": "order runs beside the gradient on a second stream and D0 beside D_{d-1}: stage times overlap",
     }
-    roofline = dict(kernel=kernel_name, **{k: hbm[k] for k in ("bound", "achieved", "peak", "unit", "frac")},
-                    traffic=None, peak_kind=peak_kind, ms_per_launch=round(g_ms, 4))
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     tr = None
     if os.path.exists(prof):
@@ -302,19 +357,18 @@ def main():
         roofline["traffic"] = tr["bytes_per_launch"]
         roofline["traffic_source"] = tr.get("source")
         if tr.get("warp_inst_per_launch"):
-            # The kernel is bound by integer issue (ncu: ALU pipe ~89 % busy, DRAM < 1 %), so
-            # its roofline is the issue rate: warp instructions per
-            # launch (ncu, fixed for the input) over the live launch time, against one warp
-            # instruction per cycle per SMSP, 148 SMs x 4 SMSPs, at the sampled SM clock.
-            # The north star's HBM fraction stays in roofline["hbm"].
+            # the kernel is bound by integer issue (ncu: ALU pipe busy, DRAM a few %): its
+            # issue rate, warp instructions per launch (ncu, fixed for the input) over the
+            # live launch time against 1 warp instruction / cycle / SMSP x 148 SMs x 4 SMSPs
+            # at the sampled SM clock
             issue_peak = 148 * 4 * (clk.get("sm_mhz") or 1965.0) * 1e6
             ach = tr["warp_inst_per_launch"] / (g_ms / 1e3)
-            roofline.update({"bound": "alu", "achieved": round(ach / 1e9, 1), "peak": round(issue_peak / 1e9, 1),
-                             "unit": "G warp-inst/s", "frac": round(ach / issue_peak, 3),
-                             "peak_kind": "derived: 148 SMs x 4 SMSPs x 1 warp-instruction/cycle x sampled SM clock",
-                             "lane_efficiency": tr.get("lane_efficiency"),
-                             "alu_pipe_pct_ncu": tr.get("alu_pipe_pct")})
-    roofline["hbm"] = hbm
+            roofline["issue"] = {
+                "bound": "alu", "achieved": round(ach / 1e9, 1), "peak": round(issue_peak / 1e9, 1),
+                "unit": "G warp-inst/s", "frac": round(ach / issue_peak, 3),
+                "warp_inst_per_launch": tr["warp_inst_per_launch"],
+                "peak_kind": "derived: 148 SMs x 4 SMSPs x 1 warp-instruction/cycle x sampled SM clock",
+                "lane_efficiency": tr.get("lane_efficiency"), "alu_pipe_pct_ncu": tr.get("alu_pipe_pct")}
 
     # end to end through the public API: pinned host input -> device, run, diagrams back
     e2e = None

@@ -22,6 +22,7 @@
 
 #include "../../include/dms.h"
 #include "common.cuh"
+#include "order.cuh"
 #include "diag.cuh"
 #include "grad.cuh"
 #include "sort.cuh"
@@ -83,6 +84,7 @@ struct UFBuf {
     unsigned long long* best = nullptr;
     uint32_t *flags = nullptr, *pos = nullptr;
     int64_t cap_arcs = 0, cap_nodes = 0;
+    int64_t last_m = 0, last_grid = 0, last_batch = 0;  // diagnostics of the last launch
 };
 
 // a second issue lane (stream + scan scratch + pinned scratch): D0 runs on it beside
@@ -127,6 +129,14 @@ struct dms_ctx {
     // order sort
     uint32_t *okeys[2] = {nullptr, nullptr}, *ovals[2] = {nullptr, nullptr};
     SortScratch ss;
+    // order by sample sort (order.cuh): B buckets, S samples
+    int ord_B = 0, ord_S = 0;
+    uint64_t* ord_keys = nullptr;                  // [N]
+    uint16_t* ord_bid = nullptr;                   // [N]
+    uint64_t* ord_skeys[2] = {nullptr, nullptr};   // [S]
+    uint32_t* ord_svals[2] = {nullptr, nullptr};   // [S]
+    uint64_t* ord_spl = nullptr;                   // [B]
+    uint32_t *ord_counts = nullptr, *ord_offs = nullptr;  // [B * sms]
     // critical records
     int64_t cap[4] = {0, 0, 0, 0};
     int64_t* cid[2][4] = {};     // [0]: ids in emission order, [1]: ids in lexicographic order
@@ -355,11 +365,30 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     // CTAs (c4: 46.6 -> 45.3 ms; in 1D / 2D the order is the longer branch and keeps the
     // full grid).  DMS_ORDER_CTAS overrides (0: full grid).
     static const int octas_env = getenv("DMS_ORDER_CTAS") ? atoi(getenv("DMS_ORDER_CTAS")) : -1;
-    // 1 CTA per SM on large fields, where the gradient runs long enough to hide the slower
-    // order (c4: 2 -> 1 CTA, 44.38 -> 42.62 ms); 2 below 2^25 vertices, where the order
-    // would become the longer branch (c3 9.07 vs 9.11, c2 1.76 vs 1.80 ms)
-    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? (c->N > (1 << 25) ? 1 : 2) : 0);
+    // 2 CTAs per SM beside the closed-form 3D gradient (c4, 1/2/3/4/full grid: 35.8 /
+    // 32.8 / 34.2 / 35.3 / 34.3 ms; order first, then the gradient: 34.0 ms)
+    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? 2 : 0);
     const int64_t order_cap = octas > 0 ? (int64_t)c->sms * octas : 0;
+    if (c->ord_B > 0) {  // sample sort (order.cuh)
+        const int B = c->ord_B, S = c->ord_S, G = c->sms;
+        static const int ocap_env = getenv("DMS_ORD_CAP") ? atoi(getenv("DMS_ORD_CAP")) : kOrdCap;  // tests: fallback path
+        k_ord_sample<<<(unsigned)ceil_div(S, kBlock), kBlock, 0, c->st>>>(c->f, c->N, S, c->ord_skeys[0], c->ord_svals[0]);
+        const int w = radix_sort<uint64_t, uint32_t, 8>(c->ord_skeys[0], c->ord_svals[0], c->ord_skeys[1], c->ord_svals[1],
+                                                         S, 0, 64, c->ss, c->st, &c->launches);
+        k_ord_splitters<<<(unsigned)ceil_div(B, kBlock), kBlock, 0, c->st>>>(c->ord_skeys[w], S, B, c->ord_spl);
+        k_ord_count<<<G, kOrdT, (size_t)B * 12, c->st>>>(c->f, c->N, B, c->ord_spl, c->ord_bid, c->ord_counts, c->err,
+                                                         c->kmax);
+        scan_excl(c->ord_counts, c->ord_offs, (int64_t)B * G, c->ss, c->st, &c->launches);
+        k_ord_scatter<<<G, kOrdT, (size_t)B * 4, c->st>>>(c->f, c->N, B, c->ord_bid, c->ord_offs, c->ord_keys);
+        k_ord_bucket<<<B, kOrdT, kOrdBucketSmem, c->st>>>(c->ord_keys, c->N, B, G, c->ord_offs, c->rank,
+                                                         std::min(ocap_env, kOrdCap));
+        c->launches += 6;
+        CU(cudaGetLastError());
+        c->have_order = true;
+        c->order_fresh = true;
+        c->have_crit = c->have_d[0] = c->have_d[1] = false;
+        return DMS_OK;
+    }
     // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
     // (and detects NaN / the highest vertex), the last pass writes rank[index]
 #ifndef DMS_ORDER_ITEMS
@@ -597,6 +626,9 @@ dms_status uf_issue(dms_ctx* c, UFBuf& u, int64_t m, int64_t nodes, int karcs, i
         CU(cudaMemcpyAsync(u.nlive, hz, sizeof hz, cudaMemcpyHostToDevice, c->st));
     }
     void* args[] = {&U};
+    u.last_m = m;
+    u.last_grid = grid;
+    u.last_batch = U.batch;
     CU(cudaLaunchCooperativeKernel((void*)k_uf_coop, grid, kBlock, args, 0, c->st));
     c->launches++;
     CU(cudaMemcpyAsync(u.h_status, u.nlive + 2, sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -1027,9 +1059,38 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
         CA(dalloc(&c->dctab, 1));
         if (cudaMemcpy(c->dctab, &ct, sizeof(ChaseTab), cudaMemcpyHostToDevice) != cudaSuccess) return bail(DMS_ERR_CUDA);
     }
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     CA(dalloc(&c->rank_scratch, N));
     CA(cudaMalloc(&c->grad_scratch, dms_gradient_bytes(c)));
     for (int b = 0; b < 2; b++) { CA(dalloc(&c->okeys[b], N)); CA(dalloc(&c->ovals[b], N)); }
+    {
+        // the order by sample sort while the mean bucket (N / B, B <= 16384 buckets)
+        // stays <= 8192 keys, i.e. N <= 2^27; LSD radix sort otherwise and below 2^16
+        static const int samp_env = getenv("DMS_ORDER_SAMPLE") ? atoi(getenv("DMS_ORDER_SAMPLE")) : 0;
+        int B = 2;
+        while (B < kOrdMaxB && (int64_t)B * kOrdMeanMax < N) B <<= 1;
+        if (samp_env && N >= (1 << 16) && (int64_t)B * kOrdMeanMax >= N) {
+            c->ord_B = B;
+            c->ord_S = B * kOrdOversample;
+            CA(dalloc(&c->ord_keys, N));
+            CA(dalloc(&c->ord_bid, N));
+            for (int b = 0; b < 2; b++) { CA(dalloc(&c->ord_skeys[b], c->ord_S)); CA(dalloc(&c->ord_svals[b], c->ord_S)); }
+            CA(dalloc(&c->ord_spl, B));
+            CA(dalloc(&c->ord_counts, (int64_t)B * c->sms));
+            CA(dalloc(&c->ord_offs, (int64_t)B * c->sms));
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_ord_count, cudaFuncAttributeMaxDynamicSharedMemorySize, kOrdMaxB * 12);
+                cudaFuncSetAttribute(k_ord_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, kOrdMaxB * 4);
+                cudaFuncSetAttribute(k_ord_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, kOrdBucketSmem);
+                attr = true;
+            }
+        }
+    }
     const int64_t max_tiles = ceil_div(N, (int64_t)kBlock * 8);
     CA(dalloc(&c->ss.counts, max_tiles * kRadix));
     CA(dalloc(&c->ss.counts_scan, max_tiles * kRadix));
@@ -1071,11 +1132,6 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
     static const int64_t cap_env = getenv("DMS_CRIT_CAP") ? atoll(getenv("DMS_CRIT_CAP")) : -1;
     for (int k = 0; k <= ndim; k++) c->cap[k] = cap_env >= 0 ? cap_env : N / 2 + 1024;
     if (alloc_crit(c) != DMS_OK) return bail(DMS_ERR_OOM);
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
-    }
     {  // 3D: the dual chases read one packed word per vertex (DMS_CHASEWORD=0: the gradient words)
         static const int cw_env = getenv("DMS_CHASEWORD") ? atoi(getenv("DMS_CHASEWORD")) : 1;
         if (ndim == 3 && cw_env) CA(dalloc(&c->cw, N));
@@ -1357,6 +1413,15 @@ int dms_internal_uf_trace2(dms_ctx* c, int which, int out[64], unsigned long lon
     if (cudaMemcpy(out, c->uf[which].trace, 64 * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
     return cudaMemcpy(t, c->uf[which].trace + 128, 64 * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
 }
+// the last union-find launch of a diagram: arcs, cooperative grid, batch size (tests
+// assert the residency-capped multi-tile rounds were reached: arcs > grid * kBlock)
+int dms_internal_uf_launch(dms_ctx* c, int which, int64_t out[3]) {
+    if (!c || which < 0 || which > 1 || !out) return 1;
+    out[0] = c->uf[which].last_m;
+    out[1] = c->uf[which].last_grid;
+    out[2] = c->uf[which].last_batch;
+    return 0;
+}
 int dms_internal_uf_trace(dms_ctx* c, int which, int out[64]) {
     if (!c || which < 0 || which > 1 || !c->uf[which].trace) return 1;
     cudaStreamSynchronize(c->st);
@@ -1395,6 +1460,12 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);
     for (int b = 0; b < 2; b++) { cudaFree(c->okeys[b]); cudaFree(c->ovals[b]); }
+    cudaFree(c->ord_keys);
+    cudaFree(c->ord_bid);
+    for (int b = 0; b < 2; b++) { cudaFree(c->ord_skeys[b]); cudaFree(c->ord_svals[b]); }
+    cudaFree(c->ord_spl);
+    cudaFree(c->ord_counts);
+    cudaFree(c->ord_offs);
     cudaFree(c->ss.counts);
     cudaFree(c->ss.counts_scan);
     cudaFree(c->ss.status);

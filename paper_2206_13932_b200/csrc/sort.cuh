@@ -198,12 +198,109 @@ __global__ void __launch_bounds__(kBlock, DMS_SCATTER_MINB) k_scatter(const Key*
         if (RANK_OUT) {
             rank_out[sv[j]] = (int32_t)p;
         } else {
-            kout[p] = kk;
+            if (kout) kout[p] = kk;  // (null: the last pass of the windowed rank inversion)
             vout[p] = sv[j];
         }
     }
     __syncthreads();
     }
+}
+
+// ---- windowed rank inversion (the vertex order's last step).  rank[v] = p for the
+// sorted vertices ord[p] is a random permutation: 4-byte stores straight into the
+// 537 MB rank array (c4) cost a DRAM read-modify-write of a 32-byte sector each (ncu:
+// 4.1 GB written + 4.2 GB read for 0.54 GB of ranks).  Instead the (v, p) pairs are
+// bucketed by the window v >> kWinBits (2^21 vertices = 8 MB of ranks) with coalesced
+// runs, then stored window by window, so the sectors a window touches stay in L2 until
+// they are complete.
+constexpr int kWinBits = 21;
+constexpr int kWinItems = 16;
+constexpr int kWinTile = kBlock * kWinItems;
+constexpr int kWinMax = 1024;  // windows (N < 2^31)
+
+__global__ void __launch_bounds__(kBlock) k_win_hist(const uint32_t* __restrict__ ord, int64_t n, int nwin,
+                                                     uint32_t* __restrict__ counts, int64_t ntiles) {
+    __shared__ uint32_t h[kWinMax];
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int i = threadIdx.x; i < nwin; i += kBlock) h[i] = 0;
+        __syncthreads();
+        const int64_t base = tile * kWinTile;
+#pragma unroll
+        for (int i = 0; i < kWinItems; i++) {
+            const int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
+            if (idx < n) atomicAdd(&h[ord[idx] >> kWinBits], 1u);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nwin; i += kBlock) counts[(int64_t)i * ntiles + tile] = h[i];
+        __syncthreads();
+    }
+}
+
+// pairs (v, p) of a tile to their windows: staged window by window in shared memory (the
+// order inside a window is irrelevant), written as runs
+__global__ void __launch_bounds__(kBlock) k_win_scatter(const uint32_t* __restrict__ ord, int64_t n, int nwin,
+                                                        const uint32_t* __restrict__ scanned, int64_t ntiles,
+                                                        uint32_t* __restrict__ pv, uint32_t* __restrict__ pp) {
+    __shared__ uint32_t cur[kWinMax], start[kWinMax], gb[kWinMax];
+    __shared__ uint32_t sv[kWinTile], sp[kWinTile];
+    __shared__ uint32_t sw[kBlock / 32 + 1];
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int i = threadIdx.x; i < nwin; i += kBlock) {
+            cur[i] = 0;
+            gb[i] = scanned[(int64_t)i * ntiles + tile];
+        }
+        __syncthreads();
+        const int64_t base = tile * kWinTile;
+        uint32_t v[kWinItems], lp[kWinItems];
+#pragma unroll
+        for (int i = 0; i < kWinItems; i++) {
+            const int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
+            v[i] = idx < n ? ord[idx] : 0xffffffffu;
+            lp[i] = idx < n ? atomicAdd(&cur[v[i] >> kWinBits], 1u) : 0u;
+        }
+        __syncthreads();
+        // tile-local window starts: exclusive scan of cur (nwin <= kWinMax = 4 x kBlock)
+        uint32_t c4[kWinMax / kBlock], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kWinMax / kBlock; j++) {
+            const int w = threadIdx.x * (kWinMax / kBlock) + j;
+            c4[j] = w < nwin ? cur[w] : 0u;
+            sum += c4[j];
+        }
+        uint32_t tot;
+        uint32_t run = block_excl_sum<kBlock / 32>(sum, sw, &tot);
+#pragma unroll
+        for (int j = 0; j < kWinMax / kBlock; j++) {
+            const int w = threadIdx.x * (kWinMax / kBlock) + j;
+            if (w < nwin) start[w] = run;
+            run += c4[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kWinItems; i++) {
+            const int64_t idx = base + (int64_t)i * kBlock + threadIdx.x;
+            if (idx < n) {
+                const uint32_t at = start[v[i] >> kWinBits] + lp[i];
+                sv[at] = v[i];
+                sp[at] = (uint32_t)idx;  // the rank
+            }
+        }
+        __syncthreads();
+        const int tn = (int)((n - base) < (int64_t)kWinTile ? (n - base) : (int64_t)kWinTile);
+        for (int j = threadIdx.x; j < tn; j += kBlock) {
+            const uint32_t w = sv[j] >> kWinBits;
+            const uint32_t p = gb[w] + (uint32_t)j - start[w];
+            pv[p] = sv[j];
+            pp[p] = sp[j];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_win_rank(const uint32_t* __restrict__ pv, const uint32_t* __restrict__ pp, int64_t n,
+                           int32_t* __restrict__ rank) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) rank[pv[i]] = (int32_t)pp[i];
 }
 
 struct SortScratch {
@@ -250,6 +347,12 @@ inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, i
     // grid_cap > 0: a small tile-strided grid (leaves SM room for a concurrent kernel)
     const unsigned grid = (unsigned)(grid_cap > 0 ? std::min<int64_t>(tiles, grid_cap) : tiles);
     int cur = 0;
+    // windowed rank inversion for large orders (see k_win_scatter); DMS_RANK_WIN overrides
+    // the size threshold (0: always direct stores)
+    static const long long win_env = getenv("DMS_RANK_WIN") ? atoll(getenv("DMS_RANK_WIN")) : -1;
+    bool windowed = false;
+    if constexpr (sizeof(Key) == 4 && sizeof(Val) == 4)
+        windowed = rank_out && (win_env < 0 ? n >= (int64_t(1) << 23) : (win_env > 0 && n >= win_env));
     for (int shift = bit0; shift < bit1; shift += 8) {
         const bool first = shift == bit0 && f != nullptr;
         const bool last = shift + 8 >= bit1;
@@ -261,9 +364,10 @@ inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, i
         else k_hist<Key, ITEMS, false><<<grid, kBlock, 0, st>>>(ki, f, n, shift, s.counts, tiles, err, kmax);
         *launches += 1;
         scan_excl(s.counts, s.counts_scan, tiles * kRadix, s, st, launches);
-        const bool ro = last && rank_out;
-#define DMS_SCATTER(RO, FF)                                                                             \
-    k_scatter<Key, Val, ITEMS, RO, FF><<<grid, kBlock, smem, st>>>(ki, vi, f, ko, vo, rank_out, n, shift, \
+        const bool ro = last && rank_out && !windowed;
+        Key* kout = (last && windowed) ? nullptr : ko;  // windowed: the sorted vertex ids only
+#define DMS_SCATTER(RO, FF)                                                                               \
+    k_scatter<Key, Val, ITEMS, RO, FF><<<grid, kBlock, smem, st>>>(ki, vi, f, kout, vo, rank_out, n, shift, \
                                                                           s.counts_scan, tiles)
         if (ro && first) DMS_SCATTER(true, true);
         else if (ro) DMS_SCATTER(true, false);
@@ -271,6 +375,21 @@ inline int radix_sort(Key* ka, Val* va, Key* kb, Val* vb, int64_t n, int bit0, i
         else DMS_SCATTER(false, false);
 #undef DMS_SCATTER
         *launches += 1;
+        if (last && windowed) {
+            if constexpr (sizeof(Key) == 4 && sizeof(Val) == 4) {
+                const uint32_t* ord = reinterpret_cast<const uint32_t*>(vo);
+                uint32_t* pv = reinterpret_cast<uint32_t*>(ki);  // free now: the last pass's input
+                uint32_t* pp = reinterpret_cast<uint32_t*>(vi);
+                const int nwin = (int)((n + (int64_t(1) << kWinBits) - 1) >> kWinBits);
+                const int64_t wt = ceil_div(n, (int64_t)kWinTile);
+                const unsigned wg = (unsigned)(grid_cap > 0 ? std::min<int64_t>(wt, grid_cap) : wt);
+                k_win_hist<<<wg, kBlock, 0, st>>>(ord, n, nwin, s.counts, wt);
+                scan_excl(s.counts, s.counts_scan, wt * nwin, s, st, launches);
+                k_win_scatter<<<wg, kBlock, 0, st>>>(ord, n, nwin, s.counts_scan, wt, pv, pp);
+                k_win_rank<<<(unsigned)ceil_div(n, (int64_t)kBlock), kBlock, 0, st>>>(pv, pp, n, rank_out);
+                *launches += 3;
+            }
+        }
         cur ^= 1;
     }
     return cur;

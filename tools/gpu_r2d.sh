@@ -1,0 +1,9 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/r2d_parity.log 2>&1; echo "rc=$?" >> gpurun_out/r2d_parity.log
+DMS_ORD_CAP=3000 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "c2 or c5" > gpurun_out/r2d_parity_cap.log 2>&1; echo "rc=$?" >> gpurun_out/r2d_parity_cap.log
+for cfg in c4 c5b c5a c3; do
+  timeout 300 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2d_$cfg.json 2>&1
+done
+DMS_ORDER_SEQ=1 timeout 300 python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2d_c4_seq.json 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_ord -c 12 --csv python bench.py --config c4 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/r2d_ncu_ord.csv 2>&1
