@@ -347,99 +347,128 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
 //       only the full sphere, an interior maximum, depends on that order); when none
 //       is left, the minimum-key unclassified edge is critical (a hole of L) and
 //       peeling resumes; a triangle left over is critical (the sphere's 2-cycle).
-// Kruskal in key order builds T (union-find over ranks packed in nibbles), a traversal
-// from the component roots orients it.  The result equals process_star() on every
-// star (tests/test_gpu_*: every gradient vector against the oracle).
+// Kruskal in key order builds T directly as an oriented forest (per-thread union-find
+// and parent arrays in shared memory; a component joined through a later vertex is
+// re-rooted there), so (1) needs no traversal.  The result equals process_star() on
+// every star (tests/test_star_closed_form.py on random stars; tests/test_gpu_*: every
+// gradient vector against the oracle).
 __device__ __forceinline__ int nib4(uint64_t P, int i) { return (int)((P >> (4 * i)) & 15ull); }
-__device__ __forceinline__ uint64_t setnib4(uint64_t P, int i, int v) {
-    return (P & ~(15ull << (4 * i))) | ((uint64_t)v << (4 * i));
-}
-__device__ __forceinline__ int uf_find4(uint64_t P, int j) {
-    int p = nib4(P, j);
-    while (p != j) { j = p; p = nib4(P, j); }
-    return j;
-}
-// re-test the unclassified link triangles in nb after an edge of theirs was classified:
-// ready <=> exactly one unclassified edge left (none left: not ready, ends critical)
-__device__ __forceinline__ uint32_t retest_ready(const StarTab& S, uint32_t nb, uint64_t U, uint32_t ready) {
-    for (; nb; nb &= nb - 1) {
-        const int q = __ffs(nb) - 1;
-        const uint32_t b = 1u << q;
-        ready = (__popcll(S.tet_tmask[q] & U) == 1) ? (ready | b) : (ready & ~b);
+// per-thread byte arrays in shared memory, laid out [slot][thread] (conflict free): the
+// union-find parents (par) and the oriented forest (tp: parent towards the component's
+// lowest vertex; a root points to itself)
+__device__ __forceinline__ int sfind(const uint8_t* par, int u) {
+    int p = par[u * kBlockG];
+    while (p != u) {
+        u = p;
+        p = par[u * kBlockG];
     }
-    return ready;
+    return u;
 }
-__device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, uint64_t IV, int n, StarState& st) {
-    const int s0 = nib4(IV, 0);  // delta = (x, lowest lower neighbour)
-    st.vcode = s0;
-    // (1) minimum spanning forest of L by Kruskal: link vertices in rank order, each
-    // with its edges to lower-ranked link vertices in rank order
-    uint64_t P = 0, T = 0;
-    uint32_t done = 1u << s0, crit_e = 0;
+// re-root the tree holding v at v and hang it below newp (reverse the path v -> root)
+__device__ __forceinline__ void reroot(uint8_t* tp, int v, int newp) {
+    int prev = newp, cur = v;
 #pragma unroll 1
-    for (int k = 1; k < n; k++) {
-        const int s = nib4(IV, k);
-        uint32_t nm = S.adj[s] & done;
+    while (true) {
+        const int nxt = tp[cur * kBlockG];
+        tp[cur * kBlockG] = (uint8_t)prev;
+        if (nxt == cur) break;
+        prev = cur;
+        cur = nxt;
+    }
+}
+// bit-sliced per-link-triangle counters of unclassified edges (c1 c0): minus one on M
+__device__ __forceinline__ void dec_count(uint32_t& c0, uint32_t& c1, uint32_t M) {
+    const uint32_t borrow = M & ~c0;
+    c0 ^= M;
+    c1 ^= borrow;
+}
+__device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, uint64_t IV, int n, StarState& st,
+                                                  uint8_t* par, uint8_t* tp) {
+    const int s0 = (int)(IV & 15ull);  // delta = (x, lowest lower neighbour)
+    st.vcode = s0;
+    par[s0 * kBlockG] = (uint8_t)s0;
+    tp[s0 * kBlockG] = (uint8_t)s0;
+    // (1) the minimum spanning forest of L by Kruskal in key order (link vertices by rank,
+    // each with its edges to lower-ranked link vertices by rank), kept as an oriented
+    // forest: a vertex hangs below its lowest-ranked lower neighbour in the component
+    // with the lowest root; the other components it joins are re-rooted and hung below it
+    uint32_t done = 1u << s0;
+    uint64_t iv = IV >> 4;
+    int ncomp = 1;
+#pragma unroll 1
+    for (int k = 1; k < n; k++, iv >>= 4) {
+        const int s = (int)(iv & 15ull);
+        const uint32_t nm = S.adj[s] & done;
         done |= 1u << s;
-        if (!nm) {  // no lower-ranked neighbour yet: a new root (may merge later)
-            P = setnib4(P, k, k);
+        if (!nm) {  // no lower-ranked neighbour yet: a new root (may be absorbed later)
+            par[s * kBlockG] = (uint8_t)s;
+            tp[s * kBlockG] = (uint8_t)s;
+            ncomp++;
             continue;
         }
-        uint32_t MR = 0;
-        do {
-            MR |= 1u << nib4(R, __ffs(nm) - 1);
-            nm &= nm - 1;
-        } while (nm);
-        int j = __ffs(MR) - 1;
-        MR &= MR - 1;
-        int cr = uf_find4(P, j);
-        T |= 1ull << S.tri_of[s][nib4(IV, j)];
-        while (MR) {
-            j = __ffs(MR) - 1;
+        int att, cr;
+        if (!(nm & (nm - 1))) {  // one lower-ranked neighbour
+            att = __ffs(nm) - 1;
+            cr = ncomp == 1 ? s0 : sfind(par, att);
+        } else if (ncomp == 1) {  // several, one component (rooted at s0): the lowest-ranked
+            att = __ffs(nm) - 1;
+            int ra = rk(R, att);
+            for (uint32_t m = nm & (nm - 1); m; m &= m - 1) {
+                const int u = __ffs(m) - 1;
+                const int ru = rk(R, u);
+                if (ru < ra) { ra = ru; att = u; }
+            }
+            cr = s0;
+        } else {  // several, maybe several components: neighbours in rank order
+            uint32_t MR = 0;
+            for (uint32_t m = nm; m; m &= m - 1) MR |= 1u << rk(R, __ffs(m) - 1);
+            att = nib4(IV, __ffs(MR) - 1);
             MR &= MR - 1;
-            const int rj = uf_find4(P, j);
-            if (rj != cr) {
-                T |= 1ull << S.tri_of[s][nib4(IV, j)];
-                if (rj < cr) { P = setnib4(P, cr, rj); cr = rj; }
-                else P = setnib4(P, rj, cr);
+            cr = sfind(par, att);
+            while (MR) {
+                const int b = nib4(IV, __ffs(MR) - 1);
+                MR &= MR - 1;
+                const int cb = sfind(par, b);
+                if (cb == cr) continue;
+                ncomp--;
+                if (rk(R, cb) < rk(R, cr)) {  // b's component is older: s moves into it
+                    reroot(tp, att, s);
+                    par[cr * kBlockG] = (uint8_t)cb;
+                    cr = cb;
+                    att = b;
+                } else {
+                    reroot(tp, b, s);
+                    par[cb * kBlockG] = (uint8_t)cr;
+                }
             }
         }
-        P = setnib4(P, k, cr);
+        par[s * kBlockG] = (uint8_t)cr;
+        tp[s * kBlockG] = (uint8_t)att;
     }
-    // the roots left are the components' lowest vertices: all but rank 0 are critical
-    for (int k = 1; k < n; k++)
-        if (nib4(P, k) == k) crit_e |= 1u << nib4(IV, k);
-    st.crit_e = crit_e;
-    // orient T away from the roots: the star triangle of forest edge (u, w), w the
-    // child, pairs with the star edge (x, w)
-    {
-        uint32_t fr = crit_e | (1u << s0);
-        uint64_t Trem = T;
+    // forest edge (w, tp[w]) -> star triangle paired with the star edge (x, w); roots other
+    // than s0 are the critical star edges; the triangle counters lose the forest edges
+    uint64_t T = 0;
+    uint32_t crit_e = 0, c0 = st.Lq, c1 = st.Lq;  // every link triangle: 3 unclassified edges
 #pragma unroll 1
-        while (Trem && fr) {
-            const int u = __ffs(fr) - 1;
-            fr &= fr - 1;
-            uint64_t te = S.edge_tri_mask[u] & Trem;
-            Trem &= ~te;
-            while (te) {
-                const int t = __ffsll((long long)te) - 1;
-                te &= te - 1;
-                const int a = S.tri_a[t];
-                const bool ca = a != u;
-                set_tcode(st, t, ca ? 1ull : 2ull);
-                fr |= 1u << (ca ? a : (int)S.tri_b[t]);
-            }
+    for (uint32_t le = st.Le & ~(1u << s0); le; le &= le - 1) {
+        const int w = __ffs(le) - 1;
+        const int p = tp[w * kBlockG];
+        if (p == w) {
+            crit_e |= 1u << w;
+            continue;
         }
+        const int t = S.tri_of[w][p];
+        T |= 1ull << t;
+        set_tcode(st, t, S.tri_a[t] == w ? 1ull : 2ull);
+        dec_count(c0, c1, S.tri_tet_mask[t] & st.Lq);
     }
+    st.crit_e = crit_e;
     // (2) peel the link triangles against the non-forest edges U
     uint64_t U = st.Lt & ~T;
-    if (!st.Lq && !U) return;
+    if (!U) return;  // (then no link triangles either: each has a non-forest edge)
     const bool ordered = st.Le == 0x3fffu;  // the full sphere: peeling order matters
-    uint32_t ready = 0, clsq = 0;
-    for (uint32_t m = st.Lq; m; m &= m - 1) {
-        const int q = __ffs(m) - 1;
-        if (__popcll(S.tet_tmask[q] & U) == 1) ready |= 1u << q;
-    }
+    uint32_t clsq = 0;
+    uint32_t ready = st.Lq & c0 & ~c1;
     uint64_t crit_t = 0;
 #pragma unroll 1
     while (true) {
@@ -454,13 +483,13 @@ __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, 
                     if (k2 < best) { best = k2; q = q2; }
                 }
             }
-            ready &= ~(1u << q);
             const int e = __ffsll((long long)(S.tet_tmask[q] & U)) - 1;
             const int j = (e == S.tet_tri[q][0]) ? 0 : ((e == S.tet_tri[q][1]) ? 1 : 2);
             st.qcode |= (uint64_t)(j + 1) << (2 * q);
             clsq |= 1u << q;
             U &= ~(1ull << e);
-            ready = retest_ready(S, S.tri_tet_mask[e] & st.Lq & ~clsq, U, ready);
+            dec_count(c0, c1, S.tri_tet_mask[e] & st.Lq & ~clsq);
+            ready = st.Lq & ~clsq & c0 & ~c1;
         }
         if (!U) break;
         // a hole of L: the minimum-key unclassified edge is critical
@@ -475,7 +504,8 @@ __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, 
         }
         crit_t |= 1ull << e;
         U &= ~(1ull << e);
-        ready = retest_ready(S, S.tri_tet_mask[e] & st.Lq & ~clsq, U, ready);
+        dec_count(c0, c1, S.tri_tet_mask[e] & st.Lq & ~clsq);
+        ready = st.Lq & ~clsq & c0 & ~c1;
     }
     st.crit_t = crit_t;
     st.crit_q = st.Lq & ~clsq;
@@ -510,6 +540,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
     __shared__ StarTab S;
     __shared__ uint8_t s_tki[FAST ? 1 : kMaxNT * kBlockG];
     __shared__ uint16_t s_qk[(D == 3 && !FAST ? kMaxNQ : 1) * kBlockG];
+    __shared__ uint8_t s_par[(FAST ? kMaxNE : 1) * kBlockG], s_tp[(FAST ? kMaxNE : 1) * kBlockG];
     __shared__ uint64_t s_R[POOL];
     __shared__ uint32_t s_W[POOL];  // Le | delta << 16 | active << 24 | work << 25
     __shared__ uint16_t s_perm[POOL];
@@ -661,7 +692,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             st.Lt = ta & tb;
             st.Lq = qa & qb & qc;
             if constexpr (FAST) {
-                process_star_fast(S, R, IV, __popc(st.Le), st);
+                process_star_fast(S, R, IV, __popc(st.Le), st, s_par + tid, s_tp + tid);
             } else {
             for (uint64_t m = st.Lt; m; m &= m - 1) {
                 const int tt = __ffsll((long long)m) - 1;

@@ -35,6 +35,7 @@ int main(int argc, char** argv) {
     std::mt19937_64 rng(seed);
     static uint8_t tki[kMaxNT * kBlockG];
     static uint16_t qk[kMaxNQ * kBlockG];
+    static uint8_t par[kMaxNE * kBlockG], tp[kMaxNE * kBlockG];
     long bad = 0, tot = 0;
     for (long it = 0; it < iters; it++) {
         // random lower mask + random ranks
@@ -54,7 +55,7 @@ int main(int argc, char** argv) {
         for (uint32_t m = a.Lq; m; m &= m - 1) { int q = __builtin_ctz(m); qk[q * kBlockG] = (uint16_t)cmp_tet(S, R, q); }
         KeyCache C; C.tki = tki; C.qk = qk; C.IV = IV; C.S = &S; C.R = R;
         process_star<3, true>(S, C, R, IV, n, delta, a);
-        process_star_fast(S, R, IV, n, b);
+        process_star_fast(S, R, IV, n, b, par, tp);
         tot++;
         bool ok = a.vcode == b.vcode && a.tcode_lo == b.tcode_lo && a.tcode_hi == b.tcode_hi && a.qcode == b.qcode &&
                   a.crit_e == b.crit_e && a.crit_t == b.crit_t && a.crit_q == b.crit_q;
