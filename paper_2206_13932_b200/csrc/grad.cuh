@@ -45,9 +45,28 @@ __device__ __forceinline__ int off_c(int s, int ax) {
     return D == 3 ? kOff3[s][ax] : kOff2[s][ax];
 }
 
+// n / d for 0 <= n < 2^31 by multiply-high: m = ceil(2^(32+l) / d) (33 bits: lo + hi),
+// l = ceil(log2 d); floor(n m / 2^(32+l)) = floor(n / d) since m d - 2^(32+l) < d <= 2^l
+struct FastDiv {
+    uint32_t m_lo, m_hi, l, d;
+    __host__ void init(uint32_t dd) {
+        d = dd;
+        l = 0;
+        while ((1ull << l) < dd) l++;
+        const unsigned __int128 num = (unsigned __int128)1 << (32 + l);
+        const unsigned __int128 m = (num + dd - 1) / dd;
+        m_lo = (uint32_t)m;
+        m_hi = (uint32_t)(m >> 32);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return (__umulhi(n, m_lo) + (m_hi ? n : 0u)) >> l;
+    }
+};
+
 struct GradArgs {
     const float* f;
     int32_t Lx, Ly, Lz;
+    FastDiv divx, divy;
     int64_t N;
     int64_t v0, v1;  // this launch's vertex range [v0, v1)
     const StarTab* tab;
@@ -564,11 +583,11 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
         uint64_t R = 0;
         int w = 0;
         if (v < A.v1) {
-            const int vv = (int)v;
-            const int cx = vv % A.Lx;
-            const int t = vv / A.Lx;
-            const int cy = t % A.Ly;
-            const int cz = t / A.Ly;
+            const uint32_t vv = (uint32_t)v;
+            const uint32_t t = A.divx.div(vv);
+            const int cx = (int)(vv - t * (uint32_t)A.Lx);
+            const int cz = (int)A.divy.div(t);
+            const int cy = (int)(t - (uint32_t)cz * (uint32_t)A.Ly);
             const float fx = A.f[v];
             if (is_nan_bits(fx)) atomicOr(A.err, 1);
             const uint32_t ox = ord_of(fx);
@@ -591,7 +610,37 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 }
             }
             int delta = 0;
-            if (Le) {
+            if constexpr (FAST) {
+              if (Le) {
+                // local ranks as packed nibble counters (slots 0-7 in lo, 8-13 in hi): for
+                // every pair s < u one compare and one add to the later of the two
+                static_assert(NE == 14, "3D star");
+                uint32_t lo = 0, hi = 0;  // (o[s] <= o[u] for s < u: equal values, smaller slot first)
+#pragma unroll
+                for (int s = 0; s < 8; s++)
+#pragma unroll
+                    for (int u = s + 1; u < 8; u++) lo += (o[s] <= o[u]) ? (1u << (4 * u)) : (1u << (4 * s));
+#pragma unroll
+                for (int s = 8; s < NE; s++)
+#pragma unroll
+                    for (int u = s + 1; u < NE; u++)
+                        hi += (o[s] <= o[u]) ? (1u << (4 * (u - 8))) : (1u << (4 * (s - 8)));
+#pragma unroll
+                for (int s = 0; s < 8; s++)
+#pragma unroll
+                    for (int u = 8; u < NE; u++) {
+                        if (o[s] <= o[u]) hi += 1u << (4 * (u - 8));
+                        else lo += 1u << (4 * s);
+                    }
+                R = (uint64_t)lo | ((uint64_t)hi << 32);  // (non-lower slots rank above all lower ones)
+                uint64_t z = ~(R | 0xff00000000000000ull);  // the rank-0 (zero) nibble is delta's
+                z &= z >> 1;
+                z &= z >> 2;
+                delta = (__ffsll((long long)(z & 0x1111111111111111ull)) - 1) >> 2;
+                w = __popc(Le);  // the closed form's loops run over the lower link
+              }
+            } else {
+              if (Le) {
                 int r[NE];
 #pragma unroll
                 for (int s = 0; s < NE; s++) r[s] = 0;
@@ -610,9 +659,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                         if (r[s] == 0) delta = s;
                     }
                 }
-                if (FAST) {
-                    w = __popc(Le);  // the closed form's loops run over the lower link
-                } else {
+                {
                 uint64_t ta = 0, tb = 0;
                 uint32_t qa = 0, qb = 0, qc = 0;
                 for (uint32_t le = Le; le; le &= le - 1) {
@@ -629,6 +676,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 // (|Lt| + |Lq| + 1 or tet-weighted forms measured 0.5-1.3 % slower)
                 w = min(63, __popc(Le) + __popcll(ta & tb) + __popc(qa & qb & qc));
                 }
+            }
             }
             word = Le | ((uint32_t)delta << 16) | (1u << 24);  // bit 24: active
         }

@@ -1,0 +1,10 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_random_sweep.py -x -q > gpurun_out/r2k_parity.log 2>&1; echo "rc=$?" >> gpurun_out/r2k_parity.log
+for i in 1 2; do
+for cfg in c4 c3; do
+  DMS_ORDER_SEQ=1 timeout 300 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2k_${cfg}_new$i.json 2>&1
+  DMS_LIB=ab/libdms_head.so DMS_ORDER_SEQ=1 timeout 300 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2k_${cfg}_head$i.json 2>&1
+done
+done
+timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,smsp__thread_inst_executed_per_inst_executed.ratio --clock-control none -k regex:k_gradient_pool -c 1 --csv python bench.py --config c4 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/r2k_ncu_grad.csv 2>&1
