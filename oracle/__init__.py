@@ -16,6 +16,11 @@ Parity status per function:
   critical lists   pinned  (brute-force lexicographic sort, hand-built fields)
   D0               pinned  (brute-force Kruskal over all edges; boundary-matrix reduction)
   D_{d-1}          pinned  (brute-force boundary-matrix reduction, vertex level)
+  D1 (3D)          pinned  (brute-force boundary-matrix reduction, vertex level; count
+                            identities |D1| = |C1|-|D0| = |C2|-|D2|; solid-torus field)
+  generators       pinned  (mod-2 cycles, highest edge = the birth edge, homologous to
+                            the death triangle's boundary: cycle + boundary in the span of
+                            earlier triangles' boundaries, by GF(2) rank)
 """
 from __future__ import annotations
 
@@ -40,7 +45,8 @@ PAIR_DTYPE = np.dtype(
     ]
 )
 
-ORC_CRIT, ORC_PAIRS, ORC_D0, ORC_DTOP, ORC_UN0, ORC_UNTOP, ORC_ARCS0, ORC_ARCSTOP, ORC_MS = range(9)
+(ORC_CRIT, ORC_PAIRS, ORC_D0, ORC_DTOP, ORC_UN0, ORC_UNTOP, ORC_ARCS0, ORC_ARCSTOP, ORC_MS, ORC_D1,
+ ORC_GEN_OFF, ORC_GEN, ORC_UN1) = range(13)
 
 
 def build(force: bool = False) -> str:
@@ -68,6 +74,8 @@ def lib():
         L.orc_ranks.restype = ctypes.c_int
         L.orc_run.argtypes = [ctypes.c_int, p, p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(p)]
         L.orc_run.restype = ctypes.c_int
+        L.orc_run2.argtypes = [ctypes.c_int, p, p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(p)]
+        L.orc_run2.restype = ctypes.c_int
         L.orc_gradient_sample.argtypes = [ctypes.c_int, p, p, p, i64, ctypes.c_int, ctypes.POINTER(p)]
         L.orc_gradient_sample.restype = ctypes.c_int
         L.orc_count.argtypes = [p, ctypes.c_int, ctypes.c_int]
@@ -133,15 +141,22 @@ class Result:
             self.arcs0 = arr(ORC_ARCS0, 0, np.int64, 2)
             self.arcs_top = arr(ORC_ARCSTOP, 0, np.int64, 2)
             self.ms = arr(ORC_MS, 0, np.float64)
+            # 3D with want_d1: D1 (Alg. 3), its generators (Sec. 9), unpaired 1-saddles
+            self.d1 = arr(ORC_D1, 0, PAIR_DTYPE)
+            self.gen_off = arr(ORC_GEN_OFF, 0, np.int64)
+            self.gen = arr(ORC_GEN, 0, np.int64)
+            self.unpaired1 = arr(ORC_UN1, 0, np.int64)
         L.orc_free(handle)
 
 
-def run(f: np.ndarray, nthreads: int = 1, want_pairs: bool = True) -> Result:
-    """Whole front end on a field given as a numpy array of shape [Lz,Ly,Lx], [Ly,Lx] or [Lx]."""
+def run(f: np.ndarray, nthreads: int = 1, want_pairs: bool = True, want_d1: bool = False) -> Result:
+    """Whole front end on a field given as a numpy array of shape [Lz,Ly,Lx], [Ly,Lx] or [Lx].
+    want_d1 (3D): also D1 by Alg. 3 "PairCriticalSimplices" and its generators (Sec. 9)."""
     f = np.ascontiguousarray(f, dtype=np.float32)
     ndim, L = _dims(f.shape)
     h = ctypes.c_void_p()
-    st = lib().orc_run(ndim, L.ctypes.data, f.ctypes.data, int(nthreads), int(want_pairs), ctypes.byref(h))
+    flags = (1 if want_pairs else 0) | (2 if want_d1 else 0)
+    st = lib().orc_run2(ndim, L.ctypes.data, f.ctypes.data, int(nthreads), flags, ctypes.byref(h))
     if st:
         raise OracleError(st)
     return Result(h, ndim, True)

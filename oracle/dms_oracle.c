@@ -320,6 +320,8 @@ typedef struct {
     const grid *g;
     int64_t *vpart;    /* [N]: id of the edge paired with vertex v, -1 if critical */
     int64_t *toppart;  /* [ncell[d]*N]: id of the facet paired with a d-simplex, -1 critical */
+    int64_t *epart;    /* optional [ncell[1]*N]: id of the triangle an edge is paired with (the
+                        * edge is the tail of a vector), else untouched (-1) -- for D1 */
     vec pairs;         /* int64 triples (tail dim, tail id, head id) */
     vec crit;          /* simp */
     int want_pairs;
@@ -351,6 +353,7 @@ static void emit_pair(lsctx *c, const simp *tail, const simp *head)
     int64_t tid = simp_id(c->g, tail), hid = simp_id(c->g, head);
     if (tail->dim == 0 && c->vpart) c->vpart[tail->v[0]] = hid;
     if (head->dim == c->g->ndim && c->toppart) c->toppart[hid] = tid;
+    if (tail->dim == 1 && head->dim == 2 && c->epart) c->epart[tid] = hid;
     if (c->want_pairs) {
         int64_t t[3] = {tail->dim, tid, hid};
         vpush(&c->pairs, t);
@@ -470,7 +473,13 @@ typedef struct orc_result {
     int64_t nun0, nuntop;
     int64_t *un0, *untop;        /* unpaired saddles after D0 / D_{d-1} */
     int64_t *arcs0, *arcstop;    /* per arc: the two extremum ends (ids; -1 = VIRTUAL) */
-    double ms[8];                /* stage times: order, gradient, sort C_k, D0, Dtop */
+    int64_t nd1;
+    orc_pair *d1;                /* 3D, want_d1: D1 pairs in increasing death (2-saddle) order */
+    int64_t *gen_off, *gen;      /* the generator (earliest cycle, edge ids) of D1 pair i:
+                                    gen[gen_off[i] .. gen_off[i+1]) */
+    int64_t nun1;
+    int64_t *un1;                /* 1-saddles left unpaired after D1 (infinite D1 classes) */
+    double ms[8];                /* stage times: order, gradient, sort C_k, D0, Dtop, D1 */
 } orc_result;
 
 typedef struct {
@@ -496,7 +505,7 @@ static double now_ms(void)
 
 /* run ProcessLowerStars over the given vertices (all if verts == NULL) */
 static void gradient(const grid *g, const int64_t *verts, int64_t nv, int nthreads, int want_pairs,
-                     int64_t *vpart, int64_t *toppart, vec *pairs, vec *crit)
+                     int64_t *vpart, int64_t *toppart, int64_t *epart, vec *pairs, vec *crit)
 {
     if (nthreads < 1) nthreads = 1;
     if (nthreads > 256) nthreads = 256;
@@ -506,6 +515,7 @@ static void gradient(const grid *g, const int64_t *verts, int64_t nv, int nthrea
         jobs[t].c.g = g;
         jobs[t].c.vpart = vpart;
         jobs[t].c.toppart = toppart;
+        jobs[t].c.epart = epart;
         jobs[t].c.want_pairs = want_pairs;
         jobs[t].c.pairs.el = 3 * sizeof(int64_t);
         jobs[t].c.crit.el = sizeof(simp);
@@ -662,8 +672,12 @@ static orc_pair mkpair(const grid *g, int bdim, int64_t bid, int ddim, int64_t d
 
 /* Full front end. nthreads only fans the per-vertex gradient loop out;
  * everything else is sequential as in the paper's D0/D_{d-1} union-find. */
-int orc_run(int ndim, const int64_t *L, const float *f, int nthreads, int want_pairs, orc_result **out)
+/* flags: bit 0 want_pairs (the gradient vectors), bit 1 want_d1 (3D: D1 by Alg. 3 and
+ * the generators of Sec. 9) */
+int orc_run2(int ndim, const int64_t *L, const float *f, int nthreads, int flags, orc_result **out)
 {
+    const int want_pairs = flags & 1;
+    const int want_d1 = (flags & 2) && ndim == 3;
     int st = check_args(ndim, L);
     if (st) return st;
     orc_result *r = calloc(1, sizeof(orc_result));
@@ -684,7 +698,13 @@ int orc_run(int ndim, const int64_t *L, const float *f, int nthreads, int want_p
     vec pairs = {0}, crit = {0};
     pairs.el = 3 * sizeof(int64_t);
     crit.el = sizeof(simp);
-    gradient(g, NULL, g->N, nthreads, want_pairs, vpart, toppart, &pairs, &crit);
+    int64_t *epart = NULL;
+    if (want_d1) {
+        int64_t ne = g->ncell[1] * g->N;
+        epart = malloc(ne * sizeof(int64_t));
+        for (int64_t i = 0; i < ne; i++) epart[i] = -1;
+    }
+    gradient(g, NULL, g->N, nthreads, want_pairs, vpart, toppart, epart, &pairs, &crit);
     r->ms[1] = now_ms() - t0;
 
     /* O4: Alg. 2 -- critical simplices into C_k, each sorted lexicographically */
@@ -820,11 +840,132 @@ int orc_run(int ndim, const int64_t *L, const float *f, int nthreads, int want_p
         free(tmp);
     }
     r->ms[4] = now_ms() - t0;
+
+    /* O9 (3D, want_d1): D1 by Alg. 3 "PairCriticalSimplices" with boundary
+     * caching, on the 2-saddles that D_{d-1} left unpaired (sandwiching:
+     * the critical simplices already paired in D0 and D_{d-1} are discarded,
+     * P:1125-1155), in increasing lexicographic order.  Boundary(sigma) starts as the
+     * boundary of sigma (its three edges); while it is not empty, tau = its highest edge
+     * in the lexicographic order:
+     *   tau critical, not yet paired in D1: it created the 1-cycle; pair (tau, sigma);
+     *   tau critical, paired with sigma' in D1: Boundary += Boundary(sigma') (cached);
+     *   tau regular: Pair(tau) is the triangle t of its discrete vector:
+     *     Boundary += boundary of t.
+     * Additions are mod 2.  The final Boundary of a pair is its generator,
+     * the earliest 1-cycle homologous to the boundary of sigma (Sec. 9). */
+    t0 = now_ms();
+    if (want_d1) {
+        int64_t ne = g->ncell[1] * g->N;
+        signed char *estate = calloc(ne, 1);  /* 1: critical, paired in D0; 2: critical, positive */
+        int32_t *owner = malloc(ne * sizeof(int32_t));
+        for (int64_t i = 0; i < ne; i++) owner[i] = -1;
+        for (int64_t i = 0; i < r->ncrit[1]; i++) estate[r->crit[1][i]] = 1;
+        for (int64_t i = 0; i < r->nun0; i++) estate[r->un0[i]] = 2;
+        int64_t m = r->nuntop;
+        r->d1 = malloc((m + 1) * sizeof(orc_pair));
+        r->gen_off = malloc((m + 2) * sizeof(int64_t));
+        simp **cache = calloc(m + 1, sizeof(simp *));
+        int64_t *ncache = calloc(m + 1, sizeof(int64_t));
+        vec gen = {0};
+        gen.el = sizeof(int64_t);
+        int64_t capB = 64, nB = 0;
+        simp *B = malloc(capB * sizeof(simp)), *T = malloc(capB * sizeof(simp));
+        r->nd1 = 0;
+        r->gen_off[0] = 0;
+        for (int64_t i = 0; i < m; i++) {
+            simp sg;
+            simp_from_id(g, 2, r->untop[i], &sg);
+            simp fac[3];
+            for (int j = 0; j < 3; j++) {  /* facets of sg, vertices still decreasing */
+                fac[j].dim = 1;
+                int q = 0;
+                for (int u = 0; u < 3; u++) if (u != 2 - j) fac[j].v[q++] = sg.v[u];
+            }
+            qsort_r(fac, 3, sizeof(simp), cmp_simp_r, g);
+            nB = 3;
+            memcpy(B, fac, 3 * sizeof(simp));
+            while (nB > 0) {
+                const simp *tau = &B[nB - 1];
+                int64_t tid = simp_id(g, tau);
+                const simp *add;
+                int64_t nadd;
+                simp tf[3];
+                if (estate[tid] == 2) {
+                    if (owner[tid] < 0) break;  /* unpaired: tau created the cycle */
+                    add = cache[owner[tid]];
+                    nadd = ncache[owner[tid]];
+                } else if (estate[tid] == 1) {
+                    abort();  /* a D0 death edge is negative: never the highest edge of a cycle */
+                } else {
+                    int64_t t = epart[tid];
+                    if (t < 0) abort();  /* a regular edge on a cycle is the tail of a vector */
+                    simp st;
+                    simp_from_id(g, 2, t, &st);
+                    for (int j = 0; j < 3; j++) {
+                        tf[j].dim = 1;
+                        int q = 0;
+                        for (int u = 0; u < 3; u++) if (u != 2 - j) tf[j].v[q++] = st.v[u];
+                    }
+                    qsort_r(tf, 3, sizeof(simp), cmp_simp_r, g);
+                    add = tf;
+                    nadd = 3;
+                }
+                /* Boundary += add (mod 2): merge of two sorted lists, equal entries cancel */
+                if (nB + nadd > capB) {
+                    while (nB + nadd > capB) capB *= 2;
+                    B = realloc(B, capB * sizeof(simp));
+                    T = realloc(T, capB * sizeof(simp));
+                }
+                int64_t a = 0, b = 0, n = 0;
+                while (a < nB || b < nadd) {
+                    int c = a >= nB ? 1 : (b >= nadd ? -1 : lexcmp(g, &B[a], &add[b]));
+                    if (c < 0) T[n++] = B[a++];
+                    else if (c > 0) T[n++] = add[b++];
+                    else { a++; b++; }
+                }
+                simp *sw = B; B = T; T = sw;
+                nB = n;
+            }
+            if (nB == 0) abort();  /* grids are balls: every such 2-saddle kills a 1-cycle */
+            int64_t tid = simp_id(g, &B[nB - 1]);
+            int64_t k = r->nd1;
+            owner[tid] = (int32_t)k;
+            cache[k] = malloc(nB * sizeof(simp));
+            memcpy(cache[k], B, nB * sizeof(simp));
+            ncache[k] = nB;
+            r->d1[k] = mkpair(g, 1, tid, 2, r->untop[i], fstar);
+            for (int64_t j = 0; j < nB; j++) {
+                int64_t eid = simp_id(g, &B[j]);
+                vpush(&gen, &eid);
+            }
+            r->nd1++;
+            r->gen_off[r->nd1] = gen.n;
+        }
+        r->gen = gen.p ? gen.p : malloc(sizeof(int64_t));
+        r->un1 = malloc((r->nun0 + 1) * sizeof(int64_t));
+        r->nun1 = 0;
+        for (int64_t i = 0; i < r->nun0; i++)
+            if (owner[r->un0[i]] < 0) r->un1[r->nun1++] = r->un0[i];
+        for (int64_t k = 0; k < r->nd1; k++) free(cache[k]);
+        free(cache);
+        free(ncache);
+        free(B);
+        free(T);
+        free(estate);
+        free(owner);
+    }
+    r->ms[5] = now_ms() - t0;
+    free(epart);
     for (int k = 0; k <= d; k++) free(cs[k]);
     free(vpart);
     free(toppart);
     *out = r;
     return 0;
+}
+
+int orc_run(int ndim, const int64_t *L, const float *f, int nthreads, int want_pairs, orc_result **out)
+{
+    return orc_run2(ndim, L, f, nthreads, want_pairs ? 1 : 0, out);
 }
 
 /* Gradient restricted to the lower stars of the given vertices (for sampled parity
@@ -841,7 +982,7 @@ int orc_gradient_sample(int ndim, const int64_t *L, const float *f, const int64_
     vec pairs = {0}, crit = {0};
     pairs.el = 3 * sizeof(int64_t);
     crit.el = sizeof(simp);
-    gradient(g, verts, nv, nthreads, 1, NULL, NULL, &pairs, &crit);
+    gradient(g, verts, nv, nthreads, 1, NULL, NULL, NULL, &pairs, &crit);
     r->npairs = pairs.n;
     r->pairs = pairs.p;
     qsort(r->pairs, r->npairs, 3 * sizeof(int64_t), cmp_triple);
@@ -862,7 +1003,8 @@ int orc_gradient_sample(int ndim, const int64_t *L, const float *f, const int64_
 /* ------------------------------------------------------------------ accessors */
 
 enum { ORC_CRIT = 0, ORC_PAIRS = 1, ORC_D0 = 2, ORC_DTOP = 3, ORC_UN0 = 4, ORC_UNTOP = 5,
-       ORC_ARCS0 = 6, ORC_ARCSTOP = 7, ORC_MS = 8 };
+       ORC_ARCS0 = 6, ORC_ARCSTOP = 7, ORC_MS = 8, ORC_D1 = 9, ORC_GEN_OFF = 10, ORC_GEN = 11,
+       ORC_UN1 = 12 };
 
 int64_t orc_count(const orc_result *r, int what, int k)
 {
@@ -875,7 +1017,11 @@ int64_t orc_count(const orc_result *r, int what, int k)
     case ORC_UNTOP: return r->nuntop;
     case ORC_ARCS0: return r->arcs0 ? r->ncrit[1] : 0;
     case ORC_ARCSTOP: return r->arcstop ? r->ncrit[r->g.ndim - 1] : 0;
-    case ORC_MS: return 5;
+    case ORC_MS: return 6;
+    case ORC_D1: return r->d1 ? r->nd1 : 0;
+    case ORC_GEN_OFF: return r->gen_off ? r->nd1 + 1 : 0;
+    case ORC_GEN: return r->gen_off ? r->gen_off[r->nd1] : 0;
+    case ORC_UN1: return r->un1 ? r->nun1 : 0;
     }
     return 0;
 }
@@ -892,7 +1038,11 @@ void orc_copy(const orc_result *r, int what, int k, void *dst)
     case ORC_UNTOP: memcpy(dst, r->untop, n * sizeof(int64_t)); break;
     case ORC_ARCS0: memcpy(dst, r->arcs0, 2 * n * sizeof(int64_t)); break;
     case ORC_ARCSTOP: memcpy(dst, r->arcstop, 2 * n * sizeof(int64_t)); break;
-    case ORC_MS: memcpy(dst, r->ms, 5 * sizeof(double)); break;
+    case ORC_MS: memcpy(dst, r->ms, 6 * sizeof(double)); break;
+    case ORC_D1: memcpy(dst, r->d1, n * sizeof(orc_pair)); break;
+    case ORC_GEN_OFF: memcpy(dst, r->gen_off, n * sizeof(int64_t)); break;
+    case ORC_GEN: memcpy(dst, r->gen, n * sizeof(int64_t)); break;
+    case ORC_UN1: memcpy(dst, r->un1, n * sizeof(int64_t)); break;
     }
 }
 
@@ -907,6 +1057,10 @@ void orc_free(orc_result *r)
     free(r->untop);
     free(r->arcs0);
     free(r->arcstop);
+    free(r->d1);
+    free(r->gen_off);
+    free(r->gen);
+    free(r->un1);
     free(r);
 }
 
