@@ -17,6 +17,7 @@ static inline int __ffs(unsigned x) { return __builtin_ffs((int)x); }
 static inline int __ffsll(long long x) { return __builtin_ffsll(x); }
 static inline int __popc(unsigned x) { return __builtin_popcount(x); }
 static inline int __popcll(unsigned long long x) { return __builtin_popcountll(x); }
+static inline unsigned __umulhi(unsigned a, unsigned b) { return (unsigned)(((unsigned long long)a * b) >> 32); }
 using std::max; using std::min;
 #include <algorithm>
 #include "star.cuh"
