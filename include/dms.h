@@ -2,14 +2,15 @@
  * dms.h -- C ABI of the B200-native Discrete Morse Sandwich front end.
  *
  * Computes, for a float32 scalar field on a Freudenthal-triangulated regular grid
- * (1D/2D/3D), the pieces of arXiv 2206.13932 ("Discrete Morse Sandwich") that
- * precede the D1 stage:
+ * (1D/2D/3D), the pieces of arXiv 2206.13932 ("Discrete Morse Sandwich"):
  *   dms_order        global vertex order              PAPER.md 1368-1372 (Sec. 2.1), 1069-1071 (Sec. 7.1)
  *   dms_gradient     lower-star discrete gradient     PAPER.md 1965-1971 (Sec. 2.6), 272-294 (Sec. 4.1c)
  *   dms_critical     critical simplices C_k, sorted   PAPER.md 317-362 (Alg. 2)
  *   dms_diagram0     D0 (minimum-saddle pairs)        PAPER.md 2481-2685 (Sec. 5.1)
  *   dms_diagram_top  D_{d-1} (saddle-maximum pairs)   PAPER.md 2690-2825 (Sec. 5.2)
  *   infinite classes (inside the two diagram calls)   PAPER.md 2860-2878 (Sec. 6)
+ *   dms_diagram1     D1 (3D) by PairCriticalSimplices PAPER.md 364-417 (Alg. 3), 1125-1150 (Sec. 7.2)
+ *   dms_generators   persistent 1-cycle generators    PAPER.md 1188-1215 (Sec. 9)
  * Everything runs in hand-written CUDA kernels for sm_100a on the caller's stream;
  * there is no CPU fallback.  Readings of the paper's silent points (tie-break,
  * simplex ids, boundary handling, output order) are listed in DESIGN.md.
@@ -131,10 +132,36 @@ dms_status dms_diagram0(dms_ctx* ctx, const dms_pair** d_pairs, int64_t* h_n);
  * follows.  mode must be DMS_BOUNDARY_EXACT.  Synchronises. */
 dms_status dms_diagram_top(dms_ctx* ctx, int mode, const dms_pair** d_pairs, int64_t* h_n);
 
-/* Critical saddles left unpaired (hand-off to the D1 stage): which = 0: critical edges
- * unpaired by D0 (1-cycle creators); which = 1: critical (d-1)-simplices unpaired by
- * D_{d-1}.  Ascending lex order; library-owned device int64.  Synchronises. */
+/* Critical saddles left unpaired (the "sandwich" hand-off, PAPER.md 1125-1155:
+ * PairCriticalSimplices only sees the critical simplices that D0 and D_{d-1} did not
+ * pair).  which = 0: critical edges unpaired by D0 (the 1-cycle creators, Sec. 5.1(d),
+ * PAPER.md 2660-2685); which = 1: critical (d-1)-simplices unpaired by D_{d-1}
+ * (Sec. 5.2, PAPER.md 2767-2769; in 3D the 1-cycle destroyers); which = 2 (3D):
+ * critical edges still unpaired after D1 (infinite D1 classes, Sec. 6; none on a grid,
+ * which is a ball), runs dms_diagram1 if needed.  Ascending lex order; library-owned
+ * device int64 anchored ids.  Synchronises. */
 dms_status dms_unpaired_saddles(dms_ctx* ctx, int which, const int64_t** d_ids, int64_t* h_n);
+
+/* D1 of a 3D field (Alg. 3 "PairCriticalSimplices", PAPER.md 364-417, with boundary
+ * caching PAPER.md 452-501, on the saddles of dms_unpaired_saddles 0 and 1): for each
+ * critical triangle sigma left unpaired by D2, in increasing lexicographic order, the
+ * pair (tau, sigma), tau = the highest edge of the propagated Boundary(sigma) once it is
+ * unpaired.  Computed in parallel rounds with temporary pairs replaced by earlier
+ * claimants (PAPER.md 1136-1150); the pairs equal the sequential
+ * algorithm's.  *d_pairs: library-owned device array of *h_n records, one per 2-saddle,
+ * in increasing death order (no infinite records: see dms_unpaired_saddles 2).
+ * ndim != 3 -> DMS_ERR_ARG (2D: D1 is D_{d-1}; 1D: no D1).  Runs the diagrams it needs.
+ * An internal inconsistency -> DMS_ERR_INVARIANT.  Synchronises. */
+dms_status dms_diagram1(dms_ctx* ctx, const dms_pair** d_pairs, int64_t* h_n);
+
+/* Persistent 1-cycle generators (Sec. 9, PAPER.md 1188-1215): for D1 pair i of
+ * dms_diagram1, the earliest 1-cycle homologous to the boundary of its 2-saddle -- the
+ * Boundary(sigma) Alg. 3 holds when it stops -- as anchored edge ids in ascending
+ * lexicographic order: edges d_edges[d_off[i] .. d_off[i+1]).  d_off: library-owned
+ * device int64[*h_n + 1]; d_edges: library-owned device int64[d_off[*h_n]].  Equal to
+ * the sequential algorithm's columns (a second round-based pass with the final pairs).
+ * 3D only (DMS_ERR_ARG otherwise).  Synchronises. */
+dms_status dms_generators(dms_ctx* ctx, const int64_t** d_off, const int64_t** d_edges, int64_t* h_n);
 
 /* Run the whole front end (order, gradient, critical lists, D0, D_{d-1}); the vertex
  * order runs on an internal second stream concurrently with the gradient and is joined
@@ -170,9 +197,10 @@ dms_status dms_copy(dms_ctx* ctx, void* dst, const void* src, size_t bytes);
  * the stream and writes the accumulated milliseconds of stages
  * 0 order, 1 gradient (+ compaction), 2 critical sort, 3 D0, 4 D_{d-1},
  * 5 gradient kernel alone, 6 the number of timed gradient launches,
- * 7 D0 v-path tracing, 8 D_{d-1} dual tracing, 9 D0 union-find, 10 D_{d-1} union-find. */
+ * 7 D0 v-path tracing, 8 D_{d-1} dual tracing, 9 D0 union-find, 10 D_{d-1} union-find,
+ * 11 D1 pairs, 12 D1 generators. */
 dms_status dms_set_timing(dms_ctx* ctx, int enable);
-dms_status dms_stage_ms(dms_ctx* ctx, double ms_out[11]);
+dms_status dms_stage_ms(dms_ctx* ctx, double ms_out[13]);
 
 /* Number of kernel launches issued by this context so far (bench accounting). */
 int64_t dms_launch_count(const dms_ctx* ctx);

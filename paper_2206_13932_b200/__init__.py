@@ -52,6 +52,8 @@ ABI_SYMBOLS = [
     "dms_diagram0",
     "dms_diagram_top",
     "dms_unpaired_saddles",
+    "dms_diagram1",
+    "dms_generators",
     "dms_run_all",
     "dms_run_all_host",
     "dms_sync",
@@ -94,6 +96,8 @@ def lib():
     L.dms_diagram0.argtypes = [p, P(p), P(i64)]
     L.dms_diagram_top.argtypes = [p, i32, P(p), P(i64)]
     L.dms_unpaired_saddles.argtypes = [p, i32, P(p), P(i64)]
+    L.dms_diagram1.argtypes = [p, P(p), P(i64)]
+    L.dms_generators.argtypes = [p, P(p), P(p), P(i64)]
     L.dms_run_all.argtypes = [p, p, p]
     L.dms_run_all_host.argtypes = [p, p, p, p]
     L.dms_sync.argtypes = [p]
@@ -109,7 +113,7 @@ def lib():
     L.dms_destroy.argtypes = [p]
     L.dms_destroy.restype = None
     for name in ("dms_create", "dms_order", "dms_gradient", "dms_critical", "dms_diagram0", "dms_diagram_top",
-                 "dms_unpaired_saddles", "dms_run_all", "dms_run_all_host", "dms_sync", "dms_copy", "dms_set_timing",
+                 "dms_unpaired_saddles", "dms_diagram1", "dms_generators", "dms_run_all", "dms_run_all_host", "dms_sync", "dms_copy", "dms_set_timing",
                  "dms_stage_ms"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
@@ -189,6 +193,19 @@ def dms_unpaired_saddles(ctx, which):
     return p.value, int(n.value)
 
 
+def dms_diagram1(ctx):
+    p, n = ctypes.c_void_p(), ctypes.c_int64()
+    _check(ctx, lib().dms_diagram1(ctx, ctypes.byref(p), ctypes.byref(n)))
+    return p.value, int(n.value)
+
+
+def dms_generators(ctx):
+    """-> (device pointer of int64 offsets [n+1], device pointer of int64 edge ids, n)"""
+    po, pe, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+    _check(ctx, lib().dms_generators(ctx, ctypes.byref(po), ctypes.byref(pe), ctypes.byref(n)))
+    return po.value, pe.value, int(n.value)
+
+
 def dms_run_all(ctx, rank=None, grad=None):
     _check(ctx, lib().dms_run_all(ctx, ctypes.c_void_p(rank.data_ptr() if rank is not None else 0),
                                   ctypes.c_void_p(grad.data_ptr() if grad is not None else 0)))
@@ -210,14 +227,14 @@ def dms_set_timing(ctx, enable=True):
 
 
 STAGES = ("order", "gradient", "critical", "d0", "dtop", "gradient_kernel", None, "d0_trace", "dtop_trace",
-          "d0_uf", "dtop_uf")
+          "d0_uf", "dtop_uf", "d1", "generators")
 
 
 def dms_stage_ms(ctx):
     """-> dict stage -> accumulated ms, plus 'gradient_launches'"""
-    out = (ctypes.c_double * 11)()
+    out = (ctypes.c_double * len(STAGES))()
     _check(ctx, lib().dms_stage_ms(ctx, out))
-    d = {STAGES[i]: float(out[i]) for i in range(11) if STAGES[i]}
+    d = {STAGES[i]: float(out[i]) for i in range(len(STAGES)) if STAGES[i]}
     d["gradient_launches"] = int(out[6])
     return d
 
@@ -335,6 +352,21 @@ class DMS:
         if n:
             self._copy(a.ctypes.data, p, n * 8)
         return a
+
+    def diagram1(self, out=None) -> np.ndarray:
+        """D1 (3D): one pair per 2-saddle left by D2, in increasing death order."""
+        return self._pairs(*dms_diagram1(self.ctx), out=out)
+
+    def generators(self):
+        """-> (offsets int64 [n+1], edge ids int64): the generator of D1 pair i is
+        edges[offsets[i]:offsets[i+1]] (ascending lexicographic order)."""
+        po, pe, n = dms_generators(self.ctx)
+        off = np.empty(n + 1, dtype=np.int64)
+        self._copy(off.ctypes.data, po, (n + 1) * 8)
+        e = np.empty(int(off[-1]), dtype=np.int64)
+        if e.size:
+            self._copy(e.ctypes.data, pe, e.size * 8)
+        return off, e
 
     def launch_count(self):
         return dms_launch_count(self.ctx)

@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "order.cuh"
 #include "diag.cuh"
+#include "d1.cuh"
 #include "grad.cuh"
 #include "sort.cuh"
 #include "star.cuh"
@@ -85,6 +86,30 @@ struct UFBuf {
     uint32_t *flags = nullptr, *pos = nullptr;
     int64_t cap_arcs = 0, cap_nodes = 0;
     int64_t last_m = 0, last_grid = 0, last_batch = 0;  // diagnostics of the last launch
+};
+
+// D1 (d1.cuh): grow-only buffers
+struct D1Buf {
+    int32_t* order = nullptr;                 // [N] inverse of rank
+    unsigned long long* hkey = nullptr;       // hash of the positive 1-saddles
+    int32_t* hval = nullptr;
+    int64_t hcap = 0;
+    int32_t *owner = nullptr, *stop = nullptr, *done = nullptr, *col_len = nullptr, *big = nullptr;
+    int32_t* act[2] = {nullptr, nullptr};
+    unsigned long long* claim = nullptr;
+    long long* col_off = nullptr;
+    uint8_t* status = nullptr;
+    unsigned long long* arena = nullptr;
+    unsigned long long arena_cap = 0;
+    int32_t* ctr = nullptr;                   // [0] nbig, [1] grab, [2] nnext, [3] err; [4..5] arena top (u64),
+                                              // [6..13] first failure (4 x i64)
+    int32_t* h_ctr = nullptr;                 // pinned copy
+    uint32_t *flags = nullptr, *pos = nullptr;
+    PairRec* pairs = nullptr;
+    int64_t *un1 = nullptr, *gen_off = nullptr, *gen = nullptr;
+    int64_t n0 = 0, nsig = 0, nun1 = 0, ngen = 0;
+    int64_t cap0 = 0, capsig = 0, capgen = 0, capN = 0;
+    int rounds[2] = {0, 0};
 };
 
 // a second issue lane (stream + scan scratch + pinned scratch): D0 runs on it beside
@@ -173,8 +198,10 @@ struct dms_ctx {
     // state
     bool order_fresh = false;  // an order computed since the last gradient pass
     bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
+    bool have_d1 = false, have_gen = false;  // D1 pairs / generators of the current diagrams
+    D1Buf d1;
     bool timing = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[10];
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[12];
     int64_t launches = 0;
     dms_status sticky = DMS_OK;
     char msg[256] = {0};
@@ -386,7 +413,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
         CU(cudaGetLastError());
         c->have_order = true;
         c->order_fresh = true;
-        c->have_crit = c->have_d[0] = c->have_d[1] = false;
+        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;
         return DMS_OK;
     }
     // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
@@ -405,7 +432,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     CU(cudaGetLastError());
     c->have_order = true;
     c->order_fresh = true;
-    c->have_crit = c->have_d[0] = c->have_d[1] = false;  // the gradient does not depend on ranks
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;  // the gradient does not depend on ranks
     return DMS_OK;
 }
 
@@ -504,7 +531,7 @@ dms_status run_gradient(dms_ctx* c, void* d_grad) {
     dms_status s = launch_gradient(c, 0, c->N);
     if (s) return s;
     c->have_grad = true;
-    c->have_crit = c->have_d[0] = c->have_d[1] = false;
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;
     return DMS_OK;
 }
 
@@ -1006,6 +1033,241 @@ dms_status run_diagrams(dms_ctx* c) {
     return DMS_OK;
 }
 
+
+// ------------------------------------------------------------------ D1 (d1.cuh)
+
+}  // namespace
+static int64_t unpaired_count(dms_ctx* c, int which);
+namespace {
+
+dms_status d1_grow_arena(dms_ctx* c, unsigned long long need) {
+    D1Buf& b = c->d1;
+    if (need <= b.arena_cap) return DMS_OK;
+    unsigned long long cap = std::max<unsigned long long>(need, 2 * b.arena_cap);
+    unsigned long long* a = nullptr;
+    CU(dalloc(&a, (int64_t)cap));
+    if (b.arena) {
+        CU(cudaMemcpyAsync(a, b.arena, b.arena_cap * 8, cudaMemcpyDeviceToDevice, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        cudaFree(b.arena);
+    }
+    b.arena = a;
+    b.arena_cap = cap;
+    return DMS_OK;
+}
+
+dms_status d1_alloc(dms_ctx* c, int64_t n0, int64_t nsig) {
+    D1Buf& b = c->d1;
+    if (!b.ctr) {
+        CU(dalloc(&b.ctr, 16));
+        if (cudaMallocHost(&b.h_ctr, 16 * sizeof(int32_t)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
+    }
+    if (c->N > b.capN) {
+        cudaFree(b.order);
+        CU(dalloc(&b.order, c->N));
+        b.capN = c->N;
+    }
+    if (n0 + 1 > b.cap0) {
+        const int64_t cap = 2 * (n0 + 1) + 1024;
+        for (int32_t** q : {&b.owner}) { cudaFree(*q); CU(dalloc(q, cap)); }
+        for (uint32_t** q : {&b.flags, &b.pos}) { cudaFree(*q); CU(dalloc(q, cap)); }
+        cudaFree(b.claim);
+        CU(dalloc(&b.claim, cap));
+        cudaFree(b.un1);
+        CU(dalloc(&b.un1, cap));
+        int64_t h = 1024;
+        while (h < 2 * cap) h *= 2;
+        cudaFree(b.hkey);
+        cudaFree(b.hval);
+        CU(dalloc(&b.hkey, h));
+        CU(dalloc(&b.hval, h));
+        b.hcap = h;
+        b.cap0 = cap;
+    }
+    if (nsig + 1 > b.capsig) {
+        const int64_t cap = 2 * (nsig + 1) + 1024;
+        for (int32_t** q : {&b.stop, &b.done, &b.col_len, &b.big, &b.act[0], &b.act[1]}) { cudaFree(*q); CU(dalloc(q, cap)); }
+        cudaFree(b.col_off);
+        CU(dalloc(&b.col_off, cap));
+        cudaFree(b.status);
+        CU(dalloc(&b.status, cap));
+        cudaFree(b.pairs);
+        CU(dalloc(&b.pairs, cap));
+        cudaFree(b.gen_off);
+        CU(dalloc(&b.gen_off, cap + 1));
+        b.capsig = cap;
+    }
+    static const long long arena_env = getenv("DMS_D1_ARENA") ? atoll(getenv("DMS_D1_ARENA")) : 0;
+    const unsigned long long want = arena_env > 0 ? (unsigned long long)arena_env
+                                                  : std::max<unsigned long long>(1ull << 20, 48ull * (unsigned long long)nsig);
+    return d1_grow_arena(c, std::max<unsigned long long>(want, 3ull * nsig + 64));
+}
+
+D1Args d1_args(dms_ctx* c, int phase) {
+    D1Buf& b = c->d1;
+    D1Args A;
+    A.g = geo(c);
+    A.rank = c->rank;
+    A.order = b.order;
+    A.hkey = b.hkey;
+    A.hval = b.hval;
+    A.hmask = (uint32_t)(b.hcap - 1);
+    A.owner = b.owner;
+    A.claim = b.claim;
+    A.stop = b.stop;
+    A.done = b.done;
+    A.col_off = b.col_off;
+    A.col_len = b.col_len;
+    A.status = b.status;
+    A.arena = b.arena;
+    A.arena_top = reinterpret_cast<unsigned long long*>(b.ctr + 4);
+    A.arena_cap = b.arena_cap;
+    A.active = nullptr;
+    A.nactive = 0;
+    A.big = b.big;
+    A.nbig = b.ctr + 0;
+    A.grab = b.ctr + 1;
+    A.err = b.ctr + 3;
+    A.dbg = reinterpret_cast<long long*>(b.ctr + 6);
+    A.tag = 0;
+    A.phase = phase;
+    static const int lcap_env = getenv("DMS_D1_LCAP") ? atoi(getenv("DMS_D1_LCAP")) : kD1Cap;
+    A.lcap = std::max(4, std::min(kD1Cap, lcap_env));
+    return A;
+}
+
+// rounds of one phase until no sigma is active (d1.cuh); the host reads the active
+// count (and the arena / invariant flags) once per round
+dms_status d1_rounds(dms_ctx* c, int phase) {
+    D1Buf& b = c->d1;
+    int64_t nact = b.nsig;
+    int cur = 0;
+    int r = 0;
+    static const int d1_ctas = getenv("DMS_D1_CTAS") ? atoi(getenv("DMS_D1_CTAS")) : 8;
+    while (nact > 0) {
+        if (r > 1000000) return fail(c, DMS_ERR_INVARIANT, "D1: no progress");
+        D1Args A = d1_args(c, phase);
+        A.active = b.act[cur];
+        A.nactive = (int32_t)nact;
+        A.tag = (unsigned long long)(0xffffffffu - (uint32_t)r) << 32;
+        CU(cudaMemsetAsync(b.ctr, 0, 4 * sizeof(int32_t), c->st));
+        const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nact, 128), (int64_t)c->sms * d1_ctas);
+        k_d1_round<<<grid, 128, 0, c->st>>>(A);
+        k_d1_big<<<c->sms, 64, 0, c->st>>>(A);
+        k_d1_resolve<<<grid_for(nact), kBlock, 0, c->st>>>(A, b.act[cur ^ 1], b.ctr + 2);
+        c->launches += 3;
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(b.h_ctr, b.ctr, 16 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        if (b.h_ctr[3] & 30) {
+            const long long* d = reinterpret_cast<const long long*>(b.h_ctr + 6);
+            char m[200];
+            std::snprintf(m, sizeof m, "D1 phase %d round %d: propagation invariant %d broken (sigma %lld tau %llx edge %lld owner %lld)",
+                          phase, r, b.h_ctr[3] & 30, d[0], (unsigned long long)d[1], d[2], d[3]);
+            return fail(c, DMS_ERR_INVARIANT, m);
+        }
+        nact = b.h_ctr[2];
+        cur ^= 1;
+        r++;
+        if (b.h_ctr[3] & 1) {  // arena full: grow it (the sigmas that did not fit are retried)
+            unsigned long long used = std::min<unsigned long long>(
+                *reinterpret_cast<unsigned long long*>(b.h_ctr + 4), b.arena_cap);
+            dms_status s = d1_grow_arena(c, 2 * b.arena_cap);
+            if (s) return s;
+            CU(cudaMemcpyAsync(b.ctr + 4, &used, 8, cudaMemcpyHostToDevice, c->st));
+            CU(cudaStreamSynchronize(c->st));
+        }
+    }
+    // the active list of the next phase starts as every sigma again
+    b.rounds[phase - 1] = r;
+    return DMS_OK;
+}
+
+// D1 pairs (phase 1) and, with want_gen, the generators (phase 2)
+dms_status run_d1(dms_ctx* c, bool want_gen) {
+    if (c->ndim != 3) return fail(c, DMS_ERR_ARG, "D1 by PairCriticalSimplices is built for 3D fields");
+    if (!c->have_d[0] || !c->have_d[1]) {
+        dms_status s = run_diagrams(c);
+        if (s) return s;
+    }
+    CU(cudaStreamSynchronize(c->st));
+    D1Buf& b = c->d1;
+    const int64_t n0 = unpaired_count(c, 0), nsig = unpaired_count(c, 1);
+    dms_status s = d1_alloc(c, n0, nsig);
+    if (s) return s;
+    b.n0 = n0;
+    b.nsig = nsig;
+    const Geo3 g = geo(c);
+    if (!c->have_d1) {
+        StageTimer tm(c, 10);
+        k_d1_invert<<<grid_for(c->N), kBlock, 0, c->st>>>(c->rank, c->N, b.order);
+        CU(cudaMemsetAsync(b.hkey, 0, b.hcap * 8, c->st));
+        if (n0) k_d1_hash<<<grid_for(n0), kBlock, 0, c->st>>>(g, c->rank, c->unp[0], n0, b.hkey, b.hval, (uint32_t)(b.hcap - 1));
+        CU(cudaMemsetAsync(b.owner, 0xff, n0 * sizeof(int32_t), c->st));
+        CU(cudaMemsetAsync(b.claim, 0xff, n0 * sizeof(unsigned long long), c->st));
+        unsigned long long top = 3ull * nsig;
+        CU(cudaMemcpyAsync(b.ctr + 4, &top, 8, cudaMemcpyHostToDevice, c->st));
+        if (nsig) k_d1_init<<<grid_for(nsig), kBlock, 0, c->st>>>(g, c->rank, c->unp[1], nsig, b.arena, b.col_off, b.col_len, b.act[0], b.done);
+        c->launches += 3;
+        CU(cudaGetLastError());
+        *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = top;
+        if ((s = d1_rounds(c, 1))) return s;
+        if (nsig) {
+            k_d1_emit<<<grid_for(nsig), kBlock, 0, c->st>>>(g, b.stop, b.owner, c->unp[0], c->unp[1], nsig, b.pairs, b.ctr + 3);
+            c->launches++;
+        }
+        // 1-saddles no 2-saddle claimed: infinite D1 classes (none on a grid, a ball)
+        b.nun1 = 0;
+        if (n0) {
+            k_d1_unowned<<<grid_for(n0), kBlock, 0, c->st>>>(b.owner, n0, b.flags);
+            scan_excl(b.flags, b.pos, n0, c->ss, c->st, &c->launches);
+            k_d1_emit_unowned<<<grid_for(n0), kBlock, 0, c->st>>>(b.flags, b.pos, c->unp[0], n0, b.un1);
+            c->launches += 2;
+            uint32_t h[2];
+            CU(cudaMemcpyAsync(&h[0], b.pos + (n0 - 1), 4, cudaMemcpyDeviceToHost, c->st));
+            CU(cudaMemcpyAsync(&h[1], b.flags + (n0 - 1), 4, cudaMemcpyDeviceToHost, c->st));
+            int32_t e = 0;
+            CU(cudaMemcpyAsync(&e, b.ctr + 3, 4, cudaMemcpyDeviceToHost, c->st));
+            CU(cudaStreamSynchronize(c->st));
+            if (e & 30) return fail(c, DMS_ERR_INVARIANT, "D1: a 2-saddle does not own its stop");
+            b.nun1 = (int64_t)h[0] + h[1];
+        }
+        c->have_d1 = true;
+    }
+    if (want_gen && !c->have_gen) {
+        StageTimer tm(c, 11);
+        unsigned long long top = 3ull * nsig;
+        CU(cudaMemcpyAsync(b.ctr + 4, &top, 8, cudaMemcpyHostToDevice, c->st));
+        if (nsig) k_d1_init<<<grid_for(nsig), kBlock, 0, c->st>>>(g, c->rank, c->unp[1], nsig, b.arena, b.col_off, b.col_len, b.act[0], b.done);
+        c->launches++;
+        *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = top;
+        if ((s = d1_rounds(c, 2))) return s;
+        b.ngen = 0;
+        if (nsig) {
+            k_d1_gen_len<<<grid_for(nsig), kBlock, 0, c->st>>>(b.col_len, nsig, b.flags);
+            scan_excl(b.flags, b.pos, nsig, c->ss, c->st, &c->launches);
+            uint32_t h[2];
+            CU(cudaMemcpyAsync(&h[0], b.pos + (nsig - 1), 4, cudaMemcpyDeviceToHost, c->st));
+            CU(cudaMemcpyAsync(&h[1], b.flags + (nsig - 1), 4, cudaMemcpyDeviceToHost, c->st));
+            CU(cudaStreamSynchronize(c->st));
+            const int64_t ng = (int64_t)h[0] + h[1];
+            if (ng + 1 > b.capgen) {
+                cudaFree(b.gen);
+                CU(dalloc(&b.gen, 2 * ng + 1024));
+                b.capgen = 2 * ng + 1024;
+            }
+            k_d1_gen_emit<<<(unsigned)ceil_div(nsig * 32, kBlock), kBlock, 0, c->st>>>(g, b.order, b.col_off, b.col_len, b.pos, nsig, b.arena, b.gen_off, b.gen);
+            c->launches += 2;
+            b.ngen = ng;
+        } else {
+            CU(cudaMemsetAsync(b.gen_off, 0, 8, c->st));
+        }
+        CU(cudaGetLastError());
+        c->have_gen = true;
+    }
+    return DMS_OK;
+}
+
 }  // namespace
 
 // counts left on the device by the asynchronous emissions, read once the caller's stream
@@ -1230,7 +1492,14 @@ dms_status dms_diagram_top(dms_ctx* c, int mode, const dms_pair** d_pairs, int64
 dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, int64_t* h_n) {
     dms_status s = check_sticky(c);
     if (s) return s;
-    if (!d_ids || !h_n || (which != 0 && which != 1)) return DMS_ERR_ARG;
+    if (!d_ids || !h_n || which < 0 || which > 2) return DMS_ERR_ARG;
+    if (which == 2) {
+        if (!c->have_d1 && (s = run_d1(c, false))) return s;
+        if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+        *d_ids = c->d1.un1;
+        *h_n = c->d1.nun1;
+        return DMS_OK;
+    }
     if (!c->have_d[which]) {
         s = which == 0 ? run_d0(c) : run_dtop(c);
         if (s) return s;
@@ -1238,6 +1507,29 @@ dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, in
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
     *d_ids = c->unp[which];
     *h_n = unpaired_count(c, which);
+    return DMS_OK;
+}
+
+dms_status dms_diagram1(dms_ctx* c, const dms_pair** d_pairs, int64_t* h_n) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!d_pairs || !h_n) return DMS_ERR_ARG;
+    if (!c->have_d1 && (s = run_d1(c, false))) return s;
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+    *d_pairs = reinterpret_cast<const dms_pair*>(c->d1.pairs);
+    *h_n = c->d1.nsig;
+    return DMS_OK;
+}
+
+dms_status dms_generators(dms_ctx* c, const int64_t** d_off, const int64_t** d_edges, int64_t* h_n) {
+    dms_status s = check_sticky(c);
+    if (s) return s;
+    if (!d_off || !d_edges || !h_n) return DMS_ERR_ARG;
+    if ((!c->have_d1 || !c->have_gen) && (s = run_d1(c, true))) return s;
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+    *d_off = c->d1.gen_off;
+    *d_edges = c->d1.gen;
+    *h_n = c->d1.nsig;
     return DMS_OK;
 }
 
@@ -1303,7 +1595,7 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
     }
     c->have_grad = true;
     c->order_fresh = false;
-    c->have_crit = c->have_d[0] = c->have_d[1] = false;
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;
     if ((s = run_critical(c))) return s;
     if ((s = run_diagrams(c))) return s;
     return DMS_OK;
@@ -1385,10 +1677,10 @@ dms_status dms_set_timing(dms_ctx* c, int enable) {
     return DMS_OK;
 }
 
-dms_status dms_stage_ms(dms_ctx* c, double ms_out[11]) {
+dms_status dms_stage_ms(dms_ctx* c, double ms_out[13]) {
     if (!c || !ms_out) return DMS_ERR_ARG;
     CU(cudaStreamSynchronize(c->st));
-    for (int s = 0; s < 10; s++) {
+    for (int s = 0; s < 12; s++) {
         double t = 0;
         for (auto& p : c->ev[s]) {
             float x = 0;
@@ -1428,6 +1720,14 @@ int dms_internal_uf_launch(dms_ctx* c, int which, int64_t out[3]) {
     out[2] = c->uf[which].last_batch;
     return 0;
 }
+// rounds of the last D1 phases (1: pairs, 2: generators)
+int dms_internal_d1_rounds(dms_ctx* c, int out[2]) {
+    if (!c) return -1;
+    out[0] = c->d1.rounds[0];
+    out[1] = c->d1.rounds[1];
+    return 0;
+}
+
 int dms_internal_uf_trace(dms_ctx* c, int which, int out[64]) {
     if (!c || which < 0 || which > 1 || !c->uf[which].trace) return 1;
     cudaStreamSynchronize(c->st);
@@ -1503,6 +1803,15 @@ void dms_destroy(dms_ctx* c) {
         if (u.h_cnt) cudaFreeHost(u.h_cnt);
         cudaFree(c->pairs[b]);
         cudaFree(c->unp[b]);
+    }
+    {
+        D1Buf& b = c->d1;
+        for (void* p : {(void*)b.order, (void*)b.hkey, (void*)b.hval, (void*)b.owner, (void*)b.stop, (void*)b.done,
+                        (void*)b.col_len, (void*)b.big, (void*)b.act[0], (void*)b.act[1], (void*)b.claim,
+                        (void*)b.col_off, (void*)b.status, (void*)b.arena, (void*)b.ctr, (void*)b.flags,
+                        (void*)b.pos, (void*)b.pairs, (void*)b.un1, (void*)b.gen_off, (void*)b.gen})
+            cudaFree(p);
+        if (b.h_ctr) cudaFreeHost(b.h_ctr);
     }
     delete c;
 }
