@@ -126,22 +126,29 @@ def host_cpu_info():
     return info
 
 
-ORACLE_STAGES = ("nan_scan_fstar", "gradient", "critical_sort", "d0", "dtop")
+ORACLE_STAGES = ("nan_scan_fstar", "gradient", "critical_sort", "d0", "dtop", "d1_and_generators")
 
 
-def oracle_timed(crop, nthreads):
+def oracle_timed(crop, nthreads, want_d1=False):
     """One timed oracle pass over `crop`: the vertex order (orc_ranks) and the
-    rest of the front end (orc_run: gradient, C_k, D0, D_{d-1}), per stage in ms."""
+    rest of the front end (orc_run: gradient, C_k, D0, D_{d-1}), per stage in ms.  With
+    want_d1 (3D) the oracle also runs D1 + generators (Alg. 3, Sec. 9): reported as its
+    own stage and NOT included in the returned front-end time."""
     import oracle
 
     t0 = time.perf_counter()
     oracle.ranks(crop)
     t_order = (time.perf_counter() - t0) * 1e3
     t0 = time.perf_counter()
-    r = oracle.run(crop, nthreads=nthreads, want_pairs=False)
+    r = oracle.run(crop, nthreads=nthreads, want_pairs=False, want_d1=want_d1)
     t_run = (time.perf_counter() - t0) * 1e3
     stages = {"order": round(t_order, 2)}
-    stages.update({k: round(float(v), 2) for k, v in zip(ORACLE_STAGES, r.ms[:5])})
+    stages.update({k: round(float(v), 2) for k, v in zip(ORACLE_STAGES, r.ms[:6])})
+    if not want_d1:
+        stages.pop("d1_and_generators", None)
+    else:
+        t_run -= float(r.ms[5])
+        stages["d1_pairs"] = int(len(r.d1))
     return t_order + t_run, stages
 
 
@@ -157,12 +164,12 @@ def cpu_oracle_sample(f_full, budget_s=24.0):
     side = {3: 32, 2: 256, 1: 1 << 16}[d]
     while True:
         crop = np.ascontiguousarray(f_full[tuple(slice(0, min(side, s)) for s in f_full.shape)])
-        t_all, st_all = oracle_timed(crop, cores)
+        t_all, st_all = oracle_timed(crop, cores, want_d1=(d == 3))
         grown = tuple(min(int(side * (1.26 if d == 3 else (1.41 if d == 2 else 2))), s) for s in f_full.shape)
         if t_all >= budget_s * 250 or grown == tuple(min(side, s) for s in f_full.shape):
             break
         side = max(grown)
-    t_one, st_one = oracle_timed(crop, 1)
+    t_one, st_one = oracle_timed(crop, 1, want_d1=(d == 3))
     n = crop.size
     return {"value": round(n / (t_all / 1e3) / 1e6, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": "one pass of the full front end (order, gradient, C_k, D0, D_{d-1}) on the crop %s of "
@@ -173,7 +180,9 @@ def cpu_oracle_sample(f_full, budget_s=24.0):
                           "stages_ms": st_all},
             "host": host_cpu_info(),
             "note": "the oracle fans out only the per-vertex gradient over threads (the paper's "
-                    "parallel structure, P:1121-1124); order, C_k sort and the union-finds are sequential"}
+                    "parallel structure, P:1121-1124); order, C_k sort and the union-finds are sequential. "
+                    "3D: stages_ms.d1_and_generators is the oracle's sequential Alg. 3 + Sec. 9 generators on "
+                    "the same crop (not in value)"}
 
 
 def max_over_ranks(value, dist):
@@ -246,6 +255,7 @@ def main():
     ap.add_argument("--impl", default="dms", choices=["dms", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-d1", action="store_true", help="skip the D1 / generator timing (3D)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -406,6 +416,42 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": round(ms_e2e / args.steps, 3)}
 
+    # D1 (Alg. 3 PairCriticalSimplices + the Sec. 9 generators, 3D only):
+    # timed after the front end, by the library's stage events (the diagrams it consumes
+    # are recomputed by run_all each step but not counted)
+    d1 = None
+    if ndim == 3 and not args.no_d1:
+        def d1_step():
+            ctx.run_all(rank_buf, grad_buf)
+            dms.dms_diagram1(ctx.ctx)
+            dms.dms_generators(ctx.ctx)
+
+        d1_step()
+        torch.cuda.synchronize()
+        dms.dms_set_timing(ctx.ctx, True)
+        for _ in range(args.steps):
+            d1_step()
+        st = dms.dms_stage_ms(ctx.ctx)
+        dms.dms_set_timing(ctx.ctx, False)
+        _, n1 = dms.dms_diagram1(ctx.ctx)
+        po, _, _ = dms.dms_generators(ctx.ctx)
+        off = np.empty(n1 + 1, dtype=np.int64)
+        ctx._copy(off.ctypes.data, po, off.nbytes)
+        rr = np.zeros(2, dtype=np.int32)
+        import ctypes as _ct
+        L = dms.lib()
+        L.dms_internal_d1_rounds.argtypes = [_ct.c_void_p, _ct.c_void_p]
+        ntaint = int(L.dms_internal_d1_rounds(ctx.ctx, rr.ctypes.data))
+        ms_p, ms_g = st["d1"] / args.steps, st["generators"] / args.steps
+        d1 = {"pairs": int(n1), "generator_edges": int(off[-1]), "rounds": [int(rr[0]), int(rr[1])],
+              "rerun_for_generators": ntaint,
+              "ms_pairs": round(ms_p, 4), "ms_generators": round(ms_g, 4),
+              "mvertices_per_s_pairs": round(N / ms_p / 1e3, 1) if ms_p > 0 else None,
+              "mpairs_per_s": round(n1 / ms_p / 1e3, 2) if ms_p > 0 else None,
+              "output_bytes": int(32 * n1 + 8 * (n1 + 1) + 8 * int(off[-1])),
+              "note": "latency-bound propagation rounds (host reads the active count per round); "
+                      "ms include the round-trip gaps; pairs = |C1| - |D0| = |C2| - |D2|"}
+
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_base = cpu_oracle_sample(f_host)
@@ -426,6 +472,7 @@ def main():
                                        if k in ("order", "gradient", "critical", "d0", "dtop") and v > 0},
             "counts": {"critical": ncrit, "d0_pairs": nd0, "dtop_pairs": ndt},
             "roofline": roofline,
+            "d1": d1,
             "cpu_baseline": cpu_base,
             "e2e": e2e,
             "gpu_launches": launches,

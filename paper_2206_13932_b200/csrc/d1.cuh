@@ -43,10 +43,38 @@ namespace dms {
 
 constexpr int kD1Cap = 96;  // local-memory heap entries per thread
 
+// star tables of the propagation step (built on the host from StarTab)
+struct alignas(16) D1Tab {
+    int32_t lin[kMaxNE];
+    uint8_t etri[kMaxNE][6];   // triangle slots containing the edge x-n_s (255: none)
+    uint8_t eoth[kMaxNE][6];   // the triangle's other link vertex slot u
+    uint8_t ecode[kMaxNE][6];  // the gradient code that pairs the triangle with that edge (1: tri_a, 2: tri_b)
+    uint8_t sdiff[kMaxNE][kMaxNE];  // slot w with lin[w] == lin[u] - lin[s] (255: not a neighbour)
+};
+
+inline void build_d1_tab(const StarTab& S, D1Tab* T) {
+    for (int a = 0; a < kMaxNE; a++) {
+        T->lin[a] = a < S.ne ? S.lin[a] : 0x7fffffff;
+        for (int i = 0; i < 6; i++) {
+            const int t = a < S.ne ? S.edge_tri[a][i] : 255;
+            T->etri[a][i] = (uint8_t)t;
+            T->eoth[a][i] = t == 255 ? 0 : (S.tri_a[t] == a ? S.tri_b[t] : S.tri_a[t]);
+            T->ecode[a][i] = t == 255 ? 0 : (S.tri_a[t] == a ? 1 : 2);
+        }
+        for (int b = 0; b < kMaxNE; b++) {
+            T->sdiff[a][b] = 255;
+            if (a >= S.ne || b >= S.ne) continue;
+            for (int w = 0; w < S.ne; w++)
+                if (S.lin[w] == S.lin[b] - S.lin[a]) T->sdiff[a][b] = (uint8_t)w;
+        }
+    }
+}
+
 enum : uint8_t { D1_STOP = 1, D1_DONE = 2, D1_WAIT = 3, D1_BIG = 4, D1_RETRY = 5, D1_ERR = 6 };
 
 struct D1Args {
     Geo3 g;
+    const D1Tab* tab;
     const int32_t* rank;
     const int32_t* order;  // order[rank[v]] = v
     const unsigned long long* hkey;  // hash of the positive 1-saddles: key -> index
@@ -72,6 +100,12 @@ struct D1Args {
     unsigned long long tag;  // phase-1 claim tag (decreasing over rounds)
     int phase;
     int lcap;  // local heap capacity used (<= kD1Cap; smaller only to exercise the global path)
+    int4* deps;          // phase 1: (sigma, owner, edge) of every column added, for the taint pass
+    int* ndeps;
+    long long deps_cap;
+    unsigned* st_steps;  // diagnostics (DMS_D1_STATS): per sigma, regular steps / column adds / pushed keys
+    unsigned* st_adds;
+    unsigned* st_pushed;
 };
 
 __device__ __forceinline__ uint32_t d1_hash(unsigned long long k) {
@@ -104,7 +138,8 @@ __device__ __forceinline__ int d1_lookup(const D1Args& A, unsigned long long key
 }
 
 // slot s of the neighbour at linear offset d (slots sorted by offset)
-__device__ __forceinline__ int slot_of_offset(const StarTab& S, int32_t d) {
+template <typename TB>
+__device__ __forceinline__ int slot_of_offset(const TB& S, int32_t d) {
     int s = 0;
 #pragma unroll
     for (int b = 8; b > 0; b >>= 1)
@@ -113,30 +148,45 @@ __device__ __forceinline__ int slot_of_offset(const StarTab& S, int32_t d) {
     return s;
 }
 
+// One regular step's lookups for the edge (x, x + lin[s]): its gradient word and, in the
+// same round of loads, the ranks of the third vertex of every triangle containing the
+// edge (speculatively, clamped to the grid; only the paired one is used).  Returns the
+// slot u of the paired triangle's third vertex (rz = its rank), or -1 if the edge is
+// critical.  Edges paired with a vertex never get here: they are never the highest edge
+// of a cycle (the lowest lower neighbour of x comes last).
+__device__ __forceinline__ int d1_pair_lookup(const D1Args& A, const D1Tab& T, int32_t x, int s, uint32_t& rz) {
+    const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(A.g.grad) + x);
+    uint32_t r[6];
+    const int64_t nmax = A.g.N - 1;
+#pragma unroll
+    for (int i = 0; i < 6; i++) {
+        const int64_t z = (int64_t)x + T.lin[T.eoth[s][i]];
+        r[i] = (uint32_t)__ldg(A.rank + (z < 0 ? 0 : (z > nmax ? nmax : z)));
+    }
+    int u = -1;
+#pragma unroll
+    for (int i = 5; i >= 0; i--) {  // at most one triangle matches
+        const int t = T.etri[s][i];
+        const uint32_t code = (uint32_t)((t < 32 ? (w.x >> (2 * t)) : (w.y >> (2 * (t - 32)))) & 3ull);
+        if (t != 255 && code == T.ecode[s][i]) {
+            rz = r[i];
+            u = T.eoth[s][i];
+        }
+    }
+    return u;
+}
+
 // tau regular: the boundary of its paired triangle minus tau -> k1, k2; returns true.
-// tau critical: returns false.  Edges paired with a vertex never reach here (they are
-// never the highest edge of a cycle: the lowest lower neighbour of x comes last).
-__device__ __forceinline__ bool d1_regular(const D1Args& A, const StarTab& S, unsigned long long tau,
+__device__ __forceinline__ bool d1_regular(const D1Args& A, const D1Tab& T, unsigned long long tau,
                                            unsigned long long& k1, unsigned long long& k2) {
     const uint32_t rh = (uint32_t)(tau >> 32), rl = (uint32_t)tau;
     const int32_t x = __ldg(A.order + rh), y = __ldg(A.order + rl);
-    const int s = slot_of_offset(S, y - x);
-    const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(A.g.grad) + x);
-#pragma unroll 1
-    for (int i = 0; i < 6; i++) {
-        const int t = S.edge_tri[s][i];
-        if (t == 255) break;
-        const uint32_t code = (uint32_t)((t < 32 ? (w.x >> (2 * t)) : (w.y >> (2 * (t - 32)))) & 3ull);
-        const int a = S.tri_a[t], b = S.tri_b[t];
-        if ((code == 1u && a == s) || (code == 2u && b == s)) {
-            const int u = a == s ? b : a;
-            const uint32_t rz = (uint32_t)__ldg(A.rank + x + S.lin[u]);
-            k1 = (unsigned long long)rh << 32 | rz;
-            k2 = ekey(rl, rz);
-            return true;
-        }
-    }
-    return false;
+    const int s = slot_of_offset(T, y - x);
+    uint32_t rz;
+    if (d1_pair_lookup(A, T, x, s, rz) < 0) return false;
+    k1 = (unsigned long long)rh << 32 | rz;
+    k2 = ekey(rl, rz);
+    return true;
 }
 
 __device__ __forceinline__ bool arena_alloc(const D1Args& A, unsigned long long n, unsigned long long& off) {
@@ -146,6 +196,14 @@ __device__ __forceinline__ bool arena_alloc(const D1Args& A, unsigned long long 
         return false;
     }
     return true;
+}
+
+// phase 1: sigma added the column of owner o at edge j (its column stays the sequential
+// one iff o still owns j at the end and o's own column is -- see k_d1_taint*)
+__device__ __forceinline__ void d1_dep(const D1Args& A, int sig, int o, int j) {
+    if (A.phase != 1 || !A.deps) return;
+    const int k = atomicAdd(A.ndeps, 1);
+    if (k < A.deps_cap) A.deps[k] = make_int4(sig, o, j, 0);
 }
 
 __device__ __noinline__ void d1_fail(const D1Args& A, int bit, int sig, unsigned long long tau, int j, int o) {
@@ -250,7 +308,7 @@ __device__ __forceinline__ bool d1_store(const D1Args& A, int sig, Heap<P>& H, u
 // Propagate sigma from the column in H (Alg. 3 lines 5-15).  Returns the
 // status; on D1_BIG the heap (tau pushed back) is the column as a multiset.
 template <typename P, typename Room>
-__device__ __forceinline__ uint8_t d1_propagate(const D1Args& A, const StarTab& S, int sig, Heap<P>& H, Room room,
+__device__ __forceinline__ uint8_t d1_propagate(const D1Args& A, const D1Tab& S, int sig, Heap<P>& H, Room room,
                                                 unsigned long long& tau_out, int& j_out) {
     while (true) {
         const unsigned long long tau = H.popmax();
@@ -266,6 +324,7 @@ __device__ __forceinline__ uint8_t d1_propagate(const D1Args& A, const StarTab& 
             }
             H.push(k1);
             H.push(k2);
+            if (A.st_steps) A.st_steps[sig]++;
             continue;
         }
         const int j = d1_lookup(A, tau);
@@ -300,6 +359,11 @@ __device__ __forceinline__ uint8_t d1_propagate(const D1Args& A, const StarTab& 
             // L2 loads: in phase 2 the column may have been written during this kernel by
             // another SM (its done flag was seen), so a stale L1 line must not serve it
             for (int i = 1; i < len; i++) H.push(__ldcg(A.arena + off + i));
+            d1_dep(A, sig, o, j);
+            if (A.st_adds) {
+                A.st_adds[sig]++;
+                A.st_pushed[sig] += len - 1;
+            }
             continue;
         }
         tau_out = tau;
@@ -328,7 +392,10 @@ __device__ __forceinline__ void d1_finish(const D1Args& A, int sig, Heap<P>& H, 
 
 // one round over the active sigmas, local-memory heaps; persistent threads grab work
 __global__ void __launch_bounds__(128) k_d1_round(D1Args A) {
-    const StarTab& S = *A.g.tab;
+    __shared__ D1Tab S;
+    for (int i = threadIdx.x; i < (int)(sizeof(D1Tab) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&S)[i] = reinterpret_cast<const uint32_t*>(A.tab)[i];
+    __syncthreads();
     Heap<LocalArr> H;
     while (true) {
         int i;
@@ -374,40 +441,479 @@ __global__ void __launch_bounds__(128) k_d1_round(D1Args A) {
     }
 }
 
-// the deferred (large) sigmas: one thread each, heap in the arena
-__global__ void k_d1_big(D1Args A) {
-    const StarTab& S = *A.g.tab;
-    const int nb = *A.nbig;
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
-        const int sig = A.big[b];
-        const long long off = A.col_off[sig];
-        const int len0 = A.col_len[sig];
-        const int len = len0 < 0 ? -len0 : len0;
-        int cap = 256;
-        while (cap < 2 * len) cap *= 2;
-        unsigned long long hoff;
-        if (!arena_alloc(A, (unsigned long long)cap, hoff)) {
-            A.status[sig] = D1_RETRY;
-            continue;
-        }
-        Heap<GlobalArr> H;
-        H.h.a = A.arena + hoff;
-        H.n = 0;
-        if (len0 >= 0) {
-            for (int k = 0; k < len; k++) H.h.a[k] = A.arena[off + k];
-            H.n = len;
+// ---------------------------------------------------------------- large sigmas
+// One CTA of kBigT threads per deferred sigma (k_d1_bigc).  The boundary is split in two
+// (an LSM pair): A, a sorted, duplicate-free array of keys in the arena (read through a
+// prefetched ring of resolved entries), and P, a binary max-heap of 16-byte entries
+// (key + both vertices, so a regular step needs no order[] lookups) in shared memory.
+// Thread 0 runs the propagation serially: the maximum is the larger of A's head and P's
+// top (equal keys cancel, mod 2); the pushed edges of regular steps go to P.  The whole
+// CTA merges: P into A when P fills up (bitonic sort + parity dedup + merge), a long
+// owner column straight into A, and the final column at a stop.  Merges cancel equal
+// keys; their output is always sorted and duplicate-free, so every stored column is.
+
+constexpr int kBigT = 128;
+constexpr int kBigP = 2048;     // P capacity (entries)
+constexpr int kBigRing = kBigT; // resolved A entries
+constexpr int kBigAddSmall = 1024;
+
+struct E16 {
+    unsigned long long key;
+    int32_t hi;    // the edge's higher vertex (in K)
+    int32_t slot;  // the lower vertex's slot around hi
+};
+
+struct BigSmem {
+    E16 P[kBigP];                     // 32 KB
+    unsigned long long S[2 * kBigP];  // 32 KB: sort buffer / staging (E16 x 2048)
+    E16 ring[kBigRing];
+    int cnt[kBigT + 1];
+    // control block (written by thread 0 before a barrier)
+    int action, pn, head, alen, rbase, rcnt, j, m, status, ok;
+    long long aoff, oo;               // A's offset in the arena; owner column offset
+    long long o_out, o_tmp;           // merge output / scratch of the current merge
+    long long bbuf[2], tbuf;          // this run's reusable A buffers and merge scratch
+    int bcap[2], tcap, cur, next;     // their capacities; which buffer holds A (-1: the stored column)
+    E16 tau;
+};
+
+enum : int { BA_REFILL = 1, BA_MERGEP = 2, BA_ADDS = 3, BA_ADDB = 4, BA_STOP = 5, BA_ABORT = 6 };
+
+__device__ __forceinline__ E16 d1_resolve_key(const D1Args& A, const D1Tab& T, unsigned long long key) {
+    E16 e;
+    e.key = key;
+    e.hi = __ldg(A.order + (key >> 32));
+    e.slot = slot_of_offset(T, __ldg(A.order + (uint32_t)key) - e.hi);
+    return e;
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// 4-ary max-heap over E16 entries in shared memory (half the levels of a binary heap:
+// the serial thread's pops are its largest cost)
+__device__ __forceinline__ void sh_push(E16* P, int& n, const E16& e) {
+    int i = n++;
+    while (i > 0) {
+        const int p = (i - 1) >> 2;
+        if (P[p].key >= e.key) break;
+        P[i] = P[p];
+        i = p;
+    }
+    P[i] = e;
+}
+__device__ __forceinline__ E16 sh_pop(E16* P, int& n) {
+    const E16 top = P[0];
+    const E16 k = P[--n];
+    int i = 0;
+    while (true) {
+        const int c = 4 * i + 1;
+        if (c >= n) break;
+        int b = c;
+        unsigned long long bk = P[c].key;
+        if (c + 3 < n) {
+            const unsigned long long k1 = P[c + 1].key, k2 = P[c + 2].key, k3 = P[c + 3].key;
+            const int b01 = k1 > bk ? c + 1 : c;
+            const unsigned long long m01 = k1 > bk ? k1 : bk;
+            const int b23 = k3 > k2 ? c + 3 : c + 2;
+            const unsigned long long m23 = k3 > k2 ? k3 : k2;
+            b = m23 > m01 ? b23 : b01;
+            bk = m23 > m01 ? m23 : m01;
         } else {
-            for (int k = 0; k < len; k++) H.push(A.arena[off + k]);
+            for (int q = c + 1; q < n; q++) {
+                const unsigned long long kq = P[q].key;
+                if (kq > bk) { bk = kq; b = q; }
+            }
         }
-        unsigned long long tau = 0;
-        int j = -1;
-        uint8_t st = d1_propagate(A, S, sig, H, [&](int m) { return heap_room(A, H, m, cap); }, tau, j);
-        if (st == D1_BIG) st = D1_RETRY;  // the arena is full; the host grows it and repeats
-        if (st == D1_RETRY) {
-            A.status[sig] = D1_RETRY;
-            continue;
+        if (bk <= k.key) break;
+        P[i] = P[b];
+        i = b;
+    }
+    if (n > 0) P[i] = k;
+    return top;
+}
+
+// regular step on an entry with known vertices (d1_regular without the order[] loads);
+// the gradient word of the new entry k2's higher vertex is prefetched (k1's is x's)
+__device__ __forceinline__ bool d1_regular16(const D1Args& A, const D1Tab& T, const E16& t, E16& k1, E16& k2) {
+    const int32_t x = t.hi;
+    const int s = t.slot;
+    uint32_t rz;
+    const int u = d1_pair_lookup(A, T, x, s, rz);
+    if (u < 0) return false;
+    const uint32_t rh = (uint32_t)(t.key >> 32), rl = (uint32_t)t.key;
+    k1.key = (unsigned long long)rh << 32 | rz;
+    k1.hi = x;
+    k1.slot = u;
+    if (rl > rz) {  // (y, z), y = x + lin[s] higher: z = y + (lin[u] - lin[s])
+        k2.key = (unsigned long long)rl << 32 | rz;
+        k2.hi = x + T.lin[s];
+        k2.slot = T.sdiff[s][u];
+    } else {        // (z, y): y = z + (lin[s] - lin[u])
+        k2.key = (unsigned long long)rz << 32 | rl;
+        k2.hi = x + T.lin[u];
+        k2.slot = T.sdiff[u][s];
+    }
+    prefetch_l1(reinterpret_cast<const ulonglong2*>(A.g.grad) + k2.hi);
+    return true;
+}
+
+// CTA exclusive scan of one int per thread (kBigT threads); returns the prefix, *total
+__device__ __forceinline__ int cta_scan(BigSmem& sm, int v, int* total) {
+    const int t = threadIdx.x;
+    sm.cnt[t] = v;
+    __syncthreads();
+    if (t == 0) {
+        int acc = 0;
+        for (int i = 0; i < kBigT; i++) {
+            const int c = sm.cnt[i];
+            sm.cnt[i] = acc;
+            acc += c;
         }
-        d1_finish(A, sig, H, st, tau, j);
+        sm.cnt[kBigT] = acc;
+    }
+    __syncthreads();
+    const int r = sm.cnt[t];
+    *total = sm.cnt[kBigT];
+    __syncthreads();
+    return r;
+}
+
+// merge of two sorted (descending), duplicate-free key arrays with mod-2 cancellation:
+// out[0 .. result) = X xor Y, sorted descending.  tmp: scratch of nx + ny keys.
+// Merge path: every thread takes one diagonal range; an equal pair straddling a
+// boundary is kept on the left side so that it cancels.
+template <bool YCG>
+__device__ int cta_merge(BigSmem& sm, const unsigned long long* X, int nx, const unsigned long long* Yp, int ny,
+                         unsigned long long* out, unsigned long long* tmp) {
+    const int t = threadIdx.x;
+    // Y may be a column another SM wrote during this kernel (phase 2): read it from L2
+    auto Yld = [&](int i) { return YCG ? __ldcg(Yp + i) : Yp[i]; };
+    const int total = nx + ny;
+    const int per = (total + kBigT - 1) / kBigT;
+    auto corank = [&](int k) {
+        int lo = max(0, k - ny), hi = min(k, nx);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const int jj = k - mid;
+            if (jj > 0 && X[mid] >= Yld(jj - 1)) lo = mid + 1;
+            else hi = mid;
+        }
+        int i = lo, jj = k - lo;
+        if (i > 0 && jj < ny && X[i - 1] == Yld(jj)) jj++;
+        return make_int2(i, jj);
+    };
+    const int d0 = min(t * per, total), d1 = min(d0 + per, total);
+    const int2 s0 = corank(d0), s1 = d1 == total ? make_int2(nx, ny) : corank(d1);
+    int a = s0.x, b = s0.y;
+    const int base = s0.x + s0.y;
+    int c = 0;
+    while (a < s1.x || b < s1.y) {
+        if (b >= s1.y) tmp[base + c++] = X[a++];
+        else if (a >= s1.x) tmp[base + c++] = Yld(b++);
+        else {
+            const unsigned long long x = X[a], y = Yld(b);
+            if (x > y) { tmp[base + c++] = x; a++; }
+            else if (y > x) { tmp[base + c++] = y; b++; }
+            else { a++; b++; }
+        }
+    }
+    int n;
+    const int dst = cta_scan(sm, c, &n);
+    for (int k = 0; k < c; k++) out[dst + k] = tmp[base + k];
+    __syncthreads();
+    return n;
+}
+
+// P's keys -> sm.S sorted descending with the mod-2 duplicates removed; returns the count
+__device__ int cta_sort_pending(BigSmem& sm, int pn) {
+    const int t = threadIdx.x;
+    int p2 = 1;
+    while (p2 < pn) p2 <<= 1;
+    for (int i = t; i < p2; i += kBigT) sm.S[i] = i < pn ? sm.P[i].key : 0ull;
+    __syncthreads();
+    for (int k = 2; k <= p2; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int i = t; i < p2; i += kBigT) {
+                const int l = i ^ jj;
+                if (l > i) {
+                    const unsigned long long x = sm.S[i], y = sm.S[l];
+                    const bool desc = (i & k) == 0;
+                    if (desc ? x < y : x > y) { sm.S[i] = y; sm.S[l] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    // keep the last element of each run of equal keys iff the run length is odd
+    const int per = (pn + kBigT - 1) / kBigT;
+    const int i0 = min(t * per, pn), i1 = min(i0 + per, pn);
+    int c = 0;
+    for (int i = i0; i < i1; i++) {
+        const unsigned long long k = sm.S[i];
+        if (i + 1 < pn && sm.S[i + 1] == k) continue;
+        int r = 1;
+        while (i - r >= 0 && sm.S[i - r] == k) r++;
+        if (r & 1) c++;
+    }
+    int n;
+    const int dst = cta_scan(sm, c, &n);
+    // compact into the upper half of P's storage (viewed as keys), then back into S
+    unsigned long long* Q = reinterpret_cast<unsigned long long*>(sm.P);
+    int w = dst;
+    for (int i = i0; i < i1; i++) {
+        const unsigned long long k = sm.S[i];
+        if (i + 1 < pn && sm.S[i + 1] == k) continue;
+        int r = 1;
+        while (i - r >= 0 && sm.S[i - r] == k) r++;
+        if (r & 1) Q[w++] = k;
+    }
+    __syncthreads();
+    for (int i = t; i < n; i += kBigT) sm.S[i] = Q[i];
+    __syncthreads();
+    return n;
+}
+
+__global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
+    extern __shared__ __align__(16) unsigned char d1_smem[];
+    BigSmem& sm = *reinterpret_cast<BigSmem*>(d1_smem);
+    __shared__ D1Tab S;
+    for (int i = threadIdx.x; i < (int)(sizeof(D1Tab) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&S)[i] = reinterpret_cast<const uint32_t*>(A.tab)[i];
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int nb = *A.nbig;
+    for (int bi = blockIdx.x; bi < nb; bi += gridDim.x) {
+        const int sig = A.big[bi];
+        if (t == 0) {
+            const long long off = A.col_off[sig];
+            const int len0 = A.col_len[sig];
+            sm.pn = 0;
+            sm.head = 0;
+            sm.rbase = 0;
+            sm.rcnt = 0;
+            sm.cur = -1;
+            sm.bcap[0] = sm.bcap[1] = sm.tcap = 0;
+            if (len0 >= 0) {  // [tau, sorted rest]: A = rest, P = {tau}
+                sm.aoff = off + 1;
+                sm.alen = len0 - 1;
+                sh_push(sm.P, sm.pn, d1_resolve_key(A, S, A.arena[off]));
+            } else {          // a bag from the local path: everything into P
+                sm.aoff = 0;
+                sm.alen = 0;
+                for (int k = 0; k < -len0; k++) sh_push(sm.P, sm.pn, d1_resolve_key(A, S, A.arena[off + k]));
+            }
+        }
+        __syncthreads();
+        while (true) {
+            if (t == 0) {
+                // serial propagation until the CTA is needed
+                int pn = sm.pn, head = sm.head;
+                const int alen = sm.alen, rbase = sm.rbase, rcnt = sm.rcnt;
+                int action = 0;
+                while (true) {
+                    if (pn > kBigP - 3) { action = BA_MERGEP; break; }
+                    if (head < alen && head >= rbase + rcnt) { action = BA_REFILL; break; }
+                    const unsigned long long a = head < alen ? sm.ring[head - rbase].key : 0ull;
+                    const unsigned long long p = pn ? sm.P[0].key : 0ull;
+                    if (!a && !p) {
+                        d1_fail(A, 2, sig, 0ull, -1, -1);
+                        action = BA_ABORT;
+                        break;
+                    }
+                    if (a == p) {
+                        head++;
+                        sh_pop(sm.P, pn);
+                        continue;
+                    }
+                    E16 tv;
+                    if (p > a) {
+                        tv = sh_pop(sm.P, pn);
+                        if (pn && sm.P[0].key == tv.key) {
+                            sh_pop(sm.P, pn);
+                            continue;
+                        }
+                    } else {
+                        tv = sm.ring[head - rbase];
+                        head++;
+                    }
+                    E16 k1, k2;
+                    if (d1_regular16(A, S, tv, k1, k2)) {
+                        sh_push(sm.P, pn, k1);
+                        sh_push(sm.P, pn, k2);
+                        if (A.st_steps) A.st_steps[sig]++;
+                        continue;
+                    }
+                    const int j = d1_lookup(A, tv.key);
+                    if (j < 0) {
+                        d1_fail(A, 4, sig, tv.key, j, -1);
+                        action = BA_ABORT;
+                        break;
+                    }
+                    const int o = A.owner[j];
+                    bool add;
+                    uint8_t st = A.phase == 1 ? D1_STOP : D1_WAIT;
+                    if (A.phase == 1) {
+                        add = o >= 0 && o < sig;
+                    } else if (o == sig) {
+                        add = false;
+                        st = D1_DONE;
+                    } else {
+                        if (o < 0 || o > sig) {
+                            d1_fail(A, 8, sig, tv.key, j, o);
+                            action = BA_ABORT;
+                            break;
+                        }
+                        add = *(volatile const int32_t*)(A.done + o) != 0;
+                        if (add) __threadfence();
+                    }
+                    if (add) {
+                        d1_dep(A, sig, o, j);
+                        sm.oo = *(volatile const long long*)(A.col_off + o);
+                        sm.m = *(volatile const int32_t*)(A.col_len + o);
+                        if (A.st_adds) {
+                            A.st_adds[sig]++;
+                            A.st_pushed[sig] += sm.m - 1;
+                        }
+                        action = (sm.m - 1 <= kBigAddSmall && pn + sm.m <= kBigP - 3) ? BA_ADDS : BA_ADDB;
+                        break;
+                    }
+                    sm.tau = tv;
+                    sm.j = j;
+                    sm.status = st;
+                    action = BA_STOP;
+                    break;
+                }
+                sm.pn = pn;
+                sm.head = head;
+                sm.action = action;
+            }
+            __syncthreads();
+            const int action = sm.action;
+            if (action == BA_ABORT) {
+                if (t == 0) A.status[sig] = D1_ERR;
+                __syncthreads();
+                break;
+            }
+            if (action == BA_REFILL) {
+                const int head = sm.head, alen = sm.alen;
+                const int n = min(kBigRing, alen - head);
+                if (t < n) {
+                    sm.ring[t] = d1_resolve_key(A, S, A.arena[sm.aoff + head + t]);
+                    prefetch_l1(reinterpret_cast<const ulonglong2*>(A.g.grad) + sm.ring[t].hi);
+                }
+                __syncthreads();
+                if (t == 0) {
+                    sm.rbase = head;
+                    sm.rcnt = n;
+                }
+                __syncthreads();
+                continue;
+            }
+            if (action == BA_ADDS) {
+                // stage the owner column's entries (minus its tau) resolved, then push
+                const int m1 = sm.m - 1;
+                E16* stage = reinterpret_cast<E16*>(sm.S);
+                for (int k = t; k < m1; k += kBigT) stage[k] = d1_resolve_key(A, S, __ldcg(A.arena + sm.oo + 1 + k));
+                __syncthreads();
+                if (t == 0) {
+                    int pn = sm.pn;
+                    for (int k = 0; k < m1; k++) sh_push(sm.P, pn, stage[k]);
+                    sm.pn = pn;
+                }
+                __syncthreads();
+                continue;
+            }
+            // the remaining actions rebuild A by a merge: MERGEP (P into A), ADDB (an owner
+            // column into A), STOP (P into A, then the column [tau, A] is stored)
+            const bool withP = action != BA_ADDB && sm.pn > 0;
+            int ny = 0;
+            const unsigned long long* Y = nullptr;
+            if (withP) {
+                ny = cta_sort_pending(sm, sm.pn);
+                Y = sm.S;
+            } else if (action == BA_ADDB) {
+                ny = sm.m - 1;
+                Y = A.arena + sm.oo + 1;  // written in an earlier kernel or fenced (done flag)
+            }
+            const int nx = sm.alen - sm.head;
+            const unsigned long long* X = A.arena + sm.aoff + sm.head;
+            const int lead = action == BA_STOP ? 1 : 0;
+            __syncthreads();  // every thread has read the control block
+            if (t == 0) {
+                // A's buffers and the merge scratch are reused across this run's merges
+                // (grown by doubling); only the stored column at a stop is a fresh block
+                const int need = nx + ny;
+                bool ok = true;
+                unsigned long long o;
+                if (ny > 0 && sm.tcap < need) {
+                    const int cap = max(2 * sm.tcap, need);
+                    ok = arena_alloc(A, (unsigned long long)cap, o);
+                    sm.tbuf = (long long)o;
+                    sm.tcap = ok ? cap : 0;
+                }
+                if (ok && action == BA_STOP) {
+                    ok = arena_alloc(A, (unsigned long long)(lead + need), o);
+                    sm.o_out = (long long)o;
+                } else if (ok) {
+                    const int other = sm.cur == 0 ? 1 : 0;
+                    if (sm.bcap[other] < need) {
+                        const int cap = max(2 * sm.bcap[other], need);
+                        ok = arena_alloc(A, (unsigned long long)cap, o);
+                        sm.bbuf[other] = (long long)o;
+                        sm.bcap[other] = ok ? cap : 0;
+                    }
+                    sm.o_out = sm.bbuf[other];
+                    sm.next = other;
+                }
+                sm.o_tmp = sm.tbuf;
+                sm.ok = ok ? 1 : 0;
+            }
+            __syncthreads();
+            if (!sm.ok) {
+                if (t == 0) A.status[sig] = D1_RETRY;
+                __syncthreads();
+                break;
+            }
+            const long long outoff = sm.o_out;
+            int n;
+            if (ny > 0) {
+                n = (action == BA_ADDB && A.phase == 2)
+                        ? cta_merge<true>(sm, X, nx, Y, ny, A.arena + outoff + lead, A.arena + sm.o_tmp)
+                        : cta_merge<false>(sm, X, nx, Y, ny, A.arena + outoff + lead, A.arena + sm.o_tmp);
+            } else {
+                for (int k = t; k < nx; k += kBigT) A.arena[outoff + lead + k] = X[k];
+                n = nx;
+                __syncthreads();
+            }
+            if (action != BA_STOP) {
+                if (t == 0) {
+                    sm.aoff = outoff;
+                    sm.cur = sm.next;
+                    sm.alen = n;
+                    sm.head = 0;
+                    sm.rbase = 0;
+                    sm.rcnt = 0;
+                    if (withP) sm.pn = 0;
+                }
+                __syncthreads();
+                continue;
+            }
+            if (t == 0) {
+                A.arena[outoff] = sm.tau.key;
+                A.col_off[sig] = outoff;
+                A.col_len[sig] = n + 1;
+                A.stop[sig] = sm.j;
+                const uint8_t st = (uint8_t)sm.status;
+                if (st == D1_STOP) {
+                    atomicMin(A.claim + sm.j, A.tag | (unsigned)sig);
+                } else if (st == D1_DONE) {
+                    __threadfence();
+                    *(volatile int32_t*)(A.done + sig) = 1;
+                }
+                A.status[sig] = st;
+            }
+            __syncthreads();
+            break;
+        }
     }
 }
 
@@ -517,6 +1023,77 @@ __global__ void k_d1_emit_unowned(const uint32_t* __restrict__ flags, const uint
                                   const int64_t* __restrict__ un0, int64_t n0, int64_t* out) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < n0 && flags[j]) out[pos[j]] = un0[j];
+}
+
+__global__ void k_fill_u32(uint32_t* a, int64_t n, uint32_t v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = v;
+}
+
+// taint (phase 1 -> phase 2): a sigma's phase-1 column is the sequential algorithm's
+// unless it added a column whose owner lost that edge later, or a tainted owner's column
+__global__ void k_d1_taint_direct(const int4* __restrict__ deps, int64_t nd, const int32_t* __restrict__ owner,
+                                  uint32_t* taint) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nd) return;
+    const int4 d = deps[i];
+    if (owner[d.z] != d.y) taint[d.x] = 1u;
+}
+__global__ void k_d1_taint_prop(const int4* __restrict__ deps, int64_t nd, uint32_t* taint, int* changed) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nd) return;
+    const int4 d = deps[i];
+    if (taint[d.y] && !taint[d.x]) {
+        taint[d.x] = 1u;
+        *changed = 1;
+    }
+}
+// phase 2 starts with the tainted sigmas only: their boundaries at arena[base + 3 k]
+__global__ void k_d1_init_tainted(Geo3 g, const int32_t* __restrict__ rank, const int64_t* __restrict__ sig_ids,
+                                  int64_t nsig, const uint32_t* __restrict__ taint, const uint32_t* __restrict__ pos,
+                                  unsigned long long base, unsigned long long* arena, long long* col_off,
+                                  int32_t* col_len, int32_t* active, int32_t* done) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nsig) return;
+    if (!taint[i]) {
+        done[i] = 1;
+        return;
+    }
+    done[i] = 0;
+    const StarTab& S = *g.tab;
+    const int64_t id = sig_ids[i];
+    const int64_t a = id / g.ncell[2];
+    const int k = (int)(id % g.ncell[2]);
+    const uint32_t r0 = (uint32_t)rank[a];
+    const uint32_t r1 = (uint32_t)rank[a + lin_mask(g, S.chain[2][k][0])];
+    const uint32_t r2 = (uint32_t)rank[a + lin_mask(g, S.chain[2][k][1])];
+    unsigned long long e[3] = {ekey(r0, r1), ekey(r0, r2), ekey(r1, r2)};
+    if (e[0] < e[1]) { unsigned long long t = e[0]; e[0] = e[1]; e[1] = t; }
+    if (e[1] < e[2]) { unsigned long long t = e[1]; e[1] = e[2]; e[2] = t; }
+    if (e[0] < e[1]) { unsigned long long t = e[0]; e[0] = e[1]; e[1] = t; }
+    const unsigned long long o = base + 3ull * pos[i];
+    for (int q = 0; q < 3; q++) arena[o + q] = e[q];
+    col_off[i] = (long long)o;
+    col_len[i] = 3;
+    active[pos[i]] = (int32_t)i;
+}
+
+// arena compaction: the live columns (one per sigma) copied to new offsets; one warp each
+__global__ void k_d1_abs_len(const int32_t* __restrict__ col_len, int64_t nsig, uint32_t* len) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nsig) len[i] = (uint32_t)abs(col_len[i]);
+}
+__global__ void k_d1_compact(long long* col_off, const int32_t* __restrict__ col_len, const uint32_t* __restrict__ pos,
+                             int64_t nsig, const unsigned long long* __restrict__ src, unsigned long long* dst) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= nsig) return;
+    const int len = abs(col_len[i]);
+    const long long off = col_off[i];
+    const long long to = pos[i];
+    for (int k = lane; k < len; k += 32) dst[to + k] = src[off + k];
+    __syncwarp();
+    if (lane == 0) col_off[i] = to;
 }
 
 __global__ void k_d1_gen_len(const int32_t* __restrict__ col_len, int64_t nsig, uint32_t* len) {

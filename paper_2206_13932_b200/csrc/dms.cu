@@ -102,7 +102,7 @@ struct D1Buf {
     unsigned long long* arena = nullptr;
     unsigned long long arena_cap = 0;
     int32_t* ctr = nullptr;                   // [0] nbig, [1] grab, [2] nnext, [3] err; [4..5] arena top (u64),
-                                              // [6..13] first failure (4 x i64)
+                                              // [6..13] first failure (4 x i64), [14] deps, [15] changed
     int32_t* h_ctr = nullptr;                 // pinned copy
     uint32_t *flags = nullptr, *pos = nullptr;
     PairRec* pairs = nullptr;
@@ -110,6 +110,12 @@ struct D1Buf {
     int64_t n0 = 0, nsig = 0, nun1 = 0, ngen = 0;
     int64_t cap0 = 0, capsig = 0, capgen = 0, capN = 0;
     int rounds[2] = {0, 0};
+    unsigned* stats = nullptr;                // DMS_D1_STATS: [3 * capsig] per-sigma counters
+    int4* deps = nullptr;                     // phase-1 column additions (taint pass)
+    int64_t capdeps = 0;
+    uint32_t* taint = nullptr;
+    int64_t ntaint = 0;
+    D1Tab* tab = nullptr;                     // device copy of the propagation tables
 };
 
 // a second issue lane (stream + scan scratch + pinned scratch): D0 runs on it beside
@@ -1058,6 +1064,12 @@ dms_status d1_grow_arena(dms_ctx* c, unsigned long long need) {
 
 dms_status d1_alloc(dms_ctx* c, int64_t n0, int64_t nsig) {
     D1Buf& b = c->d1;
+    if (!b.tab) {
+        D1Tab h;
+        build_d1_tab(c->htab, &h);
+        CU(dalloc(&b.tab, 1));
+        CU(cudaMemcpy(b.tab, &h, sizeof(D1Tab), cudaMemcpyHostToDevice));
+    }
     if (!b.ctr) {
         CU(dalloc(&b.ctr, 16));
         if (cudaMallocHost(&b.h_ctr, 16 * sizeof(int32_t)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
@@ -1095,6 +1107,11 @@ dms_status d1_alloc(dms_ctx* c, int64_t n0, int64_t nsig) {
         CU(dalloc(&b.pairs, cap));
         cudaFree(b.gen_off);
         CU(dalloc(&b.gen_off, cap + 1));
+        cudaFree(b.taint);
+        CU(dalloc(&b.taint, cap));
+        cudaFree(b.deps);
+        b.capdeps = std::max<int64_t>(1 << 20, 4 * cap);
+        CU(dalloc(&b.deps, b.capdeps));
         b.capsig = cap;
     }
     static const long long arena_env = getenv("DMS_D1_ARENA") ? atoll(getenv("DMS_D1_ARENA")) : 0;
@@ -1103,10 +1120,39 @@ dms_status d1_alloc(dms_ctx* c, int64_t n0, int64_t nsig) {
     return d1_grow_arena(c, std::max<unsigned long long>(want, 3ull * nsig + 64));
 }
 
+// copying collection of the arena: only the current column of every sigma is live
+// (owners' columns included); the new arena doubles when the live part exceeds a quarter
+dms_status d1_compact(dms_ctx* c, bool grow) {
+    D1Buf& b = c->d1;
+    const int64_t n = b.nsig;
+    if (n == 0) return DMS_OK;
+    k_d1_abs_len<<<grid_for(n), kBlock, 0, c->st>>>(b.col_len, n, b.flags);
+    scan_excl(b.flags, b.pos, n, c->ss, c->st, &c->launches);
+    uint32_t h[2];
+    CU(cudaMemcpyAsync(&h[0], b.pos + (n - 1), 4, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaMemcpyAsync(&h[1], b.flags + (n - 1), 4, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    const unsigned long long live = (unsigned long long)h[0] + h[1];
+    unsigned long long cap = grow ? 2 * b.arena_cap : b.arena_cap;
+    while (live > cap / 4) cap *= 2;
+    unsigned long long* a = nullptr;
+    CU(dalloc(&a, (int64_t)cap));
+    k_d1_compact<<<(unsigned)ceil_div(n * 32, kBlock), kBlock, 0, c->st>>>(b.col_off, b.col_len, b.pos, n, b.arena, a);
+    c->launches += 2;
+    CU(cudaMemcpyAsync(b.ctr + 4, &live, 8, cudaMemcpyHostToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    cudaFree(b.arena);
+    b.arena = a;
+    b.arena_cap = cap;
+    *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = live;
+    return DMS_OK;
+}
+
 D1Args d1_args(dms_ctx* c, int phase) {
     D1Buf& b = c->d1;
     D1Args A;
     A.g = geo(c);
+    A.tab = b.tab;
     A.rank = c->rank;
     A.order = b.order;
     A.hkey = b.hkey;
@@ -1133,17 +1179,34 @@ D1Args d1_args(dms_ctx* c, int phase) {
     A.phase = phase;
     static const int lcap_env = getenv("DMS_D1_LCAP") ? atoi(getenv("DMS_D1_LCAP")) : kD1Cap;
     A.lcap = std::max(4, std::min(kD1Cap, lcap_env));
+    A.deps = b.deps;
+    A.ndeps = b.ctr + 14;
+    A.deps_cap = b.capdeps;
+    A.st_steps = b.stats ? b.stats : nullptr;
+    A.st_adds = b.stats ? b.stats + b.capsig : nullptr;
+    A.st_pushed = b.stats ? b.stats + 2 * b.capsig : nullptr;
     return A;
 }
 
 // rounds of one phase until no sigma is active (d1.cuh); the host reads the active
 // count (and the arena / invariant flags) once per round
-dms_status d1_rounds(dms_ctx* c, int phase) {
+dms_status d1_rounds(dms_ctx* c, int phase, int64_t nact) {
     D1Buf& b = c->d1;
-    int64_t nact = b.nsig;
     int cur = 0;
     int r = 0;
     static const int d1_ctas = getenv("DMS_D1_CTAS") ? atoi(getenv("DMS_D1_CTAS")) : 8;
+    static const bool stats = getenv("DMS_D1_STATS") && atoi(getenv("DMS_D1_STATS"));
+    static bool attr = false;
+    if (!attr) {
+        CU(cudaFuncSetAttribute(k_d1_bigc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+        attr = true;
+    }
+    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    if (stats) {
+        for (auto& x : e) cudaEventCreate(&x);
+        if (!b.stats) CU(dalloc(&b.stats, 3 * b.capsig));
+        CU(cudaMemsetAsync(b.stats, 0, 3 * b.capsig * sizeof(unsigned), c->st));
+    }
     while (nact > 0) {
         if (r > 1000000) return fail(c, DMS_ERR_INVARIANT, "D1: no progress");
         D1Args A = d1_args(c, phase);
@@ -1152,8 +1215,11 @@ dms_status d1_rounds(dms_ctx* c, int phase) {
         A.tag = (unsigned long long)(0xffffffffu - (uint32_t)r) << 32;
         CU(cudaMemsetAsync(b.ctr, 0, 4 * sizeof(int32_t), c->st));
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nact, 128), (int64_t)c->sms * d1_ctas);
+        if (stats) cudaEventRecord(e[0], c->st);
         k_d1_round<<<grid, 128, 0, c->st>>>(A);
-        k_d1_big<<<c->sms, 64, 0, c->st>>>(A);
+        if (stats) cudaEventRecord(e[1], c->st);
+        k_d1_bigc<<<c->sms * 3, kBigT, sizeof(BigSmem), c->st>>>(A);
+        if (stats) cudaEventRecord(e[2], c->st);
         k_d1_resolve<<<grid_for(nact), kBlock, 0, c->st>>>(A, b.act[cur ^ 1], b.ctr + 2);
         c->launches += 3;
         CU(cudaGetLastError());
@@ -1166,19 +1232,40 @@ dms_status d1_rounds(dms_ctx* c, int phase) {
                           phase, r, b.h_ctr[3] & 30, d[0], (unsigned long long)d[1], d[2], d[3]);
             return fail(c, DMS_ERR_INVARIANT, m);
         }
+        if (stats) {
+            float m0 = 0, m1 = 0;
+            cudaEventElapsedTime(&m0, e[0], e[1]);
+            cudaEventElapsedTime(&m1, e[1], e[2]);
+            std::fprintf(stderr, "[d1] phase %d round %d active %lld big %d round %.3f ms big %.3f ms arena %llu\n", phase, r,
+                         (long long)nact, b.h_ctr[0], m0, m1, *reinterpret_cast<unsigned long long*>(b.h_ctr + 4));
+        }
         nact = b.h_ctr[2];
         cur ^= 1;
         r++;
-        if (b.h_ctr[3] & 1) {  // arena full: grow it (the sigmas that did not fit are retried)
-            unsigned long long used = std::min<unsigned long long>(
-                *reinterpret_cast<unsigned long long*>(b.h_ctr + 4), b.arena_cap);
-            dms_status s = d1_grow_arena(c, 2 * b.arena_cap);
+        // arena more than half used (or full: the sigmas that did not fit are retried):
+        // collect it, doubling when the live columns need it
+        if ((b.h_ctr[3] & 1) || *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) > b.arena_cap / 2) {
+            dms_status s = d1_compact(c, (b.h_ctr[3] & 1) != 0);
             if (s) return s;
-            CU(cudaMemcpyAsync(b.ctr + 4, &used, 8, cudaMemcpyHostToDevice, c->st));
-            CU(cudaStreamSynchronize(c->st));
         }
     }
-    // the active list of the next phase starts as every sigma again
+    if (stats) {
+        for (auto& x : e) cudaEventDestroy(x);
+        std::vector<unsigned> h(3 * b.nsig);
+        for (int q = 0; q < 3; q++)
+            CU(cudaMemcpy(h.data() + q * b.nsig, b.stats + q * b.capsig, b.nsig * sizeof(unsigned), cudaMemcpyDeviceToHost));
+        std::vector<int64_t> idx(b.nsig);
+        for (int64_t i = 0; i < b.nsig; i++) idx[i] = i;
+        auto work = [&](int64_t i) { return (double)h[i] + h[2 * b.nsig + i]; };
+        std::sort(idx.begin(), idx.end(), [&](int64_t x, int64_t y) { return work(x) > work(y); });
+        double tot_s = 0, tot_p = 0, tot_a = 0;
+        for (int64_t i = 0; i < b.nsig; i++) { tot_s += h[i]; tot_a += h[b.nsig + i]; tot_p += h[2 * b.nsig + i]; }
+        std::fprintf(stderr, "[d1] phase %d totals: steps %.0f adds %.0f pushed %.0f\n", phase, tot_s, tot_a, tot_p);
+        for (int64_t k = 0; k < std::min<int64_t>(12, b.nsig); k++) {
+            const int64_t i = idx[k];
+            std::fprintf(stderr, "[d1]   sigma %lld steps %u adds %u pushed %u\n", (long long)i, h[i], h[b.nsig + i], h[2 * b.nsig + i]);
+        }
+    }
     b.rounds[phase - 1] = r;
     return DMS_OK;
 }
@@ -1211,7 +1298,8 @@ dms_status run_d1(dms_ctx* c, bool want_gen) {
         c->launches += 3;
         CU(cudaGetLastError());
         *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = top;
-        if ((s = d1_rounds(c, 1))) return s;
+        CU(cudaMemsetAsync(b.ctr + 14, 0, sizeof(int32_t), c->st));
+        if ((s = d1_rounds(c, 1, nsig))) return s;
         if (nsig) {
             k_d1_emit<<<grid_for(nsig), kBlock, 0, c->st>>>(g, b.stop, b.owner, c->unp[0], c->unp[1], nsig, b.pairs, b.ctr + 3);
             c->launches++;
@@ -1236,12 +1324,49 @@ dms_status run_d1(dms_ctx* c, bool want_gen) {
     }
     if (want_gen && !c->have_gen) {
         StageTimer tm(c, 11);
-        unsigned long long top = 3ull * nsig;
-        CU(cudaMemcpyAsync(b.ctr + 4, &top, 8, cudaMemcpyHostToDevice, c->st));
-        if (nsig) k_d1_init<<<grid_for(nsig), kBlock, 0, c->st>>>(g, c->rank, c->unp[1], nsig, b.arena, b.col_off, b.col_len, b.act[0], b.done);
-        c->launches++;
-        *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = top;
-        if ((s = d1_rounds(c, 2))) return s;
+        // taint: only the sigmas whose phase-1 column may differ from the sequential
+        // algorithm's are propagated again (d1.cuh k_d1_taint_*)
+        int32_t nd = 0;
+        CU(cudaMemcpyAsync(&nd, b.ctr + 14, 4, cudaMemcpyDeviceToHost, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        static const int all_env = getenv("DMS_D1_RERUN_ALL") ? atoi(getenv("DMS_D1_RERUN_ALL")) : 0;
+        if (nsig) {
+            if (nd > b.capdeps || all_env) {
+                k_fill_u32<<<grid_for(nsig), kBlock, 0, c->st>>>(b.taint, nsig, 1u);
+                c->launches++;
+            } else {
+                CU(cudaMemsetAsync(b.taint, 0, nsig * sizeof(uint32_t), c->st));
+                if (nd) k_d1_taint_direct<<<grid_for(nd), kBlock, 0, c->st>>>(b.deps, nd, b.owner, b.taint);
+                c->launches++;
+                for (int it = 0; nd && it < 100000; it++) {
+                    CU(cudaMemsetAsync(b.ctr + 15, 0, sizeof(int32_t), c->st));
+                    k_d1_taint_prop<<<grid_for(nd), kBlock, 0, c->st>>>(b.deps, nd, b.taint, b.ctr + 15);
+                    c->launches++;
+                    int32_t ch = 0;
+                    CU(cudaMemcpyAsync(&ch, b.ctr + 15, 4, cudaMemcpyDeviceToHost, c->st));
+                    CU(cudaStreamSynchronize(c->st));
+                    if (!ch) break;
+                }
+            }
+            scan_excl(b.taint, b.pos, nsig, c->ss, c->st, &c->launches);
+            uint32_t h[2];
+            CU(cudaMemcpyAsync(&h[0], b.pos + (nsig - 1), 4, cudaMemcpyDeviceToHost, c->st));
+            CU(cudaMemcpyAsync(&h[1], b.taint + (nsig - 1), 4, cudaMemcpyDeviceToHost, c->st));
+            CU(cudaStreamSynchronize(c->st));
+            b.ntaint = (int64_t)h[0] + h[1];
+            unsigned long long top = *reinterpret_cast<unsigned long long*>(b.h_ctr + 4);
+            if (top + 3ull * b.ntaint + 1024 > b.arena_cap) {
+                if ((s = d1_compact(c, true))) return s;
+                top = *reinterpret_cast<unsigned long long*>(b.h_ctr + 4);
+            }
+            k_d1_init_tainted<<<grid_for(nsig), kBlock, 0, c->st>>>(g, c->rank, c->unp[1], nsig, b.taint, b.pos, top,
+                                                                   b.arena, b.col_off, b.col_len, b.act[0], b.done);
+            c->launches++;
+            top += 3ull * b.ntaint;
+            CU(cudaMemcpyAsync(b.ctr + 4, &top, 8, cudaMemcpyHostToDevice, c->st));
+            *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = top;
+        }
+        if ((s = d1_rounds(c, 2, b.ntaint))) return s;
         b.ngen = 0;
         if (nsig) {
             k_d1_gen_len<<<grid_for(nsig), kBlock, 0, c->st>>>(b.col_len, nsig, b.flags);
@@ -1725,7 +1850,7 @@ int dms_internal_d1_rounds(dms_ctx* c, int out[2]) {
     if (!c) return -1;
     out[0] = c->d1.rounds[0];
     out[1] = c->d1.rounds[1];
-    return 0;
+    return (int)std::min<int64_t>(c->d1.ntaint, 0x7fffffff);
 }
 
 int dms_internal_uf_trace(dms_ctx* c, int which, int out[64]) {
@@ -1809,7 +1934,8 @@ void dms_destroy(dms_ctx* c) {
         for (void* p : {(void*)b.order, (void*)b.hkey, (void*)b.hval, (void*)b.owner, (void*)b.stop, (void*)b.done,
                         (void*)b.col_len, (void*)b.big, (void*)b.act[0], (void*)b.act[1], (void*)b.claim,
                         (void*)b.col_off, (void*)b.status, (void*)b.arena, (void*)b.ctr, (void*)b.flags,
-                        (void*)b.pos, (void*)b.pairs, (void*)b.un1, (void*)b.gen_off, (void*)b.gen})
+                        (void*)b.pos, (void*)b.pairs, (void*)b.un1, (void*)b.gen_off, (void*)b.gen, (void*)b.stats,
+                        (void*)b.deps, (void*)b.taint, (void*)b.tab})
             cudaFree(p);
         if (b.h_ctr) cudaFreeHost(b.h_ctr);
     }
