@@ -70,6 +70,11 @@ inline void build_d1_tab(const StarTab& S, D1Tab* T) {
     }
 }
 
+struct D1Snap {
+    int32_t sig, seq, len, pad;  // seq: owner columns added before this column was stored
+    long long off;
+};
+
 enum : uint8_t { D1_STOP = 1, D1_DONE = 2, D1_WAIT = 3, D1_BIG = 4, D1_RETRY = 5, D1_ERR = 6 };
 
 struct D1Args {
@@ -100,9 +105,14 @@ struct D1Args {
     unsigned long long tag;  // phase-1 claim tag (decreasing over rounds)
     int phase;
     int lcap;  // local heap capacity used (<= kD1Cap; smaller only to exercise the global path)
-    int4* deps;          // phase 1: (sigma, owner, edge) of every column added, for the taint pass
+    int4* deps;          // phase 1: (sigma, owner, edge, sigma's add number) of every column added
     int* ndeps;
     long long deps_cap;
+    int32_t* nadd;       // [nsig] owner columns added so far by the stored column of sigma
+    struct D1Snap* snaps;  // phase 1: every stored column (a snapshot of sigma's propagation)
+    int* nsnaps;
+    long long snaps_cap;
+    unsigned long long* prof;  // diagnostics (DMS_D1_STATS): k_d1_bigc cycles / counts per action
     unsigned* st_steps;  // diagnostics (DMS_D1_STATS): per sigma, regular steps / column adds / pushed keys
     unsigned* st_adds;
     unsigned* st_pushed;
@@ -200,10 +210,26 @@ __device__ __forceinline__ bool arena_alloc(const D1Args& A, unsigned long long 
 
 // phase 1: sigma added the column of owner o at edge j (its column stays the sequential
 // one iff o still owns j at the end and o's own column is -- see k_d1_taint*)
-__device__ __forceinline__ void d1_dep(const D1Args& A, int sig, int o, int j) {
+__device__ __forceinline__ void d1_dep(const D1Args& A, int sig, int o, int j, int seq) {
     if (A.phase != 1 || !A.deps) return;
     const int k = atomicAdd(A.ndeps, 1);
-    if (k < A.deps_cap) A.deps[k] = make_int4(sig, o, j, 0);
+    if (k < A.deps_cap) A.deps[k] = make_int4(sig, o, j, seq);
+}
+
+// phase 1: sigma's column was stored after `seq` owner columns: a restart point for the
+// generator pass if its later additions turn out not to be the sequential algorithm's
+__device__ __forceinline__ void d1_snap(const D1Args& A, int sig, int seq, long long off, int len) {
+    if (A.phase != 1 || !A.snaps) return;
+    const int k = atomicAdd(A.nsnaps, 1);
+    if (k < A.snaps_cap) {
+        D1Snap r;
+        r.sig = sig;
+        r.seq = seq;
+        r.len = len;
+        r.pad = 0;
+        r.off = off;
+        A.snaps[k] = r;
+    }
 }
 
 __device__ __noinline__ void d1_fail(const D1Args& A, int bit, int sig, unsigned long long tau, int j, int o) {
@@ -309,7 +335,7 @@ __device__ __forceinline__ bool d1_store(const D1Args& A, int sig, Heap<P>& H, u
 // status; on D1_BIG the heap (tau pushed back) is the column as a multiset.
 template <typename P, typename Room>
 __device__ __forceinline__ uint8_t d1_propagate(const D1Args& A, const D1Tab& S, int sig, Heap<P>& H, Room room,
-                                                unsigned long long& tau_out, int& j_out) {
+                                                unsigned long long& tau_out, int& j_out, int& nadds) {
     while (true) {
         const unsigned long long tau = H.popmax();
         if (!tau) {
@@ -359,7 +385,7 @@ __device__ __forceinline__ uint8_t d1_propagate(const D1Args& A, const D1Tab& S,
             // L2 loads: in phase 2 the column may have been written during this kernel by
             // another SM (its done flag was seen), so a stale L1 line must not serve it
             for (int i = 1; i < len; i++) H.push(__ldcg(A.arena + off + i));
-            d1_dep(A, sig, o, j);
+            d1_dep(A, sig, o, j, nadds++);
             if (A.st_adds) {
                 A.st_adds[sig]++;
                 A.st_pushed[sig] += len - 1;
@@ -373,12 +399,15 @@ __device__ __forceinline__ uint8_t d1_propagate(const D1Args& A, const D1Tab& S,
 }
 
 template <typename P>
-__device__ __forceinline__ void d1_finish(const D1Args& A, int sig, Heap<P>& H, uint8_t st, unsigned long long tau, int j) {
+__device__ __forceinline__ void d1_finish(const D1Args& A, int sig, Heap<P>& H, uint8_t st, unsigned long long tau, int j,
+                                          int nadds) {
     if (st == D1_STOP || st == D1_WAIT || st == D1_DONE) {
         if (!d1_store(A, sig, H, tau)) {
             A.status[sig] = D1_RETRY;
             return;
         }
+        A.nadd[sig] = nadds;
+        d1_snap(A, sig, nadds, A.col_off[sig], A.col_len[sig]);
         A.stop[sig] = j;
         if (st == D1_STOP) {
             atomicMin(A.claim + j, A.tag | (unsigned)sig);
@@ -422,7 +451,8 @@ __global__ void __launch_bounds__(128) k_d1_round(D1Args A) {
         for (int k = 0; k < len; k++) H.h[k] = A.arena[off + k];  // sorted descending = a heap
         unsigned long long tau = 0;
         int j = -1;
-        const uint8_t st = d1_propagate(A, S, sig, H, [&](int m) { return heap_room(A, H, m); }, tau, j);
+        int nadds = A.nadd[sig];
+        const uint8_t st = d1_propagate(A, S, sig, H, [&](int m) { return heap_room(A, H, m); }, tau, j, nadds);
         if (st == D1_BIG) {
             // hand the multiset over: the global path heapifies it
             unsigned long long o2;
@@ -433,11 +463,12 @@ __global__ void __launch_bounds__(128) k_d1_round(D1Args A) {
             for (int k = 0; k < H.n; k++) A.arena[o2 + k] = H.h[k];
             A.col_off[sig] = (long long)o2;
             A.col_len[sig] = -H.n;  // negative: an unsorted multiset
+            A.nadd[sig] = nadds;
             A.status[sig] = D1_BIG;
             A.big[atomicAdd(A.nbig, 1)] = sig;
             continue;
         }
-        d1_finish(A, sig, H, st, tau, j);
+        d1_finish(A, sig, H, st, tau, j, nadds);
     }
 }
 
@@ -469,7 +500,7 @@ struct BigSmem {
     E16 ring[kBigRing];
     int cnt[kBigT + 1];
     // control block (written by thread 0 before a barrier)
-    int action, pn, head, alen, rbase, rcnt, j, m, status, ok;
+    int action, pn, head, alen, rbase, rcnt, j, m, status, ok, nadds;
     long long aoff, oo;               // A's offset in the arena; owner column offset
     long long o_out, o_tmp;           // merge output / scratch of the current merge
     long long bbuf[2], tbuf;          // this run's reusable A buffers and merge scratch
@@ -692,6 +723,7 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
             sm.rcnt = 0;
             sm.cur = -1;
             sm.bcap[0] = sm.bcap[1] = sm.tcap = 0;
+            sm.nadds = A.nadd[sig];
             if (len0 >= 0) {  // [tau, sorted rest]: A = rest, P = {tau}
                 sm.aoff = off + 1;
                 sm.alen = len0 - 1;
@@ -703,7 +735,14 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
             }
         }
         __syncthreads();
+        long long pc_t = clock64(), pc_cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int pc_last = 0, pc_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         while (true) {
+            if (t == 0 && A.prof) {
+                const long long now = clock64();
+                pc_cyc[pc_last] += now - pc_t;
+                pc_t = now;
+            }
             if (t == 0) {
                 // serial propagation until the CTA is needed
                 int pn = sm.pn, head = sm.head;
@@ -766,7 +805,7 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                         if (add) __threadfence();
                     }
                     if (add) {
-                        d1_dep(A, sig, o, j);
+                        d1_dep(A, sig, o, j, sm.nadds++);
                         sm.oo = *(volatile const long long*)(A.col_off + o);
                         sm.m = *(volatile const int32_t*)(A.col_len + o);
                         if (A.st_adds) {
@@ -785,6 +824,13 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                 sm.pn = pn;
                 sm.head = head;
                 sm.action = action;
+                if (A.prof) {
+                    const long long now = clock64();
+                    pc_cyc[0] += now - pc_t;  // serial propagation
+                    pc_t = now;
+                    pc_last = action;
+                    pc_n[action]++;
+                }
             }
             __syncthreads();
             const int action = sm.action;
@@ -901,6 +947,8 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                 A.arena[outoff] = sm.tau.key;
                 A.col_off[sig] = outoff;
                 A.col_len[sig] = n + 1;
+                A.nadd[sig] = sm.nadds;
+                d1_snap(A, sig, sm.nadds, outoff, n + 1);
                 A.stop[sig] = sm.j;
                 const uint8_t st = (uint8_t)sm.status;
                 if (st == D1_STOP) {
@@ -913,6 +961,13 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
             }
             __syncthreads();
             break;
+        }
+        if (t == 0 && A.prof) {
+            pc_cyc[pc_last] += clock64() - pc_t;
+            for (int q = 0; q < 8; q++) {
+                atomicAdd(A.prof + q, (unsigned long long)pc_cyc[q]);
+                atomicAdd(A.prof + 8 + q, (unsigned long long)pc_n[q]);
+            }
         }
     }
 }
@@ -970,7 +1025,7 @@ __global__ void k_d1_hash(Geo3 g, const int32_t* __restrict__ rank, const int64_
 // the boundary of each sigma (three edge keys, sorted descending) at arena[3 i]
 __global__ void k_d1_init(Geo3 g, const int32_t* __restrict__ rank, const int64_t* __restrict__ sig_ids, int64_t nsig,
                           unsigned long long* arena, long long* col_off, int32_t* col_len, int32_t* active,
-                          int32_t* done) {
+                          int32_t* done, int32_t* nadd) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nsig) return;
     const StarTab& S = *g.tab;
@@ -989,6 +1044,7 @@ __global__ void k_d1_init(Geo3 g, const int32_t* __restrict__ rank, const int64_
     col_len[i] = 3;
     active[i] = (int32_t)i;
     done[i] = 0;
+    nadd[i] = 0;
 }
 
 // outputs ---------------------------------------------------------------------------
@@ -1030,29 +1086,46 @@ __global__ void k_fill_u32(uint32_t* a, int64_t n, uint32_t v) {
     if (i < n) a[i] = v;
 }
 
-// taint (phase 1 -> phase 2): a sigma's phase-1 column is the sequential algorithm's
-// unless it added a column whose owner lost that edge later, or a tainted owner's column
+// taint (phase 1 -> phase 2): sigma's phase-1 trajectory is the sequential algorithm's up
+// to its first addition of a column that is not the owner's final one -- the owner lost
+// that edge later, or its own final column is tainted.  first_bad[sigma] = the number of
+// that addition (0xffffffff: none, the phase-1 column is the generator).
 __global__ void k_d1_taint_direct(const int4* __restrict__ deps, int64_t nd, const int32_t* __restrict__ owner,
-                                  uint32_t* taint) {
+                                  uint32_t* first_bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nd) return;
     const int4 d = deps[i];
-    if (owner[d.z] != d.y) taint[d.x] = 1u;
+    if (owner[d.z] != d.y) atomicMin(first_bad + d.x, (uint32_t)d.w);
 }
-__global__ void k_d1_taint_prop(const int4* __restrict__ deps, int64_t nd, uint32_t* taint, int* changed) {
+__global__ void k_d1_taint_prop(const int4* __restrict__ deps, int64_t nd, uint32_t* first_bad, int* changed) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nd) return;
     const int4 d = deps[i];
-    if (taint[d.y] && !taint[d.x]) {
-        taint[d.x] = 1u;
-        *changed = 1;
+    if (first_bad[d.y] != 0xffffffffu && first_bad[d.x] > (uint32_t)d.w) {
+        if (atomicMin(first_bad + d.x, (uint32_t)d.w) > (uint32_t)d.w) *changed = 1;
     }
 }
+__global__ void k_d1_taint_flags(const uint32_t* __restrict__ first_bad, int64_t n, uint32_t* taint) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) taint[i] = first_bad[i] != 0xffffffffu ? 1u : 0u;
+}
+// the latest snapshot of a tainted sigma taken before its first bad addition
+__global__ void k_d1_snap_pick(const D1Snap* __restrict__ snaps, int64_t ns, const uint32_t* __restrict__ first_bad,
+                               unsigned long long* best) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    const D1Snap r = snaps[i];
+    const uint32_t fb = first_bad[r.sig];
+    if (fb != 0xffffffffu && (uint32_t)r.seq <= fb)
+        atomicMax(best + r.sig, ((unsigned long long)(r.seq + 1) << 32) | (unsigned long long)i);
+}
+
 // phase 2 starts with the tainted sigmas only: their boundaries at arena[base + 3 k]
 __global__ void k_d1_init_tainted(Geo3 g, const int32_t* __restrict__ rank, const int64_t* __restrict__ sig_ids,
                                   int64_t nsig, const uint32_t* __restrict__ taint, const uint32_t* __restrict__ pos,
                                   unsigned long long base, unsigned long long* arena, long long* col_off,
-                                  int32_t* col_len, int32_t* active, int32_t* done) {
+                                  int32_t* col_len, int32_t* active, int32_t* done,
+                                  const unsigned long long* __restrict__ best, const D1Snap* __restrict__ snaps) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nsig) return;
     if (!taint[i]) {
@@ -1060,6 +1133,13 @@ __global__ void k_d1_init_tainted(Geo3 g, const int32_t* __restrict__ rank, cons
         return;
     }
     done[i] = 0;
+    active[pos[i]] = (int32_t)i;
+    if (best && best[i]) {  // restart from the snapshot
+        const D1Snap r = snaps[best[i] & 0xffffffffull];
+        col_off[i] = r.off;
+        col_len[i] = r.len;
+        return;
+    }
     const StarTab& S = *g.tab;
     const int64_t id = sig_ids[i];
     const int64_t a = id / g.ncell[2];
@@ -1075,7 +1155,6 @@ __global__ void k_d1_init_tainted(Geo3 g, const int32_t* __restrict__ rank, cons
     for (int q = 0; q < 3; q++) arena[o + q] = e[q];
     col_off[i] = (long long)o;
     col_len[i] = 3;
-    active[pos[i]] = (int32_t)i;
 }
 
 // arena compaction: the live columns (one per sigma) copied to new offsets; one warp each

@@ -102,7 +102,8 @@ struct D1Buf {
     unsigned long long* arena = nullptr;
     unsigned long long arena_cap = 0;
     int32_t* ctr = nullptr;                   // [0] nbig, [1] grab, [2] nnext, [3] err; [4..5] arena top (u64),
-                                              // [6..13] first failure (4 x i64), [14] deps, [15] changed
+                                              // [6..13] first failure (4 x i64), [14] deps, [15] changed,
+                                              // [16] snapshots
     int32_t* h_ctr = nullptr;                 // pinned copy
     uint32_t *flags = nullptr, *pos = nullptr;
     PairRec* pairs = nullptr;
@@ -114,7 +115,12 @@ struct D1Buf {
     int4* deps = nullptr;                     // phase-1 column additions (taint pass)
     int64_t capdeps = 0;
     uint32_t* taint = nullptr;
-    int64_t ntaint = 0;
+    uint32_t* first_bad = nullptr;            // first non-sequential column addition per sigma
+    unsigned long long* best = nullptr;       // restart snapshot per tainted sigma
+    int32_t* nadd = nullptr;
+    D1Snap* snaps = nullptr;                  // phase-1 stored columns (restart points)
+    int64_t capsnaps = 0;
+    int64_t ntaint = 0, nrestart = 0;
     D1Tab* tab = nullptr;                     // device copy of the propagation tables
 };
 
@@ -1071,8 +1077,8 @@ dms_status d1_alloc(dms_ctx* c, int64_t n0, int64_t nsig) {
         CU(cudaMemcpy(b.tab, &h, sizeof(D1Tab), cudaMemcpyHostToDevice));
     }
     if (!b.ctr) {
-        CU(dalloc(&b.ctr, 16));
-        if (cudaMallocHost(&b.h_ctr, 16 * sizeof(int32_t)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
+        CU(dalloc(&b.ctr, 24));
+        if (cudaMallocHost(&b.h_ctr, 24 * sizeof(int32_t)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
     }
     if (c->N > b.capN) {
         cudaFree(b.order);
@@ -1109,6 +1115,15 @@ dms_status d1_alloc(dms_ctx* c, int64_t n0, int64_t nsig) {
         CU(dalloc(&b.gen_off, cap + 1));
         cudaFree(b.taint);
         CU(dalloc(&b.taint, cap));
+        cudaFree(b.first_bad);
+        CU(dalloc(&b.first_bad, cap));
+        cudaFree(b.best);
+        CU(dalloc(&b.best, cap));
+        cudaFree(b.nadd);
+        CU(dalloc(&b.nadd, cap));
+        cudaFree(b.snaps);
+        b.capsnaps = std::max<int64_t>(1 << 20, 4 * cap);
+        CU(dalloc(&b.snaps, b.capsnaps));
         cudaFree(b.deps);
         b.capdeps = std::max<int64_t>(1 << 20, 4 * cap);
         CU(dalloc(&b.deps, b.capdeps));
@@ -1182,6 +1197,11 @@ D1Args d1_args(dms_ctx* c, int phase) {
     A.deps = b.deps;
     A.ndeps = b.ctr + 14;
     A.deps_cap = b.capdeps;
+    A.nadd = b.nadd;
+    A.snaps = b.snaps;
+    A.nsnaps = b.ctr + 16;
+    A.snaps_cap = b.capsnaps;
+    A.prof = b.stats ? reinterpret_cast<unsigned long long*>(b.stats + 3 * b.capsig) : nullptr;
     A.st_steps = b.stats ? b.stats : nullptr;
     A.st_adds = b.stats ? b.stats + b.capsig : nullptr;
     A.st_pushed = b.stats ? b.stats + 2 * b.capsig : nullptr;
@@ -1204,8 +1224,8 @@ dms_status d1_rounds(dms_ctx* c, int phase, int64_t nact) {
     cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
     if (stats) {
         for (auto& x : e) cudaEventCreate(&x);
-        if (!b.stats) CU(dalloc(&b.stats, 3 * b.capsig));
-        CU(cudaMemsetAsync(b.stats, 0, 3 * b.capsig * sizeof(unsigned), c->st));
+        if (!b.stats) CU(dalloc(&b.stats, 3 * b.capsig + 64));
+        CU(cudaMemsetAsync(b.stats, 0, (3 * b.capsig + 64) * sizeof(unsigned), c->st));
     }
     while (nact > 0) {
         if (r > 1000000) return fail(c, DMS_ERR_INVARIANT, "D1: no progress");
@@ -1244,8 +1264,22 @@ dms_status d1_rounds(dms_ctx* c, int phase, int64_t nact) {
         r++;
         // arena more than half used (or full: the sigmas that did not fit are retried):
         // collect it, doubling when the live columns need it
+        // (phase 1 keeps every stored column -- the restart snapshots of the generator
+        // pass -- so it grows the arena instead of collecting it)
         if ((b.h_ctr[3] & 1) || *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) > b.arena_cap / 2) {
-            dms_status s = d1_compact(c, (b.h_ctr[3] & 1) != 0);
+            dms_status s;
+            if (phase == 1) {
+                const unsigned long long used = std::min<unsigned long long>(
+                    *reinterpret_cast<unsigned long long*>(b.h_ctr + 4), b.arena_cap);
+                s = d1_grow_arena(c, 2 * b.arena_cap);
+                if (!s) {
+                    CU(cudaMemcpyAsync(b.ctr + 4, &used, 8, cudaMemcpyHostToDevice, c->st));
+                    CU(cudaStreamSynchronize(c->st));
+                    *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = used;
+                }
+            } else {
+                s = d1_compact(c, (b.h_ctr[3] & 1) != 0);
+            }
             if (s) return s;
         }
     }
@@ -1261,6 +1295,11 @@ dms_status d1_rounds(dms_ctx* c, int phase, int64_t nact) {
         double tot_s = 0, tot_p = 0, tot_a = 0;
         for (int64_t i = 0; i < b.nsig; i++) { tot_s += h[i]; tot_a += h[b.nsig + i]; tot_p += h[2 * b.nsig + i]; }
         std::fprintf(stderr, "[d1] phase %d totals: steps %.0f adds %.0f pushed %.0f\n", phase, tot_s, tot_a, tot_p);
+        unsigned long long pr[16];
+        CU(cudaMemcpy(pr, b.stats + 3 * b.capsig, sizeof pr, cudaMemcpyDeviceToHost));
+        const char* nm[8] = {"serial", "refill", "mergeP", "addS", "addB", "stop", "abort", "-"};
+        for (int q = 0; q < 7; q++)
+            std::fprintf(stderr, "[d1]   bigc %-7s %12.3f Mcycles  n %llu\n", nm[q], pr[q] / 1e6, pr[8 + q]);
         for (int64_t k = 0; k < std::min<int64_t>(12, b.nsig); k++) {
             const int64_t i = idx[k];
             std::fprintf(stderr, "[d1]   sigma %lld steps %u adds %u pushed %u\n", (long long)i, h[i], h[b.nsig + i], h[2 * b.nsig + i]);
@@ -1294,11 +1333,12 @@ dms_status run_d1(dms_ctx* c, bool want_gen) {
         CU(cudaMemsetAsync(b.claim, 0xff, n0 * sizeof(unsigned long long), c->st));
         unsigned long long top = 3ull * nsig;
         CU(cudaMemcpyAsync(b.ctr + 4, &top, 8, cudaMemcpyHostToDevice, c->st));
-        if (nsig) k_d1_init<<<grid_for(nsig), kBlock, 0, c->st>>>(g, c->rank, c->unp[1], nsig, b.arena, b.col_off, b.col_len, b.act[0], b.done);
+        if (nsig) k_d1_init<<<grid_for(nsig), kBlock, 0, c->st>>>(g, c->rank, c->unp[1], nsig, b.arena, b.col_off, b.col_len, b.act[0], b.done, b.nadd);
         c->launches += 3;
         CU(cudaGetLastError());
         *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = top;
         CU(cudaMemsetAsync(b.ctr + 14, 0, sizeof(int32_t), c->st));
+        CU(cudaMemsetAsync(b.ctr + 16, 0, sizeof(int32_t), c->st));
         if ((s = d1_rounds(c, 1, nsig))) return s;
         if (nsig) {
             k_d1_emit<<<grid_for(nsig), kBlock, 0, c->st>>>(g, b.stop, b.owner, c->unp[0], c->unp[1], nsig, b.pairs, b.ctr + 3);
@@ -1326,26 +1366,37 @@ dms_status run_d1(dms_ctx* c, bool want_gen) {
         StageTimer tm(c, 11);
         // taint: only the sigmas whose phase-1 column may differ from the sequential
         // algorithm's are propagated again (d1.cuh k_d1_taint_*)
-        int32_t nd = 0;
+        int32_t nd = 0, nsn = 0;
         CU(cudaMemcpyAsync(&nd, b.ctr + 14, 4, cudaMemcpyDeviceToHost, c->st));
+        CU(cudaMemcpyAsync(&nsn, b.ctr + 16, 4, cudaMemcpyDeviceToHost, c->st));
         CU(cudaStreamSynchronize(c->st));
         static const int all_env = getenv("DMS_D1_RERUN_ALL") ? atoi(getenv("DMS_D1_RERUN_ALL")) : 0;
+        static const int snap_env = getenv("DMS_D1_SNAPSHOTS") ? atoi(getenv("DMS_D1_SNAPSHOTS")) : 1;
+        const bool use_snaps = snap_env && !all_env && nd <= b.capdeps;
         if (nsig) {
             if (nd > b.capdeps || all_env) {
                 k_fill_u32<<<grid_for(nsig), kBlock, 0, c->st>>>(b.taint, nsig, 1u);
                 c->launches++;
             } else {
-                CU(cudaMemsetAsync(b.taint, 0, nsig * sizeof(uint32_t), c->st));
-                if (nd) k_d1_taint_direct<<<grid_for(nd), kBlock, 0, c->st>>>(b.deps, nd, b.owner, b.taint);
+                CU(cudaMemsetAsync(b.first_bad, 0xff, nsig * sizeof(uint32_t), c->st));
+                if (nd) k_d1_taint_direct<<<grid_for(nd), kBlock, 0, c->st>>>(b.deps, nd, b.owner, b.first_bad);
                 c->launches++;
                 for (int it = 0; nd && it < 100000; it++) {
                     CU(cudaMemsetAsync(b.ctr + 15, 0, sizeof(int32_t), c->st));
-                    k_d1_taint_prop<<<grid_for(nd), kBlock, 0, c->st>>>(b.deps, nd, b.taint, b.ctr + 15);
+                    k_d1_taint_prop<<<grid_for(nd), kBlock, 0, c->st>>>(b.deps, nd, b.first_bad, b.ctr + 15);
                     c->launches++;
                     int32_t ch = 0;
                     CU(cudaMemcpyAsync(&ch, b.ctr + 15, 4, cudaMemcpyDeviceToHost, c->st));
                     CU(cudaStreamSynchronize(c->st));
                     if (!ch) break;
+                }
+                k_d1_taint_flags<<<grid_for(nsig), kBlock, 0, c->st>>>(b.first_bad, nsig, b.taint);
+                c->launches++;
+                if (use_snaps) {
+                    CU(cudaMemsetAsync(b.best, 0, nsig * sizeof(unsigned long long), c->st));
+                    const int64_t ns = std::min<int64_t>(nsn, b.capsnaps);
+                    if (ns) k_d1_snap_pick<<<grid_for(ns), kBlock, 0, c->st>>>(b.snaps, ns, b.first_bad, b.best);
+                    c->launches++;
                 }
             }
             scan_excl(b.taint, b.pos, nsig, c->ss, c->st, &c->launches);
@@ -1355,12 +1406,12 @@ dms_status run_d1(dms_ctx* c, bool want_gen) {
             CU(cudaStreamSynchronize(c->st));
             b.ntaint = (int64_t)h[0] + h[1];
             unsigned long long top = *reinterpret_cast<unsigned long long*>(b.h_ctr + 4);
-            if (top + 3ull * b.ntaint + 1024 > b.arena_cap) {
-                if ((s = d1_compact(c, true))) return s;
-                top = *reinterpret_cast<unsigned long long*>(b.h_ctr + 4);
+            if (top + 3ull * b.ntaint + 1024 > b.arena_cap) {  // grow (the snapshots must stay put)
+                if ((s = d1_grow_arena(c, 2 * (top + 3ull * b.ntaint + 1024)))) return s;
             }
             k_d1_init_tainted<<<grid_for(nsig), kBlock, 0, c->st>>>(g, c->rank, c->unp[1], nsig, b.taint, b.pos, top,
-                                                                   b.arena, b.col_off, b.col_len, b.act[0], b.done);
+                                                                   b.arena, b.col_off, b.col_len, b.act[0], b.done,
+                                                                   use_snaps ? b.best : nullptr, b.snaps);
             c->launches++;
             top += 3ull * b.ntaint;
             CU(cudaMemcpyAsync(b.ctr + 4, &top, 8, cudaMemcpyHostToDevice, c->st));
@@ -1935,7 +1986,8 @@ void dms_destroy(dms_ctx* c) {
                         (void*)b.col_len, (void*)b.big, (void*)b.act[0], (void*)b.act[1], (void*)b.claim,
                         (void*)b.col_off, (void*)b.status, (void*)b.arena, (void*)b.ctr, (void*)b.flags,
                         (void*)b.pos, (void*)b.pairs, (void*)b.un1, (void*)b.gen_off, (void*)b.gen, (void*)b.stats,
-                        (void*)b.deps, (void*)b.taint, (void*)b.tab})
+                        (void*)b.deps, (void*)b.taint, (void*)b.tab, (void*)b.first_bad, (void*)b.best,
+                        (void*)b.nadd, (void*)b.snaps})
             cudaFree(p);
         if (b.h_ctr) cudaFreeHost(b.h_ctr);
     }
