@@ -75,8 +75,8 @@ typedef enum {
 } dms_status;
 
 typedef enum {
-    DMS_BOUNDARY_EXACT = 0, /* virtual maximum on the boundary (PAPER.md 2787-2825) */
-    DMS_BOUNDARY_IGNORE = 1 /* Appendix A variant: not built, returns DMS_ERR_STATE  */
+    DMS_BOUNDARY_EXACT = 0, /* virtual maximum on the boundary (PAPER.md 2787-2825)          */
+    DMS_BOUNDARY_IGNORE = 1 /* no virtual maximum (PAPER.md 2822-2825, App. A 2927-2949)      */
 } dms_boundary;
 
 /* One persistence pair (PAPER.md 1641-1697).  death_id = -1 marks an infinite class
@@ -128,8 +128,19 @@ dms_status dms_critical(dms_ctx* ctx, int64_t h_count[4], const int64_t* d_ids_o
 dms_status dms_diagram0(dms_ctx* ctx, const dms_pair** d_pairs, int64_t* h_n);
 
 /* D_{d-1} (Sec. 5.2): pairs (critical (d-1)-simplex, critical d-simplex) in
- * decreasing birth lex order; for d = 1 the infinite class of the global minimum
- * follows.  mode must be DMS_BOUNDARY_EXACT.  Synchronises. */
+ * decreasing birth lex order.
+ * mode (a dms_boundary value):
+ *   DMS_BOUNDARY_EXACT  a virtual maximum, older than every maximum, on the outer
+ *       boundary (PAPER.md 2810-2817): every maximum dies; equals the boundary-matrix
+ *       reduction.  For d = 1 the infinite class of the global minimum follows.
+ *   DMS_BOUNDARY_IGNORE no virtual maximum (PAPER.md 2822-2825, App. A 2927-2949;
+ *       DESIGN.md reading Z7): an arc whose stable-set tracing leaves through the
+ *       boundary is dropped (its saddle stays unpaired), the global maximum stays
+ *       unpaired -- its class is D0's infinite (global min, f*) record, "paired by
+ *       convention to the global minimum" -- and there are no infinite records.
+ *       Computed from the exact mode's arcs (run first if needed); the exact results
+ *       and the D1 hand-off (dms_unpaired_saddles) are unchanged.
+ * Other values -> DMS_ERR_ARG.  Synchronises. */
 dms_status dms_diagram_top(dms_ctx* ctx, int mode, const dms_pair** d_pairs, int64_t* h_n);
 
 /* Critical saddles left unpaired (the "sandwich" hand-off, PAPER.md 1125-1155:

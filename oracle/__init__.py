@@ -16,6 +16,8 @@ Parity status per function:
   critical lists   pinned  (brute-force lexicographic sort, hand-built fields)
   D0               pinned  (brute-force Kruskal over all edges; boundary-matrix reduction)
   D_{d-1}          pinned  (brute-force boundary-matrix reduction, vertex level)
+  D_{d-1} ignore   pinned  (brute-force Kruskal over the interior facets of the dual
+                            graph, elder rule, vertex level; hand-built fields)
   D1 (3D)          pinned  (brute-force boundary-matrix reduction, vertex level; count
                             identities |D1| = |C1|-|D0| = |C2|-|D2|; solid-torus field)
   generators       pinned  (mod-2 cycles, highest edge = the birth edge, homologous to
@@ -46,7 +48,7 @@ PAIR_DTYPE = np.dtype(
 )
 
 (ORC_CRIT, ORC_PAIRS, ORC_D0, ORC_DTOP, ORC_UN0, ORC_UNTOP, ORC_ARCS0, ORC_ARCSTOP, ORC_MS, ORC_D1,
- ORC_GEN_OFF, ORC_GEN, ORC_UN1) = range(13)
+ ORC_GEN_OFF, ORC_GEN, ORC_UN1, ORC_DTOP_IGN) = range(14)
 
 
 def build(force: bool = False) -> str:
@@ -136,6 +138,8 @@ class Result:
         if full:
             self.d0 = arr(ORC_D0, 0, PAIR_DTYPE)
             self.dtop = arr(ORC_DTOP, 0, PAIR_DTYPE)
+            # D_{d-1} in the "ignore" boundary mode (no virtual maximum; App. A)
+            self.dtop_ignore = arr(ORC_DTOP_IGN, 0, PAIR_DTYPE)
             self.unpaired0 = arr(ORC_UN0, 0, np.int64)
             self.unpaired_top = arr(ORC_UNTOP, 0, np.int64)
             self.arcs0 = arr(ORC_ARCS0, 0, np.int64, 2)

@@ -16,6 +16,7 @@
  *   O5 D0                -- Sec. 5.1 unstable sets + Union-Find
  *   O6 D_{d-1}           -- Sec. 5.2 dual gradient, stable sets, UF in decreasing
  *                           order, virtual maximum on the boundary
+ *                           ("ignore" mode: boundary arcs dropped)
  *   O8 infinite classes  -- Sec. 6
  *
  * Parity pins: tests/test_oracle_pins.py (hand-built fields, SPEC examples, Euler
@@ -468,8 +469,8 @@ typedef struct orc_result {
     int64_t *crit[ORC_MAXD];     /* ids, lexicographically sorted (full run) */
     int64_t npairs;
     int64_t *pairs;              /* gradient pairs, triples */
-    int64_t nd0, ndtop;
-    orc_pair *d0, *dtop;
+    int64_t nd0, ndtop, ndtop_ign;
+    orc_pair *d0, *dtop, *dtop_ign;  /* dtop_ign: D_{d-1} in the "ignore" boundary mode */
     int64_t nun0, nuntop;
     int64_t *un0, *untop;        /* unpaired saddles after D0 / D_{d-1} */
     int64_t *arcs0, *arcstop;    /* per arc: the two extremum ends (ids; -1 = VIRTUAL) */
@@ -828,6 +829,29 @@ int orc_run2(int ndim, const int64_t *L, const float *f, int nthreads, int flags
             for (int64_t j = 0; j < r->nuntop; j++)
                 r->dtop[r->ndtop++] = mkpair(g, 0, r->untop[j], 1, -1, fstar);
         qsort(r->untop, r->nuntop, sizeof(int64_t), cmp_i64);
+
+        /* O6' "ignore" boundary mode (App. A; reading Z7): no
+         * virtual maximum -- an arc that reaches the boundary is dropped (its saddle
+         * stays unpaired), the same Union-Find in decreasing order runs on the other
+         * arcs, and the global maximum is left unpaired (its class is the D0 infinite
+         * class (global min, f*), "paired by convention to the global minimum", Sec. 6).
+         * No infinite records. */
+        for (int64_t i = 0; i < r->ncrit[d]; i++) parent[r->crit[d][i]] = r->crit[d][i];
+        r->dtop_ign = malloc((m + 1) * sizeof(orc_pair));
+        r->ndtop_ign = 0;
+        for (int64_t i = m - 1; i >= 0; i--) {
+            const int64_t e0 = r->arcstop[2 * i], e1 = r->arcstop[2 * i + 1];
+            if (e0 < 0 || e1 < 0) continue;  /* a half-arc to the outside: dropped */
+            int64_t a = uf_find(parent, e0), b = uf_find(parent, e1);
+            if (a == b) continue;
+            simp sa, sb;
+            simp_from_id(g, d, a, &sa);
+            simp_from_id(g, d, b, &sb);
+            int64_t young, old;
+            if (lexcmp(g, &sa, &sb) < 0) { young = a; old = b; } else { young = b; old = a; }
+            r->dtop_ign[r->ndtop_ign++] = mkpair(g, d - 1, r->crit[d - 1][i], d, young, fstar);
+            parent[young] = old;
+        }
         free(parent);
     }
     /* unpaired lists in ascending lexicographic order */
@@ -1004,7 +1028,7 @@ int orc_gradient_sample(int ndim, const int64_t *L, const float *f, const int64_
 
 enum { ORC_CRIT = 0, ORC_PAIRS = 1, ORC_D0 = 2, ORC_DTOP = 3, ORC_UN0 = 4, ORC_UNTOP = 5,
        ORC_ARCS0 = 6, ORC_ARCSTOP = 7, ORC_MS = 8, ORC_D1 = 9, ORC_GEN_OFF = 10, ORC_GEN = 11,
-       ORC_UN1 = 12 };
+       ORC_UN1 = 12, ORC_DTOP_IGN = 13 };
 
 int64_t orc_count(const orc_result *r, int what, int k)
 {
@@ -1022,6 +1046,7 @@ int64_t orc_count(const orc_result *r, int what, int k)
     case ORC_GEN_OFF: return r->gen_off ? r->nd1 + 1 : 0;
     case ORC_GEN: return r->gen_off ? r->gen_off[r->nd1] : 0;
     case ORC_UN1: return r->un1 ? r->nun1 : 0;
+    case ORC_DTOP_IGN: return r->dtop_ign ? r->ndtop_ign : 0;
     }
     return 0;
 }
@@ -1043,6 +1068,7 @@ void orc_copy(const orc_result *r, int what, int k, void *dst)
     case ORC_GEN_OFF: memcpy(dst, r->gen_off, n * sizeof(int64_t)); break;
     case ORC_GEN: memcpy(dst, r->gen, n * sizeof(int64_t)); break;
     case ORC_UN1: memcpy(dst, r->un1, n * sizeof(int64_t)); break;
+    case ORC_DTOP_IGN: memcpy(dst, r->dtop_ign, n * sizeof(orc_pair)); break;
     }
 }
 
@@ -1053,6 +1079,7 @@ void orc_free(orc_result *r)
     free(r->pairs);
     free(r->d0);
     free(r->dtop);
+    free(r->dtop_ign);
     free(r->un0);
     free(r->untop);
     free(r->arcs0);

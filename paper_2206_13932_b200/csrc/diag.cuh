@@ -496,6 +496,25 @@ __global__ void k_uf_init(int32_t* parent, unsigned long long* best, int64_t n, 
     }
 }
 
+// "ignore" boundary mode (PAPER.md 2822-2825, App. A; reading Z7): the arcs of the exact
+// mode with every end at the virtual maximum `virt` replaced by the other end -- a
+// self-loop, which the union-find leaves unpaired (the half-arc is dropped)
+__global__ void k_arcs_drop_virtual(const int32_t* __restrict__ a_in, const int32_t* __restrict__ b_in,
+                                    const uint32_t* __restrict__ key_in, int64_t m, int32_t virt,
+                                    const int32_t* __restrict__ age_in, int64_t nodes, int32_t* a_out,
+                                    int32_t* b_out, uint32_t* key_out, int32_t* age_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        int32_t a = a_in[i], b = b_in[i];
+        if (a == virt) a = b;
+        if (b == virt) b = a;
+        a_out[i] = a;
+        b_out[i] = b;
+        key_out[i] = key_in[i];
+    }
+    if (i < nodes) age_out[i] = age_in[i];
+}
+
 // the arc records in processing (key) order for the batched rounds: src[j] = the arc
 // with key j (perm: processing index -> emission index; rev: D_{d-1}'s descending order)
 __global__ void k_uf_src(const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b,

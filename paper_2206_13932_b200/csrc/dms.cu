@@ -211,6 +211,10 @@ struct dms_ctx {
     bool order_fresh = false;  // an order computed since the last gradient pass
     bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
     bool have_d1 = false, have_gen = false;  // D1 pairs / generators of the current diagrams
+    bool have_ign = false;                   // D_{d-1} in the "ignore" boundary mode
+    UFBuf uf_ign;
+    PairRec* pairs_ign = nullptr;
+    int64_t npairs_ign = 0, cap_ign = 0;
     D1Buf d1;
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[12];
@@ -425,7 +429,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
         CU(cudaGetLastError());
         c->have_order = true;
         c->order_fresh = true;
-        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;
+        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
         return DMS_OK;
     }
     // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
@@ -444,7 +448,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     CU(cudaGetLastError());
     c->have_order = true;
     c->order_fresh = true;
-    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;  // the gradient does not depend on ranks
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;  // the gradient does not depend on ranks
     return DMS_OK;
 }
 
@@ -543,7 +547,7 @@ dms_status run_gradient(dms_ctx* c, void* d_grad) {
     dms_status s = launch_gradient(c, 0, c->N);
     if (s) return s;
     c->have_grad = true;
-    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
     return DMS_OK;
 }
 
@@ -992,6 +996,44 @@ dms_status dtop_finish(dms_ctx* c) {
     stage_end(c, 4, c->t_diag[1]);
     c->t_diag[1] = nullptr;
     c->have_d[1] = true;
+    return DMS_OK;
+}
+
+// D_{d-1} in the "ignore" boundary mode (PAPER.md 2822-2825, App. A 2927-2949; reading
+// Z7): the exact mode's arcs with the half-arcs to the virtual maximum dropped, the same
+// union-find in decreasing order; the global maximum stays unpaired (its class is D0's
+// infinite one, Sec. 6); no infinite records.  The exact results are left untouched.
+dms_status run_dtop_ignore(dms_ctx* c) {
+    const int d = c->ndim;
+    UFBuf& e = c->uf[1];
+    UFBuf& u = c->uf_ign;
+    const int64_t m = c->ncrit[d - 1], nd = c->ncrit[d];
+    dms_status s = alloc_uf(c, u, m, nd + 1);
+    if (s) return s;
+    Geo3 g = geo(c);
+    k_arcs_drop_virtual<<<grid_for(std::max(m, nd + 1)), kBlock, 0, c->st>>>(e.arc_a, e.arc_b, e.key, m, (int32_t)nd,
+                                                                          e.age, nd + 1, u.arc_a, u.arc_b, u.key,
+                                                                          u.age);
+    c->launches++;
+    if ((s = uf_issue(c, u, m, nd + 1, d - 1, 1))) return s;
+    if ((s = uf_finish(c, u, m))) return s;
+    out_to_processing(c, u, d - 1, m, 1);
+    int64_t np = 0;
+    if ((s = flag_scan(c, u, m, 0, &np))) return s;
+    if (np + 1 > c->cap_ign) {
+        cudaFree(c->pairs_ign);
+        c->pairs_ign = nullptr;
+        CU(dalloc(&c->pairs_ign, 2 * np + 1024));
+        c->cap_ign = 2 * np + 1024;
+    }
+    if (np) {
+        k_emit_dtop<<<grid_for(m), kBlock, 0, c->st>>>(g, u.out, m, u.pos, crit_ids(c, d - 1), crit_ids_emitted(c, d),
+                                                      c->pairs_ign);
+        c->launches++;
+    }
+    CU(cudaGetLastError());
+    c->npairs_ign = np;
+    c->have_ign = true;
     return DMS_OK;
 }
 
@@ -1652,11 +1694,20 @@ dms_status dms_diagram_top(dms_ctx* c, int mode, const dms_pair** d_pairs, int64
     dms_status s = check_sticky(c);
     if (s) return s;
     if (!d_pairs || !h_n) return DMS_ERR_ARG;
-    if (mode == DMS_BOUNDARY_IGNORE) return fail(c, DMS_ERR_STATE, "DMS_BOUNDARY_IGNORE is not built");
-    if (mode != DMS_BOUNDARY_EXACT) return DMS_ERR_ARG;
+    if (mode != DMS_BOUNDARY_EXACT && mode != DMS_BOUNDARY_IGNORE) return DMS_ERR_ARG;
     if (!c->have_d[1]) {
         s = run_dtop(c);
         if (s) return s;
+    }
+    if (mode == DMS_BOUNDARY_IGNORE) {
+        if (!c->have_ign) {
+            if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+            if ((s = run_dtop_ignore(c))) return s;
+        }
+        if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
+        *d_pairs = reinterpret_cast<const dms_pair*>(c->pairs_ign);
+        *h_n = c->npairs_ign;
+        return DMS_OK;
     }
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
     *d_pairs = reinterpret_cast<const dms_pair*>(c->pairs[1]);
@@ -1771,7 +1822,7 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
     }
     c->have_grad = true;
     c->order_fresh = false;
-    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = false;
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
     if ((s = run_critical(c))) return s;
     if ((s = run_diagrams(c))) return s;
     return DMS_OK;
@@ -1979,6 +2030,16 @@ void dms_destroy(dms_ctx* c) {
         if (u.h_cnt) cudaFreeHost(u.h_cnt);
         cudaFree(c->pairs[b]);
         cudaFree(c->unp[b]);
+    }
+    {
+        UFBuf& u = c->uf_ign;
+        for (void* p : {(void*)u.arc_a, (void*)u.arc_b, (void*)u.rec0, (void*)u.rec1, (void*)u.rsrc, (void*)u.out, (void*)u.list,
+                        (void*)u.live2, (void*)u.nlive, (void*)u.trace, (void*)u.outp, (void*)u.key,
+                        (void*)u.inv_a, (void*)u.age, (void*)u.parent, (void*)u.best, (void*)u.flags, (void*)u.pos})
+            cudaFree(p);
+        if (u.h_status) cudaFreeHost(u.h_status);
+        if (u.h_cnt) cudaFreeHost(u.h_cnt);
+        cudaFree(c->pairs_ign);
     }
     {
         D1Buf& b = c->d1;

@@ -40,6 +40,7 @@ def gpu_run(env, f):
         crit=[c.cpu().numpy() for c in d.critical()],
         d0=d.diagram0(),
         dtop=d.diagram_top(),
+        dtop_ign=d.diagram_top(mode=1),
         un0=d.unpaired_saddles(0),
         untop=d.unpaired_saddles(1),
         launches=d.launch_count(),
@@ -61,6 +62,7 @@ def compare_full(env, f, nthreads=NCPU):
         assert np.array_equal(got["crit"][k], ref.crit[k]), ("C_%d" % k)
     assert got["d0"].tobytes() == ref.d0.tobytes(), "D0"
     assert got["dtop"].tobytes() == ref.dtop.tobytes(), "D_{d-1}"
+    assert got["dtop_ign"].tobytes() == ref.dtop_ignore.tobytes(), "D_{d-1} ignore mode"
     assert np.array_equal(got["un0"], ref.unpaired0), "unpaired after D0"
     assert np.array_equal(got["untop"], ref.unpaired_top), "unpaired after D_{d-1}"
     assert got["launches"] > 0
@@ -132,7 +134,7 @@ def test_nan_rejected(env):
     assert e.value.name == "DMS_ERR_NAN"
 
 
-def test_degenerate_and_ignore_mode(env):
+def test_degenerate_and_bad_mode(env):
     torch, dms = env
     for shape in [(1, 4, 4), (4, 1), (1,)]:
         with pytest.raises(dms.DMSError) as e:
@@ -140,8 +142,8 @@ def test_degenerate_and_ignore_mode(env):
         assert e.value.name == "DMS_ERR_DEGENERATE"
     d = dms.DMS(torch.rand(5, 5, 5, device="cuda"))
     with pytest.raises(dms.DMSError) as e:
-        d.diagram_top(mode=1)
-    assert e.value.name == "DMS_ERR_STATE"
+        d.diagram_top(mode=7)
+    assert e.value.name == "DMS_ERR_ARG"
 
 
 def test_deterministic_repeat(env):
@@ -208,3 +210,47 @@ def test_run_all_host_pageable_input(env):
     for k in range(f.ndim + 1):
         assert np.array_equal(d.critical()[k].cpu().numpy(), ref["crit"][k])
     d.close()
+
+
+def _w2(a, b):
+    """L2-Wasserstein distance between two finite persistence diagrams (Sec. 2.4):
+    an optimal matching where a point may also go to its diagonal projection."""
+    from scipy.optimize import linear_sum_assignment
+
+    A = np.array([(float(p["birth_value"]), float(p["death_value"])) for p in a]).reshape(-1, 2)
+    B = np.array([(float(p["birth_value"]), float(p["death_value"])) for p in b]).reshape(-1, 2)
+    n, m = len(A), len(B)
+    if n + m == 0:
+        return 0.0
+    big = np.zeros((n + m, n + m))
+    dA = ((A[:, 1] - A[:, 0]) / 2.0) ** 2 * 2.0  # squared distance to the diagonal
+    dB = ((B[:, 1] - B[:, 0]) / 2.0) ** 2 * 2.0
+    big[:n, :m] = ((A[:, None, :] - B[None, :, :]) ** 2).sum(-1)
+    big[:n, m:] = dA[:, None]
+    big[n:, :m] = dB[None, :]
+    r, c = linear_sum_assignment(big)
+    return float(np.sqrt(big[r, c].sum()))
+
+
+def test_app_a_boundary_cuts(env):
+    """App. A (PAPER.md 2927-2949) on the GPU: a terrain cut by square windows at several
+    offsets and quarter turns.  Ignore mode: W2(D_{d-1}(cut), D_{d-1}(first cut)) = 0 for
+    every cut; exact mode: > 0 for some cut (the global maximum's pair follows the cut).
+    Both modes equal the oracle on every cut."""
+    from test_oracle_pins import app_a_windows
+
+    torch, dms = env
+    ign, ex = [], []
+    for w in app_a_windows():
+        ref = oracle.run(w, want_pairs=False)
+        d = dms.DMS(torch.from_numpy(w).cuda())
+        d.run_all()
+        a, b = d.diagram_top(mode=1), d.diagram_top(mode=0)
+        assert a.tobytes() == ref.dtop_ignore.tobytes() and b.tobytes() == ref.dtop.tobytes()
+        ign.append(a)
+        ex.append(b)
+        d.close()
+    w_ign = [_w2(ign[0], x) for x in ign]
+    w_ex = [_w2(ex[0], x) for x in ex]
+    assert max(w_ign) == 0.0
+    assert max(w_ex) > 0.0

@@ -501,3 +501,71 @@ def test_d1_solid_torus():
         vx, vy = v % n, (v // n) % n
         quad.add((vx > c, vy > c))
     assert len(quad) == 4
+
+
+# ------------------------------------------------------------------ O6' "ignore" boundary mode
+
+def _vals(pairs):
+    return sorted((float(p["birth_value"]), float(p["death_value"])) for p in pairs)
+
+
+def test_ignore_mode_hand_fields():
+    g = golden("ignore_mode.json")
+    f = np.array(g["1d"]["field"], np.float32)
+    assert _vals(oracle.run(f).dtop_ignore) == [tuple(x) for x in g["1d"]["dtop_ignore"]]
+    for d in (2, 3):
+        assert _vals(oracle.run(sqdist_field((5,) * d, -1)).dtop_ignore) == g["neg_paraboloid"][str(d)]
+        assert _vals(oracle.run(sqdist_field((5,) * d, +1)).dtop_ignore) == g["bowl"][str(d)]
+
+
+@pytest.mark.parametrize("shape", [(40,), (9, 11), (12, 7), (5, 6, 7), (6, 6, 6)])
+@pytest.mark.parametrize("seed", range(4))
+def test_ignore_mode_low_moat(shape, seed):
+    """Boundary vertices below every interior value: every arc of an interior saddle is
+    processed before any boundary arc, so the interior classes have all merged into the
+    global maximum's when the first boundary saddle joins it to the virtual maximum --
+    the exact diagram's only pair involving the virtual maximum is the global maximum's,
+    and the ignore mode must be the exact diagram minus exactly that pair (simplex
+    level), by the elder rule alone."""
+    rng = np.random.default_rng(seed)
+    f = rng.random(shape).astype(np.float32) + 1.0
+    core = tuple(slice(1, n - 1) for n in shape)
+    low = np.full(shape, True)
+    low[core] = False
+    f[low] = -rng.random(int(low.sum())).astype(np.float32)
+    res = oracle.run(f)
+    d = f.ndim
+    exact = [p for p in res.dtop if p["death_id"] >= 0]
+    gmax = int(np.argmax(f))
+    top = [p for p in exact if int(p["death_vertex"]) == gmax]
+    assert len(top) == 1
+    rest = sorted(p.tobytes() for p in exact if int(p["death_vertex"]) != gmax)
+    assert sorted(p.tobytes() for p in res.dtop_ignore) == rest
+
+
+def app_a_windows():
+    """App. A (PAPER.md 2927-2949) on a synthetic terrain: four Gaussian hills on a dome
+    that falls towards the edges, cut by square windows at different offsets and quarter
+    turns (exact on the grid).  The hills and their saddles are inside every window."""
+    n = 96
+    y, x = np.meshgrid(np.arange(n, dtype=np.float64), np.arange(n, dtype=np.float64), indexing="ij")
+    F = -((x - 48.0) ** 2 + (y - 48.0) ** 2) / 4000.0
+    for (cx, cy, a) in [(36, 38, 2.0), (60, 36, 1.6), (38, 60, 1.3), (61, 61, 1.1)]:
+        F += a * np.exp(-((x - cx) ** 2 + (y - cy) ** 2) / (2 * 5.0 ** 2))
+    F = F.astype(np.float32)
+    out = []
+    for (ox, oy, k) in [(16, 16, 0), (8, 12, 0), (14, 6, 1), (10, 10, 2), (6, 16, 3), (12, 14, 1)]:
+        out.append(np.ascontiguousarray(np.rot90(F[oy:oy + 64, ox:ox + 64], k)))
+    return out
+
+
+def test_app_a_ignore_mode_is_stable_under_boundary_cuts():
+    """Ignore mode: the same diagram (values) for every cut -- the W2 distance of App. A
+    is zero throughout; exact mode: the global maximum's pair follows the cut."""
+    ign, ex = [], []
+    for w in app_a_windows():
+        r = oracle.run(w, want_pairs=False)
+        ign.append(_vals(r.dtop_ignore))
+        ex.append(_vals(r.dtop))
+    assert all(v == ign[0] for v in ign) and len(ign[0]) == 3
+    assert len(set(tuple(v) for v in ex)) > 1
