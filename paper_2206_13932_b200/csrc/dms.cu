@@ -23,6 +23,7 @@
 #include "../../include/dms.h"
 #include "common.cuh"
 #include "order.cuh"
+#include "onesweep.cuh"
 #include "diag.cuh"
 #include "d1.cuh"
 #include "grad.cuh"
@@ -165,6 +166,13 @@ struct dms_ctx {
     void* grad_scratch = nullptr;
     // order sort
     uint32_t *okeys[2] = {nullptr, nullptr}, *ovals[2] = {nullptr, nullptr};
+    // order in one sweep (onesweep.cuh)
+    uint32_t* os_hist = nullptr;              // [4 * 256] digit histograms -> exclusive starts
+    uint32_t* os_wcur = nullptr;              // [kOsWinMax] window cursors
+    int* os_tctr = nullptr;                   // [4] dynamic tile counters
+    unsigned long long* os_status = nullptr;  // [tiles * 256] look-back words
+    uint2* os_wbuf = nullptr;                 // [N] (v, p) pairs by window (large N)
+    uint32_t os_epoch = 0;
     SortScratch ss;
     // order by sample sort (order.cuh): B buckets, S samples
     int ord_B = 0, ord_S = 0;
@@ -426,6 +434,70 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
         k_ord_bucket<<<B, kOrdT, kOrdBucketSmem, c->st>>>(c->ord_keys, c->N, B, G, c->ord_offs, c->rank,
                                                          std::min(ocap_env, kOrdCap));
         c->launches += 6;
+        CU(cudaGetLastError());
+        c->have_order = true;
+        c->order_fresh = true;
+        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
+        return DMS_OK;
+    }
+    // one-sweep LSD radix sort (onesweep.cuh): one histogram read of f, four look-back
+    // passes, the last one writing the ranks (by windows above 2^23 vertices)
+    static const int os_env = getenv("DMS_ORDER_OS") ? atoi(getenv("DMS_ORDER_OS")) : 1;
+    if (os_env) {
+        const int64_t n = c->N;
+        const int64_t tiles = ceil_div(n, (int64_t)kOsTile);
+        static const long long win_env = getenv("DMS_RANK_WIN") ? atoll(getenv("DMS_RANK_WIN")) : -1;
+        const bool windowed = win_env < 0 ? n >= (int64_t(1) << 23) : (win_env > 0 && n >= win_env);
+        const int nwin = (int)((n + (int64_t(1) << kWinBits) - 1) >> kWinBits);
+        if (!c->os_hist) {
+            CU(dalloc(&c->os_hist, 4 * 256));
+            CU(dalloc(&c->os_wcur, kOsWinMax));
+            CU(dalloc(&c->os_tctr, 4));
+            CU(dalloc(&c->os_status, tiles * 256));
+            CU(cudaMemsetAsync(c->os_status, 0, (size_t)tiles * 256 * 8, c->st));
+            c->os_epoch = 0;
+        }
+        if (windowed && !c->os_wbuf) CU(dalloc(&c->os_wbuf, n));
+        CU(cudaMemsetAsync(c->os_hist, 0, 4 * 256 * sizeof(uint32_t), c->st));
+        CU(cudaMemsetAsync(c->os_tctr, 0, 4 * sizeof(int), c->st));
+        int per = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_os_pass<false, 0>, kOsT, 0);
+        const int64_t res = (int64_t)c->sms * std::max(per, 1);
+        const int64_t cap = order_cap > 0 ? std::min<int64_t>(order_cap, res) : res;
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, cap));
+        k_os_hist<<<(unsigned)std::min<int64_t>(ceil_div(n, kOsT), (int64_t)c->sms * 8), kOsT, 0, c->st>>>(c->f, n, c->os_hist,
+                                                                                                    c->err, c->kmax);
+        k_os_scan<<<4, kOsT, 0, c->st>>>(c->os_hist, c->os_wcur, windowed ? nwin : 0);
+        c->launches += 2;
+        for (int p = 0; p < 4; p++) {
+            if (++c->os_epoch >= 0xffffu) {  // epochs wrap: clear the look-back words
+                CU(cudaMemsetAsync(c->os_status, 0, (size_t)tiles * 256 * 8, c->st));
+                c->os_epoch = 1;
+            }
+            uint32_t* ki = p % 2 ? c->okeys[1] : c->okeys[0];
+            uint32_t* vi = p % 2 ? c->ovals[1] : c->ovals[0];
+            uint32_t* ko = p % 2 ? c->okeys[0] : c->okeys[1];
+            uint32_t* vo = p % 2 ? c->ovals[0] : c->ovals[1];
+            const uint32_t* db = c->os_hist + 256 * p;
+            int* tc = c->os_tctr + p;
+            if (p == 0)
+                k_os_pass<true, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 0, db,
+                                                            c->os_status, c->os_epoch, tc, tiles);
+            else if (p < 3)
+                k_os_pass<false, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 8 * p,
+                                                             db, c->os_status, c->os_epoch, tc, tiles);
+            else if (windowed)
+                k_os_pass<false, 2><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
+                                                             c->os_status, c->os_epoch, tc, tiles);
+            else
+                k_os_pass<false, 1><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
+                                                             c->os_status, c->os_epoch, tc, tiles);
+            c->launches++;
+        }
+        if (windowed) {
+            k_os_rank<<<(unsigned)ceil_div(n, kBlock), kBlock, 0, c->st>>>(c->os_wbuf, n, c->rank);
+            c->launches++;
+        }
         CU(cudaGetLastError());
         c->have_order = true;
         c->order_fresh = true;
@@ -1993,6 +2065,11 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);
     for (int b = 0; b < 2; b++) { cudaFree(c->okeys[b]); cudaFree(c->ovals[b]); }
+    cudaFree(c->os_hist);
+    cudaFree(c->os_wcur);
+    cudaFree(c->os_tctr);
+    cudaFree(c->os_status);
+    cudaFree(c->os_wbuf);
     cudaFree(c->ord_keys);
     cudaFree(c->ord_bid);
     for (int b = 0; b < 2; b++) { cudaFree(c->ord_skeys[b]); cudaFree(c->ord_svals[b]); }
