@@ -25,6 +25,7 @@
 #include "order.cuh"
 #include "onesweep.cuh"
 #include "diag.cuh"
+#include "path1d.cuh"
 #include "d1.cuh"
 #include "grad.cuh"
 #include "sort.cuh"
@@ -87,6 +88,20 @@ struct UFBuf {
     uint32_t *flags = nullptr, *pos = nullptr;
     int64_t cap_arcs = 0, cap_nodes = 0;
     int64_t last_m = 0, last_grid = 0, last_batch = 0;  // diagnostics of the last launch
+};
+
+// 1D closed-form union-find scratch (path1d.cuh), one per diagram
+struct PathBuf {
+    uint32_t* sage = nullptr;
+    unsigned long long* sarc = nullptr;
+    unsigned long long *lw = nullptr, *rw = nullptr, *dw = nullptr, *bnd = nullptr, *tspan = nullptr;
+    uint8_t* unres = nullptr;
+    int32_t *pre = nullptr, *suf = nullptr, *npre = nullptr, *nsuf = nullptr;
+    uint32_t* tmin = nullptr;
+    int* bad = nullptr;
+    int* h_bad = nullptr;
+    int64_t cap = 0, capb = 0;
+    bool used = false;  // the last union-find of this diagram ran here (finish checks it)
 };
 
 // D1 (d1.cuh): grow-only buffers
@@ -219,6 +234,14 @@ struct dms_ctx {
     bool order_fresh = false;  // an order computed since the last gradient pass
     bool have_order = false, have_grad = false, have_crit = false, have_d[2] = {false, false};
     bool have_d1 = false, have_gen = false;  // D1 pairs / generators of the current diagrams
+    // 1D: the union-finds in closed form on the path graphs (path1d.cuh)
+    uint32_t *t1base[2] = {nullptr, nullptr}, *t1cnt[2] = {nullptr, nullptr}, *t1scan[2] = {nullptr, nullptr};
+    int64_t t1tiles = 0;
+    bool t1_valid = false;           // the last gradient pass filled the per-CTA tables
+    int64_t* pmap[2] = {nullptr, nullptr};  // spatial -> emission index of C_0 / C_1
+    int64_t cap_pmap = 0;
+    bool have_pmap = false;
+    PathBuf pb[2];
     bool have_ign = false;                   // D_{d-1} in the "ignore" boundary mode
     UFBuf uf_ign;
     PairRec* pairs_ign = nullptr;
@@ -582,6 +605,12 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     A.err = c->err;
     A.cw = c->cw;
     A.cw2 = c->cw2;
+    // 1D: the per-CTA record tables for the path union-finds (single launch over the line)
+    c->t1_valid = c->ndim == 1 && c->t1base[0] && v0 == 0 && v1 == c->N;
+    for (int k = 0; k < 2; k++) {
+        A.t1base[k] = c->t1_valid ? c->t1base[k] : nullptr;
+        A.t1cnt[k] = c->t1_valid ? c->t1cnt[k] : nullptr;
+    }
     A.vc = c->vc;
     StageTimer tm(c, 5);
     if (c->ndim >= 2) {
@@ -689,6 +718,102 @@ dms_status run_critical(dms_ctx* c) {
     }
     CU(cudaGetLastError());
     c->have_crit = true;
+    // 1D: spatial order of C_0 / C_1 from the gradient's per-CTA tables (path1d.cuh)
+    c->have_pmap = false;
+    // DMS_PATH1D=1: the closed form (correct, measured slower on c5b: 4.1 vs 3.1 ms per
+    // union-find alone -- DESIGN.md 8b), so the contraction rounds stay the default
+    static const int path_env = getenv("DMS_PATH1D") ? atoi(getenv("DMS_PATH1D")) : 0;
+    if (c->ndim == 1 && c->t1_valid && path_env) {
+        const int64_t need = std::max(c->ncrit[0], c->ncrit[1]) + 1;
+        if (need > c->cap_pmap) {
+            for (int k = 0; k < 2; k++) {
+                cudaFree(c->pmap[k]);
+                c->pmap[k] = nullptr;
+                CU(dalloc(&c->pmap[k], 2 * need + 1024));
+            }
+            c->cap_pmap = 2 * need + 1024;
+        }
+        for (int k = 0; k < 2; k++) {
+            scan_excl(c->t1cnt[k], c->t1scan[k], c->t1tiles, c->ss, c->st, &c->launches);
+            k_path_spatial<<<(unsigned)ceil_div(c->t1tiles * 32, kBlock), kBlock, 0, c->st>>>(c->t1base[k], c->t1cnt[k],
+                                                                                          c->t1scan[k], c->t1tiles,
+                                                                                          c->pmap[k]);
+            c->launches++;
+        }
+        CU(cudaGetLastError());
+        c->have_pmap = true;
+    }
+    return DMS_OK;
+}
+
+// 1D: the elder-rule union-find of diagram `which` in closed form on its path graph
+// (path1d.cuh) instead of the contraction rounds; checked against the traced arcs (a
+// mismatch falls back to the rounds in path_finish)
+dms_status path_issue(dms_ctx* c, UFBuf& u, int which) {
+    PathBuf& b = c->pb[which];
+    const int64_t m = c->ncrit[which == 0 ? 1 : 0];
+    const int64_t P = which == 0 ? c->ncrit[0] : c->ncrit[1] + 2;
+    const int64_t nb = ceil_div(P, (int64_t)kPB);
+    int levels = 1;
+    while ((int64_t(1) << (levels - 1)) < nb) levels++;
+    if (P > b.cap) {
+        cudaFree(b.sage); cudaFree(b.lw); cudaFree(b.rw); cudaFree(b.dw); cudaFree(b.unres); cudaFree(b.pre); cudaFree(b.suf);
+        cudaFree(b.sarc);
+        const int64_t cap = 2 * P + 1024;
+        CU(dalloc(&b.sarc, cap));
+        CU(dalloc(&b.sage, cap)); CU(dalloc(&b.lw, cap)); CU(dalloc(&b.rw, cap)); CU(dalloc(&b.dw, cap));
+        CU(dalloc(&b.unres, cap)); CU(dalloc(&b.pre, cap)); CU(dalloc(&b.suf, cap));
+        b.cap = cap;
+    }
+    if ((int64_t)levels * nb > b.capb) {
+        cudaFree(b.npre); cudaFree(b.nsuf); cudaFree(b.bnd); cudaFree(b.tmin); cudaFree(b.tspan);
+        const int64_t cap = 2 * (int64_t)levels * nb + 1024;
+        CU(dalloc(&b.npre, cap)); CU(dalloc(&b.nsuf, cap)); CU(dalloc(&b.bnd, cap)); CU(dalloc(&b.tmin, cap));
+        CU(dalloc(&b.tspan, cap));
+        b.capb = cap;
+    }
+    if (!b.bad) {
+        CU(dalloc(&b.bad, 1));
+        if (cudaMallocHost(&b.h_bad, sizeof(int)) != cudaSuccess) return fail(c, DMS_ERR_OOM, "pinned");
+    }
+    PathArgs A;
+    A.P = P;
+    A.nb = nb;
+    A.node_map = c->pmap[which == 0 ? 0 : 1];
+    A.arc_map = c->pmap[which == 0 ? 1 : 0];
+    A.node_off = which == 0 ? 0 : 1;
+    A.virt = which == 0 ? -1 : (int32_t)c->ncrit[1];
+    A.key = u.key;
+    A.age = u.age;
+    A.arc_a = u.arc_a;
+    A.arc_b = u.arc_b;
+    A.bad = b.bad;
+    A.sage = b.sage;
+    A.sarc = b.sarc;
+    A.lw = b.lw;
+    A.rw = b.rw;
+    A.dw = b.dw;
+    A.unres = b.unres;
+    A.pre = b.pre;
+    A.suf = b.suf;
+    A.npre = b.npre;
+    A.nsuf = b.nsuf;
+    A.bnd = b.bnd;
+    A.tmin = b.tmin;
+    A.tspan = b.tspan;
+    A.levels = levels;
+    A.out = u.out;
+    CU(cudaMemsetAsync(b.bad, 0, sizeof(int), c->st));
+    k_path_check<<<grid_for(P), kBlock, 0, c->st>>>(A);
+    k_path_local<<<grid_for(nb, kPT), kPT, 0, c->st>>>(A);
+    for (int k = 1; k < levels; k++) k_path_sparse<<<grid_for(nb), kBlock, 0, c->st>>>(A, k);
+    k_fill_i32<<<grid_for(m), kBlock, 0, c->st>>>(u.out, m, -1);
+    k_path_resolve<<<grid_for(P), kBlock, 0, c->st>>>(A);
+    k_path_emit<<<grid_for(P), kBlock, 0, c->st>>>(A);
+    c->launches += 5 + (levels - 1);
+    CU(cudaMemcpyAsync(b.h_bad, b.bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaGetLastError());
+    b.used = true;
     return DMS_OK;
 }
 
@@ -867,17 +992,30 @@ dms_status d0_issue(dms_ctx* c) {
     {
         StageTimer t8(c, 8);
         uf_keys_ages(c, u, 1, m, 0, n0, 0);
-        s = uf_issue(c, u, m, n0, 1, 0);
+        c->pb[0].used = false;
+        s = (c->have_pmap && m > 0) ? path_issue(c, u, 0) : uf_issue(c, u, m, n0, 1, 0);
         if (s) return s;
     }
     return DMS_OK;
+}
+
+// the union-find of diagram `which` done: the rounds' finish, or the path check (a
+// mismatch reruns it as rounds)
+dms_status uf_or_path_finish(dms_ctx* c, UFBuf& u, int which, int64_t m, int64_t nodes, int karcs, int rev) {
+    PathBuf& b = c->pb[which];
+    if (!b.used) return uf_finish(c, u, m);
+    CU(cudaStreamSynchronize(c->st));
+    if (!*b.h_bad) return DMS_OK;
+    b.used = false;
+    dms_status s = uf_issue(c, u, m, nodes, karcs, rev);
+    return s ? s : uf_finish(c, u, m);
 }
 
 dms_status d0_finish(dms_ctx* c) {
     UFBuf& u = c->uf[0];
     const int64_t m = c->ncrit[1];
     Geo3 g = geo(c);
-    dms_status s = uf_finish(c, u, m);
+    dms_status s = uf_or_path_finish(c, u, 0, m, c->ncrit[0], 1, 0);
     if (s) return s;
     out_to_processing(c, u, 1, m, 0);
     c->npairs_async[0] = 0;
@@ -999,7 +1137,8 @@ dms_status dtop_issue(dms_ctx* c) {
     {
         StageTimer t9(c, 9);
         uf_keys_ages(c, u, d - 1, m, d, nd, 1);
-        s = uf_issue(c, u, m, nd + 1, d - 1, 1);
+        c->pb[1].used = false;
+        s = (c->have_pmap && m > 0) ? path_issue(c, u, 1) : uf_issue(c, u, m, nd + 1, d - 1, 1);
         if (s) return s;
     }
     return DMS_OK;
@@ -1010,7 +1149,7 @@ dms_status dtop_finish(dms_ctx* c) {
     UFBuf& u = c->uf[1];
     const int64_t m = c->ncrit[d - 1];
     Geo3 g = geo(c);
-    dms_status s = uf_finish(c, u, m);
+    dms_status s = uf_or_path_finish(c, u, 1, m, c->ncrit[d] + 1, d - 1, 1);
     if (s) return s;
     out_to_processing(c, u, d - 1, m, 1);
     c->npairs_async[1] = 0;
@@ -1619,6 +1758,14 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
         cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
     }
     CA(dalloc(&c->rank_scratch, N));
+    if (ndim == 1) {
+        c->t1tiles = ceil_div(N, (int64_t)kBlock * kG1);
+        for (int k = 0; k < 2; k++) {
+            CA(dalloc(&c->t1base[k], c->t1tiles));
+            CA(dalloc(&c->t1cnt[k], c->t1tiles));
+            CA(dalloc(&c->t1scan[k], c->t1tiles));
+        }
+    }
     CA(cudaMalloc(&c->grad_scratch, dms_gradient_bytes(c)));
     for (int b = 0; b < 2; b++) { CA(dalloc(&c->okeys[b], N)); CA(dalloc(&c->ovals[b], N)); }
     {
@@ -2019,6 +2166,12 @@ int dms_internal_uf_launch(dms_ctx* c, int which, int64_t out[3]) {
     out[2] = c->uf[which].last_batch;
     return 0;
 }
+// 1: the last union-find of diagram `which` ran in closed form on the 1D path (path1d.cuh)
+int dms_internal_path_used(dms_ctx* c, int which) {
+    if (!c || which < 0 || which > 1) return -1;
+    return c->pb[which].used ? 1 : 0;
+}
+
 // rounds of the last D1 phases (1: pairs, 2: generators)
 int dms_internal_d1_rounds(dms_ctx* c, int out[2]) {
     if (!c) return -1;
@@ -2065,6 +2218,14 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);
     for (int b = 0; b < 2; b++) { cudaFree(c->okeys[b]); cudaFree(c->ovals[b]); }
+    for (int k = 0; k < 2; k++) {
+        cudaFree(c->t1base[k]); cudaFree(c->t1cnt[k]); cudaFree(c->t1scan[k]); cudaFree(c->pmap[k]);
+        PathBuf& b = c->pb[k];
+        for (void* p : {(void*)b.sage, (void*)b.sarc, (void*)b.lw, (void*)b.rw, (void*)b.dw, (void*)b.bnd, (void*)b.tspan, (void*)b.unres,
+                        (void*)b.pre, (void*)b.suf, (void*)b.npre, (void*)b.nsuf, (void*)b.tmin, (void*)b.bad})
+            cudaFree(p);
+        if (b.h_bad) cudaFreeHost(b.h_bad);
+    }
     cudaFree(c->os_hist);
     cudaFree(c->os_wcur);
     cudaFree(c->os_tctr);

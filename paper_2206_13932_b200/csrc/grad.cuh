@@ -79,6 +79,8 @@ struct GradArgs {
     unsigned long long* cw;      // 3D, optional: chase words (tet codes | lower mask << 48)
     uint32_t* cw2;               // 2D, optional: chase words (triangle codes | lower mask << 12)
     uint8_t* vc;                 // 2D / 3D, optional: vertex codes (15 / 7 = minimum), for the D0 descent
+    uint32_t* t1base[2];         // 1D, optional: per CTA (1024 vertices), the emission position and
+    uint32_t* t1cnt[2];          //   the count of its C_0 / C_1 records (spatial order, path1d.cuh)
     int* err;                    // bit 0: NaN seen
 };
 
@@ -1113,6 +1115,11 @@ __global__ void __launch_bounds__(kBlock) k_gradient1(GradArgs A) {
     if (threadIdx.x < 2) {
         const uint32_t t = threadIdx.x ? (tot >> 16) : (tot & 0xffffu);
         s_base[threadIdx.x] = t ? atomicAdd(&A.totals[threadIdx.x], (unsigned long long)t) : 0ull;
+        if (A.t1base[0]) {
+            const int64_t tile = A.v0 / ((int64_t)kBlock * kG1) + blockIdx.x;
+            A.t1base[threadIdx.x][tile] = (uint32_t)s_base[threadIdx.x];
+            A.t1cnt[threadIdx.x][tile] = t;
+        }
     }
     __syncthreads();
     int64_t p0 = (int64_t)s_base[0] + (ex & 0xffffu), p1 = (int64_t)s_base[1] + (ex >> 16);

@@ -52,6 +52,8 @@ def env():
     L.dms_internal_uf_launch.restype = ctypes.c_int
     L.dms_internal_uf_trace.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
     L.dms_internal_uf_trace.restype = ctypes.c_int
+    L.dms_internal_path_used.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    L.dms_internal_path_used.restype = ctypes.c_int
     return torch, dms
 
 
@@ -82,6 +84,7 @@ def run_gpu(env, f3):
         # (arcs, cooperative grid, most live arcs in a round, tiles per CTA in that round)
         uf.append((int(a[0]), int(a[1]), live, -(-live // (int(a[1]) * 256)) if a[1] else 0))
     out["uf"] = uf
+    out["path1d"] = [dms.lib().dms_internal_path_used(ctx.ctx, w) for w in (0, 1)]
     out["rank"] = rank.cpu().numpy()
     del rank
     wb = {3: 16, 2: 2, 1: 1}[f3.ndim]
@@ -184,3 +187,33 @@ def test_midsize_branches(env, name):
             x = kmax(f, simplex_vertices(f3.shape, k, got["crit"][k]))  # star of each record
             most = max(most, int(np.bincount((x // 256) % grid, minlength=grid).max()))
         assert most > 512, ("no CTA overflowed its record buffer", most)
+
+
+def test_midsize_1d_path_closed_form():
+    """The 1D walk of test_midsize_branches through the closed-form union-find on the
+    path graph (path1d.cuh, DMS_PATH1D=1, read once per process; an A/B alternative to
+    the contraction rounds), bit-exact against the oracle."""
+    import subprocess
+    import sys
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import test_gpu_fullsize_oracle as T, paper_2206_13932_b200 as dms, torch, ctypes\n"
+        "env = T.env.__wrapped__() if hasattr(T.env, '__wrapped__') else None\n"
+        % (root, os.path.join(root, "tests")))
+    code += (
+        "import __graft_entry__; __graft_entry__.build_lib()\n"
+        "L = dms.lib()\n"
+        "L.dms_internal_uf_launch.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]\n"
+        "L.dms_internal_uf_trace.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]\n"
+        "L.dms_internal_path_used.argtypes = [ctypes.c_void_p, ctypes.c_int]\n"
+        "got = T._compare_live((torch, dms), T.MID['1d_rw_2^23']())\n"
+        "assert got['path1d'] == [1, 1], got['path1d']\n"
+        "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, DMS_PATH1D="1"), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
