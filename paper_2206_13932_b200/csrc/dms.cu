@@ -439,9 +439,10 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     // CTAs (c4: 46.6 -> 45.3 ms; in 1D / 2D the order is the longer branch and keeps the
     // full grid).  DMS_ORDER_CTAS overrides (0: full grid).
     static const int octas_env = getenv("DMS_ORDER_CTAS") ? atoi(getenv("DMS_ORDER_CTAS")) : -1;
-    // 2 CTAs per SM beside the closed-form 3D gradient (c4, 1/2/3/4/full grid: 35.8 /
-    // 32.8 / 34.2 / 35.3 / 34.3 ms; order first, then the gradient: 34.0 ms)
-    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? 2 : 0);
+    // beside the closed-form 3D gradient, the one-sweep order on 1 CTA per SM (c4,
+    // 1/2/3/full grid: 22.18 / 23.52 / 25.10 / 25.10 ms, order first, then the gradient:
+    // 25.12 ms; c3 1/2/3: 6.52 / 6.59 / 6.70 ms)
+    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? 1 : 0);
     const int64_t order_cap = octas > 0 ? (int64_t)c->sms * octas : 0;
     if (c->ord_B > 0) {  // sample sort (order.cuh)
         const int B = c->ord_B, S = c->ord_S, G = c->sms;
@@ -1984,10 +1985,10 @@ dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     if (s) return s;
     static const int oseq_env = getenv("DMS_ORDER_SEQ") ? atoi(getenv("DMS_ORDER_SEQ")) : -1;
     if ((s = clear_err(c))) return s;
-    // the order beside the gradient on a second stream, except for large 3D fields, where
-    // the closed-form gradient no longer hides it (c4: order first 24.97 vs beside 25.34 ms;
-    // c3 6.92 vs 6.73 ms; DMS_ORDER_SEQ=0/1 forces either)
-    const bool seq = oseq_env >= 0 ? oseq_env != 0 : (c->ndim == 3 && c->N > (int64_t(1) << 25));
+    // the order beside the gradient on a second stream (the one-sweep order on a small
+    // grid hides behind the ALU-bound 3D gradient: c4 22.18 vs 25.12 ms order first;
+    // DMS_ORDER_SEQ=0/1 forces either)
+    const bool seq = oseq_env >= 0 ? oseq_env != 0 : false;
     if ((s = run_order(c, d_rank, !seq))) return s;
     if ((s = run_gradient(c, d_grad))) return s;
     if ((s = run_critical(c))) return s;
