@@ -563,6 +563,58 @@ __device__ __forceinline__ E16 sh_pop(E16* P, int& n) {
     return top;
 }
 
+// A few of the largest new entries in registers (sorted, descending): the serial thread
+// pops and pushes them without shared-memory latency; the heap P takes the rest.
+constexpr int kHot = 8;
+struct Hot {
+    E16 e[kHot];
+    int n = 0;
+};
+__device__ __forceinline__ void hot_pop_front(Hot& H) {
+#pragma unroll
+    for (int i = 0; i < kHot - 1; i++) H.e[i] = H.e[i + 1];
+    H.n--;
+}
+// insert x (an equal key already present cancels, mod 2); the smallest entry of a full
+// buffer (or x itself) goes to P
+__device__ __forceinline__ void hot_insert(Hot& H, const E16& x, E16* P, int& pn) {
+    int eq = -1;
+#pragma unroll
+    for (int i = 0; i < kHot; i++)
+        if (i < H.n && H.e[i].key == x.key) eq = i;
+    if (eq >= 0) {
+#pragma unroll
+        for (int i = 0; i < kHot - 1; i++)
+            if (i >= eq) H.e[i] = H.e[i + 1];
+        H.n--;
+        return;
+    }
+    if (H.n == kHot) {
+        if (x.key < H.e[kHot - 1].key) {
+            sh_push(P, pn, x);
+            return;
+        }
+        sh_push(P, pn, H.e[kHot - 1]);
+        H.n--;
+    }
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < kHot; i++) q += (i < H.n && H.e[i].key > x.key) ? 1 : 0;
+#pragma unroll
+    for (int i = kHot - 1; i > 0; i--)
+        if (i > q && i <= H.n) H.e[i] = H.e[i - 1];
+#pragma unroll
+    for (int i = 0; i < kHot; i++)
+        if (i == q) H.e[i] = x;
+    H.n++;
+}
+__device__ __forceinline__ void hot_flush(Hot& H, E16* P, int& pn) {
+#pragma unroll
+    for (int i = 0; i < kHot; i++)
+        if (i < H.n) sh_push(P, pn, H.e[i]);
+    H.n = 0;
+}
+
 // regular step on an entry with known vertices (d1_regular without the order[] loads);
 // the gradient word of the new entry k2's higher vertex is prefetched (k1's is x's)
 __device__ __forceinline__ bool d1_regular16(const D1Args& A, const D1Tab& T, const E16& t, E16& k1, E16& k2) {
@@ -735,6 +787,7 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
             }
         }
         __syncthreads();
+        Hot hot;  // thread 0's register buffer (empty at every CTA action that reads P)
         long long pc_t = clock64(), pc_cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         int pc_last = 0, pc_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         while (true) {
@@ -749,35 +802,48 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                 const int alen = sm.alen, rbase = sm.rbase, rcnt = sm.rcnt;
                 int action = 0;
                 while (true) {
-                    if (pn > kBigP - 3) { action = BA_MERGEP; break; }
+                    if (pn > kBigP - 3 - kHot) {
+                        hot_flush(hot, sm.P, pn);
+                        action = BA_MERGEP;
+                        break;
+                    }
                     if (head < alen && head >= rbase + rcnt) { action = BA_REFILL; break; }
+                    // the maximum of A's head, P's top and the register buffer's first; equal
+                    // copies cancel in pairs (mod 2)
                     const unsigned long long a = head < alen ? sm.ring[head - rbase].key : 0ull;
                     const unsigned long long p = pn ? sm.P[0].key : 0ull;
-                    if (!a && !p) {
+                    const unsigned long long h = hot.n ? hot.e[0].key : 0ull;
+                    const unsigned long long mx = max(h, max(p, a));
+                    if (!mx) {
                         d1_fail(A, 2, sig, 0ull, -1, -1);
                         action = BA_ABORT;
                         break;
                     }
-                    if (a == p) {
-                        head++;
-                        sh_pop(sm.P, pn);
-                        continue;
-                    }
                     E16 tv;
-                    if (p > a) {
-                        tv = sh_pop(sm.P, pn);
-                        if (pn && sm.P[0].key == tv.key) {
-                            sh_pop(sm.P, pn);
-                            continue;
-                        }
-                    } else {
+                    int cnt = 0;
+                    if (h == mx) {
+                        tv = hot.e[0];
+                        hot_pop_front(hot);
+                        cnt++;
+                    }
+                    if (a == mx) {
                         tv = sm.ring[head - rbase];
                         head++;
+                        cnt++;
                     }
+                    if (p == mx) {
+                        tv = sh_pop(sm.P, pn);
+                        cnt++;
+                        while (pn && sm.P[0].key == mx) {
+                            sh_pop(sm.P, pn);
+                            cnt++;
+                        }
+                    }
+                    if (!(cnt & 1)) continue;
                     E16 k1, k2;
                     if (d1_regular16(A, S, tv, k1, k2)) {
-                        sh_push(sm.P, pn, k1);
-                        sh_push(sm.P, pn, k2);
+                        hot_insert(hot, k1, sm.P, pn);
+                        hot_insert(hot, k2, sm.P, pn);
                         if (A.st_steps) A.st_steps[sig]++;
                         continue;
                     }
@@ -812,9 +878,10 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                             A.st_adds[sig]++;
                             A.st_pushed[sig] += sm.m - 1;
                         }
-                        action = (sm.m - 1 <= kBigAddSmall && pn + sm.m <= kBigP - 3) ? BA_ADDS : BA_ADDB;
+                        action = (sm.m - 1 <= kBigAddSmall && pn + sm.m <= kBigP - 3 - kHot) ? BA_ADDS : BA_ADDB;
                         break;
                     }
+                    hot_flush(hot, sm.P, pn);
                     sm.tau = tv;
                     sm.j = j;
                     sm.status = st;

@@ -70,6 +70,7 @@ def run_gpu(env, f3):
         crit=[c.cpu().numpy() for c in ctx.critical()],
         d0=ctx.diagram0(),
         dtop=ctx.diagram_top(),
+        dtop_ign=ctx.diagram_top(mode=1),
         un0=ctx.unpaired_saddles(0),
         untop=ctx.unpaired_saddles(1),
     )
@@ -127,6 +128,14 @@ def test_fullsize_vs_oracle(env, cfg):
     assert G.sha(got["dtop"]) == gold["dtop_sha256"], "D_{d-1}"
     assert G.sha(got["un0"]) == gold["unpaired0_sha256"], "unpaired 1-saddles after D0"
     assert G.sha(got["untop"]) == gold["unpaired_top_sha256"], "unpaired (d-1)-saddles after D_{d-1}"
+    # D_{d-1} in the ignore boundary mode (tests/golden/fullsize_ignore_<cfg>.json, written by
+    # tests/golden/make_fullsize_ignore.py from oracle/ only)
+    ign = os.path.join(GOLDEN, "fullsize_ignore_%s.json" % cfg)
+    if os.path.exists(ign):
+        gi = json.load(open(ign))
+        if not live and gi["field_sha256"] == gold["field_sha256"]:
+            assert len(got["dtop_ign"]) == gi["dtop_ignore_count"]
+            assert G.sha(got["dtop_ign"]) == gi["dtop_ignore_sha256"], "D_{d-1} ignore mode"
     chunks = G.gradient_chunks(cfg, f3.shape)
     assert len(chunks) == len(gold["gradient_chunk_digests"])
     for i, ch in enumerate(chunks):
