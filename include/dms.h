@@ -32,6 +32,10 @@
  *
  * Errors
  *   Every entry point returns a dms_status; no C++ exception crosses the ABI.
+ *   With DMS_CHECK_INVARIANTS=1 in the environment (debug), dms_run_all* also verify the
+ *   identities every result satisfies (ranks a permutation, Euler characteristic 1, every
+ *   extremum dying once, the D1 saddle counts of both sandwich sides) and return
+ *   DMS_ERR_INVARIANT on a violation.
  *   Argument/shape errors are synchronous.  A NaN in f is detected on the device and
  *   reported by the next synchronising call (dms_critical, dms_diagram0,
  *   dms_diagram_top, dms_sync) as DMS_ERR_NAN.  CUDA errors -> DMS_ERR_CUDA
@@ -141,7 +145,7 @@ dms_status dms_diagram0(dms_ctx* ctx, const dms_pair** d_pairs, int64_t* h_n);
  *       Computed from the exact mode's arcs (run first if needed); the exact results
  *       and the D1 hand-off (dms_unpaired_saddles) are unchanged.
  * Other values -> DMS_ERR_ARG.  Synchronises. */
-dms_status dms_diagram_top(dms_ctx* ctx, int mode, const dms_pair** d_pairs, int64_t* h_n);
+dms_status dms_diagram_top(dms_ctx* ctx, dms_boundary mode, const dms_pair** d_pairs, int64_t* h_n);
 
 /* Critical saddles left unpaired (the "sandwich" hand-off, PAPER.md 1125-1155:
  * PairCriticalSimplices only sees the critical simplices that D0 and D_{d-1} did not

@@ -11,6 +11,7 @@
 //   D_{d-1}  node map, memoised work-queue chases, union-find      (Sec. 5.2, 6)
 //            rounds, emission; D0 runs on a third stream beside it (Sec. 7.2)
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -256,15 +257,23 @@ struct dms_ctx {
 
 namespace {
 
-// records a (start, stop) event pair on the context's stream around a stage
+// NVTX names of the stages (host-side ranges for Nsight Systems / ncu --nvtx)
+const char* const kStageName[12] = {"dms order", "dms gradient", "dms critical", "dms D0", "dms Dtop", "dms gradient kernel",
+                                    "dms D0 trace", "dms Dtop trace", "dms D0 union-find", "dms Dtop union-find",
+                                    "dms D1 pairs", "dms D1 generators"};
+
+// records a (start, stop) event pair on the context's stream around a stage (and an NVTX
+// range on the host thread)
 struct StageTimer {
     dms_ctx* c;
     int stage;
     cudaEvent_t a = nullptr;
     StageTimer(dms_ctx* c_, int s) : c(c_), stage(s) {
+        nvtxRangePushA(kStageName[s < 12 ? s : 0]);
         if (c->timing && cudaEventCreate(&a) == cudaSuccess) cudaEventRecord(a, c->st);
     }
     ~StageTimer() {
+        nvtxRangePop();
         if (!a) return;
         cudaEvent_t b = nullptr;
         if (cudaEventCreate(&b) == cudaSuccess) {
@@ -1910,7 +1919,7 @@ dms_status dms_diagram0(dms_ctx* c, const dms_pair** d_pairs, int64_t* h_n) {
     return DMS_OK;
 }
 
-dms_status dms_diagram_top(dms_ctx* c, int mode, const dms_pair** d_pairs, int64_t* h_n) {
+dms_status dms_diagram_top(dms_ctx* c, dms_boundary mode, const dms_pair** d_pairs, int64_t* h_n) {
     dms_status s = check_sticky(c);
     if (s) return s;
     if (!d_pairs || !h_n) return DMS_ERR_ARG;
@@ -1980,6 +1989,62 @@ dms_status dms_generators(dms_ctx* c, const int64_t** d_off, const int64_t** d_e
     return DMS_OK;
 }
 
+// DMS_CHECK_INVARIANTS=1 (debug): after a full pass, check the identities every result
+// must satisfy: the ranks are a permutation, the Euler
+// characteristic of the grid (a ball) is 1, every minimum dies once in D0 (one infinite
+// class), every top cell once in D_{d-1} (exact mode), and the saddle counts left for D1
+// agree on both sides of the sandwich.  A violation -> DMS_ERR_INVARIANT.
+__global__ void k_check_perm(const int32_t* __restrict__ rank, int64_t n, unsigned* bits, unsigned long long* bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t r = rank[i];
+    if (r < 0 || r >= n) { atomicAdd(bad, 1ull); return; }
+    const unsigned old = atomicOr(bits + (r >> 5), 1u << (r & 31));
+    if (old & (1u << (r & 31))) atomicAdd(bad, 1ull);
+}
+static dms_status check_invariants(dms_ctx* c) {
+    static const int env = getenv("DMS_CHECK_INVARIANTS") ? atoi(getenv("DMS_CHECK_INVARIANTS")) : 0;
+    if (!env) return DMS_OK;
+    CU(cudaStreamSynchronize(c->st));
+    const int d = c->ndim;
+    char m[200];
+    int64_t chi = 0;
+    for (int k = 0; k <= d; k++) chi += (k & 1) ? -c->ncrit[k] : c->ncrit[k];
+    if (chi != 1) {
+        std::snprintf(m, sizeof m, "invariant: Euler characteristic %lld != 1", (long long)chi);
+        return fail(c, DMS_ERR_INVARIANT, m);
+    }
+    const int64_t p0 = pair_count(c, 0), pt = pair_count(c, 1);
+    const int64_t u0 = unpaired_count(c, 0), ut = unpaired_count(c, 1);
+    bool ok = p0 == c->ncrit[0] && u0 == c->ncrit[1] - (c->ncrit[0] - 1);
+    if (d >= 2) ok = ok && pt == c->ncrit[d] && ut == c->ncrit[d - 1] - c->ncrit[d];
+    if (d == 1) ok = ok && pt == c->ncrit[0];
+    if (d == 2) ok = ok && u0 == pt;  // C_1 = D0 deaths + D1 (= D_{d-1}) births
+    if (d == 3) ok = ok && u0 == ut;  // |D1| from both sides of the sandwich
+    if (!ok) {
+        std::snprintf(m, sizeof m, "invariant: diagram counts (C %lld %lld %lld %lld, D0 %lld, Dtop %lld, unpaired %lld %lld)",
+                      (long long)c->ncrit[0], (long long)c->ncrit[1], (long long)c->ncrit[2], (long long)c->ncrit[3],
+                      (long long)p0, (long long)pt, (long long)u0, (long long)ut);
+        return fail(c, DMS_ERR_INVARIANT, m);
+    }
+    unsigned* bits = nullptr;
+    unsigned long long* bad = nullptr;
+    CU(dalloc(&bits, (c->N + 31) / 32 + 2));
+    CU(cudaMemsetAsync(bits, 0, ((c->N + 31) / 32 + 2) * sizeof(unsigned), c->st));
+    bad = reinterpret_cast<unsigned long long*>(bits + ((c->N + 31) / 32));
+    k_check_perm<<<grid_for(c->N), kBlock, 0, c->st>>>(c->rank, c->N, bits, bad);
+    c->launches++;
+    unsigned long long hb = 0;
+    CU(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    cudaFree(bits);
+    if (hb) {
+        std::snprintf(m, sizeof m, "invariant: rank is not a permutation (%llu collisions)", hb);
+        return fail(c, DMS_ERR_INVARIANT, m);
+    }
+    return DMS_OK;
+}
+
 dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     dms_status s = check_sticky(c);
     if (s) return s;
@@ -1993,7 +2058,7 @@ dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     if ((s = run_gradient(c, d_grad))) return s;
     if ((s = run_critical(c))) return s;
     if ((s = run_diagrams(c))) return s;
-    return DMS_OK;
+    return check_invariants(c);
 }
 
 dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void* d_grad) {
@@ -2045,7 +2110,7 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
     c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
     if ((s = run_critical(c))) return s;
     if ((s = run_diagrams(c))) return s;
-    return DMS_OK;
+    return check_invariants(c);
 }
 
 dms_status dms_sync(dms_ctx* c) {
