@@ -128,6 +128,30 @@ __global__ void k_rekey32(const uint64_t* __restrict__ keys, int64_t m, const in
     if (i < m) out[i] = (uint32_t)rank[keys[i] >> 12];
 }
 
+// Critical lists with one cell per star (C_0; C_1 in 1D): the sort keys are DISTINCT
+// ranks, so a record's lexicographic position is the number of records of lower rank --
+// a bitmap over the ranks and a prefix popcount (k_bm_set, k_bm_popc + scan, k_bm_place)
+// instead of a radix sort
+__global__ void k_bm_set(const uint64_t* __restrict__ keys, int64_t m, const int32_t* __restrict__ rank,
+                         uint32_t* __restrict__ r_out, unsigned* __restrict__ bm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t r = (uint32_t)rank[keys[i] >> 12];
+    r_out[i] = r;
+    atomicOr(bm + (r >> 5), 1u << (r & 31));
+}
+__global__ void k_bm_popc(const unsigned* __restrict__ bm, int64_t nw, uint32_t* __restrict__ cnt) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < nw) cnt[w] = (uint32_t)__popc(bm[w]);
+}
+__global__ void k_bm_place(const uint32_t* __restrict__ r, int64_t m, const unsigned* __restrict__ bm,
+                           const uint32_t* __restrict__ pre, uint32_t* __restrict__ perm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t rr = r[i], w = rr >> 5;
+    perm[pre[w] + (uint32_t)__popc(bm[w] & ((1u << (rr & 31)) - 1u))] = (uint32_t)i;
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) a[i] = (uint32_t)i;

@@ -202,6 +202,8 @@ struct dms_ctx {
     int64_t cap[4] = {0, 0, 0, 0};
     int64_t* cid[2][4] = {};     // [0]: ids in emission order, [1]: ids in lexicographic order
     uint64_t* ckey[2][4] = {};
+    unsigned* bm = nullptr;            // rank bitmap of the one-cell-per-star critical sorts
+    uint32_t *bmcnt = nullptr, *bmpre = nullptr;
     uint32_t* cidx[2][4] = {};   // sort payload: emission index; perm = cidx[cur]
     int cur[4] = {0, 0, 0, 0};
     int64_t ncrit[4] = {0, 0, 0, 0};
@@ -699,6 +701,26 @@ dms_status run_critical(dms_ctx* c) {
     for (int k = 0; k <= c->ndim; k++) {
         k_iota<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cidx[0][k], c->ncrit[k]);
         c->launches++;
+        static const int bm_env = getenv("DMS_CRIT_BITMAP") ? atoi(getenv("DMS_CRIT_BITMAP")) : 1;
+        if ((k == 0 || c->ndim == 1) && bm_env && c->ncrit[k] > 0) {
+            // one cell per star: distinct rank keys -> positions by a rank bitmap (diag.cuh)
+            const int64_t nw = (c->N + 31) / 32, m = c->ncrit[k];
+            if (!c->bm) {
+                CU(dalloc(&c->bm, nw));
+                CU(dalloc(&c->bmcnt, nw));
+                CU(dalloc(&c->bmpre, nw));
+            }
+            uint32_t* r = reinterpret_cast<uint32_t*>(c->ckey[1][k]);
+            CU(cudaMemsetAsync(c->bm, 0, nw * sizeof(unsigned), c->st));
+            k_bm_set<<<grid_for(m), kBlock, 0, c->st>>>(c->ckey[0][k], m, c->rank, r, c->bm);
+            k_bm_popc<<<grid_for(nw), kBlock, 0, c->st>>>(c->bm, nw, c->bmcnt);
+            scan_excl(c->bmcnt, c->bmpre, nw, c->ss, c->st, &c->launches);
+            k_bm_place<<<grid_for(m), kBlock, 0, c->st>>>(r, m, c->bm, c->bmpre, c->cidx[1][k]);
+            c->cur[k] = 1;
+            k_gather_ids<<<grid_for(m), kBlock, 0, c->st>>>(c->cid[0][k], crit_perm(c, k), m, c->cid[1][k]);
+            c->launches += 5;
+            continue;
+        }
         if ((k == 0 || c->ndim == 1) && k32_env) {
             // one cell per star (see below): sort 32-bit ranks, half the key bytes per pass;
             // the keys go to the second buffer (ka), the first one is the ping-pong buffer
@@ -2292,6 +2314,9 @@ void dms_destroy(dms_ctx* c) {
             cudaFree(p);
         if (b.h_bad) cudaFreeHost(b.h_bad);
     }
+    cudaFree(c->bm);
+    cudaFree(c->bmcnt);
+    cudaFree(c->bmpre);
     cudaFree(c->os_hist);
     cudaFree(c->os_wcur);
     cudaFree(c->os_tctr);
