@@ -152,6 +152,48 @@ __global__ void k_bm_place(const uint32_t* __restrict__ r, int64_t m, const unsi
     perm[pre[w] + (uint32_t)__popc(bm[w] & ((1u << (rr & 31)) - 1u))] = (uint32_t)i;
 }
 
+// Critical lists with several cells per star (C_1..C_d in 2D / 3D): lexicographic order
+// = by the star's rank, then by the local key G (PAPER.md 1380-1414).  The present stars
+// get consecutive indices from the rank bitmap (k_bm_set with its popcount scan), every
+// record an arrival slot inside its star's run (k_ms_count), the runs are laid out by a
+// scan of the star counts, and each run (<= 36 cells) is sorted by G by one thread
+// (k_ms_fix) -- the result does not depend on the arrival order.
+__global__ void k_ms_count(const uint32_t* __restrict__ r, int64_t m, const unsigned* __restrict__ bm,
+                           const uint32_t* __restrict__ pre, uint32_t* __restrict__ sidx, uint32_t* __restrict__ scnt,
+                           uint32_t* __restrict__ slot) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t rr = r[i], w = rr >> 5;
+    const uint32_t s = pre[w] + (uint32_t)__popc(bm[w] & ((1u << (rr & 31)) - 1u));
+    sidx[i] = s;
+    slot[i] = atomicAdd(scnt + s, 1u);
+}
+__global__ void k_ms_place(const uint64_t* __restrict__ keys, int64_t m, const uint32_t* __restrict__ sidx,
+                           const uint32_t* __restrict__ slot, const uint32_t* __restrict__ sbase,
+                           unsigned long long* __restrict__ stage) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    stage[sbase[sidx[i]] + slot[i]] = ((keys[i] & 0xfffull) << 32) | (unsigned long long)i;
+}
+__global__ void k_ms_fix(const unsigned long long* __restrict__ stage, int64_t nstars, const uint32_t* __restrict__ sbase,
+                         const uint32_t* __restrict__ scnt, uint32_t* __restrict__ perm) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nstars) return;
+    const uint32_t b = sbase[s], n = scnt[s];
+    unsigned long long e[40];
+    const uint32_t nn = n < 40 ? n : 40;
+    for (uint32_t k = 0; k < nn; k++) {
+        const unsigned long long x = stage[b + k];
+        uint32_t j = k;
+        while (j > 0 && e[j - 1] > x) {
+            e[j] = e[j - 1];
+            j--;
+        }
+        e[j] = x;
+    }
+    for (uint32_t k = 0; k < nn; k++) perm[b + k] = (uint32_t)e[k];
+}
+
 __global__ void k_iota(uint32_t* __restrict__ a, int64_t m) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) a[i] = (uint32_t)i;

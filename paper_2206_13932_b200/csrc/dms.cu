@@ -202,8 +202,11 @@ struct dms_ctx {
     int64_t cap[4] = {0, 0, 0, 0};
     int64_t* cid[2][4] = {};     // [0]: ids in emission order, [1]: ids in lexicographic order
     uint64_t* ckey[2][4] = {};
-    unsigned* bm = nullptr;            // rank bitmap of the one-cell-per-star critical sorts
+    unsigned* bm = nullptr;            // rank bitmap of the critical sorts
     uint32_t *bmcnt = nullptr, *bmpre = nullptr;
+    uint32_t *ms_sidx = nullptr, *ms_slot = nullptr, *ms_cnt = nullptr, *ms_base = nullptr;  // [cap] star runs
+    unsigned long long* ms_stage = nullptr;
+    int64_t ms_cap = 0;
     uint32_t* cidx[2][4] = {};   // sort payload: emission index; perm = cidx[cur]
     int cur[4] = {0, 0, 0, 0};
     int64_t ncrit[4] = {0, 0, 0, 0};
@@ -732,6 +735,39 @@ dms_status run_critical(dms_ctx* c) {
             k_gather_ids<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->cid[0][k], crit_perm(c, k), c->ncrit[k],
                                                                      c->cid[1][k]);
             c->launches += 2;
+            continue;
+        }
+        static const int ms_env = getenv("DMS_CRIT_RUNS") ? atoi(getenv("DMS_CRIT_RUNS")) : 1;
+        if (ms_env && bm_env && c->ncrit[k] > 0) {
+            // several cells per star: star runs by the rank bitmap, each run sorted by G
+            const int64_t nw = (c->N + 31) / 32, m = c->ncrit[k];
+            if (!c->bm) {
+                CU(dalloc(&c->bm, nw));
+                CU(dalloc(&c->bmcnt, nw));
+                CU(dalloc(&c->bmpre, nw));
+            }
+            if (m + 1 > c->ms_cap) {
+                for (uint32_t** q : {&c->ms_sidx, &c->ms_slot, &c->ms_cnt, &c->ms_base}) { cudaFree(*q); *q = nullptr; }
+                cudaFree(c->ms_stage);
+                const int64_t cap = 2 * m + 1024;
+                for (uint32_t** q : {&c->ms_sidx, &c->ms_slot, &c->ms_cnt, &c->ms_base}) CU(dalloc(q, cap));
+                CU(dalloc(&c->ms_stage, cap));
+                c->ms_cap = cap;
+            }
+            uint32_t* r = reinterpret_cast<uint32_t*>(c->ckey[1][k]);
+            CU(cudaMemsetAsync(c->bm, 0, nw * sizeof(unsigned), c->st));
+            CU(cudaMemsetAsync(c->ms_cnt, 0, m * sizeof(uint32_t), c->st));
+            k_bm_set<<<grid_for(m), kBlock, 0, c->st>>>(c->ckey[0][k], m, c->rank, r, c->bm);
+            k_bm_popc<<<grid_for(nw), kBlock, 0, c->st>>>(c->bm, nw, c->bmcnt);
+            scan_excl(c->bmcnt, c->bmpre, nw, c->ss, c->st, &c->launches);
+            k_ms_count<<<grid_for(m), kBlock, 0, c->st>>>(r, m, c->bm, c->bmpre, c->ms_sidx, c->ms_cnt, c->ms_slot);
+            // stars present <= m; unused counts are 0, so scanning all m is exact
+            scan_excl(c->ms_cnt, c->ms_base, m, c->ss, c->st, &c->launches);
+            k_ms_place<<<grid_for(m), kBlock, 0, c->st>>>(c->ckey[0][k], m, c->ms_sidx, c->ms_slot, c->ms_base, c->ms_stage);
+            k_ms_fix<<<grid_for(m), kBlock, 0, c->st>>>(c->ms_stage, m, c->ms_base, c->ms_cnt, c->cidx[1][k]);
+            c->cur[k] = 1;
+            k_gather_ids<<<grid_for(m), kBlock, 0, c->st>>>(c->cid[0][k], crit_perm(c, k), m, c->cid[1][k]);
+            c->launches += 6;
             continue;
         }
         k_rekey<<<grid_for(c->ncrit[k]), kBlock, 0, c->st>>>(c->ckey[0][k], c->ncrit[k], c->rank);
@@ -2317,6 +2353,8 @@ void dms_destroy(dms_ctx* c) {
     cudaFree(c->bm);
     cudaFree(c->bmcnt);
     cudaFree(c->bmpre);
+    for (uint32_t* q : {c->ms_sidx, c->ms_slot, c->ms_cnt, c->ms_base}) cudaFree(q);
+    cudaFree(c->ms_stage);
     cudaFree(c->os_hist);
     cudaFree(c->os_wcur);
     cudaFree(c->os_tctr);
