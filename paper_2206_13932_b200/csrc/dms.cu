@@ -138,6 +138,7 @@ struct D1Buf {
     D1Snap* snaps = nullptr;                  // phase-1 stored columns (restart points)
     int64_t capsnaps = 0;
     int64_t ntaint = 0, nrestart = 0;
+    bool snaps_ok = true;                     // phase 1 kept every stored column (no collection)
     D1Tab* tab = nullptr;                     // device copy of the propagation tables
 };
 
@@ -1589,7 +1590,14 @@ dms_status d1_rounds(dms_ctx* c, int phase, int64_t nact) {
         // pass -- so it grows the arena instead of collecting it)
         if ((b.h_ctr[3] & 1) || *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) > b.arena_cap / 2) {
             dms_status s;
-            if (phase == 1) {
+            // growing keeps the snapshots while the doubled arena (plus the copy) fits in
+            // a third of the free device memory; beyond that the snapshots are given up
+            // (the tainted 2-saddles then restart from their boundaries) and phase 1
+            // collects like phase 2
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            if (phase == 1 && b.snaps_ok && 2 * b.arena_cap * 8 > fr / 3) b.snaps_ok = false;
+            if (phase == 1 && b.snaps_ok) {
                 const unsigned long long used = std::min<unsigned long long>(
                     *reinterpret_cast<unsigned long long*>(b.h_ctr + 4), b.arena_cap);
                 s = d1_grow_arena(c, 2 * b.arena_cap);
@@ -1660,6 +1668,8 @@ dms_status run_d1(dms_ctx* c, bool want_gen) {
         *reinterpret_cast<unsigned long long*>(b.h_ctr + 4) = top;
         CU(cudaMemsetAsync(b.ctr + 14, 0, sizeof(int32_t), c->st));
         CU(cudaMemsetAsync(b.ctr + 16, 0, sizeof(int32_t), c->st));
+        static const long long snap_budget_env = getenv("DMS_D1_SNAP_BUDGET") ? atoll(getenv("DMS_D1_SNAP_BUDGET")) : -1;
+        b.snaps_ok = snap_budget_env != 0;
         if ((s = d1_rounds(c, 1, nsig))) return s;
         if (nsig) {
             k_d1_emit<<<grid_for(nsig), kBlock, 0, c->st>>>(g, b.stop, b.owner, c->unp[0], c->unp[1], nsig, b.pairs, b.ctr + 3);
@@ -1693,7 +1703,7 @@ dms_status run_d1(dms_ctx* c, bool want_gen) {
         CU(cudaStreamSynchronize(c->st));
         static const int all_env = getenv("DMS_D1_RERUN_ALL") ? atoi(getenv("DMS_D1_RERUN_ALL")) : 0;
         static const int snap_env = getenv("DMS_D1_SNAPSHOTS") ? atoi(getenv("DMS_D1_SNAPSHOTS")) : 1;
-        const bool use_snaps = snap_env && !all_env && nd <= b.capdeps;
+        const bool use_snaps = snap_env && !all_env && nd <= b.capdeps && b.snaps_ok;
         if (nsig) {
             if (nd > b.capdeps || all_env) {
                 k_fill_u32<<<grid_for(nsig), kBlock, 0, c->st>>>(b.taint, nsig, 1u);

@@ -177,6 +177,8 @@ def test_d1_large_sigma_path_and_arena_growth(env):
     _subprocess_check({"DMS_D1_LCAP": "8"}, "c4", (64, 64, 64))
     _subprocess_check({"DMS_D1_RERUN_ALL": "1"}, "c3", (48, 48, 48))
     _subprocess_check({"DMS_D1_SNAPSHOTS": "0"}, "c3", (48, 48, 48))
+    # phase 1 collecting its arena (snapshots given up) from the start
+    _subprocess_check({"DMS_D1_SNAP_BUDGET": "0", "DMS_D1_ARENA": "4096"}, "c3", (48, 48, 48))
 
 
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
