@@ -168,6 +168,10 @@ struct dms_ctx {
     cudaEvent_t ev_in = nullptr, ev_order = nullptr;
     cudaEvent_t ev_slab[kSlabs] = {};  // dms_run_all_host: upload slabs
     Lane lane3;                   // D0's lane when the diagrams run concurrently
+    Lane lane4;                   // D_{d-1}'s trace beside the critical sort
+    bool early_traces = false;    // dms_run_all*: trace D0 / D_{d-1} beside the critical sort
+    bool traced[2] = {false, false};
+    cudaEvent_t ev_grad = nullptr, ev_trace[2] = {nullptr, nullptr};
     cudaEvent_t ev_crit = nullptr, ev_d0 = nullptr;
     bool half = false;            // concurrent diagrams: the cooperative union-find grids use half the GPU
     cudaEvent_t t_diag[2] = {};   // stage timers spanning issue .. finish
@@ -678,6 +682,9 @@ const int64_t* crit_ids(dms_ctx* c, int k) { return c->cid[1][k]; }            /
 const int64_t* crit_ids_emitted(dms_ctx* c, int k) { return c->cid[0][k]; }    // emission order
 const uint32_t* crit_perm(dms_ctx* c, int k) { return c->cidx[c->cur[k]][k]; }  // sorted pos -> emission idx
 
+dms_status d0_trace(dms_ctx* c);
+dms_status dtop_trace(dms_ctx* c);
+
 dms_status run_critical(dms_ctx* c) {
     if (!c->have_grad) {
         dms_status s = run_gradient(c, nullptr);
@@ -700,6 +707,26 @@ dms_status run_critical(dms_ctx* c) {
         if (s) return s;
     }
     for (int k = 0; k <= c->ndim; k++) c->ncrit[k] = (int64_t)tot[k];
+    // the diagrams' tracing needs the emitted critical cells but no ranks: in the run_all
+    // flows it starts now on the diagram lanes, beside the sorts below
+    c->traced[0] = c->traced[1] = false;
+    // (measured: c2 1.23 -> 1.11 ms; the full configs within +-0.05 ms, the traces and the
+    // sorts then contend -- so on for fields below 2^23 vertices; DMS_EARLY_TRACE=0/1 forces)
+    static const int early_env = getenv("DMS_EARLY_TRACE") ? atoi(getenv("DMS_EARLY_TRACE")) : -1;
+    static const int conc_env2 = getenv("DMS_CONCURRENT") ? atoi(getenv("DMS_CONCURRENT")) : 1;
+    const bool early = early_env >= 0 ? early_env != 0 : c->N < (int64_t(1) << 23);
+    if (c->early_traces && early && conc_env2 && c->lane3.st && c->lane4.st) {
+        CU(cudaEventRecord(c->ev_grad, c->st));
+        for (int w = 0; w < 2; w++) {
+            Lane& L = w == 0 ? c->lane3 : c->lane4;
+            CU(cudaStreamWaitEvent(L.st, c->ev_grad, 0));
+            LaneSwap ls(c, L);
+            s = w == 0 ? d0_trace(c) : dtop_trace(c);
+            if (s) return s;
+            CU(cudaEventRecord(c->ev_trace[w], c->st));
+            c->traced[w] = true;
+        }
+    }
     const int kbits = 12 + bits_for(c->N);
     static const int k32_env = getenv("DMS_CRIT_KEY32") ? atoi(getenv("DMS_CRIT_KEY32")) : 1;
     for (int k = 0; k <= c->ndim; k++) {
@@ -1043,7 +1070,9 @@ void out_to_processing(dms_ctx* c, UFBuf& u, int karcs, int64_t m, int rev) {
     std::swap(u.out, u.outp);
 }
 
-dms_status d0_issue(dms_ctx* c) {
+// D0 part 1 (Sec. 5.1(a,b)): the unstable sets, traced from the emitted critical cells
+// (no ranks needed, so it can run beside the critical sort)
+dms_status d0_trace(dms_ctx* c) {
     c->t_diag[0] = stage_begin(c);
     UFBuf& u = c->uf[0];
     const int64_t m = c->ncrit[1], n0 = c->ncrit[0];
@@ -1057,6 +1086,19 @@ dms_status d0_issue(dms_ctx* c) {
         StageTimer t6(c, 6);
         k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
         c->launches++;
+    }
+    return DMS_OK;
+}
+
+dms_status d0_issue(dms_ctx* c) {
+    UFBuf& u = c->uf[0];
+    const int64_t m = c->ncrit[1], n0 = c->ncrit[0];
+    dms_status s;
+    if (c->traced[0]) {  // traced beside the critical sort (run_critical)
+        CU(cudaStreamWaitEvent(c->st, c->ev_trace[0], 0));
+        c->traced[0] = false;
+    } else if ((s = d0_trace(c))) {
+        return s;
     }
     {
         StageTimer t8(c, 8);
@@ -1141,7 +1183,8 @@ dms_status d0_finish(dms_ctx* c) {
     return DMS_OK;
 }
 
-dms_status dtop_issue(dms_ctx* c) {
+// D_{d-1} part 1 (Sec. 5.2): the stable sets on the dual gradient (no ranks needed)
+dms_status dtop_trace(dms_ctx* c) {
     c->t_diag[1] = stage_begin(c);
     const int d = c->ndim;
     UFBuf& u = c->uf[1];
@@ -1202,6 +1245,20 @@ dms_status dtop_issue(dms_ctx* c) {
                                                           u.arc_a, u.arc_b);
         }
         c->launches++;
+    }
+    return DMS_OK;
+}
+
+dms_status dtop_issue(dms_ctx* c) {
+    const int d = c->ndim;
+    UFBuf& u = c->uf[1];
+    const int64_t m = c->ncrit[d - 1], nd = c->ncrit[d];
+    dms_status s;
+    if (c->traced[1]) {  // traced beside the critical sort (run_critical)
+        CU(cudaStreamWaitEvent(c->st, c->ev_trace[1], 0));
+        c->traced[1] = false;
+    } else if ((s = dtop_trace(c))) {
+        return s;
     }
     {
         StageTimer t9(c, 9);
@@ -1900,6 +1957,19 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
         CA(dalloc(&L.tile_ctr, 1));
         if (cudaMallocHost(&L.h_pinned, 64) != cudaSuccess) return bail(DMS_ERR_OOM);
     }
+    {
+        Lane& L = c->lane4;
+        if (cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking) != cudaSuccess) return bail(DMS_ERR_CUDA);
+        CA(dalloc(&L.ss.counts, max_tiles * kRadix));
+        CA(dalloc(&L.ss.counts_scan, max_tiles * kRadix));
+        CA(dalloc(&L.ss.status, ceil_div(std::max<int64_t>(max_tiles * kRadix, N), (int64_t)kBlock * kScanItems) + 1));
+        CA(dalloc(&L.ss.tile_ctr, 1));
+        L.ss.max_tiles = max_tiles;
+        CA(dalloc(&L.tile_ctr, 1));
+        if (cudaMallocHost(&L.h_pinned, 64) != cudaSuccess) return bail(DMS_ERR_OOM);
+    }
+    for (cudaEvent_t* e : {&c->ev_grad, &c->ev_trace[0], &c->ev_trace[1]})
+        if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_crit, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_d0, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
     if (cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess) return bail(DMS_ERR_CUDA);
@@ -2124,7 +2194,10 @@ dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     const bool seq = oseq_env >= 0 ? oseq_env != 0 : false;
     if ((s = run_order(c, d_rank, !seq))) return s;
     if ((s = run_gradient(c, d_grad))) return s;
-    if ((s = run_critical(c))) return s;
+    c->early_traces = true;
+    s = run_critical(c);
+    c->early_traces = false;
+    if (s) return s;
     if ((s = run_diagrams(c))) return s;
     return check_invariants(c);
 }
@@ -2176,7 +2249,10 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
     c->have_grad = true;
     c->order_fresh = false;
     c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
-    if ((s = run_critical(c))) return s;
+    c->early_traces = true;
+    s = run_critical(c);
+    c->early_traces = false;
+    if (s) return s;
     if ((s = run_diagrams(c))) return s;
     return check_invariants(c);
 }
@@ -2327,10 +2403,13 @@ void dms_destroy(dms_ctx* c) {
     cudaStreamSynchronize(c->st);
     if (c->st2) cudaStreamSynchronize(c->st2);
     if (c->lane3.st) cudaStreamSynchronize(c->lane3.st);
+    if (c->lane4.st) cudaStreamSynchronize(c->lane4.st);
     clear_events(c);
     if (c->st2) cudaStreamDestroy(c->st2);
-    {
-        Lane& L = c->lane3;
+    for (cudaEvent_t e : {c->ev_grad, c->ev_trace[0], c->ev_trace[1]})
+        if (e) cudaEventDestroy(e);
+    for (Lane* Lp : {&c->lane3, &c->lane4}) {
+        Lane& L = *Lp;
         if (L.st) cudaStreamDestroy(L.st);
         cudaFree(L.ss.counts);
         cudaFree(L.ss.counts_scan);

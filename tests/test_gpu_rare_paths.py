@@ -63,7 +63,7 @@ def test_critical_record_overflow():
     {"DMS_CHASEWORD": "0", "DMS_ORDER_CTAS": "0", "DMS_VCODES": "0"},
     {"DMS_PATH1D": "1", "DMS_ORDER_OS": "0"},
     {"DMS_CHECK_INVARIANTS": "1", "DMS_CRIT_BITMAP": "0"},
-    {"DMS_CRIT_RUNS": "0"},
+    {"DMS_CRIT_RUNS": "0", "DMS_EARLY_TRACE": "1"},
 ])
 def test_knobs_keep_results(knobs):
     """Every A/B knob of DESIGN.md 8c leaves the results bit-exact."""
