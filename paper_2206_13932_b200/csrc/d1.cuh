@@ -105,6 +105,7 @@ struct D1Args {
     unsigned long long tag;  // phase-1 claim tag (decreasing over rounds)
     int phase;
     int lcap;  // local heap capacity used (<= kD1Cap; smaller only to exercise the global path)
+    int adds;  // large-2-saddle path: owner columns up to this length are pushed, longer merged
     int4* deps;          // phase 1: (sigma, owner, edge, sigma's add number) of every column added
     int* ndeps;
     long long deps_cap;
@@ -494,17 +495,28 @@ struct E16 {
     int32_t slot;  // the lower vertex's slot around hi
 };
 
+// one sorted, duplicate-free level of the large-2-saddle boundary (A: the big base, B:
+// the medium one that absorbs additions and is merged into A when it grows past half A)
+struct Level {
+    long long off;           // the level's array in the arena
+    int len, head;           // entries [head, len) are live
+    int rbase, rcnt;         // ring = resolved entries [rbase, rbase + rcnt)
+    long long buf[2];        // this run's reusable buffers
+    int cap[2], cur;         // their capacities; which buffer holds the level (-1: the stored column)
+};
+
 struct BigSmem {
     E16 P[kBigP];                     // 32 KB
     unsigned long long S[2 * kBigP];  // 32 KB: sort buffer / staging (E16 x 2048)
-    E16 ring[kBigRing];
+    E16 ring[2][kBigRing];            // resolved heads of A and B
     int cnt[kBigT + 1];
+    Level lv[2];
     // control block (written by thread 0 before a barrier)
-    int action, pn, head, alen, rbase, rcnt, j, m, status, ok, nadds;
-    long long aoff, oo;               // A's offset in the arena; owner column offset
-    long long o_out, o_tmp;           // merge output / scratch of the current merge
-    long long bbuf[2], tbuf;          // this run's reusable A buffers and merge scratch
-    int bcap[2], tcap, cur, next;     // their capacities; which buffer holds A (-1: the stored column)
+    int action, arg, pn, j, m, status, ok, nadds;
+    long long oo;                     // owner column offset
+    long long o_out;                  // merge output of the current merge
+    long long tbuf;                   // merge scratch (reused)
+    int tcap;
     E16 tau;
 };
 
@@ -755,6 +767,86 @@ __device__ int cta_sort_pending(BigSmem& sm, int pn) {
     return n;
 }
 
+// thread 0: an arena block for the merge of nx + ny keys into level l's other buffer
+// (lead = 1: a fresh block with a leading slot for tau -- the stored column at a stop)
+__device__ __forceinline__ bool big_alloc(const D1Args& A, BigSmem& sm, int l, int need, int lead) {
+    unsigned long long o;
+    if (sm.tcap < need) {
+        const int cap = max(2 * sm.tcap, need);
+        if (!arena_alloc(A, (unsigned long long)cap, o)) return false;
+        sm.tbuf = (long long)o;
+        sm.tcap = cap;
+    }
+    if (lead) {
+        if (!arena_alloc(A, (unsigned long long)(need + 1), o)) return false;
+        sm.o_out = (long long)o;
+        return true;
+    }
+    Level& L = sm.lv[l];
+    const int other = L.cur == 0 ? 1 : 0;
+    if (L.cap[other] < need) {
+        const int cap = max(2 * L.cap[other], need);
+        if (!arena_alloc(A, (unsigned long long)cap, o)) return false;
+        L.buf[other] = (long long)o;
+        L.cap[other] = cap;
+    }
+    sm.o_out = L.buf[other];
+    return true;
+}
+
+// the CTA merges Y (ny sorted keys, smem or global) into level l; with into_out, the
+// result goes to the fresh block sm.o_out + 1 (the stored column) instead.  Returns false
+// if the arena is full (the caller retries the 2-saddle next round).
+template <bool YCG>
+__device__ bool big_merge(const D1Args& A, BigSmem& sm, int l, const unsigned long long* Y, int ny, bool into_out) {
+    const int t = threadIdx.x;
+    Level& L = sm.lv[l];
+    const int nx = L.len - L.head;
+    const unsigned long long* X = A.arena + L.off + L.head;
+    __syncthreads();
+    if (t == 0) sm.ok = big_alloc(A, sm, l, nx + ny, into_out ? 1 : 0) ? 1 : 0;
+    __syncthreads();
+    if (!sm.ok) return false;
+    const long long outoff = sm.o_out + (into_out ? 1 : 0);
+    int n;
+    if (ny > 0) {
+        n = cta_merge<YCG>(sm, X, nx, Y, ny, A.arena + outoff, A.arena + sm.tbuf);
+    } else {
+        for (int k = t; k < nx; k += kBigT) A.arena[outoff + k] = X[k];
+        n = nx;
+        __syncthreads();
+    }
+    if (t == 0) {
+        if (into_out) {
+            sm.m = n;  // the merged length (the stop writes the column)
+        } else {
+            L.cur = L.cur == 0 ? 1 : 0;
+            L.off = outoff;
+            L.len = n;
+            L.head = 0;
+            L.rbase = 0;
+            L.rcnt = 0;
+        }
+    }
+    __syncthreads();
+    return true;
+}
+
+// B into A once B holds more than half of A (each key is merged O(log) times)
+__device__ bool big_settle(const D1Args& A, BigSmem& sm) {
+    const int nb = sm.lv[1].len - sm.lv[1].head, na = sm.lv[0].len - sm.lv[0].head;
+    if (nb == 0 || 2 * nb <= na) return true;
+    if (!big_merge<false>(A, sm, 0, A.arena + sm.lv[1].off + sm.lv[1].head, nb, false)) return false;
+    if (threadIdx.x == 0) {
+        sm.lv[1].len = 0;
+        sm.lv[1].head = 0;
+        sm.lv[1].rbase = 0;
+        sm.lv[1].rcnt = 0;
+    }
+    __syncthreads();
+    return true;
+}
+
 __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
     extern __shared__ __align__(16) unsigned char d1_smem[];
     BigSmem& sm = *reinterpret_cast<BigSmem*>(d1_smem);
@@ -770,19 +862,20 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
             const long long off = A.col_off[sig];
             const int len0 = A.col_len[sig];
             sm.pn = 0;
-            sm.head = 0;
-            sm.rbase = 0;
-            sm.rcnt = 0;
-            sm.cur = -1;
-            sm.bcap[0] = sm.bcap[1] = sm.tcap = 0;
+            sm.tcap = 0;
+            for (int l = 0; l < 2; l++) {
+                Level& L = sm.lv[l];
+                L.off = 0;
+                L.len = L.head = L.rbase = L.rcnt = 0;
+                L.cap[0] = L.cap[1] = 0;
+                L.cur = -1;
+            }
             sm.nadds = A.nadd[sig];
-            if (len0 >= 0) {  // [tau, sorted rest]: A = rest, P = {tau}
-                sm.aoff = off + 1;
-                sm.alen = len0 - 1;
+            if (len0 >= 0) {  // [tau, sorted rest]: A = rest (in place), P = {tau}
+                sm.lv[0].off = off + 1;
+                sm.lv[0].len = len0 - 1;
                 sh_push(sm.P, sm.pn, d1_resolve_key(A, S, A.arena[off]));
             } else {          // a bag from the local path: everything into P
-                sm.aoff = 0;
-                sm.alen = 0;
                 for (int k = 0; k < -len0; k++) sh_push(sm.P, sm.pn, d1_resolve_key(A, S, A.arena[off + k]));
             }
         }
@@ -798,22 +891,26 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
             }
             if (t == 0) {
                 // serial propagation until the CTA is needed
-                int pn = sm.pn, head = sm.head;
-                const int alen = sm.alen, rbase = sm.rbase, rcnt = sm.rcnt;
-                int action = 0;
+                int pn = sm.pn;
+                int h0 = sm.lv[0].head, h1 = sm.lv[1].head;
+                const int l0 = sm.lv[0].len, l1 = sm.lv[1].len;
+                const int rb0 = sm.lv[0].rbase, rc0 = sm.lv[0].rcnt, rb1 = sm.lv[1].rbase, rc1 = sm.lv[1].rcnt;
+                int action = 0, arg = 0;
                 while (true) {
                     if (pn > kBigP - 3 - kHot) {
                         hot_flush(hot, sm.P, pn);
                         action = BA_MERGEP;
                         break;
                     }
-                    if (head < alen && head >= rbase + rcnt) { action = BA_REFILL; break; }
-                    // the maximum of A's head, P's top and the register buffer's first; equal
-                    // copies cancel in pairs (mod 2)
-                    const unsigned long long a = head < alen ? sm.ring[head - rbase].key : 0ull;
+                    if (h0 < l0 && h0 >= rb0 + rc0) { action = BA_REFILL; arg = 0; break; }
+                    if (h1 < l1 && h1 >= rb1 + rc1) { action = BA_REFILL; arg = 1; break; }
+                    // the maximum of the levels' heads, P's top and the register buffer's
+                    // first; equal copies cancel in pairs (mod 2)
+                    const unsigned long long a0 = h0 < l0 ? sm.ring[0][h0 - rb0].key : 0ull;
+                    const unsigned long long a1 = h1 < l1 ? sm.ring[1][h1 - rb1].key : 0ull;
                     const unsigned long long p = pn ? sm.P[0].key : 0ull;
                     const unsigned long long h = hot.n ? hot.e[0].key : 0ull;
-                    const unsigned long long mx = max(h, max(p, a));
+                    const unsigned long long mx = max(max(h, p), max(a0, a1));
                     if (!mx) {
                         d1_fail(A, 2, sig, 0ull, -1, -1);
                         action = BA_ABORT;
@@ -826,9 +923,14 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                         hot_pop_front(hot);
                         cnt++;
                     }
-                    if (a == mx) {
-                        tv = sm.ring[head - rbase];
-                        head++;
+                    if (a0 == mx) {
+                        tv = sm.ring[0][h0 - rb0];
+                        h0++;
+                        cnt++;
+                    }
+                    if (a1 == mx) {
+                        tv = sm.ring[1][h1 - rb1];
+                        h1++;
                         cnt++;
                     }
                     if (p == mx) {
@@ -878,7 +980,9 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                             A.st_adds[sig]++;
                             A.st_pushed[sig] += sm.m - 1;
                         }
-                        action = (sm.m - 1 <= kBigAddSmall && pn + sm.m <= kBigP - 3 - kHot) ? BA_ADDS : BA_ADDB;
+                        // a short column goes to P (serial pushes), a longer one is merged
+                        // into level B by the CTA
+                        action = (sm.m - 1 <= A.adds && pn + sm.m <= kBigP - 3 - kHot) ? BA_ADDS : BA_ADDB;
                         break;
                     }
                     hot_flush(hot, sm.P, pn);
@@ -889,8 +993,10 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                     break;
                 }
                 sm.pn = pn;
-                sm.head = head;
+                sm.lv[0].head = h0;
+                sm.lv[1].head = h1;
                 sm.action = action;
+                sm.arg = arg;
                 if (A.prof) {
                     const long long now = clock64();
                     pc_cyc[0] += now - pc_t;  // serial propagation
@@ -907,16 +1013,17 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                 break;
             }
             if (action == BA_REFILL) {
-                const int head = sm.head, alen = sm.alen;
-                const int n = min(kBigRing, alen - head);
+                const int l = sm.arg;
+                const int head = sm.lv[l].head, len = sm.lv[l].len;
+                const int n = min(kBigRing, len - head);
                 if (t < n) {
-                    sm.ring[t] = d1_resolve_key(A, S, A.arena[sm.aoff + head + t]);
-                    prefetch_l1(reinterpret_cast<const ulonglong2*>(A.g.grad) + sm.ring[t].hi);
+                    sm.ring[l][t] = d1_resolve_key(A, S, A.arena[sm.lv[l].off + head + t]);
+                    prefetch_l1(reinterpret_cast<const ulonglong2*>(A.g.grad) + sm.ring[l][t].hi);
                 }
                 __syncthreads();
                 if (t == 0) {
-                    sm.rbase = head;
-                    sm.rcnt = n;
+                    sm.lv[l].rbase = head;
+                    sm.lv[l].rcnt = n;
                 }
                 __syncthreads();
                 continue;
@@ -935,99 +1042,52 @@ __global__ void __launch_bounds__(kBigT) k_d1_bigc(D1Args A) {
                 __syncthreads();
                 continue;
             }
-            // the remaining actions rebuild A by a merge: MERGEP (P into A), ADDB (an owner
-            // column into A), STOP (P into A, then the column [tau, A] is stored)
-            const bool withP = action != BA_ADDB && sm.pn > 0;
-            int ny = 0;
-            const unsigned long long* Y = nullptr;
-            if (withP) {
-                ny = cta_sort_pending(sm, sm.pn);
-                Y = sm.S;
-            } else if (action == BA_ADDB) {
-                ny = sm.m - 1;
-                Y = A.arena + sm.oo + 1;  // written in an earlier kernel or fenced (done flag)
-            }
-            const int nx = sm.alen - sm.head;
-            const unsigned long long* X = A.arena + sm.aoff + sm.head;
-            const int lead = action == BA_STOP ? 1 : 0;
-            __syncthreads();  // every thread has read the control block
-            if (t == 0) {
-                // A's buffers and the merge scratch are reused across this run's merges
-                // (grown by doubling); only the stored column at a stop is a fresh block
-                const int need = nx + ny;
-                bool ok = true;
-                unsigned long long o;
-                if (ny > 0 && sm.tcap < need) {
-                    const int cap = max(2 * sm.tcap, need);
-                    ok = arena_alloc(A, (unsigned long long)cap, o);
-                    sm.tbuf = (long long)o;
-                    sm.tcap = ok ? cap : 0;
+            bool ok = true;
+            if (action == BA_ADDB) {
+                // the owner column (minus its tau) into B; written in an earlier kernel or
+                // fenced by its done flag (phase 2: read from L2)
+                const unsigned long long* Y = A.arena + sm.oo + 1;
+                const int ny = sm.m - 1;
+                ok = A.phase == 2 ? big_merge<true>(A, sm, 1, Y, ny, false) : big_merge<false>(A, sm, 1, Y, ny, false);
+                ok = ok && big_settle(A, sm);
+            } else {  // MERGEP or STOP: the pending heap (sorted, mod-2 deduplicated) into B
+                if (sm.pn > 0) {
+                    const int ny = cta_sort_pending(sm, sm.pn);
+                    ok = big_merge<false>(A, sm, 1, sm.S, ny, false);
+                    if (ok && t == 0) sm.pn = 0;
+                    __syncthreads();
                 }
-                if (ok && action == BA_STOP) {
-                    ok = arena_alloc(A, (unsigned long long)(lead + need), o);
-                    sm.o_out = (long long)o;
-                } else if (ok) {
-                    const int other = sm.cur == 0 ? 1 : 0;
-                    if (sm.bcap[other] < need) {
-                        const int cap = max(2 * sm.bcap[other], need);
-                        ok = arena_alloc(A, (unsigned long long)cap, o);
-                        sm.bbuf[other] = (long long)o;
-                        sm.bcap[other] = ok ? cap : 0;
+                if (ok && action == BA_MERGEP) ok = big_settle(A, sm);
+            }
+            if (ok && action == BA_STOP) {
+                // the stored column: [tau, A merged with B]
+                const int nb1 = sm.lv[1].len - sm.lv[1].head;
+                ok = big_merge<false>(A, sm, 0, A.arena + sm.lv[1].off + sm.lv[1].head, nb1, true);
+                if (ok && t == 0) {
+                    const long long outoff = sm.o_out;
+                    A.arena[outoff] = sm.tau.key;
+                    A.col_off[sig] = outoff;
+                    A.col_len[sig] = sm.m + 1;
+                    A.nadd[sig] = sm.nadds;
+                    d1_snap(A, sig, sm.nadds, outoff, sm.m + 1);
+                    A.stop[sig] = sm.j;
+                    const uint8_t st = (uint8_t)sm.status;
+                    if (st == D1_STOP) {
+                        atomicMin(A.claim + sm.j, A.tag | (unsigned)sig);
+                    } else if (st == D1_DONE) {
+                        __threadfence();
+                        *(volatile int32_t*)(A.done + sig) = 1;
                     }
-                    sm.o_out = sm.bbuf[other];
-                    sm.next = other;
+                    A.status[sig] = st;
                 }
-                sm.o_tmp = sm.tbuf;
-                sm.ok = ok ? 1 : 0;
             }
-            __syncthreads();
-            if (!sm.ok) {
+            if (!ok) {
                 if (t == 0) A.status[sig] = D1_RETRY;
                 __syncthreads();
                 break;
             }
-            const long long outoff = sm.o_out;
-            int n;
-            if (ny > 0) {
-                n = (action == BA_ADDB && A.phase == 2)
-                        ? cta_merge<true>(sm, X, nx, Y, ny, A.arena + outoff + lead, A.arena + sm.o_tmp)
-                        : cta_merge<false>(sm, X, nx, Y, ny, A.arena + outoff + lead, A.arena + sm.o_tmp);
-            } else {
-                for (int k = t; k < nx; k += kBigT) A.arena[outoff + lead + k] = X[k];
-                n = nx;
-                __syncthreads();
-            }
-            if (action != BA_STOP) {
-                if (t == 0) {
-                    sm.aoff = outoff;
-                    sm.cur = sm.next;
-                    sm.alen = n;
-                    sm.head = 0;
-                    sm.rbase = 0;
-                    sm.rcnt = 0;
-                    if (withP) sm.pn = 0;
-                }
-                __syncthreads();
-                continue;
-            }
-            if (t == 0) {
-                A.arena[outoff] = sm.tau.key;
-                A.col_off[sig] = outoff;
-                A.col_len[sig] = n + 1;
-                A.nadd[sig] = sm.nadds;
-                d1_snap(A, sig, sm.nadds, outoff, n + 1);
-                A.stop[sig] = sm.j;
-                const uint8_t st = (uint8_t)sm.status;
-                if (st == D1_STOP) {
-                    atomicMin(A.claim + sm.j, A.tag | (unsigned)sig);
-                } else if (st == D1_DONE) {
-                    __threadfence();
-                    *(volatile int32_t*)(A.done + sig) = 1;
-                }
-                A.status[sig] = st;
-            }
             __syncthreads();
-            break;
+            if (action == BA_STOP) break;
         }
         if (t == 0 && A.prof) {
             pc_cyc[pc_last] += clock64() - pc_t;

@@ -1573,6 +1573,8 @@ D1Args d1_args(dms_ctx* c, int phase) {
     A.phase = phase;
     static const int lcap_env = getenv("DMS_D1_LCAP") ? atoi(getenv("DMS_D1_LCAP")) : kD1Cap;
     A.lcap = std::max(4, std::min(kD1Cap, lcap_env));
+    static const int adds_env = getenv("DMS_D1_ADDS") ? atoi(getenv("DMS_D1_ADDS")) : 32;
+    A.adds = std::max(0, std::min(kBigAddSmall, adds_env));
     A.deps = b.deps;
     A.ndeps = b.ctr + 14;
     A.deps_cap = b.capdeps;
