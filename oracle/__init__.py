@@ -90,6 +90,14 @@ def lib():
         L.orc_simplex_vertices.restype = ctypes.c_int
         L.orc_cells_per_vertex.argtypes = [ctypes.c_int, ctypes.c_int]
         L.orc_cells_per_vertex.restype = i64
+        L.orc_run3.argtypes = [ctypes.c_int, p, p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(p)]
+        L.orc_run3.restype = ctypes.c_int
+        L.orc_gradient_sample2.argtypes = [ctypes.c_int, p, p, p, i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(p)]
+        L.orc_gradient_sample2.restype = ctypes.c_int
+        L.orc_simplex_vertices2.argtypes = [ctypes.c_int, p, ctypes.c_int, i64, ctypes.c_int, p]
+        L.orc_simplex_vertices2.restype = ctypes.c_int
+        L.orc_cells_per_vertex2.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.orc_cells_per_vertex2.restype = i64
         _lib = L
     return _lib
 
@@ -153,42 +161,54 @@ class Result:
         L.orc_free(handle)
 
 
-def run(f: np.ndarray, nthreads: int = 1, want_pairs: bool = True, want_d1: bool = False) -> Result:
+COMPLEXES = {"freudenthal": 0, "5tet": 1}
+
+
+def _cplx(complex) -> int:
+    """complex: "freudenthal" (Kuhn triangulation, 1D/2D/3D) or "5tet" (five tetrahedra per
+    cube, 3D only -- the paper's benchmark subdivision; reading Z21)."""
+    if isinstance(complex, str):
+        return COMPLEXES[complex]
+    return int(complex)
+
+
+def run(f: np.ndarray, nthreads: int = 1, want_pairs: bool = True, want_d1: bool = False,
+        complex="freudenthal") -> Result:
     """Whole front end on a field given as a numpy array of shape [Lz,Ly,Lx], [Ly,Lx] or [Lx].
     want_d1 (3D): also D1 by Alg. 3 "PairCriticalSimplices" and its generators (Sec. 9)."""
     f = np.ascontiguousarray(f, dtype=np.float32)
     ndim, L = _dims(f.shape)
     h = ctypes.c_void_p()
     flags = (1 if want_pairs else 0) | (2 if want_d1 else 0)
-    st = lib().orc_run2(ndim, L.ctypes.data, f.ctypes.data, int(nthreads), flags, ctypes.byref(h))
+    st = lib().orc_run3(ndim, L.ctypes.data, f.ctypes.data, int(nthreads), flags, _cplx(complex), ctypes.byref(h))
     if st:
         raise OracleError(st)
     return Result(h, ndim, True)
 
 
-def gradient_sample(f: np.ndarray, verts, nthreads: int = 1) -> Result:
+def gradient_sample(f: np.ndarray, verts, nthreads: int = 1, complex="freudenthal") -> Result:
     """Gradient pairs and critical ids of the lower stars of the given vertices only."""
     f = np.ascontiguousarray(f, dtype=np.float32)
     ndim, L = _dims(f.shape)
     v = np.ascontiguousarray(verts, dtype=np.int64)
     h = ctypes.c_void_p()
-    st = lib().orc_gradient_sample(
-        ndim, L.ctypes.data, f.ctypes.data, v.ctypes.data, v.size, int(nthreads), ctypes.byref(h)
+    st = lib().orc_gradient_sample2(
+        ndim, L.ctypes.data, f.ctypes.data, v.ctypes.data, v.size, int(nthreads), _cplx(complex), ctypes.byref(h)
     )
     if st:
         raise OracleError(st)
     return Result(h, ndim, False)
 
 
-def simplex_vertices(shape, dim: int, sid: int) -> np.ndarray:
-    """Vertex ids of the anchored simplex id (ascending vertex id), reading Z13."""
+def simplex_vertices(shape, dim: int, sid: int, complex="freudenthal") -> np.ndarray:
+    """Vertex ids of the anchored simplex id (ascending vertex id), readings Z13 / Z21."""
     ndim, L = _dims(shape)
     out = np.zeros(4, dtype=np.int64)
-    st = lib().orc_simplex_vertices(ndim, L.ctypes.data, dim, int(sid), out.ctypes.data)
+    st = lib().orc_simplex_vertices2(ndim, L.ctypes.data, dim, int(sid), _cplx(complex), out.ctypes.data)
     if st:
         raise OracleError(st)
     return np.sort(out[: dim + 1])
 
 
-def cells_per_vertex(ndim: int, dim: int) -> int:
-    return int(lib().orc_cells_per_vertex(ndim, dim))
+def cells_per_vertex(ndim: int, dim: int, complex="freudenthal") -> int:
+    return int(lib().orc_cells_per_vertex2(ndim, dim, _cplx(complex)))

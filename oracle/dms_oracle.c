@@ -18,6 +18,8 @@
  *                           order, virtual maximum on the boundary
  *                           ("ignore" mode: boundary arcs dropped)
  *   O8 infinite classes  -- Sec. 6
+ *   O2' complex (3D)     -- five tetrahedra per cube, the subdivision of the paper's
+ *                           benchmarks                                 P:662-664 (Sec. 8.1)
  *
  * Parity pins: tests/test_oracle_pins.py (hand-built fields, SPEC examples, Euler
  * characteristic, gradient validity, Robins' guarantee, brute-force Kruskal and
@@ -38,7 +40,8 @@ typedef struct {
     int64_t L[3];      /* extents, unused axes = 1 */
     int64_t N;
     const float *f;
-    int64_t ncell[4];  /* anchored chains per vertex for each simplex dimension */
+    int64_t ncell[4];  /* anchored cells per vertex for each simplex dimension */
+    int cplx;          /* 0: Freudenthal (Kuhn) triangulation; 1: five tetrahedra per cube (3D) */
 } grid;
 
 /* K(u) < K(v): compare values (IEEE <, so -0 == +0), break ties by vertex index.
@@ -161,14 +164,89 @@ static void build_chains(int ndim)
     chain_ndim_built |= 1 << ndim;
 }
 
-static void grid_init(grid *g, int ndim, const int64_t *L, const float *f)
+/* ------------------------------------------------------------------ five-tetrahedra complex
+ * P:662-664 (Sec. 8.1): the paper's 3D benchmark volumes are "triangulated into a
+ * simplicial complex by breaking up each cell into ... five tetrahedra".  Reading Z21
+ * (DESIGN.md): the cube with minimum corner a, parity p = (ax + ay + az) mod 2, is cut
+ * into the central tetrahedron on its four corners c (local offsets, bit masks x=1,
+ * y=2, z=4) with popcount(c) + p even, and the four corner tetrahedra {o, o^1, o^2, o^4}
+ * at its other four corners o.  The central corners are the vertices of even coordinate
+ * sum in every cube, so each square face is cut along the diagonal joining its two
+ * even-sum corners from both sides: the cubes fit together (a conforming complex).
+ *
+ * Ids (reading Z21): a k-simplex is anchored at its component-wise minimum a (not
+ * necessarily one of its vertices); its id is t5_count[k] * vid(a) + idx, idx = the
+ * position of its vertex offsets from a (ascending masks) among all k-simplices of the
+ * cube at a with component-wise minimum a, for a's parity, sorted ascending as tuples. */
+
+static int t5_built = 0;
+static int t5_count[4];              /* cells per anchor: 1, 6, 10, 5 */
+static int t5_tab[2][4][16][4];      /* [parity][k][idx][j]: ascending vertex masks */
+
+/* the five tetrahedra of a cube of parity p, as local corner masks */
+static void t5_cube_tets(int p, int tets[5][4])
+{
+    int nc = 0, nt = 1;
+    for (int c = 0; c < 8; c++)
+        if (((popc(c) + p) & 1) == 0) tets[0][nc++] = c;                 /* central */
+        else { tets[nt][0] = c; tets[nt][1] = c ^ 1; tets[nt][2] = c ^ 2; tets[nt][3] = c ^ 4; nt++; }
+}
+
+static int cmp_int(const void *a, const void *b) { return *(const int *)a - *(const int *)b; }
+
+static void build_t5(void)
+{
+    if (t5_built) return;
+    for (int p = 0; p < 2; p++) {
+        int tets[5][4];
+        t5_cube_tets(p, tets);
+        for (int k = 1; k <= 3; k++) {
+            int n = 0, cand[16][4];
+            for (int t = 0; t < 5; t++)
+                for (int sub = 1; sub < 16; sub++) {
+                    if (popc(sub) != k + 1) continue;
+                    int m[4], q = 0, andm = 7;
+                    for (int j = 0; j < 4; j++) if ((sub >> j) & 1) { m[q++] = tets[t][j]; andm &= tets[t][j]; }
+                    if (andm != 0) continue;            /* anchored elsewhere */
+                    qsort(m, k + 1, sizeof(int), cmp_int);
+                    int dup = 0;
+                    for (int i = 0; i < n && !dup; i++) dup = !memcmp(cand[i], m, (k + 1) * sizeof(int));
+                    if (!dup) { memcpy(cand[n], m, (k + 1) * sizeof(int)); n++; }
+                }
+            /* ascending tuples (insertion sort, n <= 10) */
+            for (int i = 1; i < n; i++)
+                for (int j = i; j > 0; j--) {
+                    int c = 0;
+                    for (int u = 0; u <= k && !c; u++) c = cand[j][u] - cand[j - 1][u];
+                    if (c >= 0) break;
+                    int t[4]; memcpy(t, cand[j], sizeof t); memcpy(cand[j], cand[j - 1], sizeof t);
+                    memcpy(cand[j - 1], t, sizeof t);
+                }
+            if (p == 1 && n != t5_count[k]) abort();  /* both parities have the same counts */
+            t5_count[k] = n;
+            for (int i = 0; i < n; i++) memcpy(t5_tab[p][k][i], cand[i], sizeof cand[i]);
+        }
+    }
+    t5_count[0] = 1;
+    t5_built = 1;
+}
+
+static inline int parity3(const int64_t a[3]) { return (int)((a[0] + a[1] + a[2]) & 1); }
+
+static void grid_init(grid *g, int ndim, const int64_t *L, const float *f, int cplx)
 {
     g->ndim = ndim;
+    g->cplx = cplx;
     for (int i = 0; i < 3; i++) g->L[i] = (i < ndim) ? L[i] : 1;
     g->N = g->L[0] * g->L[1] * g->L[2];
     g->f = f;
     build_chains(ndim);
     g->ncell[0] = 1;
+    if (cplx) {
+        build_t5();
+        for (int k = 1; k <= 3; k++) g->ncell[k] = t5_count[k];
+        return;
+    }
     for (int k = 1; k <= 3; k++) g->ncell[k] = (k <= ndim) ? chain_count[ndim][k] : 0;
 }
 
@@ -186,6 +264,13 @@ static int64_t simp_id(const grid *g, const simp *s)
         int m = 0;
         for (int ax = 0; ax < 3; ax++) if (c[i][ax] - a[ax] == 1) m |= 1 << ax;
         masks[nm++] = m;
+    }
+    if (g->cplx) {  /* five tetrahedra: ascending masks looked up in the anchor parity's table */
+        qsort(masks, nm, sizeof(int), cmp_int);
+        int p = parity3(a), k = s->dim;
+        for (int i = 0; i < t5_count[k]; i++)
+            if (!memcmp(t5_tab[p][k][i], masks, nm * sizeof(int))) return g->ncell[k] * vid(g, a) + i;
+        abort();  /* not a simplex of the complex: cannot happen */
     }
     /* sort masks by population count: S_0 = 0 < S_1 < ... < S_k */
     for (int i = 1; i < nm; i++)
@@ -212,6 +297,16 @@ static void simp_from_id(const grid *g, int dim, int64_t id, simp *s)
     int idx = (int)(id % g->ncell[dim]);
     int64_t a[3];
     coords(g, av, a);
+    if (g->cplx) {
+        const int *m = t5_tab[parity3(a)][dim][idx];
+        for (int j = 0; j <= dim; j++) {
+            int64_t c[3];
+            for (int ax = 0; ax < 3; ax++) c[ax] = a[ax] + ((m[j] >> ax) & 1);
+            s->v[j] = vid(g, c);
+        }
+        simp_sort(g, s);
+        return;
+    }
     s->v[0] = av;
     for (int j = 0; j < dim; j++) {
         int m = chain_tab[g->ndim][dim][idx][j];
@@ -231,7 +326,8 @@ static int id_valid(const grid *g, int dim, int64_t id)
     int64_t a[3];
     coords(g, av, a);
     int full = 0;
-    for (int j = 0; j < dim; j++) full |= chain_tab[g->ndim][dim][idx][j];
+    if (g->cplx) for (int j = 0; j <= dim; j++) full |= t5_tab[parity3(a)][dim][idx][j];
+    else for (int j = 0; j < dim; j++) full |= chain_tab[g->ndim][dim][idx][j];
     for (int ax = 0; ax < 3; ax++) if (((full >> ax) & 1) && a[ax] + 1 >= g->L[ax]) return 0;
     return 1;
 }
@@ -242,19 +338,43 @@ static const int perm1[1][3] = {{0}};
 static const int perm2[2][3] = {{0, 1}, {1, 0}};
 static const int perm3[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
 
-/* All simplices of the Freudenthal triangulation containing x:
- * every d-cube incident to x is split into d! simplices q_0 < ... < q_d with
- * q_{j+1} = q_j + e_{pi(j)}; the star of x is every face of those simplices that
- * contains x.  If lower_only, keep the lower star St^-(x): faces whose
- * other vertices all precede x in K order.  Returns the number of simplices
+/* The top simplices of the d-cube with minimum corner a, as vertex ids:
+ * Freudenthal -- d! simplices q_0 < ... < q_d with q_{j+1} = q_j + e_{pi(j)}, one per
+ * permutation pi; five tetrahedra (cplx = 1) -- t5_cube_tets.  Returns the count. */
+static int cube_simplices(const grid *g, const int64_t a[3], int64_t q[6][4])
+{
+    int d = g->ndim;
+    if (g->cplx) {
+        int tets[5][4];
+        t5_cube_tets(parity3(a), tets);
+        for (int t = 0; t < 5; t++)
+            for (int j = 0; j < 4; j++) {
+                int64_t qc[3];
+                for (int ax = 0; ax < 3; ax++) qc[ax] = a[ax] + ((tets[t][j] >> ax) & 1);
+                q[t][j] = vid(g, qc);
+            }
+        return 5;
+    }
+    int nperm = d == 1 ? 1 : d == 2 ? 2 : 6;
+    const int (*perm)[3] = d == 1 ? perm1 : d == 2 ? perm2 : perm3;
+    for (int p = 0; p < nperm; p++) {
+        int64_t qc[3] = {a[0], a[1], a[2]};
+        q[p][0] = vid(g, qc);
+        for (int j = 0; j < d; j++) { qc[perm[p][j]] += 1; q[p][j + 1] = vid(g, qc); }
+    }
+    return nperm;
+}
+
+/* All simplices of the complex containing x: every d-cube incident to x is split into
+ * its top simplices (cube_simplices); the star of x is every face of those simplices
+ * that contains x.  If lower_only, keep the lower star St^-(x): faces
+ * whose other vertices all precede x in K order.  Returns the number of simplices
  * (excluding the vertex x itself). */
 static int star(const grid *g, int64_t x, int lower_only, simp *out)
 {
     int d = g->ndim;
     int64_t c[3];
     coords(g, x, c);
-    int nperm = d == 1 ? 1 : d == 2 ? 2 : 6;
-    const int (*perm)[3] = d == 1 ? perm1 : d == 2 ? perm2 : perm3;
     int n = 0;
     for (int b = 0; b < (1 << d); b++) {
         int64_t a[3] = {c[0], c[1], c[2]};
@@ -264,11 +384,10 @@ static int star(const grid *g, int64_t x, int lower_only, simp *out)
             if (a[ax] < 0 || a[ax] > g->L[ax] - 2) ok = 0;
         }
         if (!ok) continue;
-        for (int p = 0; p < nperm; p++) {
-            int64_t q[4];
-            int64_t qc[3] = {a[0], a[1], a[2]};
-            q[0] = vid(g, qc);
-            for (int j = 0; j < d; j++) { qc[perm[p][j]] += 1; q[j + 1] = vid(g, qc); }
+        int64_t qs[6][4];
+        int nq = cube_simplices(g, a, qs);
+        for (int p = 0; p < nq; p++) {
+            const int64_t *q = qs[p];
             int j0 = -1;
             for (int j = 0; j <= d; j++) if (q[j] == x) j0 = j;
             if (j0 < 0) continue;
@@ -608,17 +727,14 @@ static int cmp_triple(const void *a, const void *b)
 }
 
 /* the d-simplices having the (d-1)-simplex s as a facet (1 on the grid boundary,
- * else 2), sorted by id: scan the d-simplices of every d-cube around s's first vertex
- * (each d-simplex of the Freudenthal triangulation comes from exactly one cube and
- * one permutation). */
+ * else 2), sorted by id: scan the top simplices of every d-cube around s's first vertex
+ * (each top simplex comes from exactly one cube). */
 static int cofacets(const grid *g, const simp *s, int64_t out[2])
 {
     int d = g->ndim;
     int64_t c[3];
     int64_t x = s->v[0];
     coords(g, x, c);
-    int nperm = d == 1 ? 1 : d == 2 ? 2 : 6;
-    const int (*perm)[3] = d == 1 ? perm1 : d == 2 ? perm2 : perm3;
     int nf = 0;
     for (int b = 0; b < (1 << d); b++) {
         int64_t a[3] = {c[0], c[1], c[2]};
@@ -628,12 +744,12 @@ static int cofacets(const grid *g, const simp *s, int64_t out[2])
             if (a[ax] < 0 || a[ax] > g->L[ax] - 2) ok = 0;
         }
         if (!ok) continue;
-        for (int p = 0; p < nperm; p++) {
+        int64_t qs[6][4];
+        int nq = cube_simplices(g, a, qs);
+        for (int p = 0; p < nq; p++) {
             simp t;
-            int64_t qc[3] = {a[0], a[1], a[2]};
             t.dim = d;
-            t.v[0] = vid(g, qc);
-            for (int j = 0; j < d; j++) { qc[perm[p][j]] += 1; t.v[j + 1] = vid(g, qc); }
+            for (int j = 0; j <= d; j++) t.v[j] = qs[p][j];
             int contains = 1;
             for (int i = 0; i <= s->dim && contains; i++) {
                 int found = 0;
@@ -675,15 +791,17 @@ static orc_pair mkpair(const grid *g, int bdim, int64_t bid, int ddim, int64_t d
  * everything else is sequential as in the paper's D0/D_{d-1} union-find. */
 /* flags: bit 0 want_pairs (the gradient vectors), bit 1 want_d1 (3D: D1 by Alg. 3 and
  * the generators of Sec. 9) */
-int orc_run2(int ndim, const int64_t *L, const float *f, int nthreads, int flags, orc_result **out)
+/* cplx: 0 Freudenthal, 1 five tetrahedra per cube (3D only; else status 1) */
+int orc_run3(int ndim, const int64_t *L, const float *f, int nthreads, int flags, int cplx, orc_result **out)
 {
     const int want_pairs = flags & 1;
     const int want_d1 = (flags & 2) && ndim == 3;
     int st = check_args(ndim, L);
     if (st) return st;
+    if (cplx < 0 || cplx > 1 || (cplx == 1 && ndim != 3)) return 1;
     orc_result *r = calloc(1, sizeof(orc_result));
     grid *g = &r->g;
-    grid_init(g, ndim, L, f);
+    grid_init(g, ndim, L, f, cplx);
     int d = ndim;
     double t0 = now_ms();
     for (int64_t i = 0; i < g->N; i++) if (isnan(f[i])) { free(r); return 3; }
@@ -987,22 +1105,28 @@ int orc_run2(int ndim, const int64_t *L, const float *f, int nthreads, int flags
     return 0;
 }
 
+int orc_run2(int ndim, const int64_t *L, const float *f, int nthreads, int flags, orc_result **out)
+{
+    return orc_run3(ndim, L, f, nthreads, flags, 0, out);
+}
+
 int orc_run(int ndim, const int64_t *L, const float *f, int nthreads, int want_pairs, orc_result **out)
 {
-    return orc_run2(ndim, L, f, nthreads, want_pairs ? 1 : 0, out);
+    return orc_run3(ndim, L, f, nthreads, want_pairs ? 1 : 0, 0, out);
 }
 
 /* Gradient restricted to the lower stars of the given vertices (for sampled parity
  * at sizes where the full run is too slow).  Pairs sorted; critical ids per dim
  * sorted by id. */
-int orc_gradient_sample(int ndim, const int64_t *L, const float *f, const int64_t *verts, int64_t nv,
-                        int nthreads, orc_result **out)
+int orc_gradient_sample2(int ndim, const int64_t *L, const float *f, const int64_t *verts, int64_t nv,
+                         int nthreads, int cplx, orc_result **out)
 {
     int st = check_args(ndim, L);
     if (st) return st;
+    if (cplx < 0 || cplx > 1 || (cplx == 1 && ndim != 3)) return 1;
     orc_result *r = calloc(1, sizeof(orc_result));
     grid *g = &r->g;
-    grid_init(g, ndim, L, f);
+    grid_init(g, ndim, L, f, cplx);
     vec pairs = {0}, crit = {0};
     pairs.el = 3 * sizeof(int64_t);
     crit.el = sizeof(simp);
@@ -1022,6 +1146,12 @@ int orc_gradient_sample(int ndim, const int64_t *L, const float *f, const int64_
     free(crit.p);
     *out = r;
     return 0;
+}
+
+int orc_gradient_sample(int ndim, const int64_t *L, const float *f, const int64_t *verts, int64_t nv,
+                        int nthreads, orc_result **out)
+{
+    return orc_gradient_sample2(ndim, L, f, verts, nv, nthreads, 0, out);
 }
 
 /* ------------------------------------------------------------------ accessors */
@@ -1092,18 +1222,28 @@ void orc_free(orc_result *r)
 }
 
 /* anchored id <-> vertices, exported for the oracle's own tests */
-int orc_simplex_vertices(int ndim, const int64_t *L, int dim, int64_t id, int64_t *verts_out)
+int orc_simplex_vertices2(int ndim, const int64_t *L, int dim, int64_t id, int cplx, int64_t *verts_out)
 {
     if (check_args(ndim, L)) return 2;
+    if (cplx < 0 || cplx > 1 || (cplx == 1 && ndim != 3)) return 1;
     grid g;
-    grid_init(&g, ndim, L, NULL);
+    grid_init(&g, ndim, L, NULL, cplx);
     if (dim < 0 || dim > ndim) return 1;
     if (id < 0 || id >= g.ncell[dim] * g.N || !id_valid(&g, dim, id)) return 1;
-    /* vertices sorted by id (no values needed) */
+    /* vertices (no values needed) */
     int64_t av = dim ? id / g.ncell[dim] : id;
     int idx = dim ? (int)(id % g.ncell[dim]) : 0;
     int64_t a[3];
     coords(&g, av, a);
+    if (cplx) {
+        const int *m = t5_tab[parity3(a)][dim][idx];
+        for (int j = 0; j <= dim; j++) {
+            int64_t c[3];
+            for (int ax = 0; ax < 3; ax++) c[ax] = a[ax] + ((m[j] >> ax) & 1);
+            verts_out[j] = vid(&g, c);
+        }
+        return 0;
+    }
     verts_out[0] = av;
     for (int j = 0; j < dim; j++) {
         int m = chain_tab[ndim][dim][idx][j];
@@ -1114,8 +1254,22 @@ int orc_simplex_vertices(int ndim, const int64_t *L, int dim, int64_t id, int64_
     return 0;
 }
 
-int64_t orc_cells_per_vertex(int ndim, int dim)
+int orc_simplex_vertices(int ndim, const int64_t *L, int dim, int64_t id, int64_t *verts_out)
 {
+    return orc_simplex_vertices2(ndim, L, dim, id, 0, verts_out);
+}
+
+int64_t orc_cells_per_vertex2(int ndim, int dim, int cplx)
+{
+    if (cplx) {
+        build_t5();
+        return (ndim == 3 && dim >= 0 && dim <= 3) ? t5_count[dim] : 0;
+    }
     build_chains(ndim);
     return dim == 0 ? 1 : chain_count[ndim][dim];
+}
+
+int64_t orc_cells_per_vertex(int ndim, int dim)
+{
+    return orc_cells_per_vertex2(ndim, dim, 0);
 }

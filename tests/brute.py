@@ -49,6 +49,43 @@ def freudenthal(shape):
     return cx
 
 
+# the even cube's five tetrahedra written out by hand (local corner coordinates); the
+# central one spans the corners of even coordinate sum
+_EVEN_CUBE_TETS = [
+    [(0, 0, 0), (1, 1, 0), (1, 0, 1), (0, 1, 1)],
+    [(1, 0, 0), (0, 0, 0), (1, 1, 0), (1, 0, 1)],
+    [(0, 1, 0), (0, 0, 0), (1, 1, 0), (0, 1, 1)],
+    [(0, 0, 1), (0, 0, 0), (1, 0, 1), (0, 1, 1)],
+    [(1, 1, 1), (1, 1, 0), (1, 0, 1), (0, 1, 1)],
+]
+
+
+def five_tet(shape):
+    """The five-tetrahedra subdivision of a 3D grid: cubes whose minimum
+    corner has an even coordinate sum are cut as _EVEN_CUBE_TETS, the others as its
+    mirror image x -> 1 - x, so neighbouring cubes cut their common face along the same
+    diagonal.  Returns {dim: set(frozenset(vertex ids))}."""
+    assert len(shape) == 3
+    L = grid_shape_xfirst(shape)
+    cx = {k: set() for k in range(4)}
+    for a in itertools.product(*[range(L[i] - 1) for i in range(3)]):
+        odd = sum(a) % 2 == 1
+        for tet in _EVEN_CUBE_TETS:
+            vs = []
+            for (x, y, z) in tet:
+                if odd:
+                    x = 1 - x
+                vs.append(vertex_id((a[0] + x, a[1] + y, a[2] + z), L))
+            for k in range(4):
+                for sub in itertools.combinations(vs, k + 1):
+                    cx[k].add(frozenset(sub))
+    return cx
+
+
+def complex_of(shape, complex="freudenthal"):
+    return five_tet(shape) if complex == "5tet" else freudenthal(shape)
+
+
 def ranks(f):
     """rank(v) = #{u : (f(u), u) < (f(v), v)} -- P:1368-1372 with the index tie-break."""
     flat = [float(x) for x in np.asarray(f, dtype=np.float32).ravel()]
@@ -102,10 +139,10 @@ def reduce_all(cx, r):
     return pairs, unpaired
 
 
-def diagrams_by_reduction(f):
+def diagrams_by_reduction(f, complex="freudenthal"):
     """{p: [(birth simplex, death simplex)]} with zero-persistence pairs removed
     (same highest vertex, reading Z8), plus infinite births."""
-    cx = freudenthal(f.shape)
+    cx = complex_of(f.shape, complex)
     r = ranks(f)
     pairs, unpaired = reduce_all(cx, r)
     out = {}
@@ -116,10 +153,10 @@ def diagrams_by_reduction(f):
     return out, unpaired, r
 
 
-def kruskal_d0(f):
+def kruskal_d0(f, complex="freudenthal"):
     """D0 by Kruskal over ALL edges in lexicographic order, Elder rule, dropping the
     pairs whose dying vertex is the edge's own highest vertex (zero persistence)."""
-    cx = freudenthal(f.shape)
+    cx = complex_of(f.shape, complex)
     r = ranks(f)
     n = len(r)
     parent = list(range(n))

@@ -19,8 +19,8 @@ import oracle
 from synth import fields
 
 
-def ids_to_sets(shape, dim, ids):
-    return [frozenset(int(v) for v in oracle.simplex_vertices(shape, dim, int(i))) for i in ids]
+def ids_to_sets(shape, dim, ids, complex="freudenthal"):
+    return [frozenset(int(v) for v in oracle.simplex_vertices(shape, dim, int(i), complex)) for i in ids]
 
 
 def sqdist_field(shape, sign):
@@ -104,18 +104,18 @@ def test_cells_per_vertex_and_counts():
 
 # ------------------------------------------------------------------ O3 gradient validity
 
-def check_gradient(f, res):
+def check_gradient(f, res, complex="freudenthal"):
     """Validity of a discrete gradient plus the partition of
     the complex into pairs and critical simplices."""
     shape = f.shape
     d = len(shape)
-    cx = brute.freudenthal(shape)
+    cx = brute.complex_of(shape, complex)
     r = brute.ranks(f)
     seen = set()
     head_of = {}  # tail -> head
     for tdim, tid, hid in res.pairs:
-        t = ids_to_sets(shape, int(tdim), [tid])[0]
-        h = ids_to_sets(shape, int(tdim) + 1, [hid])[0]
+        t = ids_to_sets(shape, int(tdim), [tid], complex)[0]
+        h = ids_to_sets(shape, int(tdim) + 1, [hid], complex)[0]
         assert t < h and len(h) == len(t) + 1  # facet / cofacet
         assert brute.maxvertex(t, r) == brute.maxvertex(h, r)  # same lower star: zero persistence
         assert t not in seen and h not in seen  # at most one vector per simplex
@@ -124,7 +124,7 @@ def check_gradient(f, res):
         head_of[t] = h
     crit = set()
     for k in range(d + 1):
-        for s in ids_to_sets(shape, k, res.crit[k]):
+        for s in ids_to_sets(shape, k, res.crit[k], complex):
             assert s not in seen and s not in crit
             crit.add(s)
     allsimp = set(s for k in cx for s in cx[k])
@@ -159,14 +159,14 @@ def check_gradient(f, res):
     return cx, r
 
 
-def robins_guarantee(f, res, cx, r):
+def robins_guarantee(f, res, cx, r, complex="freudenthal"):
     """Robins et al.: the critical k-simplices in St^-(x) number beta~_{k-1}(Lk^-(x))
     (P:1049-1054); critical edges are canonical (reading Z16)."""
     shape = f.shape
     d = len(shape)
     crit_by_x = {}
     for k in range(d + 1):
-        for s in ids_to_sets(shape, k, res.crit[k]):
+        for s in ids_to_sets(shape, k, res.crit[k], complex):
             crit_by_x.setdefault(brute.maxvertex(s, r), []).append(s)
     for x in range(len(r)):
         lk = brute.lower_link(cx, x, r)
@@ -283,13 +283,13 @@ def test_bowl(d):
 
 # ------------------------------------------------------------------ O5 / O6 vs brute force
 
-def pair_sets(shape, res_pairs, bdim):
+def pair_sets(shape, res_pairs, bdim, complex="freudenthal"):
     out = set()
     for p in res_pairs:
         if p["death_id"] < 0:
             continue
-        b = ids_to_sets(shape, bdim, [p["birth_id"]])[0]
-        dd = ids_to_sets(shape, bdim + 1, [p["death_id"]])[0]
+        b = ids_to_sets(shape, bdim, [p["birth_id"]], complex)[0]
+        dd = ids_to_sets(shape, bdim + 1, [p["death_id"]], complex)[0]
         out.add((b, dd))
     return out
 
@@ -396,8 +396,8 @@ def test_degenerate_rejected():
 D1_SHAPES = [(3, 3, 3), (4, 3, 4), (4, 4, 4), (3, 5, 4), (5, 5, 5)]
 
 
-def _edge_sets(shape, ids):
-    return [frozenset(int(v) for v in oracle.simplex_vertices(shape, 1, int(i))) for i in ids]
+def _edge_sets(shape, ids, complex="freudenthal"):
+    return [frozenset(int(v) for v in oracle.simplex_vertices(shape, 1, int(i), complex)) for i in ids]
 
 
 @pytest.mark.parametrize("shape", D1_SHAPES)
@@ -436,14 +436,14 @@ def test_d1_vs_brute_force(shape, seed):
     _check_generators(f, res, r)
 
 
-def _check_generators(f, res, r):
+def _check_generators(f, res, r, complex="freudenthal"):
     """Sec. 9: the generator of a D1 pair (tau, sigma) is a 1-cycle (every
     vertex has even degree), its highest edge is tau, and it is homologous to the
     boundary of sigma through triangles entering no later than sigma: generator +
     boundary(sigma) lies in the GF(2) span of the boundaries of the triangles preceding
     sigma in the filtration."""
     shape = f.shape
-    cx = brute.freudenthal(shape)
+    cx = brute.complex_of(shape, complex)
     tris = sorted(cx[2], key=lambda s: brute.lexkey(s, r))
     edges = sorted(cx[1], key=lambda s: brute.lexkey(s, r))
     eidx = {e: i for i, e in enumerate(edges)}
@@ -458,16 +458,16 @@ def _check_generators(f, res, r):
     tri_bits = [bits_of_edges([t - {v} for v in t]) for t in tris]
     for i, p in enumerate(res.d1):
         g_ids = res.gen[res.gen_off[i]:res.gen_off[i + 1]]
-        g_edges = _edge_sets(shape, g_ids)
+        g_edges = _edge_sets(shape, g_ids, complex)
         assert len(set(g_edges)) == len(g_edges) > 0
         deg = {}
         for e in g_edges:
             for v in e:
                 deg[v] = deg.get(v, 0) + 1
         assert all(x % 2 == 0 for x in deg.values()), "not a cycle"
-        tau = _edge_sets(shape, [p["birth_id"]])[0]
+        tau = _edge_sets(shape, [p["birth_id"]], complex)[0]
         assert max(g_edges, key=lambda e: brute.lexkey(e, r)) == tau
-        sigma = ids_to_sets(shape, 2, [p["death_id"]])[0]
+        sigma = ids_to_sets(shape, 2, [p["death_id"]], complex)[0]
         target = bits_of_edges(g_edges) ^ tri_bits[tpos[sigma]]
         earlier = tri_bits[: tpos[sigma]]
         assert brute.gf2_rank(earlier + [target]) == brute.gf2_rank(list(earlier)), "not homologous"
