@@ -78,6 +78,18 @@ typedef enum {
     DMS_ERR_INVARIANT = 8   /* an internal invariant check failed                */
 } dms_status;
 
+/* The simplicial complex on the grid.  DMS_COMPLEX_FREUDENTHAL: the Kuhn/Freudenthal
+ * triangulation (PAPER.md 1360-1366; 1D/2D/3D; in 2D the paper's own "two triangles" per
+ * cell).  DMS_COMPLEX_5TET (3D only): five tetrahedra per cube, the subdivision of
+ * the paper's benchmark volumes (PAPER.md 662-664, Sec. 8.1; reading Z21): the
+ * cube with minimum corner a is cut into the central tetrahedron on its corners of even
+ * coordinate sum and the four corner tetrahedra at the others.  Anchored ids: the
+ * component-wise minimum of the simplex, C_k = 1/6/10/5. */
+typedef enum {
+    DMS_COMPLEX_FREUDENTHAL = 0,
+    DMS_COMPLEX_5TET = 1
+} dms_complex;
+
 typedef enum {
     DMS_BOUNDARY_EXACT = 0, /* virtual maximum on the boundary (PAPER.md 2787-2825)          */
     DMS_BOUNDARY_IGNORE = 1 /* no virtual maximum (PAPER.md 2822-2825, App. A 2927-2949)      */
@@ -97,6 +109,17 @@ typedef struct {
  * and allocates the device workspace. */
 dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* stream, dms_ctx** out);
 
+/* dms_create on the complex `cplx` (dms_complex; DMS_COMPLEX_5TET needs ndim = 3, else
+ * DMS_ERR_ARG).  Every call below works on both complexes, except dms_diagram1,
+ * dms_generators and dms_unpaired_saddles(which = 2), which return DMS_ERR_STATE on the
+ * five-tetrahedra complex (its D1 is in the oracle only).  Five-tetrahedra gradient
+ * layout (16 bytes per vertex, one byte per cell indexed by cell id): [0, N) vertex codes
+ * (star slot of the paired edge, 0xFF minimum), [N, 11N) triangle codes, [11N, 16N)
+ * tetrahedron codes (j < dim + 1: paired with the facet omitting vertex j of the cell's
+ * ascending-mask vertex list, 0xFE: paired with a cofacet, 0xFF: critical). */
+dms_status dms_create2(const int64_t dims[3], int ndim, const float* d_f, void* stream, dms_complex cplx,
+                       dms_ctx** out);
+
 /* Vertex order (PAPER.md 1368-1372; Sec. 7.1 "global sort"): d_rank[v] = number of
  * vertices u with K(u) < K(v), i.e. a key-value radix sort of (value, index).
  * d_rank: caller-owned device int32[N]; it must stay valid until the next
@@ -105,7 +128,7 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
  * Asynchronous. */
 dms_status dms_order(dms_ctx* ctx, int32_t* d_rank);
 
-/* Bytes of the packed gradient: 3D 16 B/vertex, 2D 2 B/vertex, 1D 1 B/vertex. */
+/* Bytes of the packed gradient: 3D 16 B/vertex (both complexes), 2D 2 B/vertex, 1D 1 B/vertex. */
 size_t dms_gradient_bytes(const dms_ctx* ctx);
 
 /* Lower-star discrete gradient (Robins et al. ProcessLowerStars, PAPER.md 1965-1971)
@@ -202,6 +225,12 @@ dms_status dms_sync(dms_ctx* ctx);
  * words of those vertices.  Returns the number of triples written (<= cap), or -1. */
 int64_t dms_decode_pairs(const int64_t dims[3], int ndim, const void* h_words, int64_t v0, int64_t v1,
                          int64_t* h_triples, int64_t cap);
+
+/* dms_decode_pairs on either complex.  Five tetrahedra: h_words is the WHOLE gradient
+ * buffer (16 N bytes) and the triples are the vectors whose head cell is anchored at a
+ * vertex of [v0, v1) (the vertex itself for vertex -> edge vectors). */
+int64_t dms_decode_pairs2(const int64_t dims[3], int ndim, dms_complex cplx, const void* h_words, int64_t v0,
+                          int64_t v1, int64_t* h_triples, int64_t cap);
 
 /* Copy `bytes` between device/host buffers on the context's stream and wait
  * (cudaMemcpyDefault); used by the binding to move library-owned results. */

@@ -45,6 +45,7 @@ STATUS = {
 # every symbol include/dms.h declares
 ABI_SYMBOLS = [
     "dms_create",
+    "dms_create2",
     "dms_order",
     "dms_gradient_bytes",
     "dms_gradient",
@@ -58,6 +59,7 @@ ABI_SYMBOLS = [
     "dms_run_all_host",
     "dms_sync",
     "dms_decode_pairs",
+    "dms_decode_pairs2",
     "dms_copy",
     "dms_set_timing",
     "dms_stage_ms",
@@ -88,6 +90,7 @@ def lib():
     p, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     P = ctypes.POINTER
     L.dms_create.argtypes = [p, i32, p, p, P(p)]
+    L.dms_create2.argtypes = [p, i32, p, p, i32, P(p)]
     L.dms_order.argtypes = [p, p]
     L.dms_gradient_bytes.argtypes = [p]
     L.dms_gradient_bytes.restype = ctypes.c_size_t
@@ -103,6 +106,8 @@ def lib():
     L.dms_sync.argtypes = [p]
     L.dms_decode_pairs.argtypes = [p, i32, p, i64, i64, p, i64]
     L.dms_decode_pairs.restype = i64
+    L.dms_decode_pairs2.argtypes = [p, i32, i32, p, i64, i64, p, i64]
+    L.dms_decode_pairs2.restype = i64
     L.dms_copy.argtypes = [p, p, p, ctypes.c_size_t]
     L.dms_set_timing.argtypes = [p, i32]
     L.dms_stage_ms.argtypes = [p, p]
@@ -112,7 +117,7 @@ def lib():
     L.dms_last_error.restype = ctypes.c_char_p
     L.dms_destroy.argtypes = [p]
     L.dms_destroy.restype = None
-    for name in ("dms_create", "dms_order", "dms_gradient", "dms_critical", "dms_diagram0", "dms_diagram_top",
+    for name in ("dms_create", "dms_create2", "dms_order", "dms_gradient", "dms_critical", "dms_diagram0", "dms_diagram_top",
                  "dms_unpaired_saddles", "dms_diagram1", "dms_generators", "dms_run_all", "dms_run_all_host", "dms_sync", "dms_copy", "dms_set_timing",
                  "dms_stage_ms"):
         getattr(L, name).restype = ctypes.c_int
@@ -140,8 +145,12 @@ def _dims_of(shape):
 
 # ---------------------------------------------------------------- ABI-named functions
 
-def dms_create(f, stream=None):
-    """f: contiguous float32 CUDA tensor of shape [Lz,Ly,Lx] / [Ly,Lx] / [Lx]."""
+COMPLEXES = {"freudenthal": 0, "5tet": 1}  # dms_complex
+
+
+def dms_create(f, stream=None, complex="freudenthal"):
+    """f: contiguous float32 CUDA tensor of shape [Lz,Ly,Lx] / [Ly,Lx] / [Lx].
+    complex: "freudenthal" (DMS_COMPLEX_FREUDENTHAL) or "5tet" (DMS_COMPLEX_5TET, 3D)."""
     import torch
 
     if not (isinstance(f, torch.Tensor) and f.is_cuda and f.dtype == torch.float32 and f.is_contiguous()):
@@ -150,8 +159,8 @@ def dms_create(f, stream=None):
         stream = torch.cuda.current_stream(f.device)
     dims, ndim = _dims_of(f.shape)
     h = ctypes.c_void_p()
-    _check(None, lib().dms_create(dims, ndim, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(stream.cuda_stream),
-                                  ctypes.byref(h)))
+    _check(None, lib().dms_create2(dims, ndim, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(stream.cuda_stream),
+                                   COMPLEXES[complex], ctypes.byref(h)))
     return h
 
 
@@ -248,13 +257,16 @@ def dms_destroy(ctx):
         lib().dms_destroy(ctx)
 
 
-def dms_decode_pairs(shape, words: np.ndarray, v0: int, v1: int) -> np.ndarray:
-    """Decode host gradient words of vertices [v0, v1) into (tail dim, tail id, head id)."""
+def dms_decode_pairs(shape, words: np.ndarray, v0: int, v1: int, complex="freudenthal") -> np.ndarray:
+    """Decode host gradient words of vertices [v0, v1) into (tail dim, tail id, head id).
+    complex "5tet": words = the whole gradient buffer; the vectors whose head cell is
+    anchored in [v0, v1) (dms_decode_pairs2)."""
     dims, ndim = _dims_of(shape)
     words = np.ascontiguousarray(words)
     cap = max(1, (v1 - v0) * 40)
     out = np.empty((cap, 3), dtype=np.int64)
-    n = lib().dms_decode_pairs(dims, ndim, words.ctypes.data, int(v0), int(v1), out.ctypes.data, cap)
+    n = lib().dms_decode_pairs2(dims, ndim, COMPLEXES[complex], words.ctypes.data, int(v0), int(v1),
+                                out.ctypes.data, cap)
     if n < 0:
         raise DMSError(1, "decode")
     return out[:n]
@@ -265,7 +277,7 @@ def dms_decode_pairs(shape, words: np.ndarray, v0: int, v1: int) -> np.ndarray:
 class DMS:
     """One field on one stream.  Results come back as torch tensors / numpy arrays."""
 
-    def __init__(self, f, stream=None):
+    def __init__(self, f, stream=None, complex="freudenthal"):
         import torch
 
         self.torch = torch
@@ -273,7 +285,8 @@ class DMS:
         self.shape = tuple(f.shape)
         self.ndim = f.dim()
         self.N = f.numel()
-        self.ctx = dms_create(f, stream)
+        self.complex = complex
+        self.ctx = dms_create(f, stream, complex)
 
     def close(self):
         dms_destroy(self.ctx)

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "star.cuh"
+#include "tet5.cuh"
 
 namespace dms {
 
@@ -34,6 +35,7 @@ struct Geo3 {
     const unsigned long long* cw;  // 3D, optional: chase word per vertex = tet codes | lower mask << 48
     const uint32_t* cw2;           // 2D, optional: chase word = triangle codes | lower mask << 12
     const uint8_t* vc;             // 2D / 3D, optional: vertex codes (the D0 descent), 1 byte each
+    const T5Tab* t5;               // the five-tetrahedra complex (tet5.cuh), else null
 };
 
 __device__ __forceinline__ int64_t lin_mask(const Geo3& g, int m) {
@@ -844,6 +846,7 @@ struct alignas(16) PairRec {  // 32 B, two 16-byte stores per record
 // highest vertex (in K) of an anchored simplex
 __device__ __forceinline__ int64_t max_vertex(const Geo3& g, const StarTab& S, int dim, int64_t id) {
     if (dim == 0) return id;
+    if (g.t5) return t5_max_vertex(g.f, g.Lx, g.Ly, g.t5, dim, id);
     const int64_t a = id / g.ncell[dim];
     const int k = (int)(id % g.ncell[dim]);
     int64_t best = a;

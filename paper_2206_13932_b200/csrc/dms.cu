@@ -32,6 +32,7 @@
 #include "sort.cuh"
 #include "star.cuh"
 #include "star_build.cuh"
+#include "tet5.cuh"
 
 using namespace dms;
 
@@ -160,6 +161,8 @@ constexpr int kSlabs = DMS_SLABS;  // dms_run_all_host: at most this many upload
 
 struct dms_ctx {
     int ndim = 0;
+    int cplx = DMS_COMPLEX_FREUDENTHAL;  // DMS_COMPLEX_5TET: five tetrahedra per cube (tet5.cuh)
+    T5Tab* dt5 = nullptr;                // its tables (device)
     int64_t L[3] = {1, 1, 1};
     int64_t N = 0;
     const float* f = nullptr;
@@ -374,6 +377,16 @@ Geo3 geo(const dms_ctx* c) {
     g.cw = c->cw;
     g.cw2 = c->cw2;
     g.vc = c->vc;
+    g.t5 = c->cplx == DMS_COMPLEX_5TET ? c->dt5 : nullptr;
+    return g;
+}
+
+T5Geo t5geo(const dms_ctx* c) {
+    T5Geo g;
+    g.Lx = (int32_t)c->L[0];
+    g.Ly = (int32_t)c->L[1];
+    g.Lz = (int32_t)c->L[2];
+    g.N = c->N;
     return g;
 }
 
@@ -633,7 +646,26 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     }
     A.vc = c->vc;
     StageTimer tm(c, 5);
-    if (c->ndim >= 2) {
+    if (c->cplx == DMS_COMPLEX_5TET) {  // the five-tetrahedra complex (tet5.cuh)
+        T5Args B;
+        B.f = c->f;
+        B.Lx = A.Lx;
+        B.Ly = A.Ly;
+        B.Lz = A.Lz;
+        B.N = c->N;
+        B.v0 = v0;
+        B.v1 = v1;
+        B.tab = c->dt5;
+        B.grad = static_cast<uint8_t*>(c->grad);
+        for (int k = 0; k < 4; k++) {
+            B.crit_id[k] = A.crit_id[k];
+            B.crit_key[k] = A.crit_key[k];
+            B.cap[k] = A.cap[k];
+        }
+        B.totals = c->totals;
+        B.err = c->err;
+        k_gradient_t5<<<(unsigned)ceil_div(v1 - v0, kT5Block), kT5Block, 0, c->st>>>(B);
+    } else if (c->ndim >= 2) {
         static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
         // 3D: pools of 8 x 128 vertices per CTA, expanded in work order
         // DMS_GRAD_PAD: unused dynamic shared memory per 3D gradient CTA (bytes), to leave
@@ -804,7 +836,8 @@ dms_status run_critical(dms_ctx* c) {
         // star (x itself), and in 1D so does C_1 (the second lower edge), so their keys
         // sort on the rank bits alone; edge keys have G's low 8 bits zero, triangle keys
         // its low 4 (key_edge / key_tri) -- fewer 8-bit passes
-        const int bit0 = (k == 0 || c->ndim == 1) ? 12 : (k == 1 ? 8 : (k == 2 ? 4 : 0));
+        // (the five-tetrahedra keys use every G bit: tet5.cuh t5_key)
+        const int bit0 = (k == 0 || c->ndim == 1) ? 12 : c->cplx ? 0 : (k == 1 ? 8 : (k == 2 ? 4 : 0));
         c->cur[k] = radix_sort<uint64_t, uint32_t, 8>(c->ckey[0][k], c->cidx[0][k], c->ckey[1][k], c->cidx[1][k],
                                                      c->ncrit[k], bit0, kbits, c->ss, c->st, &c->launches);
         // lexicographically sorted ids = emitted ids gathered through the permutation
@@ -1084,7 +1117,11 @@ dms_status d0_trace(dms_ctx* c) {
     c->launches++;
     if (m) {
         StageTimer t6(c, 6);
-        k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
+        if (c->cplx == DMS_COMPLEX_5TET)
+            k_d0_arcs_t5<<<grid_for(m), kBlock, 0, c->st>>>(t5geo(c), c->dt5, static_cast<const uint8_t*>(c->grad),
+                                                           crit_ids_emitted(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
+        else
+            k_d0_arcs<<<grid_for(m), kBlock, 0, c->st>>>(g, crit_ids_emitted(c, 1), m, c->node_of0, u.arc_a, u.arc_b);
         c->launches++;
     }
     return DMS_OK;
@@ -1195,7 +1232,13 @@ dms_status dtop_trace(dms_ctx* c) {
     // nodes = critical d-simplices in emission order, plus the virtual maximum nd
     k_node_map<<<grid_for(nd), kBlock, 0, c->st>>>(crit_ids_emitted(c, d), nd, c->node_oftop);
     c->launches++;
-    if (m) {
+    if (m && c->cplx == DMS_COMPLEX_5TET) {
+        StageTimer t7(c, 7);
+        k_dtop_arcs_t5<<<grid_for(2 * m), kBlock, 0, c->st>>>(t5geo(c), c->dt5, static_cast<const uint8_t*>(c->grad),
+                                                             crit_ids_emitted(c, d - 1), m, c->node_oftop, (int32_t)nd,
+                                                             u.arc_a, u.arc_b);
+        c->launches++;
+    } else if (m) {
         StageTimer t7(c, 7);
         if (d >= 2) {
             // persistent work-queue chases, 2 jobs per arc (ascending paths of very uneven
@@ -1700,6 +1743,8 @@ dms_status d1_rounds(dms_ctx* c, int phase, int64_t nact) {
 // D1 pairs (phase 1) and, with want_gen, the generators (phase 2)
 dms_status run_d1(dms_ctx* c, bool want_gen) {
     if (c->ndim != 3) return fail(c, DMS_ERR_ARG, "D1 by PairCriticalSimplices is built for 3D fields");
+    if (c->cplx != DMS_COMPLEX_FREUDENTHAL)
+        return fail(c, DMS_ERR_STATE, "D1 on the GPU is built for the Freudenthal complex (the 5-tet one: oracle only)");
     if (!c->have_d[0] || !c->have_d[1]) {
         dms_status s = run_diagrams(c);
         if (s) return s;
@@ -1859,9 +1904,16 @@ static int64_t unpaired_count(dms_ctx* c, int which) {
 extern "C" {
 
 dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* stream, dms_ctx** out) {
+    return dms_create2(dims, ndim, d_f, stream, DMS_COMPLEX_FREUDENTHAL, out);
+}
+
+dms_status dms_create2(const int64_t dims[3], int ndim, const float* d_f, void* stream, dms_complex cplx,
+                       dms_ctx** out) {
     if (!dims || !d_f || !out) return DMS_ERR_ARG;
     *out = nullptr;
+    if (cplx != DMS_COMPLEX_FREUDENTHAL && cplx != DMS_COMPLEX_5TET) return DMS_ERR_ARG;
     if (ndim < 1 || ndim > 3) return DMS_ERR_DEGENERATE;
+    if (cplx == DMS_COMPLEX_5TET && ndim != 3) return DMS_ERR_ARG;
     int64_t N = 1;
     for (int i = 0; i < ndim; i++) {
         if (dims[i] < 2) return DMS_ERR_DEGENERATE;
@@ -1875,14 +1927,28 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
     c->N = N;
     c->f = d_f;
     c->st = (cudaStream_t)stream;
+    c->cplx = cplx;
     const int64_t per[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 3, 2, 0}, {1, 7, 12, 6}};
-    for (int k = 0; k < 4; k++) c->ncell[k] = per[ndim][k];
+    const int64_t per5[4] = {1, 6, 10, 5};  // tet5.cuh
+    for (int k = 0; k < 4; k++) c->ncell[k] = cplx == DMS_COMPLEX_5TET ? per5[k] : per[ndim][k];
     if (c->ncell[ndim] * N >= ((int64_t)1 << 31)) { delete c; return DMS_ERR_TOO_LARGE; }
+    // the five-tetrahedra ids of triangles reach 10 N (the gradient's byte offsets 16 N)
+    if (cplx == DMS_COMPLEX_5TET && 16 * N >= ((int64_t)1 << 35)) { delete c; return DMS_ERR_TOO_LARGE; }
     if (!build_star_tables(ndim, c->L, &c->htab)) { delete c; return DMS_ERR_INVARIANT; }
     auto bail = [&](dms_status s) { dms_destroy(c); return s; };
 #define CA(call) do { if ((call) != cudaSuccess) return bail(DMS_ERR_OOM); } while (0)
     CA(dalloc(&c->dtab, 1));
     if (cudaMemcpy(c->dtab, &c->htab, sizeof(StarTab), cudaMemcpyHostToDevice) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    if (cplx == DMS_COMPLEX_5TET) {
+        T5Tab* ht = new (std::nothrow) T5Tab;
+        if (!ht) return bail(DMS_ERR_OOM);
+        const bool ok = build_t5_tables(ht);
+        cudaError_t e = ok ? cudaMalloc(&c->dt5, sizeof(T5Tab)) : cudaSuccess;
+        if (ok && e == cudaSuccess) e = cudaMemcpy(c->dt5, ht, sizeof(T5Tab), cudaMemcpyHostToDevice);
+        delete ht;
+        if (!ok) return bail(DMS_ERR_INVARIANT);
+        if (e != cudaSuccess) return bail(DMS_ERR_CUDA);
+    }
     {
         ChaseTab ct;
         build_chase_tables(c->htab, &ct);
@@ -1985,10 +2051,11 @@ dms_status dms_create(const int64_t dims[3], int ndim, const float* d_f, void* s
     if (alloc_crit(c) != DMS_OK) return bail(DMS_ERR_OOM);
     {  // 3D: the dual chases read one packed word per vertex (DMS_CHASEWORD=0: the gradient words)
         static const int cw_env = getenv("DMS_CHASEWORD") ? atoi(getenv("DMS_CHASEWORD")) : 1;
-        if (ndim == 3 && cw_env) CA(dalloc(&c->cw, N));
+        const bool kuhn = cplx == DMS_COMPLEX_FREUDENTHAL;  // (the 5-tet path reads its gradient bytes)
+        if (ndim == 3 && cw_env && kuhn) CA(dalloc(&c->cw, N));
         if (ndim == 2 && cw_env) CA(dalloc(&c->cw2, N));
         static const int vc_env = getenv("DMS_VCODES") ? atoi(getenv("DMS_VCODES")) : 1;
-        if (ndim >= 2 && vc_env) CA(dalloc(&c->vc, N));
+        if (ndim >= 2 && vc_env && kuhn) CA(dalloc(&c->vc, N));
     }
     if (ndim == 2) {  // 2D: the ProcessLowerStars table of all 1957 star patterns
         int acc = 0;
@@ -2319,6 +2386,72 @@ int64_t dms_decode_pairs(const int64_t dims[3], int ndim, const void* h_words, i
     return n;
 }
 
+int64_t dms_decode_pairs2(const int64_t dims[3], int ndim, dms_complex cplx, const void* h_words, int64_t v0,
+                          int64_t v1, int64_t* h_triples, int64_t cap) {
+    if (cplx == DMS_COMPLEX_FREUDENTHAL) return dms_decode_pairs(dims, ndim, h_words, v0, v1, h_triples, cap);
+    if (cplx != DMS_COMPLEX_5TET || !dims || !h_words || !h_triples || ndim != 3 || v0 < 0 || v1 < v0) return -1;
+    const int64_t Lx = dims[0], Ly = dims[1], Lz = dims[2], N = Lx * Ly * Lz;
+    if (v1 > N) return -1;
+    T5Tab* T = new (std::nothrow) T5Tab;
+    if (!T || !build_t5_tables(T)) { delete T; return -1; }
+    const uint8_t* w = static_cast<const uint8_t*>(h_words);
+    int64_t n = 0;
+    auto put = [&](int64_t a, int64_t b, int64_t c3) {
+        if (n < cap) { h_triples[3 * n] = a; h_triples[3 * n + 1] = b; h_triples[3 * n + 2] = c3; }
+        n++;
+    };
+    // id of the cell spanned by the lattice points pts (tet5.cuh, reading Z21)
+    auto id_of = [&](const int64_t (*pts)[3], int np) -> int64_t {
+        int64_t a[3] = {pts[0][0], pts[0][1], pts[0][2]};
+        for (int i = 1; i < np; i++)
+            for (int ax = 0; ax < 3; ax++) a[ax] = std::min(a[ax], pts[i][ax]);
+        int m[4];
+        for (int i = 0; i < np; i++) m[i] = (int)((pts[i][0] - a[0]) | ((pts[i][1] - a[1]) << 1) | ((pts[i][2] - a[2]) << 2));
+        std::sort(m, m + np);
+        const int p = (int)((a[0] + a[1] + a[2]) & 1), k = np - 1;
+        for (int i = 0; i < T->cnt[k]; i++) {
+            bool eq = true;
+            for (int j = 0; j < np; j++) eq = eq && T->ids[p][k][i][j] == m[j];
+            if (eq) return (int64_t)T->cnt[k] * (a[0] + Lx * (a[1] + Ly * a[2])) + i;
+        }
+        return -1;
+    };
+    for (int64_t v = v0; v < v1; v++) {
+        const int64_t x = v % Lx, y = (v / Lx) % Ly, z = v / (Lx * Ly);
+        const int p = (int)((x + y + z) & 1);
+        const int vc = w[v];
+        if (vc != 0xff) {
+            const T5Star& S = T->star[p];
+            if (vc >= S.ne) { delete T; return -1; }
+            put(0, v, 6 * (v + S.e_anc[vc][0] + Lx * S.e_anc[vc][1] + Lx * Ly * S.e_anc[vc][2]) + S.e_k[vc]);
+        }
+        for (int k = 2; k <= 3; k++) {
+            const int64_t base = k == 2 ? N + 10 * v : 11 * N + 5 * v;
+            for (int i = 0; i < T->cnt[k]; i++) {
+                int64_t pts[4][3];
+                bool inside = true;
+                for (int j = 0; j <= k; j++) {
+                    const int mm = T->ids[p][k][i][j];
+                    pts[j][0] = x + (mm & 1);
+                    pts[j][1] = y + ((mm >> 1) & 1);
+                    pts[j][2] = z + ((mm >> 2) & 1);
+                    inside = inside && pts[j][0] < Lx && pts[j][1] < Ly && pts[j][2] < Lz;
+                }
+                if (!inside) continue;
+                const int code = w[base + i];
+                if (code > k) continue;  // critical, or the tail of a vector
+                int64_t fp[3][3];
+                int q = 0;
+                for (int j = 0; j <= k; j++)
+                    if (j != code) { fp[q][0] = pts[j][0]; fp[q][1] = pts[j][1]; fp[q][2] = pts[j][2]; q++; }
+                put(k - 1, id_of(fp, k), (int64_t)T->cnt[k] * v + i);
+            }
+        }
+    }
+    delete T;
+    return n;
+}
+
 dms_status dms_copy(dms_ctx* c, void* dst, const void* src, size_t bytes) {
     if (!c || (!dst && bytes) || (!src && bytes)) return DMS_ERR_ARG;
     if (!bytes) return DMS_OK;
@@ -2407,6 +2540,7 @@ void dms_destroy(dms_ctx* c) {
     if (c->lane3.st) cudaStreamSynchronize(c->lane3.st);
     if (c->lane4.st) cudaStreamSynchronize(c->lane4.st);
     clear_events(c);
+    if (c->dt5) cudaFree(c->dt5);
     if (c->st2) cudaStreamDestroy(c->st2);
     for (cudaEvent_t e : {c->ev_grad, c->ev_trace[0], c->ev_trace[1]})
         if (e) cudaEventDestroy(e);

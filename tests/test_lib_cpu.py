@@ -2,6 +2,7 @@
 declares, and its host-side gradient decoder agrees with the oracle's simplex ids."""
 from __future__ import annotations
 
+import itertools
 import os
 import re
 
@@ -133,3 +134,43 @@ def test_too_large_rejected_before_any_device_work(dms, dims, ndim):
     out = ctypes.c_void_p()
     st = L.dms_create(arr, ndim, ctypes.c_void_p(0x1000), None, ctypes.byref(out))
     assert st == 4 and not out.value  # DMS_ERR_TOO_LARGE, no context
+
+
+def _t5_slots(parity):
+    """Neighbour offsets of a five-tetrahedra star, in vertex-id order: every vertex has its
+    6 axis neighbours; an even-sum vertex also the 12 face-diagonal ones (reading Z21)."""
+    offs = [o for o in itertools.product((-1, 0, 1), repeat=3) if sum(map(abs, o)) == 1]
+    if parity == 0:
+        offs += [o for o in itertools.product((-1, 0, 1), repeat=3) if sum(map(abs, o)) == 2]
+    return sorted(offs, key=lambda o: (o[2], o[1], o[0]))
+
+
+@pytest.mark.parametrize("shape", [(3, 4, 5), (5, 4, 3), (4, 4, 4)])
+def test_t5_decode_matches_oracle_ids(dms, shape):
+    """dms_decode_pairs2 on the five-tetrahedra complex (host code, no GPU) against the
+    oracle: gradient bytes built from the oracle's vectors in the layout of dms.h decode
+    back to exactly those vectors -- the library's and the oracle's simplex ids and
+    facet numbering (derived independently) agree."""
+    import oracle
+
+    f = np.random.default_rng(7).random(shape, dtype=np.float32)
+    res = oracle.run(f, complex="5tet")
+    Lz, Ly, Lx = shape
+    N = f.size
+    w = np.full(16 * N, 0xEE, np.uint8)  # cells that are no head: any code > dim
+    w[:N] = 0xFF  # minima
+    for tdim, tid, hid in res.pairs:
+        tv = set(oracle.simplex_vertices(shape, int(tdim), int(tid), "5tet"))
+        hv = sorted(oracle.simplex_vertices(shape, int(tdim) + 1, int(hid), "5tet"))
+        if tdim == 0:
+            v = int(tid)
+            (u,) = set(hv) - {v}
+            c = lambda q: (q % Lx, (q // Lx) % Ly, q // (Lx * Ly))
+            o = tuple(np.subtract(c(u), c(v)))
+            w[v] = _t5_slots(sum(c(v)) % 2).index(o)
+        else:
+            j = hv.index((set(hv) - tv).pop())  # the omitted vertex, in ascending-id order
+            w[(N if tdim == 1 else 11 * N) + hid] = j
+    got = dms.dms_decode_pairs(shape, w, 0, N, complex="5tet")
+    got = got[np.lexsort((got[:, 2], got[:, 1], got[:, 0]))]
+    assert np.array_equal(got, res.pairs)
