@@ -256,7 +256,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-d1", action="store_true", help="skip the D1 / generator timing (3D)")
+    ap.add_argument("--complex", default="freudenthal", choices=["freudenthal", "5tet"],
+                    help="5tet: the paper's five-tetrahedra cut of the 3D configs (SURVEY 8(f) #4; no D1, "
+                         "no cpu_baseline leg)")
     args = ap.parse_args()
+    if args.complex == "5tet":
+        args.no_d1 = True
+        args.no_cpu_baseline = True
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -287,7 +293,9 @@ def main():
     ndim = f_host.ndim
     f_dev = torch.from_numpy(f_host).cuda()
     stream = torch.cuda.current_stream()
-    ctx = dms.DMS(f_dev, stream)
+    if args.complex == "5tet" and ndim != 3:
+        raise SystemExit("--complex 5tet needs a 3D config")
+    ctx = dms.DMS(f_dev, stream, complex=args.complex)
     rank_buf = torch.empty(N, dtype=torch.int32, device="cuda")
     grad_buf = torch.empty(dms.dms_gradient_bytes(ctx.ctx), dtype=torch.uint8, device="cuda")
 
@@ -335,6 +343,8 @@ def main():
     kernel_name = {3: "k_gradient_pool<3,8,1,true> (closed-form lower-star gradient + critical records)",
                    2: "k_gradient_lut2 (2D lower-star gradient by table lookup + critical records)",
                    1: "k_gradient1 (1D lower-star gradient + critical records)"}[ndim]
+    if args.complex == "5tet":
+        kernel_name = "k_gradient_t5 (ProcessLowerStars on the five-tetrahedra stars + critical records)"
     # roofline: the dominant kernel's ALGORITHMIC bytes per launch
     # (N (4 + G_w) + 8 sum|C_k|) over its average launch time (CUDA events on the
     # library's stream, inside the timed region) against the measured HBM peak
@@ -363,6 +373,8 @@ def main():
                 tr = json.load(fh).get(args.config)
         except Exception:
             tr = None
+    if tr and args.complex == "5tet":
+        tr = None  # the ncu traffic figures are the Freudenthal kernel's
     if tr:
         roofline["traffic"] = tr["bytes_per_launch"]
         roofline["traffic_source"] = tr.get("source")
@@ -462,7 +474,7 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 in, integer arithmetic (ordered uint32 keys)", "data": "synthetic",
-            "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "N": N,
+            "config": {"workload": args.config, "desc": CONFIG_DESC[args.config], "N": N, "complex": args.complex,
                        "l2": "input (%d MB) larger than L2; no flush" % (N * 4 >> 20),
                        "parallelism": "replicas" if world > 1 else "single"},
             "stages_ms_per_step": {k: round(v / args.steps, 4) for k, v in stages.items() if k != "gradient_launches"},
