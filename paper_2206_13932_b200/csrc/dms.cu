@@ -183,6 +183,7 @@ struct dms_ctx {
     StarTab htab;
     StarTab* dtab = nullptr;
     ChaseTab* dctab = nullptr;  // dual-chase transitions (device)
+    GradLut* dlut3 = nullptr;   // 3D gradient kernel's union masks (device)
     // caller or scratch buffers
     int32_t* rank = nullptr;
     void* grad = nullptr;
@@ -627,6 +628,7 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
     A.divy.init((uint32_t)c->L[1]);
     A.N = c->N;
     A.tab = c->dtab;
+    A.lut3 = c->dlut3;
     A.grad = c->grad;
     for (int k = 0; k < 4; k++) {
         A.crit_id[k] = c->cid[0][k];
@@ -1955,6 +1957,12 @@ dms_status dms_create2(const int64_t dims[3], int ndim, const float* d_f, void* 
         CA(dalloc(&c->dctab, 1));
         if (cudaMemcpy(c->dctab, &ct, sizeof(ChaseTab), cudaMemcpyHostToDevice) != cudaSuccess) return bail(DMS_ERR_CUDA);
     }
+    if (ndim == 3 && cplx == DMS_COMPLEX_FREUDENTHAL) {
+        GradLut gl;
+        build_grad_lut(c->htab, &gl);
+        CA(dalloc(&c->dlut3, 1));
+        if (cudaMemcpy(c->dlut3, &gl, sizeof(GradLut), cudaMemcpyHostToDevice) != cudaSuccess) return bail(DMS_ERR_CUDA);
+    }
     {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -2563,6 +2571,7 @@ void dms_destroy(dms_ctx* c) {
     for (cudaEvent_t e : c->ev_slab)
         if (e) cudaEventDestroy(e);
     cudaFree(c->dtab);
+    cudaFree(c->dlut3);
     cudaFree(c->dctab);
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);

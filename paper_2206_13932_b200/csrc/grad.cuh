@@ -25,6 +25,8 @@
 //   2D uint16    : vertex code (bits 0-2, 7 = minimum) | tri codes 2 bits x 6 (bits 3-14)
 //   1D uint8     : vertex code (0 = left edge, 1 = right edge, 3 = minimum)
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "star.cuh"
 
@@ -43,6 +45,15 @@ __device__ constexpr int8_t kOff2[6][3] = {{-1, -1, 0}, {0, -1, 0}, {-1, 0, 0}, 
 template <int D>
 __device__ __forceinline__ int off_c(int s, int ax) {
     return D == 3 ? kOff3[s][ax] : kOff2[s][ax];
+}
+
+// link adjacency of two 3D neighbour slots: (x, n_s, n_u) is a star triangle iff the
+// offsets differ by a Kuhn direction (all components in {0,1} or all in {0,-1}, not zero)
+__host__ __device__ constexpr bool link_adj3(int s, int u) {
+    const int dx = kOff3[u][0] - kOff3[s][0], dy = kOff3[u][1] - kOff3[s][1], dz = kOff3[u][2] - kOff3[s][2];
+    const bool pos = dx >= 0 && dy >= 0 && dz >= 0 && dx <= 1 && dy <= 1 && dz <= 1;
+    const bool neg = dx <= 0 && dy <= 0 && dz <= 0 && dx >= -1 && dy >= -1 && dz >= -1;
+    return s != u && (pos || neg);
 }
 
 // n / d for 0 <= n < 2^31 by multiply-high: m = ceil(2^(32+l) / d) (33 bits: lo + hi),
@@ -70,6 +81,7 @@ struct GradArgs {
     int64_t N;
     int64_t v0, v1;  // this launch's vertex range [v0, v1)
     const StarTab* tab;
+    const GradLut* lut3;  // 3D closed form: union masks by 7-bit halves of a slot set
     void* grad;
     int64_t* crit_id[4];
     uint64_t* crit_key[4];
@@ -403,6 +415,58 @@ __device__ __forceinline__ void dec_count(uint32_t& c0, uint32_t& c1, uint32_t M
     c0 ^= M;
     c1 ^= borrow;
 }
+// (2) of the closed form: peel the link triangles against the non-forest edges U = Lt - T.
+// c1 c0: per link triangle, its unclassified edges (3 minus the forest edges it holds).
+// ORD: the full sphere may occur (there the peeling order matters).
+template <bool ORD>
+__device__ __forceinline__ void peel_link(const StarTab& S, uint64_t R, StarState& st, uint64_t T, uint32_t c0,
+                                          uint32_t c1) {
+    uint64_t U = st.Lt & ~T;
+    if (!U) return;  // (then no link triangles either: each has a non-forest edge)
+    const bool ordered = ORD && st.Le == 0x3fffu;  // the full sphere: peeling order matters
+    uint32_t clsq = 0;
+    uint32_t ready = st.Lq & c0 & ~c1;
+    uint64_t crit_t = 0;
+#pragma unroll 1
+    while (true) {
+#pragma unroll 1
+        while (ready) {
+            int q = __ffs(ready) - 1;
+            if (ORD && ordered && (ready & (ready - 1))) {
+                uint32_t best = cmp_tet(S, R, q);
+                for (uint32_t m = ready & (ready - 1); m; m &= m - 1) {
+                    const int q2 = __ffs(m) - 1;
+                    const uint32_t k2 = cmp_tet(S, R, q2);
+                    if (k2 < best) { best = k2; q = q2; }
+                }
+            }
+            const int e = __ffsll((long long)(S.tet_tmask[q] & U)) - 1;
+            const int j = (e == S.tet_tri[q][0]) ? 0 : ((e == S.tet_tri[q][1]) ? 1 : 2);
+            st.qcode |= (uint64_t)(j + 1) << (2 * q);
+            clsq |= 1u << q;
+            U &= ~(1ull << e);
+            dec_count(c0, c1, S.tri_tet_mask[e] & st.Lq & ~clsq);
+            ready = st.Lq & ~clsq & c0 & ~c1;
+        }
+        if (!U) break;
+        // a hole of L: the minimum-key unclassified edge is critical
+        int e = __ffsll((long long)U) - 1;
+        {
+            uint32_t best = key_tri(S, R, e);
+            for (uint64_t m = U & (U - 1); m; m &= m - 1) {
+                const int e2 = __ffsll((long long)m) - 1;
+                const uint32_t k2 = key_tri(S, R, e2);
+                if (k2 < best) { best = k2; e = e2; }
+            }
+        }
+        crit_t |= 1ull << e;
+        U &= ~(1ull << e);
+        dec_count(c0, c1, S.tri_tet_mask[e] & st.Lq & ~clsq);
+        ready = st.Lq & ~clsq & c0 & ~c1;
+    }
+    st.crit_t = crit_t;
+    st.crit_q = st.Lq & ~clsq;
+}
 __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, uint64_t IV, int n, StarState& st,
                                                   uint8_t* par, uint8_t* tp) {
     const int s0 = (int)(IV & 15ull);  // delta = (x, lowest lower neighbour)
@@ -484,52 +548,40 @@ __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, 
         dec_count(c0, c1, S.tri_tet_mask[t] & st.Lq);
     }
     st.crit_e = crit_e;
-    // (2) peel the link triangles against the non-forest edges U
-    uint64_t U = st.Lt & ~T;
-    if (!U) return;  // (then no link triangles either: each has a non-forest edge)
-    const bool ordered = st.Le == 0x3fffu;  // the full sphere: peeling order matters
-    uint32_t clsq = 0;
-    uint32_t ready = st.Lq & c0 & ~c1;
-    uint64_t crit_t = 0;
+    peel_link<true>(S, R, st, T, c0, c1);
+}
+
+// A lower link whose ranks have ONE local minimum on L's graph (and that is not the full
+// sphere): every prefix of the rank order is connected, so Kruskal never merges
+// components -- every link vertex other than s0 hangs below its lowest-ranked
+// neighbour and nothing is critical in (1).  Walking the vertices u in rank order, the
+// still unassigned neighbours of u are exactly its children; their forest edges are the
+// star triangles holding u and a child (union masks by halves of the child set, GradLut).
+__device__ __forceinline__ void process_star_simple(const StarTab& S, const GradLut& G, uint64_t R, uint64_t IV, int n,
+                                                    StarState& st) {
+    const int s0 = (int)(IV & 15ull);
+    st.vcode = s0;
+    uint32_t un = st.Le & ~(1u << s0);
+    uint64_t T = 0, T1 = 0, iv = IV;
 #pragma unroll 1
-    while (true) {
-#pragma unroll 1
-        while (ready) {
-            int q = __ffs(ready) - 1;
-            if (ordered && (ready & (ready - 1))) {
-                uint32_t best = cmp_tet(S, R, q);
-                for (uint32_t m = ready & (ready - 1); m; m &= m - 1) {
-                    const int q2 = __ffs(m) - 1;
-                    const uint32_t k2 = cmp_tet(S, R, q2);
-                    if (k2 < best) { best = k2; q = q2; }
-                }
-            }
-            const int e = __ffsll((long long)(S.tet_tmask[q] & U)) - 1;
-            const int j = (e == S.tet_tri[q][0]) ? 0 : ((e == S.tet_tri[q][1]) ? 1 : 2);
-            st.qcode |= (uint64_t)(j + 1) << (2 * q);
-            clsq |= 1u << q;
-            U &= ~(1ull << e);
-            dec_count(c0, c1, S.tri_tet_mask[e] & st.Lq & ~clsq);
-            ready = st.Lq & ~clsq & c0 & ~c1;
-        }
-        if (!U) break;
-        // a hole of L: the minimum-key unclassified edge is critical
-        int e = __ffsll((long long)U) - 1;
-        {
-            uint32_t best = key_tri(S, R, e);
-            for (uint64_t m = U & (U - 1); m; m &= m - 1) {
-                const int e2 = __ffsll((long long)m) - 1;
-                const uint32_t k2 = key_tri(S, R, e2);
-                if (k2 < best) { best = k2; e = e2; }
-            }
-        }
-        crit_t |= 1ull << e;
-        U &= ~(1ull << e);
-        dec_count(c0, c1, S.tri_tet_mask[e] & st.Lq & ~clsq);
-        ready = st.Lq & ~clsq & c0 & ~c1;
+    for (int k = 0; k < n && un; k++, iv >>= 4) {
+        const int u = (int)(iv & 15ull);
+        const uint32_t kids = S.adj[u] & un;
+        un ^= kids;
+        const uint64_t ua = S.tri_amask[u], ub = S.tri_bmask[u];
+        const uint64_t Tn = (ua | ub) & (G.ort[0][kids & 127u] | G.ort[1][kids >> 7]);
+        T |= Tn;
+        T1 |= Tn & ub;  // the child is the triangle's a end: code 1
     }
-    st.crit_t = crit_t;
-    st.crit_q = st.Lq & ~clsq;
+    uint32_t c0 = st.Lq, c1 = st.Lq;
+#pragma unroll 1
+    for (uint64_t m = T; m; m &= m - 1) {
+        const int t = __ffsll((long long)m) - 1;
+        set_tcode(st, t, ((T1 >> t) & 1ull) ? 1ull : 2ull);
+        dec_count(c0, c1, S.tri_tet_mask[t] & st.Lq);
+    }
+    st.crit_e = 0;
+    peel_link<false>(S, R, st, T, c0, c1);
 }
 
 // warp-level append of `cnt` records per lane: returns this lane's first position
@@ -562,6 +614,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
     __shared__ uint8_t s_tki[FAST ? 1 : kMaxNT * kBlockG];
     __shared__ uint16_t s_qk[(D == 3 && !FAST ? kMaxNQ : 1) * kBlockG];
     __shared__ uint8_t s_par[(FAST ? kMaxNE : 1) * kBlockG], s_tp[(FAST ? kMaxNE : 1) * kBlockG];
+    __shared__ typename std::conditional<FAST, GradLut, int>::type s_G[1];
     __shared__ uint64_t s_R[POOL];
     __shared__ uint32_t s_W[POOL];  // Le | delta << 16 | active << 24 | work << 25
     __shared__ uint16_t s_perm[POOL];
@@ -570,6 +623,11 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
         const int4* src = reinterpret_cast<const int4*>(A.tab);
         int4* dst = reinterpret_cast<int4*>(&S);
         for (int i = threadIdx.x; i < (int)(sizeof(StarTab) / 16); i += kBlockG) dst[i] = src[i];
+        if constexpr (FAST) {
+            const int4* gs = reinterpret_cast<const int4*>(A.lut3);
+            int4* gd = reinterpret_cast<int4*>(&s_G[0]);
+            for (int i = threadIdx.x; i < (int)(sizeof(GradLut) / 16); i += kBlockG) gd[i] = gs[i];
+        }
     }
     if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
     __syncthreads();
@@ -618,28 +676,43 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 // every pair s < u one compare and one add to the later of the two
                 static_assert(NE == 14, "3D star");
                 uint32_t lo = 0, hi = 0;  // (o[s] <= o[u] for s < u: equal values, smaller slot first)
+                // notmin: link vertices with a lower-ranked link neighbour (the same compares)
+                uint32_t notmin = 0;
 #pragma unroll
                 for (int s = 0; s < 8; s++)
 #pragma unroll
-                    for (int u = s + 1; u < 8; u++) lo += (o[s] <= o[u]) ? (1u << (4 * u)) : (1u << (4 * s));
+                    for (int u = s + 1; u < 8; u++) {
+                        const bool p = o[s] <= o[u];
+                        lo += p ? (1u << (4 * u)) : (1u << (4 * s));
+                        if (link_adj3(s, u)) notmin |= p ? (1u << u) : (1u << s);
+                    }
 #pragma unroll
                 for (int s = 8; s < NE; s++)
 #pragma unroll
-                    for (int u = s + 1; u < NE; u++)
-                        hi += (o[s] <= o[u]) ? (1u << (4 * (u - 8))) : (1u << (4 * (s - 8)));
+                    for (int u = s + 1; u < NE; u++) {
+                        const bool p = o[s] <= o[u];
+                        hi += p ? (1u << (4 * (u - 8))) : (1u << (4 * (s - 8)));
+                        if (link_adj3(s, u)) notmin |= p ? (1u << u) : (1u << s);
+                    }
 #pragma unroll
                 for (int s = 0; s < 8; s++)
 #pragma unroll
                     for (int u = 8; u < NE; u++) {
-                        if (o[s] <= o[u]) hi += 1u << (4 * (u - 8));
+                        const bool p = o[s] <= o[u];
+                        if (p) hi += 1u << (4 * (u - 8));
                         else lo += 1u << (4 * s);
+                        if (link_adj3(s, u)) notmin |= p ? (1u << u) : (1u << s);
                     }
                 R = (uint64_t)lo | ((uint64_t)hi << 32);  // (non-lower slots rank above all lower ones)
                 uint64_t z = ~(R | 0xff00000000000000ull);  // the rank-0 (zero) nibble is delta's
                 z &= z >> 1;
                 z &= z >> 2;
                 delta = (__ffsll((long long)(z & 0x1111111111111111ull)) - 1) >> 2;
-                w = __popc(Le);  // the closed form's loops run over the lower link
+                // the closed form's loops run over the lower link; stars whose ranks have several
+                // local minima on L (Kruskal merges components) and the full sphere (ordered
+                // peeling) take the general path: sorted behind the simple ones (bit 4 of w)
+                const bool general = __popc(Le & ~notmin) > 1 || Le == 0x3fffu;
+                w = __popc(Le) + (general ? 16 : 0);
               }
             } else {
               if (Le) {
@@ -726,6 +799,16 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
         uint64_t IV = 0;
         const bool crit_v = active && st.Le == 0;
         if (active && st.Le) {
+            if constexpr (FAST) {
+                for (uint32_t le = st.Le; le; le &= le - 1) {
+                    const int s = __ffs(le) - 1;
+                    IV |= (uint64_t)s << (4 * rk(R, s));
+                }
+                const GradLut& G = s_G[0];
+                const uint32_t nl = ~st.Le & 0x3fffu;  // cells holding no vertex outside Le
+                st.Lt = ((1ull << 36) - 1) & ~(G.ort[0][nl & 127u] | G.ort[1][nl >> 7]);
+                st.Lq = ((1u << 24) - 1) & ~(G.orq[0][nl & 127u] | G.orq[1][nl >> 7]);
+            } else {
             uint64_t ta = 0, tb = 0;
             uint32_t qa = 0, qb = 0, qc = 0;
             for (uint32_t le = st.Le; le; le &= le - 1) {
@@ -741,8 +824,10 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             }
             st.Lt = ta & tb;
             st.Lq = qa & qb & qc;
+            }
             if constexpr (FAST) {
-                process_star_fast(S, R, IV, __popc(st.Le), st, s_par + tid, s_tp + tid);
+                if ((word >> 29) & 1u) process_star_fast(S, R, IV, __popc(st.Le), st, s_par + tid, s_tp + tid);
+                else process_star_simple(S, s_G[0], R, IV, __popc(st.Le), st);
             } else {
             for (uint64_t m = st.Lt; m; m &= m - 1) {
                 const int tt = __ffsll((long long)m) - 1;

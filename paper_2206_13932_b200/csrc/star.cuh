@@ -61,6 +61,16 @@ struct alignas(16) ChaseTab {
     uint32_t t_next[kMaxNT][2];  // 2D: triangles
 };
 
+// 3D gradient kernel: masks that are unions over a set of link vertices, looked up by the
+// two 7-bit halves of the set (slots 0-6, 7-13) and OR-ed: ort / orq = the star triangles
+// / tetrahedra holding any of the vertices; ex = bit i -> bit 4 i (a nibble per slot).
+struct alignas(16) GradLut {
+    uint64_t ort[2][128];
+    uint32_t orq[2][128];
+    uint32_t ex[128];
+};
+inline void build_grad_lut(const StarTab& T, GradLut* G);
+
 // Build the tables for a grid (host).  Returns false if something is inconsistent.
 bool build_star_tables(int ndim, const int64_t L[3], StarTab* T);
 inline void build_chase_tables(const StarTab& T, ChaseTab* C);

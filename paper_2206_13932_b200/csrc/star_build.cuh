@@ -254,6 +254,22 @@ inline bool build_star_tables(int ndim, const int64_t L[3], StarTab* T) {
 
 
 // the dual-chase transition table (see star.cuh ChaseTab)
+inline void build_grad_lut(const StarTab& T, GradLut* G) {
+    std::memset(G, 0, sizeof(GradLut));
+    for (int h = 0; h < 2; h++)
+        for (int m = 0; m < 128; m++)
+            for (int b = 0; b < 7; b++)
+                if ((m >> b) & 1) {
+                    const int s = 7 * h + b;
+                    if (s >= T.ne) continue;
+                    G->ort[h][m] |= T.tri_amask[s] | T.tri_bmask[s];
+                    G->orq[h][m] |= T.tet_amask[s] | T.tet_bmask[s] | T.tet_cmask[s];
+                }
+    for (int m = 0; m < 128; m++)
+        for (int b = 0; b < 7; b++)
+            if ((m >> b) & 1) G->ex[m] |= 1u << (4 * b);
+}
+
 inline void build_chase_tables(const StarTab& T, ChaseTab* C) {
     // one-lookup transitions of the ascending dual chase (diag.cuh chase_step): top cell
     // T paired with its facet #c -> the other cofacet T2 of that facet in this star

@@ -33,6 +33,9 @@ int main(int argc, char** argv) {
     int64_t L[3] = {10, 10, 10};
     static StarTab S;
     if (!build_star_tables(3, L, &S)) { printf("tables\n"); return 1; }
+    static GradLut G;
+    build_grad_lut(S, &G);
+    long nsimple = 0;
     std::mt19937_64 rng(seed);
     static uint8_t tki[kMaxNT * kBlockG];
     static uint16_t qk[kMaxNQ * kBlockG];
@@ -58,6 +61,31 @@ int main(int argc, char** argv) {
         process_star<3, true>(S, C, R, IV, n, delta, a);
         process_star_fast(S, R, IV, n, b, par, tp);
         tot++;
+        // stars with one local minimum of the ranks on L (not the full sphere): the simple path
+        {
+            int nmin = 0;
+            for (int s2 = 0; s2 < 14; s2++) if ((Le >> s2) & 1) {
+                bool ismin = true;
+                for (int u = 0; u < 14; u++) if (((S.adj[s2] & Le) >> u) & 1) if (rk(R, u) < rk(R, s2)) ismin = false;
+                nmin += ismin;
+            }
+            // Lt / Lq through the union masks
+            const uint32_t nl = ~Le & 0x3fffu;
+            const uint64_t Lt2 = ((1ull << 36) - 1) & ~(G.ort[0][nl & 127] | G.ort[1][nl >> 7]);
+            const uint32_t Lq2 = ((1u << 24) - 1) & ~(G.orq[0][nl & 127] | G.orq[1][nl >> 7]);
+            if (Lt2 != a.Lt || Lq2 != a.Lq) { if (bad < 5) printf("lut masks Le=%04x\n", Le); bad++; }
+            if (nmin == 1 && Le != 0x3fffu) {
+                StarState c{};
+                c.Le = Le; c.Lt = a.Lt; c.Lq = a.Lq; c.vcode = -1;
+                process_star_simple(S, G, R, IV, n, c);
+                nsimple++;
+                if (!(a.vcode == c.vcode && a.tcode_lo == c.tcode_lo && a.tcode_hi == c.tcode_hi && a.qcode == c.qcode &&
+                      a.crit_e == c.crit_e && a.crit_t == c.crit_t && a.crit_q == c.crit_q)) {
+                    if (bad < 5) printf("simple mismatch Le=%04x n=%d\n", Le, n);
+                    bad++;
+                }
+            }
+        }
         bool ok = a.vcode == b.vcode && a.tcode_lo == b.tcode_lo && a.tcode_hi == b.tcode_hi && a.qcode == b.qcode &&
                   a.crit_e == b.crit_e && a.crit_t == b.crit_t && a.crit_q == b.crit_q;
         if (!ok) {
@@ -67,6 +95,6 @@ int main(int argc, char** argv) {
             bad++;
         }
     }
-    printf("stars %ld mismatches %ld\n", tot, bad);
+    printf("stars %ld mismatches %ld simple %ld\n", tot, bad, nsimple);
     return bad ? 2 : 0;
 }
