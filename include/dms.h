@@ -136,7 +136,13 @@ size_t dms_gradient_bytes(const dms_ctx* ctx);
  * d_grad: caller-owned device buffer of dms_gradient_bytes(ctx) bytes, one packed
  * word per vertex encoding, for every simplex of the vertex's lower star that is the
  * head of a discrete vector, which facet it is paired with (layout: DESIGN.md
- * "Gradient words").  Independent of dms_order (it compares values and indices
+ * "Gradient words").  3D Freudenthal, 16 bytes (two uint64) per vertex x, in terms of the
+ * star slots of x (neighbours by increasing linear offset): lo bits 4w..4w+3 (w < 14) =
+ * 1 + the slot u of the third vertex of the triangle (x, n_w, n_u) that edge (x, n_w) is
+ * paired with (0: none), lo bits 56-59 = the edge slot x is paired with (15: x is
+ * critical); hi bits 2q..2q+1 (q < 24) = 1 + j if tetrahedron slot q is paired with its
+ * facet j (0: not the head of a vector), hi bits 48-61 = the mask of lower neighbours.
+ * dms_decode_pairs turns the words into (tail, head) simplex ids.  Independent of dms_order (it compares values and indices
  * directly); dms_critical needs both and runs dms_order if it has not run.
  * Each gradient pass consumes the order computed since the previous pass: calling
  * dms_gradient again without a new dms_order (a changed field) makes the next call

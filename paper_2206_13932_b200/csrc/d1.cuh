@@ -174,16 +174,11 @@ __device__ __forceinline__ int d1_pair_lookup(const D1Args& A, const D1Tab& T, i
         const int64_t z = (int64_t)x + T.lin[T.eoth[s][i]];
         r[i] = (uint32_t)__ldg(A.rank + (z < 0 ? 0 : (z > nmax ? nmax : z)));
     }
-    int u = -1;
+    // the edge slot's nibble: 1 + the slot of the paired triangle's third vertex (0: none)
+    const int u = (int)((w.x >> (4 * s)) & 15ull) - 1;
 #pragma unroll
-    for (int i = 5; i >= 0; i--) {  // at most one triangle matches
-        const int t = T.etri[s][i];
-        const uint32_t code = (uint32_t)((t < 32 ? (w.x >> (2 * t)) : (w.y >> (2 * (t - 32)))) & 3ull);
-        if (t != 255 && code == T.ecode[s][i]) {
-            rz = r[i];
-            u = T.eoth[s][i];
-        }
-    }
+    for (int i = 0; i < 6; i++)
+        if (T.eoth[s][i] == u) rz = r[i];
     return u;
 }
 

@@ -54,7 +54,7 @@ __device__ __forceinline__ int vcode_of(const Geo3& g, int64_t v) {
         return c == (g.ndim == 3 ? 15 : 7) ? -1 : c;
     }
     if (g.ndim == 3) {
-        int c = (int)((__ldg(reinterpret_cast<const uint32_t*>(g.grad) + 4 * v + 3) >> 24) & 15u);
+        int c = (int)((__ldg(reinterpret_cast<const uint32_t*>(g.grad) + 4 * v + 1) >> 24) & 15u);
         return c == 15 ? -1 : c;
     } else if (g.ndim == 2) {
         int c = (int)(__ldg(reinterpret_cast<const uint16_t*>(g.grad) + v) & 7u);
@@ -277,25 +277,24 @@ struct ChaseState {
     uint64_t w;  // x's gradient word (3D: hi half; 2D: the uint16)
 };
 
-// 3D with chase words: w = tet codes (bits 0-47) | lower mask (bits 48-61), so a hop that
-// stays in St^-(x) reads nothing and a climb reads one 8-byte word.  Otherwise w = the
-// gradient word (3D hi half, tet codes at bit 8; 2D the uint16).
+// 3D: w = the hi half of the gradient word, tet codes (bits 0-47) | lower mask (bits
+// 48-61), so a hop that stays in St^-(x) reads nothing and a climb reads one 8-byte word.
+// 2D: the chase word (triangle codes | lower mask << 12) if present, else the uint16.
 template <int D>
 __device__ __forceinline__ uint64_t load_w(const Geo3& g, uint32_t x) {
-    if (D == 3 && g.cw) return __ldg(g.cw + x);
     if (D == 3) return __ldg(reinterpret_cast<const unsigned long long*>(g.grad) + 2 * (uint64_t)x + 1);
     if (g.cw2) return __ldg(g.cw2 + x);
     return __ldg(reinterpret_cast<const uint16_t*>(g.grad) + x);
 }
 template <int D>
 __device__ __forceinline__ int top_code(const Geo3& g, uint64_t w, int T) {
-    if (D == 3) return (int)((w >> ((g.cw ? 0 : 8) + 2 * T)) & 3ull);
+    if (D == 3) return (int)((w >> (2 * T)) & 3ull);
     return (int)((w >> ((g.cw2 ? 0 : 3) + 2 * T)) & 3ull);
 }
 // chase word present: is neighbour slot s in the lower mask of the word's vertex
 template <int D>
 __device__ __forceinline__ bool has_cw(const Geo3& g) {
-    return D == 3 ? g.cw != nullptr : g.cw2 != nullptr;
+    return D == 3 ? true : g.cw2 != nullptr;
 }
 template <int D>
 __device__ __forceinline__ bool cw_lower(uint64_t w, int s) {

@@ -2057,13 +2057,13 @@ dms_status dms_create2(const int64_t dims[3], int ndim, const float* d_f, void* 
     static const int64_t cap_env = getenv("DMS_CRIT_CAP") ? atoll(getenv("DMS_CRIT_CAP")) : -1;
     for (int k = 0; k <= ndim; k++) c->cap[k] = cap_env >= 0 ? cap_env : N / 2 + 1024;
     if (alloc_crit(c) != DMS_OK) return bail(DMS_ERR_OOM);
-    {  // 3D: the dual chases read one packed word per vertex (DMS_CHASEWORD=0: the gradient words)
+    {  // 2D: the dual chases read one packed word per vertex (DMS_CHASEWORD=0: the gradient words)
+        // and the D0 descent a compact vertex-code array (DMS_VCODES=0: the gradient words).
+        // 3D: the 16-byte gradient word holds both (hi half = chase word, vertex code in lo).
         static const int cw_env = getenv("DMS_CHASEWORD") ? atoi(getenv("DMS_CHASEWORD")) : 1;
-        const bool kuhn = cplx == DMS_COMPLEX_FREUDENTHAL;  // (the 5-tet path reads its gradient bytes)
-        if (ndim == 3 && cw_env && kuhn) CA(dalloc(&c->cw, N));
         if (ndim == 2 && cw_env) CA(dalloc(&c->cw2, N));
         static const int vc_env = getenv("DMS_VCODES") ? atoi(getenv("DMS_VCODES")) : 1;
-        if (ndim >= 2 && vc_env && kuhn) CA(dalloc(&c->vc, N));
+        if (ndim == 2 && vc_env) CA(dalloc(&c->vc, N));
     }
     if (ndim == 2) {  // 2D: the ProcessLowerStars table of all 1957 star patterns
         int acc = 0;
@@ -2369,7 +2369,7 @@ int64_t dms_decode_pairs(const int64_t dims[3], int ndim, const void* h_words, i
         if (ndim == 3) {
             lo = reinterpret_cast<const uint64_t*>(h_words)[2 * i];
             hi = reinterpret_cast<const uint64_t*>(h_words)[2 * i + 1];
-            vcode = (int)((hi >> 56) & 15);
+            vcode = (int)((lo >> 56) & 15);
             if (vcode == 15) vcode = -1;
         } else {
             const uint16_t w = reinterpret_cast<const uint16_t*>(h_words)[i];
@@ -2378,17 +2378,26 @@ int64_t dms_decode_pairs(const int64_t dims[3], int ndim, const void* h_words, i
             lo = (uint64_t)(w >> 3);
         }
         if (vcode >= 0) put(0, v, nc[1] * anc(v, T.e_anc[vcode]) + T.e_k[vcode]);
+        if (ndim == 3) {  // lo: a nibble per edge slot (1 + third vertex of the paired triangle); hi: tet codes
+            for (int e = 0; e < T.ne; e++) {
+                const int u = (int)((lo >> (4 * e)) & 15) - 1;
+                if (u < 0) continue;
+                const int t = T.tri_of[e][u];
+                put(1, nc[1] * anc(v, T.e_anc[e]) + T.e_k[e], nc[2] * anc(v, T.t_anc[t]) + T.t_k[t]);
+            }
+            for (int q = 0; q < T.nq; q++) {
+                const int code = (int)((hi >> (2 * q)) & 3);
+                if (!code) continue;
+                const int t = T.tet_tri[q][code - 1];
+                put(2, nc[2] * anc(v, T.t_anc[t]) + T.t_k[t], nc[3] * anc(v, T.q_anc[q]) + T.q_k[q]);
+            }
+            continue;
+        }
         for (int t = 0; t < T.nt; t++) {
-            const int code = (int)((t < 32 ? (lo >> (2 * t)) : (hi >> (2 * (t - 32)))) & 3);
+            const int code = (int)((lo >> (2 * t)) & 3);
             if (!code) continue;
             const int e = code == 1 ? T.tri_a[t] : T.tri_b[t];
             put(1, nc[1] * anc(v, T.e_anc[e]) + T.e_k[e], nc[2] * anc(v, T.t_anc[t]) + T.t_k[t]);
-        }
-        for (int q = 0; q < T.nq; q++) {
-            const int code = (int)((hi >> (8 + 2 * q)) & 3);
-            if (!code) continue;
-            const int t = T.tet_tri[q][code - 1];
-            put(2, nc[2] * anc(v, T.t_anc[t]) + T.t_k[t], nc[3] * anc(v, T.q_anc[q]) + T.q_k[q]);
         }
     }
     return n;

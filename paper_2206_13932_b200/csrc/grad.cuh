@@ -97,6 +97,7 @@ struct GradArgs {
 };
 
 __device__ __forceinline__ int rk(uint64_t R, int s) { return (int)((R >> (4 * s)) & 15ull); }
+__device__ __forceinline__ int nib4(uint64_t P, int i) { return (int)((P >> (4 * i)) & 15ull); }
 
 __device__ __forceinline__ uint32_t key_edge(uint64_t R, int s) { return (uint32_t)(rk(R, s) + 1) << 8; }
 
@@ -227,7 +228,9 @@ struct StarState {
     uint64_t cls_t, crit_t;            // triangle slot masks
     KMask pq0_t, pq1_t;                // triangle queues, key-index space
     uint32_t cls_q, crit_q, pq0_q, pq1_q;  // tetrahedron slot masks
-    uint64_t tcode_lo, tcode_hi;       // 2 bits per tri slot
+    uint64_t tcode_lo, tcode_hi;       // 2 bits per tri slot (queue-driven expansion)
+    uint64_t ecode;                    // closed form: nibble per edge slot w, 1 + slot of the third vertex of
+                                       // the triangle paired with (x, n_w) (0: none)
     uint64_t qcode;                    // 2 bits per tet slot
     int vcode;                         // edge slot paired with x, -1 = minimum
     uint64_t U2t;                      // triangles with both edges unclassified
@@ -385,7 +388,6 @@ __device__ __forceinline__ void process_star(const StarTab& S, const KeyCache& C
 // re-rooted there), so (1) needs no traversal.  The result equals process_star() on
 // every star (tests/test_star_closed_form.py on random stars; tests/test_gpu_*: every
 // gradient vector against the oracle).
-__device__ __forceinline__ int nib4(uint64_t P, int i) { return (int)((P >> (4 * i)) & 15ull); }
 // per-thread byte arrays in shared memory, laid out [slot][thread] (conflict free): the
 // union-find parents (par) and the oriented forest (tp: parent towards the component's
 // lowest vertex; a root points to itself)
@@ -417,29 +419,36 @@ __device__ __forceinline__ void dec_count(uint32_t& c0, uint32_t& c1, uint32_t M
 }
 // (2) of the closed form: peel the link triangles against the non-forest edges U = Lt - T.
 // c1 c0: per link triangle, its unclassified edges (3 minus the forest edges it holds).
-// ORD: the full sphere may occur (there the peeling order matters).
-template <bool ORD>
-__device__ __forceinline__ void peel_link(const StarTab& S, uint64_t R, StarState& st, uint64_t T, uint32_t c0,
-                                          uint32_t c1) {
+// SPH: the full sphere may occur.  There U is a spanning tree of the dual graph and the
+// minimum-key-first peeling always has a second leaf with a smaller key than the
+// maximum-key link triangle, so that triangle is the one left over (critical) and every
+// other one pairs with its dual-tree edge towards it -- whatever the order: it is
+// withheld from the ready set and the rest is peeled in slot order.
+template <bool SPH>
+__device__ __forceinline__ void peel_link(const StarTab& S, uint64_t R, uint64_t IV, StarState& st, uint64_t T,
+                                          uint32_t c0, uint32_t c1) {
     uint64_t U = st.Lt & ~T;
     if (!U) return;  // (then no link triangles either: each has a non-forest edge)
-    const bool ordered = ORD && st.Le == 0x3fffu;  // the full sphere: peeling order matters
-    uint32_t clsq = 0;
-    uint32_t ready = st.Lq & c0 & ~c1;
+    uint32_t clsq = 0;  // classified (or withheld) link triangles
+    if (SPH && st.Le == 0x3fffu) {
+        const int top = nib4(IV, 13);  // its link triangles hold the maximum key
+        int qmax = -1;
+        uint32_t best = 0;
+        for (uint32_t m = S.tet_amask[top] | S.tet_bmask[top] | S.tet_cmask[top]; m; m &= m - 1) {
+            const int q = __ffs(m) - 1;
+            const uint32_t k = cmp_tet(S, R, q);
+            if (k > best) { best = k; qmax = q; }
+        }
+        clsq = 1u << qmax;
+    }
+    const uint32_t held = clsq;
+    uint32_t ready = st.Lq & ~clsq & c0 & ~c1;
     uint64_t crit_t = 0;
 #pragma unroll 1
     while (true) {
 #pragma unroll 1
         while (ready) {
-            int q = __ffs(ready) - 1;
-            if (ORD && ordered && (ready & (ready - 1))) {
-                uint32_t best = cmp_tet(S, R, q);
-                for (uint32_t m = ready & (ready - 1); m; m &= m - 1) {
-                    const int q2 = __ffs(m) - 1;
-                    const uint32_t k2 = cmp_tet(S, R, q2);
-                    if (k2 < best) { best = k2; q = q2; }
-                }
-            }
+            const int q = __ffs(ready) - 1;
             const int e = __ffsll((long long)(S.tet_tmask[q] & U)) - 1;
             const int j = (e == S.tet_tri[q][0]) ? 0 : ((e == S.tet_tri[q][1]) ? 1 : 2);
             st.qcode |= (uint64_t)(j + 1) << (2 * q);
@@ -465,7 +474,7 @@ __device__ __forceinline__ void peel_link(const StarTab& S, uint64_t R, StarStat
         ready = st.Lq & ~clsq & c0 & ~c1;
     }
     st.crit_t = crit_t;
-    st.crit_q = st.Lq & ~clsq;
+    st.crit_q = st.Lq & ~(clsq & ~held);
 }
 __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, uint64_t IV, int n, StarState& st,
                                                   uint8_t* par, uint8_t* tp) {
@@ -544,11 +553,11 @@ __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, 
         }
         const int t = S.tri_of[w][p];
         T |= 1ull << t;
-        set_tcode(st, t, S.tri_a[t] == w ? 1ull : 2ull);
+        st.ecode |= (uint64_t)(p + 1) << (4 * w);
         dec_count(c0, c1, S.tri_tet_mask[t] & st.Lq);
     }
     st.crit_e = crit_e;
-    peel_link<true>(S, R, st, T, c0, c1);
+    peel_link<true>(S, R, IV, st, T, c0, c1);
 }
 
 // A lower link whose ranks have ONE local minimum on L's graph (and that is not the full
@@ -562,26 +571,83 @@ __device__ __forceinline__ void process_star_simple(const StarTab& S, const Grad
     const int s0 = (int)(IV & 15ull);
     st.vcode = s0;
     uint32_t un = st.Le & ~(1u << s0);
-    uint64_t T = 0, T1 = 0, iv = IV;
+    uint64_t T = 0, E = 0, iv = IV;
 #pragma unroll 1
     for (int k = 0; k < n && un; k++, iv >>= 4) {
         const int u = (int)(iv & 15ull);
         const uint32_t kids = S.adj[u] & un;
         un ^= kids;
-        const uint64_t ua = S.tri_amask[u], ub = S.tri_bmask[u];
-        const uint64_t Tn = (ua | ub) & (G.ort[0][kids & 127u] | G.ort[1][kids >> 7]);
-        T |= Tn;
-        T1 |= Tn & ub;  // the child is the triangle's a end: code 1
+        const uint32_t kl = kids & 127u, kh = kids >> 7;
+        E |= (uint64_t)(G.ex[kl] * (uint32_t)(u + 1)) | ((uint64_t)(G.ex[kh] * (uint32_t)(u + 1)) << 28);
+        T |= (S.tri_amask[u] | S.tri_bmask[u]) & (G.ort[0][kl] | G.ort[1][kh]);
     }
+    st.ecode = E;
     uint32_t c0 = st.Lq, c1 = st.Lq;
 #pragma unroll 1
-    for (uint64_t m = T; m; m &= m - 1) {
-        const int t = __ffsll((long long)m) - 1;
-        set_tcode(st, t, ((T1 >> t) & 1ull) ? 1ull : 2ull);
-        dec_count(c0, c1, S.tri_tet_mask[t] & st.Lq);
-    }
+    for (uint64_t m = T; m; m &= m - 1) dec_count(c0, c1, S.tri_tet_mask[__ffsll((long long)m) - 1] & st.Lq);
     st.crit_e = 0;
-    peel_link<false>(S, R, st, T, c0, c1);
+    peel_link<false>(S, R, IV, st, T, c0, c1);
+}
+
+// Two local minima s0 < m of the ranks on L's graph: the walk of process_star_simple
+// builds the two descending trees (basins) rooted at s0 and m; Kruskal joins them at the
+// first vertex u (in rank order) with a lower-ranked neighbour in the other basin, through
+// the lowest-ranked such neighbour b: the path from the edge's end y in m's basin back to m
+// is reversed and y hung below the other end (m's basin is the younger component).  If no
+// such edge exists m's basin is a component of its own and (x, m) is a critical edge.
+__device__ __forceinline__ void process_star_two(const StarTab& S, const GradLut& G, uint64_t R, uint64_t IV, int n,
+                                                 StarState& st) {
+    const int s0 = (int)(IV & 15ull);
+    st.vcode = s0;
+    uint32_t un = st.Le & ~(1u << s0), done = 0, MB = 0;
+    uint64_t T = 0, iv = IV, E = 0;  // E: 1 + parent slot per slot (nibbles)
+    int m = -1;
+    bool merged = false;
+#pragma unroll 1
+    for (int k = 0; k < n && (un || !merged); k++, iv >>= 4) {
+        const int u = (int)(iv & 15ull);
+        const uint32_t bu = 1u << u;
+        if (un & bu) {  // not claimed by a lower-ranked neighbour: the second minimum
+            m = u;
+            MB = bu;
+            un ^= bu;
+        }
+        const bool inB = (MB & bu) != 0;
+        if (!merged && m >= 0) {
+            const uint32_t cross = S.adj[u] & done & (inB ? ~MB : MB);
+            if (cross) {
+                int b = __ffs(cross) - 1, rb = rk(R, b);
+                for (uint32_t c = cross & (cross - 1); c; c &= c - 1) {
+                    const int b2 = __ffs(c) - 1, r2 = rk(R, b2);
+                    if (r2 < rb) { rb = r2; b = b2; }
+                }
+                const int y = inB ? u : b, z = inB ? b : u;  // y in m's basin
+                T |= 1ull << S.tri_of[y][z];
+                int cur = y, prev = z;
+                while (true) {  // reverse y -> m and hang y below z
+                    const int nxt = nib4(E, cur) - 1;
+                    E = (E & ~(15ull << (4 * cur))) | ((uint64_t)(prev + 1) << (4 * cur));
+                    if (cur == m) break;
+                    prev = cur;
+                    cur = nxt;
+                }
+                merged = true;
+            }
+        }
+        done |= bu;
+        const uint32_t kids = S.adj[u] & un;
+        un ^= kids;
+        if (inB) MB |= kids;
+        const uint32_t kl = kids & 127u, kh = kids >> 7;
+        E |= (uint64_t)(G.ex[kl] * (uint32_t)(u + 1)) | ((uint64_t)(G.ex[kh] * (uint32_t)(u + 1)) << 28);
+        T |= (S.tri_amask[u] | S.tri_bmask[u]) & (G.ort[0][kl] | G.ort[1][kh]);
+    }
+    st.ecode = E;
+    uint32_t c0 = st.Lq, c1 = st.Lq;
+#pragma unroll 1
+    for (uint64_t mm = T; mm; mm &= mm - 1) dec_count(c0, c1, S.tri_tet_mask[__ffsll((long long)mm) - 1] & st.Lq);
+    st.crit_e = (m >= 0 && !merged) ? 1u << m : 0u;
+    peel_link<false>(S, R, IV, st, T, c0, c1);
 }
 
 // warp-level append of `cnt` records per lane: returns this lane's first position
@@ -709,10 +775,11 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 z &= z >> 2;
                 delta = (__ffsll((long long)(z & 0x1111111111111111ull)) - 1) >> 2;
                 // the closed form's loops run over the lower link; stars whose ranks have several
-                // local minima on L (Kruskal merges components) and the full sphere (ordered
-                // peeling) take the general path: sorted behind the simple ones (bit 4 of w)
-                const bool general = __popc(Le & ~notmin) > 1 || Le == 0x3fffu;
-                w = __popc(Le) + (general ? 16 : 0);
+                // local minima on L (Kruskal merges components) take the two-basin path (two
+                // minima) or the general one (more, or the full sphere): classes sorted apart
+                const int nmin = __popc(Le & ~notmin);
+                const int cls = (nmin > 2 || Le == 0x3fffu) ? 2 : nmin - 1;  // 0 simple, 1 two basins, 2 general
+                w = __popc(Le) + 16 * cls;
               }
             } else {
               if (Le) {
@@ -793,6 +860,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
         st.pq0_t.lo = st.pq0_t.hi = st.pq1_t.lo = st.pq1_t.hi = 0;
         st.cls_q = st.crit_q = st.pq0_q = st.pq1_q = 0;
         st.tcode_lo = st.tcode_hi = st.qcode = 0;
+        st.ecode = 0;
         st.vcode = -1;
         st.Lt = 0;
         st.Lq = 0;
@@ -826,8 +894,10 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             st.Lq = qa & qb & qc;
             }
             if constexpr (FAST) {
-                if ((word >> 29) & 1u) process_star_fast(S, R, IV, __popc(st.Le), st, s_par + tid, s_tp + tid);
-                else process_star_simple(S, s_G[0], R, IV, __popc(st.Le), st);
+                const uint32_t cls = (word >> 29) & 3u;
+                if (cls == 0) process_star_simple(S, s_G[0], R, IV, __popc(st.Le), st);
+                else if (cls == 1) process_star_two(S, s_G[0], R, IV, __popc(st.Le), st);
+                else process_star_fast(S, R, IV, __popc(st.Le), st, s_par + tid, s_tp + tid);
             } else {
             for (uint64_t m = st.Lt; m; m &= m - 1) {
                 const int tt = __ffsll((long long)m) - 1;
@@ -849,11 +919,18 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
         }
         if (active) {
             if (D == 3) {
+                // the 3D gradient word (dms.h): lo = a nibble per edge slot w (1 + the slot of the
+                // third vertex of the triangle paired with (x, n_w)) | vertex code << 56;
+                // hi = tetrahedron codes | lower mask << 48 (all a dual chase needs)
                 const uint64_t vc = crit_v ? 15ull : (uint64_t)st.vcode;
-                const uint64_t hi = st.tcode_hi | (st.qcode << 8) | (vc << 56);
-                reinterpret_cast<ulonglong2*>(A.grad)[v] = make_ulonglong2(st.tcode_lo, hi);
-                if (A.cw) A.cw[v] = st.qcode | ((uint64_t)st.Le << 48);
-                if (A.vc) A.vc[v] = (uint8_t)vc;
+                if constexpr (!FAST) {  // the queue-driven expansion keeps 2-bit triangle codes
+                    for (int t = 0; t < Geo<3>::NT; t++) {
+                        const int code = (int)((t < 32 ? (st.tcode_lo >> (2 * t)) : (st.tcode_hi >> (2 * (t - 32)))) & 3ull);
+                        if (code) st.ecode |= (uint64_t)((code == 1 ? S.tri_b[t] : S.tri_a[t]) + 1) << (4 * (code == 1 ? S.tri_a[t] : S.tri_b[t]));
+                    }
+                }
+                reinterpret_cast<ulonglong2*>(A.grad)[v] =
+                    make_ulonglong2(st.ecode | (vc << 56), st.qcode | ((uint64_t)st.Le << 48));
             } else {
                 const uint32_t vc = crit_v ? 7u : (uint32_t)st.vcode;
                 reinterpret_cast<uint16_t*>(A.grad)[v] = (uint16_t)(vc | ((uint32_t)st.tcode_lo << 3));

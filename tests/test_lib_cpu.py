@@ -62,8 +62,8 @@ def test_decode_vertex_codes_match_oracle_ids(dms, shape):
     for s in range(nslots):
         if d == 3:
             w = np.zeros(2, dtype=np.uint64)
-            w[1] = np.uint64(s) << np.uint64(56)
-            w[0] = 0
+            w[0] = np.uint64(s) << np.uint64(56)  # dms.h: vertex code in lo bits 56-59
+            w[1] = 0
         elif d == 2:
             w = np.array([s], dtype=np.uint16)
         else:
@@ -91,22 +91,38 @@ def test_decode_all_codes_are_facet_pairs(dms):
     contain the star centre."""
     shape = (5, 5, 5)
     v = 62  # interior
-    for t in range(36):
-        for code in (1, 2):
+    # slot -> neighbour vertex, through the vertex codes (dms.h: lo bits 56-59)
+    nb = []
+    for s in range(14):
+        w = np.zeros(2, dtype=np.uint64)
+        w[0] = np.uint64(s) << np.uint64(56)
+        tr = dms.dms_decode_pairs(shape, w.view(np.uint8), v, v + 1)
+        (u,) = _vertices(shape, 1, int(tr[0, 2])) - {v}
+        nb.append(u)
+
+    def coords(u):
+        return np.array([u % 5, (u // 5) % 5, u // 25])
+
+    npairs = 0
+    for e in range(14):
+        for u in range(14):
+            d = coords(nb[u]) - coords(nb[e])
+            if e == u or not (set(d.tolist()) <= {0, 1} or set(d.tolist()) <= {0, -1}):
+                continue  # (x, n_e, n_u) is not a triangle of the Freudenthal star
+            # edge slot e paired with the triangle whose third vertex is slot u: nibble u + 1
             w = np.zeros(2, dtype=np.uint64)
-            if t < 32:
-                w[0] = np.uint64(code) << np.uint64(2 * t)
-            else:
-                w[1] = np.uint64(code) << np.uint64(2 * (t - 32))
-            w[1] |= np.uint64(15) << np.uint64(56)
+            w[0] = (np.uint64(u + 1) << np.uint64(4 * e)) | (np.uint64(15) << np.uint64(56))
             tr = dms.dms_decode_pairs(shape, w.view(np.uint8), v, v + 1)
             assert tr.shape == (1, 3) and tr[0, 0] == 1
             a, b = _vertices(shape, 1, int(tr[0, 1])), _vertices(shape, 2, int(tr[0, 2]))
-            assert a < b and v in a
+            assert a == {v, nb[e]} and b == {v, nb[e], nb[u]}
+            npairs += 1
+    assert npairs == 72  # 36 star triangles, each from either of its two edges at x
     for q in range(24):
         for code in (1, 2, 3):
             w = np.zeros(2, dtype=np.uint64)
-            w[1] = (np.uint64(code) << np.uint64(8 + 2 * q)) | (np.uint64(15) << np.uint64(56))
+            w[0] = np.uint64(15) << np.uint64(56)
+            w[1] = np.uint64(code) << np.uint64(2 * q)
             tr = dms.dms_decode_pairs(shape, w.view(np.uint8), v, v + 1)
             assert tr.shape == (1, 3) and tr[0, 0] == 2
             a, b = _vertices(shape, 2, int(tr[0, 1])), _vertices(shape, 3, int(tr[0, 2]))

@@ -27,6 +27,16 @@ constexpr int kBlock = 256;
 #include BODY_INC  // the device helpers of grad.cuh, extracted by the test
 }
 using namespace dms;
+// the queue-driven expansion's 2-bit triangle codes as the closed form's edge nibbles
+static uint64_t ecode_of(const StarTab& S, const StarState& a) {
+    uint64_t e = 0;
+    for (int t = 0; t < 36; t++) {
+        const int code = (int)((t < 32 ? (a.tcode_lo >> (2 * t)) : (a.tcode_hi >> (2 * (t - 32)))) & 3ull);
+        if (code == 1) e |= (uint64_t)(S.tri_b[t] + 1) << (4 * S.tri_a[t]);
+        if (code == 2) e |= (uint64_t)(S.tri_a[t] + 1) << (4 * S.tri_b[t]);
+    }
+    return e;
+}
 int main(int argc, char** argv) {
     const long iters = argc > 1 ? atol(argv[1]) : 2000000;
     const unsigned long long seed = argc > 2 ? strtoull(argv[2], 0, 10) : 1;
@@ -35,7 +45,7 @@ int main(int argc, char** argv) {
     if (!build_star_tables(3, L, &S)) { printf("tables\n"); return 1; }
     static GradLut G;
     build_grad_lut(S, &G);
-    long nsimple = 0;
+    long nsimple = 0, ntwo = 0;
     std::mt19937_64 rng(seed);
     static uint8_t tki[kMaxNT * kBlockG];
     static uint16_t qk[kMaxNQ * kBlockG];
@@ -74,27 +84,28 @@ int main(int argc, char** argv) {
             const uint64_t Lt2 = ((1ull << 36) - 1) & ~(G.ort[0][nl & 127] | G.ort[1][nl >> 7]);
             const uint32_t Lq2 = ((1u << 24) - 1) & ~(G.orq[0][nl & 127] | G.orq[1][nl >> 7]);
             if (Lt2 != a.Lt || Lq2 != a.Lq) { if (bad < 5) printf("lut masks Le=%04x\n", Le); bad++; }
-            if (nmin == 1 && Le != 0x3fffu) {
+            if (nmin <= 2 && Le != 0x3fffu) {
                 StarState c{};
                 c.Le = Le; c.Lt = a.Lt; c.Lq = a.Lq; c.vcode = -1;
-                process_star_simple(S, G, R, IV, n, c);
-                nsimple++;
-                if (!(a.vcode == c.vcode && a.tcode_lo == c.tcode_lo && a.tcode_hi == c.tcode_hi && a.qcode == c.qcode &&
+                if (nmin == 1) process_star_simple(S, G, R, IV, n, c);
+                else process_star_two(S, G, R, IV, n, c);
+                if (nmin == 1) nsimple++; else ntwo++;
+                if (!(a.vcode == c.vcode && ecode_of(S, a) == c.ecode && a.qcode == c.qcode &&
                       a.crit_e == c.crit_e && a.crit_t == c.crit_t && a.crit_q == c.crit_q)) {
                     if (bad < 5) printf("simple mismatch Le=%04x n=%d\n", Le, n);
                     bad++;
                 }
             }
         }
-        bool ok = a.vcode == b.vcode && a.tcode_lo == b.tcode_lo && a.tcode_hi == b.tcode_hi && a.qcode == b.qcode &&
+        bool ok = a.vcode == b.vcode && ecode_of(S, a) == b.ecode && a.qcode == b.qcode &&
                   a.crit_e == b.crit_e && a.crit_t == b.crit_t && a.crit_q == b.crit_q;
         if (!ok) {
             if (bad < 5) printf("mismatch Le=%04x n=%d: crit_e %x/%x crit_t %llx/%llx crit_q %x/%x tc %llx/%llx q %llx/%llx\n", Le, n, a.crit_e, b.crit_e,
-                (unsigned long long)a.crit_t, (unsigned long long)b.crit_t, a.crit_q, b.crit_q, (unsigned long long)a.tcode_lo, (unsigned long long)b.tcode_lo,
+                (unsigned long long)a.crit_t, (unsigned long long)b.crit_t, a.crit_q, b.crit_q, (unsigned long long)ecode_of(S, a), (unsigned long long)b.ecode,
                 (unsigned long long)a.qcode, (unsigned long long)b.qcode);
             bad++;
         }
     }
-    printf("stars %ld mismatches %ld simple %ld\n", tot, bad, nsimple);
+    printf("stars %ld mismatches %ld simple %ld two %ld\n", tot, bad, nsimple, ntwo);
     return bad ? 2 : 0;
 }
