@@ -666,6 +666,31 @@ __device__ __forceinline__ int64_t warp_append(unsigned long long* total, uint32
     return (int64_t)base + (inc - cnt);
 }
 
+// the same for four record lists at once (counts per lane < 2^16 in total per warp): one
+// packed scan, one atomic per non-empty list (lanes 0-3), q[k] = this lane's first position
+__device__ __forceinline__ void warp_append4(unsigned long long* totals, uint32_t c0, uint32_t c1, uint32_t c2,
+                                             uint32_t c3, int64_t q[4]) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long own = (unsigned long long)c0 | ((unsigned long long)c1 << 16) |
+                                   ((unsigned long long)c2 << 32) | ((unsigned long long)c3 << 48);
+    unsigned long long inc = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const unsigned long long tot = __shfl_sync(0xffffffffu, inc, 31);
+    unsigned long long base = 0;
+    if (lane < 4) {
+        const unsigned long long t = (tot >> (16 * lane)) & 0xffffull;
+        if (t) base = atomicAdd(totals + lane, t);
+    }
+    const unsigned long long ex = inc - own;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+        q[k] = (int64_t)(__shfl_sync(0xffffffffu, base, k) + ((ex >> (16 * k)) & 0xffffull));
+}
+
 // ---- pooled variant: a CTA of 128 threads takes P x 128 consecutive vertices; phase A
 // ranks the neighbours of all of them (compact state: local ranks + lower mask), the
 // pool is counting-sorted by the work estimate |Le| + |Lt| + |Lq|, and phase C expands the
@@ -732,6 +757,9 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 if (in) {
                     const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
                     const bool lower = (os < ox) || (os == ox && s < NE / 2);
+                    // (closed form: true values -- every lower slot precedes every other one in
+                    // the order K anyway, so the ranks of the lower slots are 0 .. n-1 either way)
+                    if (FAST) o[s] = os;
                     if (lower) { o[s] = os; Le |= 1u << s; }
                 }
             }
@@ -741,7 +769,11 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 // local ranks as packed nibble counters (slots 0-7 in lo, 8-13 in hi): for
                 // every pair s < u one compare and one add to the later of the two
                 static_assert(NE == 14, "3D star");
-                uint32_t lo = 0, hi = 0;  // (o[s] <= o[u] for s < u: equal values, smaller slot first)
+                // (o[s] <= o[u] for s < u: equal values, the smaller slot first.)  Each pair adds one
+                // to the later slot's nibble: the counters start from "s first" for every pair
+                // within a word and take a predicated correction otherwise
+                constexpr uint32_t kLo0 = 0x76543210u, kHi0 = 0x00543210u;  // sum over s < u of 1 << 4u (per word)
+                uint32_t lo = kLo0, hi = kHi0;
                 // notmin: link vertices with a lower-ranked link neighbour (the same compares)
                 uint32_t notmin = 0;
 #pragma unroll
@@ -749,7 +781,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
 #pragma unroll
                     for (int u = s + 1; u < 8; u++) {
                         const bool p = o[s] <= o[u];
-                        lo += p ? (1u << (4 * u)) : (1u << (4 * s));
+                        if (!p) lo += (1u << (4 * s)) - (1u << (4 * u));
                         if (link_adj3(s, u)) notmin |= p ? (1u << u) : (1u << s);
                     }
 #pragma unroll
@@ -757,7 +789,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
 #pragma unroll
                     for (int u = s + 1; u < NE; u++) {
                         const bool p = o[s] <= o[u];
-                        hi += p ? (1u << (4 * (u - 8))) : (1u << (4 * (s - 8)));
+                        if (!p) hi += (1u << (4 * (s - 8))) - (1u << (4 * (u - 8)));
                         if (link_adj3(s, u)) notmin |= p ? (1u << u) : (1u << s);
                     }
 #pragma unroll
@@ -848,7 +880,8 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
     // ---- phase C: P rounds of 128 stars in work order
 #pragma unroll 1
     for (int round = 0; round < P; round++) {
-        const int p = s_perm[round * kBlockG + tid];
+        // (odd rounds take the warps' chunks in reverse, so every warp gets light and heavy ones)
+        const int p = s_perm[round * kBlockG + ((round & 1) ? (kBlockG - 32 - (tid & ~31)) + (tid & 31) : tid)];
         const int64_t v = pool0 + p;
         const uint32_t word = s_W[p];
         const bool active = (word >> 24) & 1u;
@@ -943,12 +976,11 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
         // placeholder sort key x << 12 | G; dms_critical rewrites it to rank(x) << 12 | G
         // once the vertex order (which runs concurrently on a second stream) is done
         const uint64_t rkey = (uint64_t)v << 12;
+        int64_t qq[4];
+        warp_append4(A.totals, c0, c1, c2, c3, qq);
+        if (c0 && qq[0] < A.cap[0]) { A.crit_id[0][qq[0]] = v; A.crit_key[0][qq[0]] = rkey; }
         {
-            const int64_t q0 = warp_append(&A.totals[0], c0);
-            if (c0 && q0 < A.cap[0]) { A.crit_id[0][q0] = v; A.crit_key[0][q0] = rkey; }
-        }
-        {
-            int64_t q1 = warp_append(&A.totals[1], c1);
+            int64_t q1 = qq[1];
             for (uint32_t m = st.crit_e; m; m &= m - 1, q1++) {
                 const int s = __ffs(m) - 1;
                 if (q1 < A.cap[1]) {
@@ -959,7 +991,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             }
         }
         {
-            int64_t q2 = warp_append(&A.totals[2], c2);
+            int64_t q2 = qq[2];
             for (uint64_t m = st.crit_t; m; m &= m - 1, q2++) {
                 const int t = __ffsll((long long)m) - 1;
                 if (q2 < A.cap[2]) {
@@ -970,7 +1002,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
             }
         }
         if (D == 3) {
-            int64_t q3 = warp_append(&A.totals[3], c3);
+            int64_t q3 = qq[3];
             for (uint32_t m = st.crit_q; m; m &= m - 1, q3++) {
                 const int q = __ffs(m) - 1;
                 if (q3 < A.cap[3]) {
