@@ -54,6 +54,22 @@ __global__ void k_emit_inf_k(Geo3 g, int dim, const int64_t* id_ptr, const unsig
     *slot = r;
 }
 
+// 1D, exact mode: D_{d-1} listed from D0.  For d = 1 the two are the same diagram (the
+// dimension-0 pairs of the one lexicographic filtration, PAPER.md 2736-2746; both
+// computations reproduce the boundary-matrix reduction at simplex level), so
+// the records are D0's, ordered by birth in decreasing order (Z11) instead of by death:
+// record of the minimum of age a (its position in C_0) -> slot n0 - 1 - a; the global
+// minimum (a = 0, D0's infinite record) comes last, and is the one unpaired minimum.
+__global__ void k_dtop_from_d0(const PairRec* __restrict__ d0, int64_t n0, const int32_t* __restrict__ node_of0,
+                               const int32_t* __restrict__ age, PairRec* __restrict__ out, const int64_t* c0,
+                               int64_t* unp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) unp[0] = c0[0];
+    if (i >= n0) return;
+    const PairRec r = d0[i];
+    out[n0 - 1 - age[node_of0[r.birth_vertex]]] = r;
+}
+
 // the infinite class with its slot after the np finite pairs, np read on the device from
 // the pair scan (np = scan end + last flag)
 __global__ void k_emit_inf_dev(Geo3 g, int dim, const int64_t* id_ptr, const unsigned long long* kmax, PairRec* base,
@@ -258,6 +274,7 @@ struct dms_ctx {
     bool have_pmap = false;
     PathBuf pb[2];
     bool have_ign = false;                   // D_{d-1} in the "ignore" boundary mode
+    bool dtop_short = false;                 // 1D: D_{d-1} was listed from D0 (run_dtop_from_d0), no dual union-find yet
     UFBuf uf_ign;
     PairRec* pairs_ign = nullptr;
     int64_t npairs_ign = 0, cap_ign = 0;
@@ -494,7 +511,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
         CU(cudaGetLastError());
         c->have_order = true;
         c->order_fresh = true;
-        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
+        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = c->dtop_short = false;
         return DMS_OK;
     }
     // one-sweep LSD radix sort (onesweep.cuh): one histogram read of f, four look-back
@@ -558,7 +575,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
         CU(cudaGetLastError());
         c->have_order = true;
         c->order_fresh = true;
-        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
+        c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = c->dtop_short = false;
         return DMS_OK;
     }
     // key-value LSD radix sort of (ordered f, index); the first pass reads f directly
@@ -577,7 +594,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     CU(cudaGetLastError());
     c->have_order = true;
     c->order_fresh = true;
-    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;  // the gradient does not depend on ranks
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = c->dtop_short = false;  // the gradient does not depend on ranks
     return DMS_OK;
 }
 
@@ -702,7 +719,7 @@ dms_status run_gradient(dms_ctx* c, void* d_grad) {
     dms_status s = launch_gradient(c, 0, c->N);
     if (s) return s;
     c->have_grad = true;
-    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = c->dtop_short = false;
     return DMS_OK;
 }
 
@@ -718,6 +735,8 @@ const uint32_t* crit_perm(dms_ctx* c, int k) { return c->cidx[c->cur[k]][k]; }  
 
 dms_status d0_trace(dms_ctx* c);
 dms_status dtop_trace(dms_ctx* c);
+bool dtop1d_short(const dms_ctx* c);
+dms_status run_dtop_from_d0(dms_ctx* c);
 
 dms_status run_critical(dms_ctx* c) {
     if (!c->have_grad) {
@@ -752,6 +771,7 @@ dms_status run_critical(dms_ctx* c) {
     if (c->early_traces && early && conc_env2 && c->lane3.st && c->lane4.st) {
         CU(cudaEventRecord(c->ev_grad, c->st));
         for (int w = 0; w < 2; w++) {
+            if (w == 1 && dtop1d_short(c)) continue;  // (D_{d-1} is listed from D0)
             Lane& L = w == 0 ? c->lane3 : c->lane4;
             CU(cudaStreamWaitEvent(L.st, c->ev_grad, 0));
             LaneSwap ls(c, L);
@@ -1437,6 +1457,44 @@ dms_status run_dtop(dms_ctx* c) {
     return s ? s : dtop_finish(c);
 }
 
+// DMS_DTOP1D=0: the dual union-find in 1D too (A/B; the ignore mode always runs it)
+bool dtop1d_short(const dms_ctx* c) {
+    static const int env = getenv("DMS_DTOP1D") ? atoi(getenv("DMS_DTOP1D")) : 1;
+    return c->ndim == 1 && env != 0;
+}
+
+// 1D, exact mode: D_{d-1} = D0's records in decreasing birth order (k_dtop_from_d0)
+dms_status run_dtop_from_d0(dms_ctx* c) {
+    dms_status s;
+    if (!c->have_d[0] && (s = run_d0(c))) return s;
+    cudaEvent_t t0 = stage_begin(c);
+    const int64_t n0 = c->ncrit[0];  // |C_0| - 1 finite pairs + the infinite class (a line is connected)
+    if (n0 + 1 > c->cap_pairs[1]) {
+        cudaFree(c->pairs[1]);
+        c->pairs[1] = nullptr;
+        CU(dalloc(&c->pairs[1], 2 * n0 + 1024));
+        c->cap_pairs[1] = 2 * n0 + 1024;
+    }
+    if (c->cap_unp[1] < 1) {
+        cudaFree(c->unp[1]);
+        c->unp[1] = nullptr;
+        CU(dalloc(&c->unp[1], 1024));
+        c->cap_unp[1] = 1024;
+    }
+    k_dtop_from_d0<<<grid_for(n0), kBlock, 0, c->st>>>(c->pairs[0], n0, c->node_of0, c->uf[0].age, c->pairs[1],
+                                                      crit_ids(c, 0), c->unp[1]);
+    c->launches++;
+    CU(cudaGetLastError());
+    c->npairs[1] = n0;
+    c->npairs_async[1] = 0;
+    c->nunp[1] = 1;
+    c->nunp_async[1] = false;
+    stage_end(c, 4, t0);
+    c->have_d[1] = true;
+    c->dtop_short = true;
+    return DMS_OK;
+}
+
 // D0 on the second lane beside D_{d-1} (both only read the gradient and the critical
 // lists): issue both, then finish both, so the host's count reads for one overlap the
 // other's kernels; the cooperative union-find grids take half the GPU each (two
@@ -1444,6 +1502,10 @@ dms_status run_dtop(dms_ctx* c) {
 // full (it never waits on other work, and halving it measured slower).
 dms_status run_diagrams(dms_ctx* c) {
     static const int conc_env = getenv("DMS_CONCURRENT") ? atoi(getenv("DMS_CONCURRENT")) : 1;
+    if (dtop1d_short(c)) {  // 1D: one union-find on the whole GPU, D_{d-1} listed from D0
+        dms_status s = run_d0(c);
+        return s ? s : run_dtop_from_d0(c);
+    }
     if (!conc_env || !c->lane3.st) {
         dms_status s = run_d0(c);
         return s ? s : run_dtop(c);
@@ -2140,10 +2202,14 @@ dms_status dms_diagram_top(dms_ctx* c, dms_boundary mode, const dms_pair** d_pai
     if (!d_pairs || !h_n) return DMS_ERR_ARG;
     if (mode != DMS_BOUNDARY_EXACT && mode != DMS_BOUNDARY_IGNORE) return DMS_ERR_ARG;
     if (!c->have_d[1]) {
-        s = run_dtop(c);
+        s = (dtop1d_short(c) && mode == DMS_BOUNDARY_EXACT) ? run_dtop_from_d0(c) : run_dtop(c);
         if (s) return s;
     }
     if (mode == DMS_BOUNDARY_IGNORE) {
+        if (c->dtop_short) {  // the ignore mode drops arcs of the dual union-find: run it now
+            if ((s = run_dtop(c))) return s;
+            c->dtop_short = false;
+        }
         if (!c->have_ign) {
             if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
             if ((s = run_dtop_ignore(c))) return s;
@@ -2172,7 +2238,7 @@ dms_status dms_unpaired_saddles(dms_ctx* c, int which, const int64_t** d_ids, in
         return DMS_OK;
     }
     if (!c->have_d[which]) {
-        s = which == 0 ? run_d0(c) : run_dtop(c);
+        s = which == 0 ? run_d0(c) : (dtop1d_short(c) ? run_dtop_from_d0(c) : run_dtop(c));
         if (s) return s;
     }
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, DMS_ERR_CUDA, "sync");
@@ -2325,7 +2391,7 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
     }
     c->have_grad = true;
     c->order_fresh = false;
-    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = false;
+    c->have_crit = c->have_d[0] = c->have_d[1] = c->have_d1 = c->have_gen = c->have_ign = c->dtop_short = false;
     c->early_traces = true;
     s = run_critical(c);
     c->early_traces = false;

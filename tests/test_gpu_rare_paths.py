@@ -62,6 +62,8 @@ def test_critical_record_overflow():
     {"DMS_AGG": "1", "DMS_UFBATCH": "4"},
     {"DMS_CHASEWORD": "0", "DMS_ORDER_CTAS": "0", "DMS_VCODES": "0"},
     {"DMS_PATH1D": "1", "DMS_ORDER_OS": "0"},
+    {"DMS_DTOP1D": "0", "DMS_GRAD_FAST": "0"},
+    {"DMS_DTOP1D": "0", "DMS_PATH1D": "1"},
     {"DMS_CHECK_INVARIANTS": "1", "DMS_CRIT_BITMAP": "0"},
     {"DMS_CRIT_RUNS": "0", "DMS_EARLY_TRACE": "1"},
 ])
