@@ -493,7 +493,10 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     // 1/2/3/full grid: 22.18 / 23.52 / 25.10 / 25.10 ms, order first, then the gradient:
     // 25.12 ms; c3 1/2/3: 6.52 / 6.59 / 6.70 ms)
     const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? 1 : 0);
-    const int64_t order_cap = octas > 0 ? (int64_t)c->sms * octas : 0;
+    // DMS_ORDER_GRID: the persistent order grid in CTAs (finer than whole CTAs per SM; A/B)
+    static const int ogrid_env = getenv("DMS_ORDER_GRID") ? atoi(getenv("DMS_ORDER_GRID")) : 0;
+    const int64_t order_cap = (ogrid_env > 0 && beside_gradient && c->ndim == 3) ? ogrid_env
+                              : octas > 0 ? (int64_t)c->sms * octas : 0;
     if (c->ord_B > 0) {  // sample sort (order.cuh)
         const int B = c->ord_B, S = c->ord_S, G = c->sms;
         static const int ocap_env = getenv("DMS_ORD_CAP") ? atoi(getenv("DMS_ORD_CAP")) : kOrdCap;  // tests: fallback path

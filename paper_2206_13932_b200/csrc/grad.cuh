@@ -49,7 +49,7 @@ __device__ __forceinline__ int off_c(int s, int ax) {
 
 // link adjacency of two 3D neighbour slots: (x, n_s, n_u) is a star triangle iff the
 // offsets differ by a Kuhn direction (all components in {0,1} or all in {0,-1}, not zero)
-__host__ __device__ constexpr bool link_adj3(int s, int u) {
+__device__ constexpr bool link_adj3(int s, int u) {
     const int dx = kOff3[u][0] - kOff3[s][0], dy = kOff3[u][1] - kOff3[s][1], dz = kOff3[u][2] - kOff3[s][2];
     const bool pos = dx >= 0 && dy >= 0 && dz >= 0 && dx <= 1 && dy <= 1 && dz <= 1;
     const bool neg = dx <= 0 && dy <= 0 && dz <= 0 && dx >= -1 && dy >= -1 && dz >= -1;
@@ -417,6 +417,24 @@ __device__ __forceinline__ void dec_count(uint32_t& c0, uint32_t& c1, uint32_t M
     c0 ^= M;
     c1 ^= borrow;
 }
+// per link triangle (star tetrahedron in Lq), its unclassified edges = 3 minus the forest
+// edges it holds (0, 1 or 2: three would close a cycle), as bit planes c1 c0: the forest
+// set T is gathered nibble by nibble into the three "edge j is in T" masks (GradLut::gat)
+__device__ __forceinline__ void link_counters(const GradLut& G, uint64_t T, uint32_t Lq, uint32_t& c0, uint32_t& c1) {
+    uint32_t a0 = 0, a1 = 0, a2 = 0;
+    const uint32_t tl = (uint32_t)T, th = (uint32_t)(T >> 32);
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        const uint32_t m = i < 8 ? (tl >> (4 * i)) & 15u : th & 15u;
+        const Gat4 g = G.gat[i][m];
+        a0 |= g.x;
+        a1 |= g.y;
+        a2 |= g.z;
+    }
+    c0 = Lq & ~(a0 ^ a1 ^ a2);
+    c1 = Lq & ~((a0 & a1) | (a0 & a2) | (a1 & a2));
+}
+
 // (2) of the closed form: peel the link triangles against the non-forest edges U = Lt - T.
 // c1 c0: per link triangle, its unclassified edges (3 minus the forest edges it holds).
 // SPH: the full sphere may occur.  There U is a spanning tree of the dual graph and the
@@ -425,10 +443,15 @@ __device__ __forceinline__ void dec_count(uint32_t& c0, uint32_t& c1, uint32_t M
 // other one pairs with its dual-tree edge towards it -- whatever the order: it is
 // withheld from the ready set and the rest is peeled in slot order.
 template <bool SPH>
-__device__ __forceinline__ void peel_link(const StarTab& S, uint64_t R, uint64_t IV, StarState& st, uint64_t T,
-                                          uint32_t c0, uint32_t c1) {
+__device__ __forceinline__ void peel_link(const StarTab& S, const GradLut& G, uint64_t R, uint64_t IV, StarState& st,
+                                          uint64_t T) {
     uint64_t U = st.Lt & ~T;
     if (!U) return;  // (then no link triangles either: each has a non-forest edge)
+    // (link_counters() gathers the same counters without a loop: 8 % fewer instructions, but 62
+    // instead of 56 registers, and beside the vertex order the c4 step went 19.6 -> 20.0 ms)
+    uint32_t c0 = st.Lq, c1 = st.Lq;
+#pragma unroll 1
+    for (uint64_t m = T; m; m &= m - 1) dec_count(c0, c1, S.tri_tet_mask[__ffsll((long long)m) - 1] & st.Lq);
     uint32_t clsq = 0;  // classified (or withheld) link triangles
     if (SPH && st.Le == 0x3fffu) {
         const int top = nib4(IV, 13);  // its link triangles hold the maximum key
@@ -449,12 +472,14 @@ __device__ __forceinline__ void peel_link(const StarTab& S, uint64_t R, uint64_t
 #pragma unroll 1
         while (ready) {
             const int q = __ffs(ready) - 1;
-            const int e = __ffsll((long long)(S.tet_tmask[q] & U)) - 1;
-            const int j = (e == S.tet_tri[q][0]) ? 0 : ((e == S.tet_tri[q][1]) ? 1 : 2);
+            // its one unclassified edge x (a single bit); j = its position among the triangle's
+            // three edges (tet_tri[q][0] < [1] < [2] as slots); the triangle across x loses one
+            const uint64_t tm = S.tet_tmask[q], x = tm & U;
+            const int j = __popcll(tm & (x - 1));
             st.qcode |= (uint64_t)(j + 1) << (2 * q);
             clsq |= 1u << q;
-            U &= ~(1ull << e);
-            dec_count(c0, c1, S.tri_tet_mask[e] & st.Lq & ~clsq);
+            U ^= x;
+            dec_count(c0, c1, (1u << ((G.tet_nb[q] >> (8 * j)) & 31u)) & st.Lq & ~clsq);
             ready = st.Lq & ~clsq & c0 & ~c1;
         }
         if (!U) break;
@@ -476,8 +501,8 @@ __device__ __forceinline__ void peel_link(const StarTab& S, uint64_t R, uint64_t
     st.crit_t = crit_t;
     st.crit_q = st.Lq & ~(clsq & ~held);
 }
-__device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, uint64_t IV, int n, StarState& st,
-                                                  uint8_t* par, uint8_t* tp) {
+__device__ __forceinline__ void process_star_fast(const StarTab& S, const GradLut& G, uint64_t R, uint64_t IV, int n,
+                                                  StarState& st, uint8_t* par, uint8_t* tp) {
     const int s0 = (int)(IV & 15ull);  // delta = (x, lowest lower neighbour)
     st.vcode = s0;
     par[s0 * kBlockG] = (uint8_t)s0;
@@ -542,7 +567,7 @@ __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, 
     // forest edge (w, tp[w]) -> star triangle paired with the star edge (x, w); roots other
     // than s0 are the critical star edges; the triangle counters lose the forest edges
     uint64_t T = 0;
-    uint32_t crit_e = 0, c0 = st.Lq, c1 = st.Lq;  // every link triangle: 3 unclassified edges
+    uint32_t crit_e = 0;
 #pragma unroll 1
     for (uint32_t le = st.Le & ~(1u << s0); le; le &= le - 1) {
         const int w = __ffs(le) - 1;
@@ -554,10 +579,9 @@ __device__ __forceinline__ void process_star_fast(const StarTab& S, uint64_t R, 
         const int t = S.tri_of[w][p];
         T |= 1ull << t;
         st.ecode |= (uint64_t)(p + 1) << (4 * w);
-        dec_count(c0, c1, S.tri_tet_mask[t] & st.Lq);
     }
     st.crit_e = crit_e;
-    peel_link<true>(S, R, IV, st, T, c0, c1);
+    peel_link<true>(S, G, R, IV, st, T);
 }
 
 // A lower link whose ranks have ONE local minimum on L's graph (and that is not the full
@@ -582,11 +606,8 @@ __device__ __forceinline__ void process_star_simple(const StarTab& S, const Grad
         T |= (S.tri_amask[u] | S.tri_bmask[u]) & (G.ort[0][kl] | G.ort[1][kh]);
     }
     st.ecode = E;
-    uint32_t c0 = st.Lq, c1 = st.Lq;
-#pragma unroll 1
-    for (uint64_t m = T; m; m &= m - 1) dec_count(c0, c1, S.tri_tet_mask[__ffsll((long long)m) - 1] & st.Lq);
     st.crit_e = 0;
-    peel_link<false>(S, R, IV, st, T, c0, c1);
+    peel_link<false>(S, G, R, IV, st, T);
 }
 
 // Two local minima s0 < m of the ranks on L's graph: the walk of process_star_simple
@@ -643,11 +664,8 @@ __device__ __forceinline__ void process_star_two(const StarTab& S, const GradLut
         T |= (S.tri_amask[u] | S.tri_bmask[u]) & (G.ort[0][kl] | G.ort[1][kh]);
     }
     st.ecode = E;
-    uint32_t c0 = st.Lq, c1 = st.Lq;
-#pragma unroll 1
-    for (uint64_t mm = T; mm; mm &= mm - 1) dec_count(c0, c1, S.tri_tet_mask[__ffsll((long long)mm) - 1] & st.Lq);
     st.crit_e = (m >= 0 && !merged) ? 1u << m : 0u;
-    peel_link<false>(S, R, IV, st, T, c0, c1);
+    peel_link<false>(S, G, R, IV, st, T);
 }
 
 // warp-level append of `cnt` records per lane: returns this lane's first position
@@ -756,7 +774,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 o[s] = 0xffffffffu;
                 if (in) {
                     const uint32_t os = ord_of(__ldg(A.f + v + dx + A.Lx * dy + LxLy * dz));
-                    const bool lower = (os < ox) || (os == ox && s < NE / 2);
+                    const bool lower = (s < NE / 2) ? (os <= ox) : (os < ox);  // ties: the smaller index first
                     // (closed form: true values -- every lower slot precedes every other one in
                     // the order K anyway, so the ranks of the lower slots are 0 .. n-1 either way)
                     if (FAST) o[s] = os;
@@ -930,7 +948,7 @@ __global__ void __launch_bounds__(kBlockG, MINB) k_gradient_pool(GradArgs A) {
                 const uint32_t cls = (word >> 29) & 3u;
                 if (cls == 0) process_star_simple(S, s_G[0], R, IV, __popc(st.Le), st);
                 else if (cls == 1) process_star_two(S, s_G[0], R, IV, __popc(st.Le), st);
-                else process_star_fast(S, R, IV, __popc(st.Le), st, s_par + tid, s_tp + tid);
+                else process_star_fast(S, s_G[0], R, IV, __popc(st.Le), st, s_par + tid, s_tp + tid);
             } else {
             for (uint64_t m = st.Lt; m; m &= m - 1) {
                 const int tt = __ffsll((long long)m) - 1;

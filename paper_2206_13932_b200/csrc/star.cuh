@@ -64,10 +64,17 @@ struct alignas(16) ChaseTab {
 // 3D gradient kernel: masks that are unions over a set of link vertices, looked up by the
 // two 7-bit halves of the set (slots 0-6, 7-13) and OR-ed: ort / orq = the star triangles
 // / tetrahedra holding any of the vertices; ex = bit i -> bit 4 i (a nibble per slot).
+// gat: the forest triangles T (a set of star triangles) -> per star tetrahedron, which of
+// its three triangles tet_tri[q][j] are in T: nibble i of T with value m contributes
+// gat[i][m][j] (a mask over tetrahedra).  tet_nb: byte j = the other tetrahedron holding
+// the triangle tet_tri[q][j] (31: none).
+struct alignas(16) Gat4 { uint32_t x, y, z, w; };
 struct alignas(16) GradLut {
     uint64_t ort[2][128];
     uint32_t orq[2][128];
     uint32_t ex[128];
+    Gat4 gat[9][16];
+    uint32_t tet_nb[kMaxNQ];
 };
 inline void build_grad_lut(const StarTab& T, GradLut* G);
 

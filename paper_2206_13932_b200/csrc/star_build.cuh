@@ -268,6 +268,16 @@ inline void build_grad_lut(const StarTab& T, GradLut* G) {
     for (int m = 0; m < 128; m++)
         for (int b = 0; b < 7; b++)
             if ((m >> b) & 1) G->ex[m] |= 1u << (4 * b);
+    for (int q = 0; q < T.nq; q++) {
+        G->tet_nb[q] = 0;
+        for (int j = 0; j < 3; j++) {
+            const int t = T.tet_tri[q][j];
+            for (int m = 0; m < 16; m++)
+                if ((m >> (t & 3)) & 1) (j == 0 ? G->gat[t >> 2][m].x : j == 1 ? G->gat[t >> 2][m].y : G->gat[t >> 2][m].z) |= 1u << q;
+            const int o = T.tri_tet[t][0] == q ? T.tri_tet[t][1] : T.tri_tet[t][0];
+            G->tet_nb[q] |= (uint32_t)(o == 255 ? 31 : o) << (8 * j);
+        }
+    }
 }
 
 inline void build_chase_tables(const StarTab& T, ChaseTab* C) {

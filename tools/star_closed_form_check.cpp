@@ -69,7 +69,7 @@ int main(int argc, char** argv) {
         for (uint32_t m = a.Lq; m; m &= m - 1) { int q = __builtin_ctz(m); qk[q * kBlockG] = (uint16_t)cmp_tet(S, R, q); }
         KeyCache C; C.tki = tki; C.qk = qk; C.IV = IV; C.S = &S; C.R = R;
         process_star<3, true>(S, C, R, IV, n, delta, a);
-        process_star_fast(S, R, IV, n, b, par, tp);
+        process_star_fast(S, G, R, IV, n, b, par, tp);
         tot++;
         // stars with one local minimum of the ranks on L (not the full sphere): the simple path
         {
