@@ -189,6 +189,7 @@ struct dms_ctx {
     Lane lane3;                   // D0's lane when the diagrams run concurrently
     Lane lane4;                   // D_{d-1}'s trace beside the critical sort
     bool early_traces = false;    // dms_run_all*: trace D0 / D_{d-1} beside the critical sort
+    int order_ctas_beside = 1;    // CTAs per SM of the order's persistent grid beside the 3D gradient
     bool traced[2] = {false, false};
     cudaEvent_t ev_grad = nullptr, ev_trace[2] = {nullptr, nullptr};
     cudaEvent_t ev_crit = nullptr, ev_d0 = nullptr;
@@ -492,7 +493,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     // beside the closed-form 3D gradient, the one-sweep order on 1 CTA per SM (c4,
     // 1/2/3/full grid: 22.18 / 23.52 / 25.10 / 25.10 ms, order first, then the gradient:
     // 25.12 ms; c3 1/2/3: 6.52 / 6.59 / 6.70 ms)
-    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? 1 : 0);
+    const int octas = octas_env >= 0 ? octas_env : (beside_gradient && c->ndim == 3 ? c->order_ctas_beside : 0);
     // DMS_ORDER_GRID: the persistent order grid in CTAs (finer than whole CTAs per SM; A/B)
     static const int ogrid_env = getenv("DMS_ORDER_GRID") ? atoi(getenv("DMS_ORDER_GRID")) : 0;
     const int64_t order_cap = (ogrid_env > 0 && beside_gradient && c->ndim == 3) ? ogrid_env
@@ -2374,11 +2375,15 @@ dms_status dms_run_all_host(dms_ctx* c, const float* h_f, int32_t* d_rank, void*
                                cudaMemcpyHostToDevice, c->st2));
         CU(cudaEventRecord(c->ev_slab[i], c->st2));
     }
-    // the vertex order on the second stream, after the last slab
+    // the vertex order on the second stream, after the last slab: by then only the tail of
+    // the gradient is left, so its persistent grid takes 2 CTAs per SM instead of the 1 of
+    // the device-input path (c4 e2e: 1 / full grid / 2 per SM = 26.9 / 24.7 / 24.0 ms)
     {
         cudaStream_t main = c->st;
         c->st = c->st2;
+        c->order_ctas_beside = 2;
         s = run_order_on_stream(c, d_rank, true);
+        c->order_ctas_beside = 1;
         c->st = main;
         if (s) return s;
         CU(cudaEventRecord(c->ev_order, c->st2));
