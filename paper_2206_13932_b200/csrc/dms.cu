@@ -190,6 +190,10 @@ struct dms_ctx {
     Lane lane4;                   // D_{d-1}'s trace beside the critical sort
     bool early_traces = false;    // dms_run_all*: trace D0 / D_{d-1} beside the critical sort
     int order_ctas_beside = 1;    // CTAs per SM of the order's persistent grid beside the 3D gradient
+    int os_defer_from = 4;        // one-sweep order: passes [os_defer_from, 4) + the rank pass wait for run_order_rest
+    bool os_deferred = false;     // ... and are still to be issued
+    int os_resume = 4;            // first deferred pass
+    cudaEvent_t ev_grad2 = nullptr;
     bool traced[2] = {false, false};
     cudaEvent_t ev_grad = nullptr, ev_trace[2] = {nullptr, nullptr};
     cudaEvent_t ev_crit = nullptr, ev_d0 = nullptr;
@@ -481,6 +485,71 @@ dms_status read_err(dms_ctx* c) {
 
 // ------------------------------------------------------------------ stages
 
+// one-sweep order: the digit passes [p0, p1) on a persistent grid of `grid` CTAs, and after
+// pass 3 the rank pass of the windowed form (the buffers and the histograms are in place)
+dms_status os_passes(dms_ctx* c, int p0, int p1, unsigned grid) {
+    const int64_t n = c->N;
+    const int64_t tiles = ceil_div(n, (int64_t)kOsTile);
+    static const long long win_env = getenv("DMS_RANK_WIN") ? atoll(getenv("DMS_RANK_WIN")) : -1;
+    const bool windowed = win_env < 0 ? n >= (int64_t(1) << 23) : (win_env > 0 && n >= win_env);
+    for (int p = p0; p < p1; p++) {
+        if (++c->os_epoch >= 0xffffu) {  // epochs wrap: clear the look-back words
+            CU(cudaMemsetAsync(c->os_status, 0, (size_t)tiles * 256 * 8, c->st));
+            c->os_epoch = 1;
+        }
+        uint32_t* ki = p % 2 ? c->okeys[1] : c->okeys[0];
+        uint32_t* vi = p % 2 ? c->ovals[1] : c->ovals[0];
+        uint32_t* ko = p % 2 ? c->okeys[0] : c->okeys[1];
+        uint32_t* vo = p % 2 ? c->ovals[0] : c->ovals[1];
+        const uint32_t* db = c->os_hist + 256 * p;
+        int* tc = c->os_tctr + p;
+        if (p == 0)
+            k_os_pass<true, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 0, db,
+                                                        c->os_status, c->os_epoch, tc, tiles);
+        else if (p < 3)
+            k_os_pass<false, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 8 * p,
+                                                         db, c->os_status, c->os_epoch, tc, tiles);
+        else if (windowed)
+            k_os_pass<false, 2><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
+                                                         c->os_status, c->os_epoch, tc, tiles);
+        else
+            k_os_pass<false, 1><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
+                                                         c->os_status, c->os_epoch, tc, tiles);
+        c->launches++;
+    }
+    if (p1 == 4 && windowed) {
+        k_os_rank<<<(unsigned)ceil_div(n, kBlock), kBlock, 0, c->st>>>(c->os_wbuf, n, c->rank);
+        c->launches++;
+    }
+    CU(cudaGetLastError());
+    return DMS_OK;
+}
+
+// the deferred passes of the one-sweep order (dms_run_all, DMS_ORDER_SPLIT): on the order's
+// stream once the gradient kernel is done, on the full grid, beside the diagrams' tracing
+dms_status run_order_rest(dms_ctx* c) {
+    if (!c->os_deferred) return DMS_OK;
+    c->os_deferred = false;
+    if (!c->ev_grad2) CU(cudaEventCreateWithFlags(&c->ev_grad2, cudaEventDisableTiming));
+    CU(cudaEventRecord(c->ev_grad2, c->st));
+    CU(cudaStreamWaitEvent(c->st2, c->ev_grad2, 0));
+    cudaStream_t main = c->st;
+    c->st = c->st2;
+    dms_status s;
+    {
+        StageTimer tm(c, 0);
+        int per = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_os_pass<false, 0>, kOsT, 0);
+        const int64_t tiles = ceil_div(c->N, (int64_t)kOsTile);
+        const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->sms * std::max(per, 1)));
+        s = os_passes(c, c->os_resume, 4, grid);
+    }
+    c->st = main;
+    if (s) return s;
+    CU(cudaEventRecord(c->ev_order, c->st2));
+    return DMS_OK;
+}
+
 dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient = false) {
     StageTimer tm(c, 0);
     c->rank = d_rank ? d_rank : c->rank_scratch;
@@ -522,6 +591,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
     // passes, the last one writing the ranks (by windows above 2^23 vertices)
     static const int os_env = getenv("DMS_ORDER_OS") ? atoi(getenv("DMS_ORDER_OS")) : 1;
     if (os_env) {
+        dms_status s0;
         const int64_t n = c->N;
         const int64_t tiles = ceil_div(n, (int64_t)kOsTile);
         static const long long win_env = getenv("DMS_RANK_WIN") ? atoll(getenv("DMS_RANK_WIN")) : -1;
@@ -547,35 +617,10 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
                                                                                                     c->err, c->kmax);
         k_os_scan<<<4, kOsT, 0, c->st>>>(c->os_hist, c->os_wcur, windowed ? nwin : 0);
         c->launches += 2;
-        for (int p = 0; p < 4; p++) {
-            if (++c->os_epoch >= 0xffffu) {  // epochs wrap: clear the look-back words
-                CU(cudaMemsetAsync(c->os_status, 0, (size_t)tiles * 256 * 8, c->st));
-                c->os_epoch = 1;
-            }
-            uint32_t* ki = p % 2 ? c->okeys[1] : c->okeys[0];
-            uint32_t* vi = p % 2 ? c->ovals[1] : c->ovals[0];
-            uint32_t* ko = p % 2 ? c->okeys[0] : c->okeys[1];
-            uint32_t* vo = p % 2 ? c->ovals[0] : c->ovals[1];
-            const uint32_t* db = c->os_hist + 256 * p;
-            int* tc = c->os_tctr + p;
-            if (p == 0)
-                k_os_pass<true, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 0, db,
-                                                            c->os_status, c->os_epoch, tc, tiles);
-            else if (p < 3)
-                k_os_pass<false, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 8 * p,
-                                                             db, c->os_status, c->os_epoch, tc, tiles);
-            else if (windowed)
-                k_os_pass<false, 2><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
-                                                             c->os_status, c->os_epoch, tc, tiles);
-            else
-                k_os_pass<false, 1><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
-                                                             c->os_status, c->os_epoch, tc, tiles);
-            c->launches++;
-        }
-        if (windowed) {
-            k_os_rank<<<(unsigned)ceil_div(n, kBlock), kBlock, 0, c->st>>>(c->os_wbuf, n, c->rank);
-            c->launches++;
-        }
+        const int p_end = std::min(4, std::max(1, c->os_defer_from));
+        if ((s0 = os_passes(c, 0, p_end, grid))) return s0;
+        c->os_deferred = p_end < 4;
+        c->os_resume = p_end;
         CU(cudaGetLastError());
         c->have_order = true;
         c->order_fresh = true;
@@ -618,7 +663,7 @@ dms_status run_order(dms_ctx* c, int32_t* d_rank, bool concurrent = false) {
     dms_status s = run_order_on_stream(c, d_rank, true);
     c->st = main;
     if (s) return s;
-    CU(cudaEventRecord(c->ev_order, c->st2));
+    if (!c->os_deferred) CU(cudaEventRecord(c->ev_order, c->st2));  // (else by run_order_rest)
     c->order_pending = true;
     return DMS_OK;
 }
@@ -2339,8 +2384,15 @@ dms_status dms_run_all(dms_ctx* c, int32_t* d_rank, void* d_grad) {
     // grid hides behind the ALU-bound 3D gradient: c4 22.18 vs 25.12 ms order first;
     // DMS_ORDER_SEQ=0/1 forces either)
     const bool seq = oseq_env >= 0 ? oseq_env != 0 : false;
-    if ((s = run_order(c, d_rank, !seq))) return s;
+    // DMS_ORDER_SPLIT=k (3D): only the first k digit passes run beside the gradient; the
+    // rest follow it on the full grid, beside the diagrams' tracing (A/B)
+    static const int split_env = getenv("DMS_ORDER_SPLIT") ? atoi(getenv("DMS_ORDER_SPLIT")) : 0;
+    c->os_defer_from = (!seq && c->ndim == 3 && split_env > 0 && split_env < 4) ? split_env : 4;
+    s = run_order(c, d_rank, !seq);
+    c->os_defer_from = 4;
+    if (s) return s;
     if ((s = run_gradient(c, d_grad))) return s;
+    if ((s = run_order_rest(c))) return s;
     c->early_traces = true;
     s = run_critical(c);
     c->early_traces = false;
@@ -2655,6 +2707,7 @@ void dms_destroy(dms_ctx* c) {
         if (e) cudaEventDestroy(e);
     cudaFree(c->dtab);
     cudaFree(c->dlut3);
+    if (c->ev_grad2) cudaEventDestroy(c->ev_grad2);
     cudaFree(c->dctab);
     cudaFree(c->rank_scratch);
     cudaFree(c->grad_scratch);
