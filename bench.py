@@ -340,7 +340,7 @@ def main():
     peak, peak_kind = load_peaks()
     g_ms = stages["gradient_kernel"] / max(1, stages["gradient_launches"])
     g_ach = bmin_grad / (g_ms / 1e3) / 1e9
-    kernel_name = {3: "k_gradient_pool<3,8,8,true> (closed-form lower-star gradient + critical records)",
+    kernel_name = {3: "k_gradient_pool<3,8,1,true> (closed-form lower-star gradient + critical records)",
                    2: "k_gradient_lut2 (2D lower-star gradient by table lookup + critical records)",
                    1: "k_gradient1 (1D lower-star gradient + critical records)"}[ndim]
     if args.complex == "5tet":

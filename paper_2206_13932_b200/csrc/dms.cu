@@ -487,7 +487,7 @@ dms_status read_err(dms_ctx* c) {
 
 // one-sweep order: the digit passes [p0, p1) on a persistent grid of `grid` CTAs, and after
 // pass 3 the rank pass of the windowed form (the buffers and the histograms are in place)
-dms_status os_passes(dms_ctx* c, int p0, int p1, unsigned grid) {
+dms_status os_passes(dms_ctx* c, int p0, int p1, unsigned grid, bool lb4) {
     const int64_t n = c->N;
     const int64_t tiles = ceil_div(n, (int64_t)kOsTile);
     static const long long win_env = getenv("DMS_RANK_WIN") ? atoll(getenv("DMS_RANK_WIN")) : -1;
@@ -503,18 +503,20 @@ dms_status os_passes(dms_ctx* c, int p0, int p1, unsigned grid) {
         uint32_t* vo = p % 2 ? c->ovals[0] : c->ovals[1];
         const uint32_t* db = c->os_hist + 256 * p;
         int* tc = c->os_tctr + p;
-        if (p == 0)
-            k_os_pass<true, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 0, db,
-                                                        c->os_status, c->os_epoch, tc, tiles);
-        else if (p < 3)
-            k_os_pass<false, 0><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 8 * p,
-                                                         db, c->os_status, c->os_epoch, tc, tiles);
-        else if (windowed)
-            k_os_pass<false, 2><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
-                                                         c->os_status, c->os_epoch, tc, tiles);
-        else
-            k_os_pass<false, 1><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, 24, db,
-                                                         c->os_status, c->os_epoch, tc, tiles);
+#define OS_PASS(FIRST, MODE, SHIFT)                                                                                  \
+    do {                                                                                                             \
+        if (lb4)                                                                                                     \
+            k_os_pass<FIRST, MODE, 4><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, \
+                                                               SHIFT, db, c->os_status, c->os_epoch, tc, tiles);    \
+        else                                                                                                         \
+            k_os_pass<FIRST, MODE, 1><<<grid, kOsT, 0, c->st>>>(ki, vi, c->f, ko, vo, c->rank, c->os_wbuf, c->os_wcur, n, \
+                                                               SHIFT, db, c->os_status, c->os_epoch, tc, tiles);    \
+    } while (0)
+        if (p == 0) OS_PASS(true, 0, 0);
+        else if (p < 3) OS_PASS(false, 0, 8 * p);
+        else if (windowed) OS_PASS(false, 2, 24);
+        else OS_PASS(false, 1, 24);
+#undef OS_PASS
         c->launches++;
     }
     if (p1 == 4 && windowed) {
@@ -539,10 +541,10 @@ dms_status run_order_rest(dms_ctx* c) {
     {
         StageTimer tm(c, 0);
         int per = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_os_pass<false, 0>, kOsT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_os_pass<false, 0, 4>, kOsT, 0);
         const int64_t tiles = ceil_div(c->N, (int64_t)kOsTile);
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)c->sms * std::max(per, 1)));
-        s = os_passes(c, c->os_resume, 4, grid);
+        s = os_passes(c, c->os_resume, 4, grid, true);
     }
     c->st = main;
     if (s) return s;
@@ -609,7 +611,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
         CU(cudaMemsetAsync(c->os_hist, 0, 4 * 256 * sizeof(uint32_t), c->st));
         CU(cudaMemsetAsync(c->os_tctr, 0, 4 * sizeof(int), c->st));
         int per = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_os_pass<false, 0>, kOsT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_os_pass<false, 0, 4>, kOsT, 0);
         const int64_t res = (int64_t)c->sms * std::max(per, 1);
         const int64_t cap = order_cap > 0 ? std::min<int64_t>(order_cap, res) : res;
         const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, cap));
@@ -618,7 +620,7 @@ dms_status run_order_on_stream(dms_ctx* c, int32_t* d_rank, bool beside_gradient
         k_os_scan<<<4, kOsT, 0, c->st>>>(c->os_hist, c->os_wcur, windowed ? nwin : 0);
         c->launches += 2;
         const int p_end = std::min(4, std::max(1, c->os_defer_from));
-        if ((s0 = os_passes(c, 0, p_end, grid))) return s0;
+        if ((s0 = os_passes(c, 0, p_end, grid, order_cap == 0))) return s0;
         c->os_deferred = p_end < 4;
         c->os_resume = p_end;
         CU(cudaGetLastError());

@@ -88,7 +88,9 @@ __global__ void k_os_scan(uint32_t* hist, uint32_t* wcur, int nwin) {
 // (Measured variants: publishing the tile counts before the ranking,
 // ballot-built peer masks, one combined staging offset / 8-byte staging stores -- none
 // faster.)
-template <bool FIRST, int MODE>
+// LB: look-back words in flight per thread (4 on the full grid: c5b order 6.09 -> 5.70 ms,
+// c5a 4.52 -> 4.40; 1 on the small grid beside the 3D gradient, where 4 cost c4 0.3 ms).
+template <bool FIRST, int MODE, int LB>
 __global__ void __launch_bounds__(kOsT, DMS_OS_MINB) k_os_pass(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                      const float* __restrict__ f, uint32_t* __restrict__ kout,
                                                      uint32_t* __restrict__ vout, int32_t* __restrict__ rank_out,
@@ -172,11 +174,25 @@ __global__ void __launch_bounds__(kOsT, DMS_OS_MINB) k_os_pass(const uint32_t* _
             st_volatile(st, os_word(epoch, 2u, run));
         } else {
             st_volatile(st, os_word(epoch, 1u, run));
-            for (int64_t t = tile - 1; t >= 0; t--) {
-                unsigned long long w = ld_volatile(status + (size_t)t * 256 + d);
-                while ((uint32_t)(w >> 48) != epoch) w = ld_volatile(status + (size_t)t * 256 + d);
-                excl += (uint32_t)w;
-                if (((w >> 32) & 3ull) == 2ull) break;
+            // look back LB tiles at a time (independent loads in flight, consumed in order; a
+            // word of another epoch is not written yet: resume from that tile)
+            int64_t t = tile - 1;
+            bool done = false;
+            while (!done) {
+                unsigned long long w[LB];
+#pragma unroll
+                for (int j = 0; j < LB; j++)
+                    w[j] = t - j >= 0 ? ld_volatile(status + (size_t)(t - j) * 256 + d) : os_word(epoch, 2u, 0u);
+                int used = 0;
+#pragma unroll
+                for (int j = 0; j < LB; j++) {
+                    if (done || used != j) continue;
+                    if ((uint32_t)(w[j] >> 48) != epoch) continue;  // not written yet
+                    excl += (uint32_t)w[j];
+                    used = j + 1;
+                    done = ((w[j] >> 32) & 3ull) == 2ull;
+                }
+                t -= used;
             }
             st_volatile(st, os_word(epoch, 2u, excl + run));
         }

@@ -409,6 +409,10 @@ constexpr int kT5Block = 128;
 // scanning its members' keys (t5_key).  One thread per vertex.
 __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
     __shared__ T5Star S[2];
+    // the keys of the thread's lower triangles / tetrahedra, [cell][thread] (computed once
+    // per star: every queue pop scans its members' keys)
+    __shared__ uint16_t s_key[(kT5NT + kT5NQ) * kT5Block];
+    uint16_t* const mykey = s_key + threadIdx.x;
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(A.tab->star);
         uint32_t* dst = reinterpret_cast<uint32_t*>(S);
@@ -416,7 +420,9 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
     }
     __syncthreads();
     const int64_t LxLy = (int64_t)A.Lx * A.Ly;
-    const int64_t v = A.v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // consecutive vertices alternate between the 18- and the 6-neighbour class: the first two
+    // warps take the CTA's even offsets, the last two the odd ones (one class per warp within a row)
+    const int64_t v = A.v0 + (int64_t)blockIdx.x * blockDim.x + (((threadIdx.x & 63) << 1) | (threadIdx.x >> 6));
     const bool active = v < A.v1;
     uint32_t critE = 0, critQ = 0, crit_v = 0;
     uint64_t critT = 0;
@@ -470,6 +476,14 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
             if ((T.tri_emask[t] & low) == T.tri_emask[t]) lowT |= 1ull << t;
         for (int q = 0; q < T.nq; q++)
             if ((T.tet_tmask[q] & lowT) == T.tet_tmask[q]) lowQ |= 1u << q;
+        for (uint64_t m = lowT; m; m &= m - 1) {
+            const int t = __ffsll((long long)m) - 1;
+            mykey[t * kT5Block] = (uint16_t)keyT(t);
+        }
+        for (uint32_t m = lowQ; m; m &= m - 1) {
+            const int q = __ffs(m) - 1;
+            mykey[(kT5NT + q) * kT5Block] = (uint16_t)keyQ(q);
+        }
         uint64_t tc_lo = 0, tc_hi = 0;  // 2-bit triangle codes: 1 / 2 paired with edge a / b, 3 tail, 0 critical
         uint64_t qc = 0;                // 2-bit tetrahedron codes: 1..3 paired with triangle 0..2 (ab, ac, bc), 0 critical
         int vcode = 0xff;
@@ -514,12 +528,12 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
                     int bi = -1, bty = 0;
                     for (uint64_t m = oT; m; m &= m - 1) {
                         const int t = __ffsll((long long)m) - 1;
-                        const uint32_t k = keyT(t);
+                        const uint32_t k = mykey[t * kT5Block];
                         if (k < best) { best = k; bi = t; bty = 2; }
                     }
                     for (uint32_t m = oQ; m; m &= m - 1) {
                         const int q = __ffs(m) - 1;
-                        const uint32_t k = keyQ(q);
+                        const uint32_t k = mykey[(kT5NT + q) * kT5Block];
                         if (k < best) { best = k; bi = q; bty = 3; }
                     }
                     if (bty == 2) {
@@ -559,12 +573,12 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
                 }
                 for (uint64_t m = zT; m; m &= m - 1) {
                     const int t = __ffsll((long long)m) - 1;
-                    const uint32_t k = keyT(t);
+                    const uint32_t k = mykey[t * kT5Block];
                     if (k < best) { best = k; bi = t; bty = 2; }
                 }
                 for (uint32_t m = zQ; m; m &= m - 1) {
                     const int q = __ffs(m) - 1;
-                    const uint32_t k = keyQ(q);
+                    const uint32_t k = mykey[(kT5NT + q) * kT5Block];
                     if (k < best) { best = k; bi = q; bty = 3; }
                 }
                 if (bi < 0) continue;

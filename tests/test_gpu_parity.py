@@ -134,6 +134,43 @@ def test_nan_rejected(env):
     assert e.value.name == "DMS_ERR_NAN"
 
 
+@pytest.mark.parametrize("shape", [(6, 7, 8), (9, 11), (50,)])
+def test_nan_then_clean_field_on_one_context(env, shape):
+    """the NaN flag describes the current field only -- after DMS_ERR_NAN the
+    same context, with a clean field written into the same device buffer, runs and
+    matches the oracle (both through dms_run_all and through the stepwise calls)."""
+    torch, dms = env
+    rng = np.random.default_rng(11)
+    clean = rng.random(shape).astype(np.float32)
+    bad = clean.copy()
+    bad.flat[bad.size // 2] = np.nan
+    fd = torch.from_numpy(bad).cuda()
+    d = dms.DMS(fd)
+    with pytest.raises(dms.DMSError) as e:
+        d.run_all()
+        d.critical()
+    assert e.value.name == "DMS_ERR_NAN"
+    ref = oracle.run(clean, nthreads=NCPU)
+    for stepwise in (False, True):
+        fd.copy_(torch.from_numpy(bad))  # NaN again, then clean again
+        with pytest.raises(dms.DMSError):
+            d.run_all()
+            d.critical()
+        fd.copy_(torch.from_numpy(clean))
+        if stepwise:
+            rank = d.order()
+            d.gradient()
+        else:
+            rank = torch.empty(clean.size, dtype=torch.int32, device="cuda")
+            d.run_all(rank)
+        assert np.array_equal(rank.cpu().numpy(), oracle.ranks(clean))
+        for k in range(clean.ndim + 1):
+            assert np.array_equal(d.critical()[k].cpu().numpy(), ref.crit[k])
+        assert d.diagram0().tobytes() == ref.d0.tobytes()
+        assert d.diagram_top().tobytes() == ref.dtop.tobytes()
+    d.close()
+
+
 def test_degenerate_and_bad_mode(env):
     torch, dms = env
     for shape in [(1, 4, 4), (4, 1), (1,)]:
