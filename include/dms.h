@@ -165,7 +165,8 @@ dms_status dms_diagram0(dms_ctx* ctx, const dms_pair** d_pairs, int64_t* h_n);
  * mode (a dms_boundary value):
  *   DMS_BOUNDARY_EXACT  a virtual maximum, older than every maximum, on the outer
  *       boundary (PAPER.md 2810-2817): every maximum dies; equals the boundary-matrix
- *       reduction.  For d = 1 the infinite class of the global minimum follows.
+ *       reduction.  For d = 1 the infinite class of the global minimum follows (and the
+ *       records are D0's, listed by birth: for d = 1 the two are one diagram).
  *   DMS_BOUNDARY_IGNORE no virtual maximum (PAPER.md 2822-2825, App. A 2927-2949;
  *       DESIGN.md reading Z7): an arc whose stable-set tracing leaves through the
  *       boundary is dropped (its saddle stays unpaired), the global maximum stays

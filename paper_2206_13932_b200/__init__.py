@@ -307,6 +307,7 @@ class DMS:
         if rank is None:
             rank = t.empty(self.N, dtype=t.int32, device=self.f.device)
         dms_order(self.ctx, rank)
+        self._rank = rank  # the context borrows the buffer (dms.h): keep it alive with the context
         return rank
 
     def gradient(self, grad=None):
@@ -314,10 +315,12 @@ class DMS:
         if grad is None:
             grad = t.empty(dms_gradient_bytes(self.ctx), dtype=t.uint8, device=self.f.device)
         dms_gradient(self.ctx, grad)
+        self._grad = grad  # borrowed by the context until the next gradient pass
         return grad
 
     def run_all(self, rank=None, grad=None):
         dms_run_all(self.ctx, rank, grad)
+        self._rank, self._grad = rank, grad
 
     def run_all_host(self, f_host, rank=None, grad=None):
         """run_all with the field uploaded from host memory (overwrites the device field)."""
@@ -326,6 +329,7 @@ class DMS:
         if not f_host.is_contiguous():
             raise ValueError("f_host must be contiguous")
         dms_run_all_host(self.ctx, f_host, rank, grad)
+        self._rank, self._grad = rank, grad
 
     def critical(self):
         """-> list of int64 CUDA tensors C_0..C_d (lexicographically sorted)."""

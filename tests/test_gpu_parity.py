@@ -159,7 +159,7 @@ def test_nan_then_clean_field_on_one_context(env, shape):
         fd.copy_(torch.from_numpy(clean))
         if stepwise:
             rank = d.order()
-            d.gradient()
+            grad = d.gradient()  # (caller-owned: must stay alive while the context uses it)
         else:
             rank = torch.empty(clean.size, dtype=torch.int32, device="cuda")
             d.run_all(rank)
