@@ -78,12 +78,17 @@ __device__ __forceinline__ bool slot_in(const Geo3& g, const StarTab& S, int x, 
 }
 
 // follow the descending v-path from v to its minimum (Sec. 5.1(a))
+// (K decreases along the path, so it has fewer than N steps: the bound only stops a walk over
+// a gradient buffer the caller freed or overwrote from spinning on the GPU)
 __device__ __forceinline__ int64_t descend(const Geo3& g, const StarTab& S, int64_t v) {
-    while (true) {
+    for (int64_t steps = 0; steps < g.N; steps++) {
         const int c = vcode_of(g, v);
         if (c < 0) return v;
-        v += S.lin[c];
+        const int64_t u = v + S.lin[c];
+        if (u < 0 || u >= g.N) return v;
+        v = u;
     }
+    return v;
 }
 
 // sort key of a critical cell: x << 12 | G  ->  rank(x) << 12 | G
