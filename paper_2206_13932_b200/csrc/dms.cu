@@ -734,7 +734,7 @@ dms_status launch_gradient(dms_ctx* c, int64_t v0, int64_t v1) {
         }
         B.totals = c->totals;
         B.err = c->err;
-        k_gradient_t5<<<(unsigned)ceil_div(v1 - v0, kT5Block), kT5Block, 0, c->st>>>(B);
+        k_gradient_t5<<<(unsigned)(2 * ceil_div(v1 - v0, 2 * kT5Block)), kT5Block, 0, c->st>>>(B);  // CTA pairs per window
     } else if (c->ndim >= 2) {
         static const int lut_env = getenv("DMS_LUT2") ? atoi(getenv("DMS_LUT2")) : 1;
         // 3D: pools of 8 x 128 vertices per CTA, expanded in work order

@@ -420,9 +420,11 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
     }
     __syncthreads();
     const int64_t LxLy = (int64_t)A.Lx * A.Ly;
-    // consecutive vertices alternate between the 18- and the 6-neighbour class: the first two
-    // warps take the CTA's even offsets, the last two the odd ones (one class per warp within a row)
-    const int64_t v = A.v0 + (int64_t)blockIdx.x * blockDim.x + (((threadIdx.x & 63) << 1) | (threadIdx.x >> 6));
+    // consecutive vertices alternate between the 18- and the 6-neighbour class (within a row):
+    // a pair of CTAs shares a window of 2 x 128 vertices, one takes its even offsets, the other
+    // its odd ones, so a CTA (and each of its warps) runs one class and the short CTAs of
+    // 6-neighbour stars retire early instead of idling beside the long ones
+    const int64_t v = A.v0 + (int64_t)(blockIdx.x >> 1) * (2 * kT5Block) + 2 * (int64_t)threadIdx.x + (blockIdx.x & 1);
     const bool active = v < A.v1;
     uint32_t critE = 0, critQ = 0, crit_v = 0;
     uint64_t critT = 0;
