@@ -501,9 +501,14 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
             vcode = delta;
             cE = 1u << delta;
             zE = low & ~cE;
-            for (uint64_t m = T.edge_tmask[delta] & lowT; m; m &= m - 1) {
-                const int t = __ffsll((long long)m) - 1;
-                if (__popc(T.tri_emask[t] & ~cE) == 1) oT |= 1ull << t;
+            {
+                const uint64_t mm = T.edge_tmask[delta] & lowT;
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    for (uint32_t m = h ? (uint32_t)(mm >> 32) : (uint32_t)mm; m; m &= m - 1) {
+                        const int t = __ffs(m) - 1 + 32 * h;
+                        if (__popc(T.tri_emask[t] & ~cE) == 1) oT |= 1ull << t;
+                    }
             }
             auto set_tcode = [&](int t, uint64_t code) {
                 if (t < 32) tc_lo |= code << (2 * t);
@@ -511,10 +516,13 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
             };
             // push every unclassified cofacet of a classified cell with one unclassified facet
             auto push_cof_tri_of_edge = [&](int e) {
-                for (uint64_t m = T.edge_tmask[e] & lowT & ~cT; m; m &= m - 1) {
-                    const int b = __ffsll((long long)m) - 1;
-                    if (__popc(T.tri_emask[b] & ~cE) == 1) oT |= 1ull << b;
-                }
+                const uint64_t mm = T.edge_tmask[e] & lowT & ~cT;
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    for (uint32_t m = h ? (uint32_t)(mm >> 32) : (uint32_t)mm; m; m &= m - 1) {
+                        const int b = __ffs(m) - 1 + 32 * h;
+                        if (__popc(T.tri_emask[b] & ~cE) == 1) oT |= 1ull << b;
+                    }
             };
             auto push_cof_tet_of_tri = [&](int t) {
                 for (uint32_t m = T.tri_qmask[t] & lowQ & ~cQ; m; m &= m - 1) {
@@ -528,11 +536,14 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
                     // pop the minimum-key member of PQone
                     uint32_t best = 0xffffffffu;
                     int bi = -1, bty = 0;
-                    for (uint64_t m = oT; m; m &= m - 1) {
-                        const int t = __ffsll((long long)m) - 1;
-                        const uint32_t k = mykey[t * kT5Block];
-                        if (k < best) { best = k; bi = t; bty = 2; }
-                    }
+                    // (48 triangle slots: two 32-bit scans are cheaper than one over 64 bits)
+#pragma unroll
+                    for (int h = 0; h < 2; h++)
+                        for (uint32_t m = h ? (uint32_t)(oT >> 32) : (uint32_t)oT; m; m &= m - 1) {
+                            const int t = __ffs(m) - 1 + 32 * h;
+                            const uint32_t k = mykey[t * kT5Block];
+                            if (k < best) { best = k; bi = t; bty = 2; }
+                        }
                     for (uint32_t m = oQ; m; m &= m - 1) {
                         const int q = __ffs(m) - 1;
                         const uint32_t k = mykey[(kT5NT + q) * kT5Block];
@@ -573,11 +584,13 @@ __global__ void __launch_bounds__(kT5Block) k_gradient_t5(T5Args A) {
                     const uint32_t k = keyE(s);
                     if (k < best) { best = k; bi = s; bty = 1; }
                 }
-                for (uint64_t m = zT; m; m &= m - 1) {
-                    const int t = __ffsll((long long)m) - 1;
-                    const uint32_t k = mykey[t * kT5Block];
-                    if (k < best) { best = k; bi = t; bty = 2; }
-                }
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    for (uint32_t m = h ? (uint32_t)(zT >> 32) : (uint32_t)zT; m; m &= m - 1) {
+                        const int t = __ffs(m) - 1 + 32 * h;
+                        const uint32_t k = mykey[t * kT5Block];
+                        if (k < best) { best = k; bi = t; bty = 2; }
+                    }
                 for (uint32_t m = zQ; m; m &= m - 1) {
                     const int q = __ffs(m) - 1;
                     const uint32_t k = mykey[(kT5NT + q) * kT5Block];
