@@ -10,18 +10,22 @@
 //   * the two priority queues (PQzero / PQone) and the classification state as bit
 //     masks over the star's edge / triangle / tetrahedron slots (triangles keyed by
 //     C(hi,2)+lo, so a pop is a find-first-set);
-//   * 3D: k_gradient_pool -- a CTA ranks the neighbours of a pool of 1024 vertices and
-//     expands the stars in work order (warps of near-equal work); 2D: k_gradient_lut2 --
-//     the result of every one of the 1957 2D star patterns is tabulated once per
-//     context (k_build_lut2, the same process_star) and looked up; 1D: k_gradient1.
+//   * 3D: k_gradient_pool -- a CTA ranks the neighbours of a pool of 1024 vertices, sorts the
+//     stars by class and work and expands them in that order (warps of near-equal work).
+//     By default the expansion is the closed form below (process_star_simple / _two / _fast:
+//     the minimum spanning forest of the lower link + triangle peeling; the queues above are
+//     the A/B path DMS_GRAD_FAST=0 and the 2D table builder); 2D: k_gradient_lut2 -- the
+//     result of every one of the 1957 2D star patterns is tabulated once per context
+//     (k_build_lut2, the same process_star) and looked up; 1D: k_gradient1.
 // The critical cells of every lower star (Alg. 2 l. 10-12) are appended as (anchored
 // id, sort key) records; the sort key rank(x) << 12 | G gives the lexicographic order.
 //
-// Gradient words:
-//   3D uint64 lo : 2-bit code of tri slots 0..31 (1: paired with edge tri_a, 2: tri_b)
-//      uint64 hi : tri slots 32..35 (bits 0-7) | tet codes, 2 bits x 24 (bits 8-55,
-//                  j+1: paired with triangle tet_tri[T][j]) | vertex code (bits 56-59:
-//                  edge slot paired with x, 15 = x is a minimum)
+// Gradient words (dms.h):
+//   3D uint64 lo : a nibble per edge slot w (bits 4w..4w+3): 1 + the slot u of the third
+//                  vertex of the triangle (x, n_w, n_u) paired with the edge (x, n_w), 0 = none
+//                  | vertex code (bits 56-59: edge slot paired with x, 15 = x is a minimum)
+//      uint64 hi : tet codes, 2 bits x 24 (bits 0-47, j+1: paired with triangle
+//                  tet_tri[T][j]) | lower mask (bits 48-61) -- all a dual chase needs
 //   2D uint16    : vertex code (bits 0-2, 7 = minimum) | tri codes 2 bits x 6 (bits 3-14)
 //   1D uint8     : vertex code (0 = left edge, 1 = right edge, 3 = minimum)
 #pragma once
